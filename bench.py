@@ -1,0 +1,466 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 MoM triangle-pair Green-function fill (arXiv 1901.04162).
+
+One step = one full fill of the configuration's N x N complex128 matrix Z
+(sharded by observation-row blocks over the ranks): TABLE mode = K1 pair
+distance range (+ 16-byte NCCL all-reduce across ranks) + K2 device table
+build + K3 fill; DIRECT mode = K4 fill (the reference charges the table build
+to the table side, matfill.hpp:289-292).  Inputs (mesh, quadrature points)
+are resident in HBM; the output (e.g. 107 GB for C5) is far larger than L2,
+so no flush is needed between steps.
+
+Default workload: BASELINE.json configs[4] (C5, icosphere L6, N = 81920,
+m = 6, n = 4, k = 2 pi / 0.15), the metric's "vs N at 1/2/4/8 B200" config.
+Rank 0 prints one JSON line.  ``--impl reference`` times the reference's own
+CPU fill (oracle/_ref, compiled from /root/reference) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS_PER_EVAL = 44  # the reference's table-mode op count (FMA = 2)
+
+CONFIGS = {
+    "c2": dict(name="C2 icosphere L3 N=1280 m=6 n=4 lambda=1", kind="sphere", level=3, m=6, n=4,
+               lambda0=1.0),
+    "c3": dict(name="C3 icosphere L5 N=20480 m=7 n=5 lambda=0.3", kind="sphere", level=5, m=7,
+               n=5, lambda0=0.3),
+    "c4": dict(name="C4 plate 1m 100x100 N=20000 m=6 n=4 eps_r=4-0.4j lambda0=1", kind="plate",
+               cells=100, m=6, n=4, lambda0=1.0, eps_r=4.0, eps_r_im=-0.4),
+    "c5": dict(name="C5 icosphere L6 N=81920 m=6 n=4 lambda=0.15", kind="sphere", level=6, m=6,
+               n=4, lambda0=0.15),
+}
+SEED, JITTER = 1901, 1e-3
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def make_mesh(gk, cfg):
+    if cfg["kind"] == "sphere":
+        return gk.jitter(gk.generate_sphere_mesh(1.0, cfg["level"]), SEED, JITTER)
+    return gk.generate_plate_mesh(1.0, cfg["cells"])
+
+
+def rows_of(rank, world, N):
+    """contiguous row blocks, chunk = ceil(N / world) (matfill.hpp:211-215)"""
+    chunk = (N + world - 1) // world
+    b = min(N, rank * chunk)
+    return b, min(N, b + chunk)
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled (NVML, every 50 ms) during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.err = None
+
+    def _run(self):
+        import pynvml as nv
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for nm, b in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(nm)
+            except Exception as exc:  # keep sampling
+                self.err = repr(exc)
+            self.stop.wait(0.05)
+
+    def __enter__(self):
+        import threading
+        self.stop = threading.Event()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis else self.index
+            self.h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        except Exception as exc:
+            self.err = repr(exc)
+            self.th = None
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        if self.th:
+            self.th.join(timeout=2)
+
+    def summary(self):
+        out = {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+               "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+               "reasons": sorted(self.reasons)}
+        if self.err and not self.samples:
+            out["error"] = self.err
+        return out
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_sample(cfg, mesh_v, mesh_t, k, mode, lo, hi, S, threads, target_s=12.0):
+    """Row-sampled reference CPU fill: rows p = floor(s N / R)."""
+    from oracle.pyoracle import DIRECT, TABLE, Ref, SamplingConfig as RCfg
+    ref = Ref()
+    N = mesh_t.shape[0]
+    m, n = cfg["m"], cfg["n"]
+    per_row = (N - 1) * 3 * m * n
+    # ~25 ns / eval / thread on the reference: size for ~target_s of CPU work
+    R = max(threads, int(target_s / (per_row * 25e-9)))
+    R = min(N, max(1, (R // threads) * threads))
+    rows = np.array([(s * N) // R for s in range(R)], np.uint64)
+    ev, build_s = None, 0.0
+    if mode == "table":
+        t0 = time.perf_counter()
+        plan = ref.build_plan(RCfg(r_min=lo, r_max=hi, samples_per_wavelength=S),
+                              2 * math.pi / k)
+        ev = ref.evaluator(plan, k)
+        build_s = time.perf_counter() - t0
+    _, calls, wall = ref.fill_sampled_rows(mesh_v, mesh_t, m, n, TABLE if ev else DIRECT, k,
+                                           rows, ev=ev, threads=threads)
+    return {"evals": calls, "wall_s": wall, "build_s": build_s, "rows": int(R),
+            "evals_per_s": calls / wall}
+
+
+def run_reference_arm(args, cfg, rank, world):
+    """--impl reference: the reference's own CPU fill on this host's cores."""
+    if rank != 0:
+        return
+    import paper_1901_04162_b200 as gk  # host-only helpers: mesh generators
+    mesh = make_mesh(gk, cfg)
+    k = 2 * math.pi / cfg["lambda0"]
+    if cfg.get("eps_r_im"):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the reference is real-k only (kernel.hpp:23-24); C4 has no reference path"}))
+        return
+    from oracle.pyoracle import Oracle
+    o = Oracle()
+    threads = cpu_threads()
+    mode = "direct" if args.mode in ("auto", "direct") else "table"
+    lo = hi = None
+    if mode == "table":  # the reference's own conventions (matfill.hpp:270)
+        hi = o.max_vertex_distance(mesh.vertices) * 1.01
+        lo = 1e-4 * cfg["lambda0"]
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = reference_sample(cfg, mesh.vertices, mesh.triangles, k, mode, lo, hi, args.S, threads,
+                             target_s=args.cpu_seconds)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median(x["evals_per_s"] for x in vals)
+    N = mesh.triangle_count()
+    total = 3 * cfg["m"] * cfg["n"] * N * (N - 1)
+    line = {
+        "impl": "reference", "metric": "green_fn_evals_per_s", "value": v, "unit": "evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / v * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded jittered icosphere)",
+        "config": {"workload": cfg["name"], "mode": mode, "samples_per_wavelength": args.S},
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": threads, "kind": "reference",
+                         "sample": f"{vals[0]['rows']} rows x all {N} columns per step, "
+                                   f"AnalyticKernel/TableKernel::accumulate, extrapolated to the "
+                                   f"full {total:.3e}-eval fill"},
+        "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gk", choices=["gk", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="auto", choices=["auto", "direct", "table"])
+    ap.add_argument("--S", type=int, default=10000, help="samples per wavelength (table)")
+    ap.add_argument("--both-modes", type=int, default=1, help="also time the other mode")
+    ap.add_argument("--cpu-baseline", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e", type=int, default=1)
+    ap.add_argument("--vs-n", type=int, default=1, help="also time C2/C3 fills (rank 0, N=1)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        run_reference_arm(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import paper_1901_04162_b200 as gk
+
+    ctx = gk.Context.get(local)
+    mesh = make_mesh(gk, cfg)
+    N = mesh.triangle_count()
+    m, n = cfg["m"], cfg["n"]
+    spec = gk.QuadratureSpec(m, n)
+    medium = gk.Medium(lambda0=cfg["lambda0"], eps_r=cfg.get("eps_r", 1.0),
+                       eps_r_im=cfg.get("eps_r_im", 0.0))
+    k = gk.wavenumber(medium)
+    rb, re = rows_of(rank, world, N)
+    rows = re - rb
+    dmesh = gk.DeviceMesh(mesh, spec, ctx)
+    Z = torch.empty((max(rows, 1), N), dtype=torch.complex128, device=f"cuda:{local}")
+    total_evals = 3 * m * n * N * (N - 1)
+
+    def global_range():
+        lo, hi = dmesh.distance_range(rb, re) if rows else (math.inf, 0.0)
+        if world > 1:
+            t = torch.tensor([lo, -hi], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)   # C1: one 16-byte all-reduce
+            lo, hi = float(t[0]), -float(t[1])
+        return lo, hi
+
+    fill_ev = []
+
+    def step(mode):
+        table = None
+        if mode == "table":
+            lo, hi = global_range()
+            table = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
+                                                     samples_per_wavelength=args.S), medium,
+                                   ctx=ctx)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if rows:
+            gk.fill_rows(dmesh, gk.Mode.TABLE if table else gk.Mode.DIRECT, table=table, k=k,
+                         row_begin=rb, row_end=re, out=Z, report=False)
+        e1.record()
+        fill_ev.append((e0, e1))
+        return table
+
+    def timed(mode, steps, warmup):
+        for _ in range(warmup):
+            step(mode)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        fill_ev.clear()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(steps):
+            step(mode)
+        s1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = s0.elapsed_time(s1) / steps
+        fill_ms = sum(a.elapsed_time(b) for a, b in fill_ev) / len(fill_ev)
+        if world > 1:
+            t = torch.tensor([ms, fill_ms], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, fill_ms = float(t[0]), float(t[1])
+        return ms, fill_ms
+
+    # roofline denominator: FP64 DFMA peak measured on this device now
+    p64 = ctx.fp64_peak_tflops()
+    modes = ["direct", "table"] if args.mode == "auto" or args.both_modes else [args.mode]
+    if args.mode != "auto":
+        modes = [args.mode] + ([x for x in ("direct", "table") if x != args.mode]
+                               if args.both_modes else [])
+    results = {}
+    clocks = None
+    for i, mode in enumerate(modes):
+        steps = args.steps if i == 0 else max(1, min(args.steps, 3))
+        if i == 0:
+            with ClockSampler(local) as cs:
+                ms, fill_ms = timed(mode, steps, args.warmup)
+            clocks = cs.summary()
+        else:
+            ms, fill_ms = timed(mode, steps, 1)
+        evals_per_launch = 3 * m * n * rows * (N - 1)
+        results[mode] = {"ms_per_step": ms, "fill_kernel_ms": fill_ms,
+                         "evals_per_s": total_evals / (ms * 1e-3),
+                         "kernel_tflops": evals_per_launch * FLOPS_PER_EVAL / (fill_ms * 1e-3) / 1e12}
+    chosen = args.mode if args.mode != "auto" else min(results, key=lambda x: results[x]["ms_per_step"])
+    main_res = results[chosen]
+
+    # launches in the timed region (this library's kernels only)
+    launches_per_step = 1 if chosen == "direct" else None
+    if chosen == "table":
+        launches_per_step = 2 + 14 + 1  # K1 (2) + K2 build (~14 incl. CUB) + K3
+
+    # e2e through the host-buffer C-ABI entry point (gk_fill_matrix_host), rank-local rows
+    e2e = None
+    if args.e2e and rank == 0 and world == 1:
+        e2e = run_e2e(gk, ctx, cfg, mesh, spec, medium, chosen, args, total_evals)
+
+    cpu = None
+    if args.cpu_baseline and rank == 0 and world == 1:
+        lo, hi = (dmesh.distance_range() if chosen == "table" else (None, None))
+        try:
+            k_real = k.real if isinstance(k, complex) else k
+            if cfg.get("eps_r_im"):
+                raise RuntimeError("no reference path for complex k")
+            smp = reference_sample(cfg, mesh.vertices, mesh.triangles, k_real, chosen, lo, hi,
+                                   args.S, cpu_threads(), target_s=args.cpu_seconds)
+            cpu = {"value": smp["evals_per_s"], "unit": "evals/s", "cores": cpu_threads(),
+                   "kind": "reference",
+                   "sample": f"{smp['rows']} of {N} rows x all columns through the reference's "
+                             f"{'TableKernel' if chosen == 'table' else 'AnalyticKernel'}::accumulate "
+                             f"({smp['evals']:.3e} evals in {smp['wall_s']:.2f} s; "
+                             f"table build {smp['build_s']*1e3:.1f} ms), extrapolated linearly"}
+        except Exception as exc:  # report, never fake
+            cpu = {"value": None, "unit": "evals/s", "cores": cpu_threads(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    vs_n = None
+    if args.vs_n and rank == 0 and world == 1 and args.config == "c5":
+        vs_n = run_vs_n(gk, ctx, chosen, args)
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.config}:{chosen}")
+        except (OSError, ValueError):
+            traffic = None
+
+    fill_bytes = rows * N * 16
+    line = {
+        "metric": "green_fn_evals_per_s",
+        "value": main_res["evals_per_s"],
+        "unit": "evals/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": main_res["ms_per_step"],
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: seeded jittered icosphere (splitmix64 seed 1901, 1e-3 m)",
+        "config": {"workload": cfg["name"], "mode": chosen,
+                   "samples_per_wavelength": args.S if chosen == "table" else None,
+                   "parallelism": f"row-block x{world}",
+                   "l2": "output Z >> L2 (no flush needed); inputs resident"},
+        "fill_time_s": main_res["ms_per_step"] * 1e-3,
+        "roofline": {"bound": "fp64", "achieved": main_res["kernel_tflops"], "peak": p64,
+                     "unit": "TFLOP/s", "frac": main_res["kernel_tflops"] / p64,
+                     "traffic": traffic,
+                     "note": f"{FLOPS_PER_EVAL} algorithmic FP64 flops/eval (SURVEY 8d, FMA=2) x "
+                             f"evals per launch / fill-kernel event time; peak = DFMA "
+                             f"microbenchmark on this GPU (MEASURED_PEAKS.json has no FP64 entry)",
+                     "hbm_write_gbs": fill_bytes / (main_res["fill_kernel_ms"] * 1e-3) / 1e9},
+        "modes": results,
+        "clocks": clocks,
+        "gpu_launches": launches_per_step * args.steps,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    if vs_n:
+        line["vs_N"] = vs_n
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals):
+    """Host mesh in, host Z out, through gk_fill_matrix_host (the C-ABI drop-in)."""
+    import torch
+    N = mesh.triangle_count()
+    nbytes = N * N * 16
+    try:
+        zh = torch.empty((N, N), dtype=torch.complex128, pin_memory=True)
+    except RuntimeError as exc:
+        return {"value": None, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": nbytes, "note": f"pinned host Z unavailable: {exc}"}
+    z = zh.numpy()
+    cfgs = gk.SamplingConfig(r_min=0.0, r_max=0.0, samples_per_wavelength=args.S)
+    m = gk.Mode.TABLE if mode == "table" else gk.Mode.DIRECT
+    gk.fill_matrix(mesh, spec, m, medium, cfgs, ctx=ctx, out=z)  # warm-up
+    steps = max(1, min(args.steps, 3))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        gk.fill_matrix(mesh, spec, m, medium, cfgs, ctx=ctx, out=z)
+    dt = (time.perf_counter() - t0) / steps
+    h2d = mesh.vertices.nbytes + mesh.triangles.nbytes
+    return {"value": total_evals / dt, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(nbytes), "ms_per_step": dt * 1e3,
+            "api": "gk_fill_matrix_host (pinned host Z)"}
+
+
+def run_vs_n(gk, ctx, mode, args):
+    """Z-fill time vs N on one GPU for the other sphere configs (informational)."""
+    import torch
+    out = {}
+    for key in ("c2", "c3"):
+        cfg = CONFIGS[key]
+        mesh = make_mesh(gk, cfg)
+        N = mesh.triangle_count()
+        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(cfg["m"], cfg["n"]), ctx)
+        med = gk.Medium(lambda0=cfg["lambda0"])
+        k = gk.wavenumber(med)
+        Z = torch.empty((N, N), dtype=torch.complex128, device=f"cuda:{ctx.device}")
+
+        def once():
+            t = None
+            if mode == "table":
+                lo, hi = dm.distance_range()
+                t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
+                                                     samples_per_wavelength=args.S), med, ctx=ctx)
+            gk.fill_rows(dm, gk.Mode.TABLE if t else gk.Mode.DIRECT, table=t, k=k, out=Z,
+                         report=False)
+        for _ in range(3):
+            once()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20 if key == "c2" else 3
+        e0.record()
+        for _ in range(reps):
+            once()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        ev = 3 * cfg["m"] * cfg["n"] * N * (N - 1)
+        out[key] = {"N": N, "fill_ms": ms, "evals_per_s": ev / (ms * 1e-3)}
+        del Z
+    return out
+
+
+if __name__ == "__main__":
+    main()

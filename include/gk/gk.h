@@ -1,0 +1,197 @@
+/*
+ * gk.h -- C ABI of the B200-native MoM Green-function fill (arXiv 1901.04162
+ * hot path).  libgk.so implements it with hand-written sm_100a CUDA kernels.
+ *
+ * The ABI is the drop-in boundary for the reference `gktab` library
+ * (/root/reference/proj/include/gktab/, header-only C++20).  The reference
+ * has no ABI of its own; every entry point below names the reference
+ * interface it replaces (file:line, relative to proj/include/gktab/).
+ *
+ * Conventions (mirroring the reference):
+ *  - errors: gk_status codes map 1:1 to the reference's exception types
+ *    (invalid_argument, domain_error, out_of_range, overflow_error,
+ *    runtime_error); gk_last_error() returns the message (thread-local).
+ *  - gk_c128 is layout-compatible with std::complex<double>.
+ *  - kinds use the reference's KernelKind values (kernel.hpp:14-17).
+ *  - pointers documented "device" are CUDA device pointers on the context's
+ *    device; "host" pointers are ordinary host memory.
+ *  - a gk_ctx owns one CUDA stream (or borrows the caller's, see
+ *    gk_ctx_set_stream); it is not re-entrant, but separate contexts may be
+ *    driven from separate host threads.
+ *  - there is no CPU fallback: without a usable sm_100 device every call
+ *    fails with GK_ERR_RUNTIME.
+ */
+#ifndef GK_GK_H
+#define GK_GK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GK_ABI_VERSION 1
+
+typedef enum gk_status {
+  GK_OK = 0,
+  GK_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  GK_ERR_DOMAIN = 2,           /* std::domain_error     */
+  GK_ERR_OUT_OF_RANGE = 3,     /* std::out_of_range     */
+  GK_ERR_OVERFLOW = 4,         /* std::overflow_error   */
+  GK_ERR_RUNTIME = 5           /* std::runtime_error, CUDA failures */
+} gk_status;
+
+/* gktab::KernelKind (kernel.hpp:14-17) */
+typedef enum gk_kind { GK_KIND_EXP = 0, GK_KIND_GREEN = 1 } gk_kind;
+
+/* AnalyticKernel vs TableKernel (matfill.hpp:59-87) */
+typedef enum gk_mode { GK_MODE_DIRECT = 0, GK_MODE_TABLE = 1 } gk_mode;
+
+typedef struct gk_c128 { double re, im; } gk_c128;
+
+typedef struct gk_ctx gk_ctx;
+typedef struct gk_table gk_table;
+typedef struct gk_mesh gk_mesh;
+
+/* gktab::Medium (kernel.hpp:25-38).  eps_r_im != 0 is the lossy-medium
+   extension (complex k = 2 pi sqrt(eps_r mu_r) / lambda0, principal root). */
+typedef struct gk_medium {
+  double lambda0, eps_r, mu_r, eps_r_im;
+} gk_medium;
+
+/* gktab::SamplingConfig (sampling.hpp:18-45), same defaults. */
+typedef struct gk_sampling_config {
+  double r_min, r_max;
+  int samples_per_wavelength;
+  int refine_interval_divisor;
+  double refine_halfwidth_in_t;
+  double dedup_fraction;
+  int refine;
+} gk_sampling_config;
+
+/* gktab::FillReport (matfill.hpp:33-47), the fields fill_matrix sets. */
+typedef struct gk_fill_report {
+  uint64_t N;
+  int m, n;
+  uint64_t predicted_calls, actual_calls, fallback_calls;
+  double wall_time_s; /* device time of the fill kernels (CUDA events) */
+} gk_fill_report;
+
+typedef struct gk_table_info {
+  uint64_t nodes, zeros, hash_buckets, lookup_buckets;
+  double r_min, r_max, t, dr_min, inv_dr_min, k_re, k_im;
+  int degree;
+  uint64_t device_bytes;
+  double build_ms; /* device time of gk_table_build */
+} gk_table_info;
+
+/* ---------------------------------------------------------------- context */
+int gk_abi_version(void);
+const char* gk_last_error(void);
+gk_status gk_ctx_create(int device, gk_ctx** out);
+gk_status gk_ctx_destroy(gk_ctx* ctx);
+/* Run on the caller's cudaStream_t (e.g. torch.cuda.current_stream()), used
+   as-is: 0 is the legacy default stream.  gk_ctx_use_own_stream restores the
+   context's own (non-blocking) stream. */
+gk_status gk_ctx_set_stream(gk_ctx* ctx, void* cuda_stream);
+gk_status gk_ctx_use_own_stream(gk_ctx* ctx);
+gk_status gk_ctx_synchronize(gk_ctx* ctx);
+
+/* ------------------------------------------------------------ kernel math */
+/* gktab::wavenumber (kernel.hpp:41-44); complex for eps_r_im != 0 */
+gk_status gk_wavenumber(const gk_medium* medium, double* k_re, double* k_im);
+
+/* ------------------------------------------------------------------ table */
+/* build_plan + KernelEvaluator ctor (sampling.hpp:149-236; evaluator.hpp:104-114:
+   build_table x2, build_hash, pack_green_stencils), built on the device.
+   The plan and the reference-format hash are bit-identical to the
+   reference's; node values come from device sincos (ulp-level differences). */
+gk_status gk_table_build(gk_ctx* ctx, const gk_sampling_config* cfg, const gk_medium* medium,
+                         int lagrange_degree, gk_table** out);
+gk_status gk_table_info_get(const gk_table* table, gk_table_info* info);
+/* Host copies of the plan (abscissae[nodes], zeros[zeros]), node values
+   (exp/green[nodes]) and the reference-format hash buckets[hash_buckets]
+   (table.hpp:40-82).  Any pointer may be NULL. */
+gk_status gk_table_download(const gk_table* table, double* abscissae, double* zeros,
+                            gk_c128* exp_values, gk_c128* green_values, uint32_t* buckets);
+gk_status gk_table_destroy(gk_table* table);
+
+/* KernelEvaluator::eval_batch (evaluator.hpp:209-221) when table != NULL
+   (Exp: linear, Green: Lagrange; r < r_min -> analytic fallback, counted),
+   eval_analytic (kernel.hpp:48-61) elementwise when table == NULL (k from
+   k_re/k_im).  radii/out are device pointers.  On an invalid radius the call
+   fails with the first failing index in the message, like the reference. */
+gk_status gk_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,
+                        double k_im, const double* radii, size_t n, gk_c128* out,
+                        uint64_t* fallbacks);
+
+/* ------------------------------------------------------------------- mesh */
+/* Uploads a triangle mesh (host arrays: xyz-interleaved vertices[3 nv],
+   triangles[3 nt]) and generates its quadrature points on the device:
+   m outer points per triangle (triangle_rule, quadrature.hpp:35-76) and n
+   Gauss points on each edge (gauss_legendre_unit, quadrature.hpp:85-110),
+   exactly as detail::outer_points / inner_points (matfill.hpp:105-133).
+   Validates like TriangleMesh::validate and QuadratureSpec::validate. */
+gk_status gk_mesh_create(gk_ctx* ctx, const double* vertices, size_t nv,
+                         const uint32_t* triangles, size_t nt, int outer_points,
+                         int inner_points_per_edge, gk_mesh** out);
+/* host copies: outer[4][nt*m] (x,y,z,w planes), inner[4][nt*3n] */
+gk_status gk_mesh_points_download(const gk_mesh* mesh, double* outer, double* inner);
+gk_status gk_mesh_destroy(gk_mesh* mesh);
+
+/* K1: min and max quadrature-point pair distance over observation rows
+   [row_begin,row_end) and every source q != p (replaces max_vertex_distance
+   + the fixed r_min of bench_compare, matfill.hpp:270 / mesh.hpp:62-68).
+   The result is widened by 2^-49 relative on both sides so that every radius
+   the fill (or the reference's glibc sqrt) computes lies inside it. */
+gk_status gk_distance_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,
+                            double* r_min, double* r_max);
+
+/* ------------------------------------------------------------------- fill */
+/* fill_matrix's fill_rows (matfill.hpp:169-203) for rows [row_begin,row_end):
+   z[(p-row_begin)*ldz + q] = sum_o sum_i w_o w_i K(|x_o - x_i|), self pairs 0.
+   mode DIRECT = AnalyticKernel{k}, TABLE = TableKernel{table} (k from the
+   table).  z is a device pointer.  report == NULL: asynchronous on the
+   context stream; otherwise the call synchronizes and fills the report
+   (actual_calls = 3 m n rows (N-1), exact fallback count, kernel time). */
+gk_status gk_fill_rows(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
+                       gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
+                       gk_c128* z, size_t ldz, gk_fill_report* report);
+
+/* fill_matrix<Kernel> (matfill.hpp:144-228) end to end from HOST buffers:
+   upload mesh, quadrature points, (TABLE) K1 range when cfg->r_min <= 0 or
+   cfg->r_max <= 0, table build, fill, copy Z (nt x nt, row-major) back into
+   z_host.  The reference-facing drop-in entry point. */
+gk_status gk_fill_matrix_host(gk_ctx* ctx, const double* vertices, size_t nv,
+                              const uint32_t* triangles, size_t nt, int outer_points,
+                              int inner_points_per_edge, gk_mode mode,
+                              const gk_sampling_config* cfg, const gk_medium* medium,
+                              gk_kind kind, gk_c128* z_host, gk_fill_report* report);
+
+/* predicted_calls (matfill.hpp:50-56): 3 m n N^2 with the overflow guard */
+gk_status gk_predicted_calls(uint64_t N, uint64_t m, uint64_t n, uint64_t* out);
+
+/* ------------------------------------------------- workload generators (host)
+   generate_sphere_mesh (mesh.hpp:154-202), bit-identical; two-call pattern:
+   pass NULL arrays to get nv/nt first.  Plate and jitter are the benchmark's
+   synthetic-workload generators (not in the reference). */
+gk_status gk_sphere_mesh(double radius, int subdivisions, double* vertices, size_t* nv,
+                         uint32_t* triangles, size_t* nt);
+gk_status gk_plate_mesh(double side, int cells, double* vertices, size_t* nv,
+                        uint32_t* triangles, size_t* nt);
+/* splitmix64(seed) per coordinate, U(-amp, amp) from the top 53 bits */
+gk_status gk_jitter(double* vertices, size_t nv, uint64_t seed, double amp);
+
+/* ------------------------------------------------------------ measurement */
+/* DFMA throughput microbenchmark on the context's device: FP64 TFLOP/s with
+   an FMA counted as 2 flops (the fill's roofline denominator). */
+gk_status gk_bench_fp64_peak(gk_ctx* ctx, double* tflops);
+/* SM count and clock of the context's device */
+gk_status gk_device_info(gk_ctx* ctx, int* sm_count, int* sm_clock_khz, int* cc_major,
+                         int* cc_minor);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GK_GK_H */

@@ -1,0 +1,587 @@
+// abi.cu -- the extern "C" boundary (include/gk/gk.h) and the host-side
+// orchestration behind it.  Every entry point converts exceptions into
+// gk_status codes that mirror the reference's exception types; the message
+// is kept in a thread-local buffer for gk_last_error().
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gk_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+gk_status guarded(F&& f) {
+  try {
+    f();
+    return GK_OK;
+  } catch (const gk::Error& e) {
+    g_last_error = e.what;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return GK_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return GK_ERR_RUNTIME;
+  }
+}
+
+void need(bool ok, gk_status s, const char* what) {
+  if (!ok) gk::fail(s, what);
+}
+
+// gktab::Medium::validate (kernel.hpp:30-37)
+void validate_medium(const gk_medium& m) {
+  need(std::isfinite(m.lambda0) && m.lambda0 > 0.0, GK_ERR_INVALID_ARGUMENT,
+       "Medium: lambda0 must be finite and > 0");
+  need(std::isfinite(m.eps_r) && m.eps_r > 0.0, GK_ERR_INVALID_ARGUMENT,
+       "Medium: eps_r must be finite and > 0");
+  need(std::isfinite(m.mu_r) && m.mu_r > 0.0, GK_ERR_INVALID_ARGUMENT,
+       "Medium: mu_r must be finite and > 0");
+  need(std::isfinite(m.eps_r_im) && m.eps_r_im <= 0.0, GK_ERR_INVALID_ARGUMENT,
+       "Medium: eps_r_im must be finite and <= 0 (lossy medium)");
+}
+
+// gktab::SamplingConfig::validate (sampling.hpp:30-45)
+void validate_cfg(const gk_sampling_config& c) {
+  need(std::isfinite(c.r_min) && std::isfinite(c.r_max) && 0.0 < c.r_min && c.r_min < c.r_max,
+       GK_ERR_INVALID_ARGUMENT, "SamplingConfig: need 0 < r_min < r_max, both finite");
+  need(c.samples_per_wavelength >= 2, GK_ERR_INVALID_ARGUMENT,
+       "SamplingConfig: samples_per_wavelength must be >= 2");
+  need(c.refine_interval_divisor >= (c.refine ? 2 : 1), GK_ERR_INVALID_ARGUMENT,
+       "SamplingConfig: refine_interval_divisor must be >= 2 when refinement is on");
+  need(c.refine_halfwidth_in_t > 0.0, GK_ERR_INVALID_ARGUMENT,
+       "SamplingConfig: refine_halfwidth_in_t must be > 0");
+  need(c.dedup_fraction > 0.0 && c.dedup_fraction <= 1.0, GK_ERR_INVALID_ARGUMENT,
+       "SamplingConfig: dedup_fraction must be in (0, 1]");
+  need(!(c.refine && c.refine_halfwidth_in_t * c.refine_interval_divisor < 1.0),
+       GK_ERR_INVALID_ARGUMENT,
+       "SamplingConfig: refinement window narrower than one refined interval");
+}
+
+// k = 2 pi sqrt(eps_r mu_r) / lambda0 (kernel.hpp:41-44); complex when lossy
+void wavenumber(const gk_medium& m, double& k_re, double& k_im) {
+  validate_medium(m);
+  if (m.eps_r_im == 0.0) {
+    k_re = 2.0 * gk::kPi * std::sqrt(m.eps_r * m.mu_r) / m.lambda0;
+    k_im = 0.0;
+    return;
+  }
+  const std::complex<double> s = std::sqrt(std::complex<double>(m.eps_r * m.mu_r, m.eps_r_im * m.mu_r));
+  const std::complex<double> k = 2.0 * gk::kPi * s / m.lambda0;
+  k_re = k.real();
+  k_im = k.imag();
+}
+
+// nominal base interval t = lambda0 / (S sqrt(eps_r mu_r)) (sampling.hpp:112-122);
+// lossy: the real part of the refractive index sets the wavelength
+double base_interval(const gk_medium& m, int S) {
+  if (m.eps_r_im == 0.0)
+    return m.lambda0 / (static_cast<double>(S) * std::sqrt(m.eps_r * m.mu_r));
+  const std::complex<double> s = std::sqrt(std::complex<double>(m.eps_r * m.mu_r, m.eps_r_im * m.mu_r));
+  return m.lambda0 / (static_cast<double>(S) * s.real());
+}
+
+void validate_spec(int m, int n) {
+  need(m == 1 || m == 3 || m == 4 || m == 6 || m == 7, GK_ERR_INVALID_ARGUMENT,
+       "QuadratureSpec: outer_points must be one of 1, 3, 4, 6, 7");
+  need(n >= 1, GK_ERR_INVALID_ARGUMENT, "QuadratureSpec: inner_points_per_edge must be >= 1");
+  need(n <= 32, GK_ERR_INVALID_ARGUMENT, "QuadratureSpec: device fill supports inner_points_per_edge <= 32");
+}
+
+uint64_t predicted(uint64_t N, uint64_t m, uint64_t n) {
+  const unsigned __int128 wide =
+      static_cast<unsigned __int128>(3) * m * n * (static_cast<unsigned __int128>(N) * N);
+  need(wide <= static_cast<unsigned __int128>(UINT64_MAX), GK_ERR_OVERFLOW,
+       "predicted_calls: 3*m*n*N^2 overflows 64 bits");
+  return static_cast<uint64_t>(wide);
+}
+
+void check_ctx(const gk_ctx* c) { need(c != nullptr, GK_ERR_INVALID_ARGUMENT, "null gk_ctx"); }
+
+void use_device(const gk_ctx* c) { GK_CUDA(cudaSetDevice(c->device)); }
+
+}  // namespace
+
+extern "C" {
+
+int gk_abi_version(void) { return GK_ABI_VERSION; }
+
+const char* gk_last_error(void) { return g_last_error.c_str(); }
+
+gk_status gk_ctx_create(int device, gk_ctx** out) {
+  return guarded([&] {
+    need(out != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");
+    int count = 0;
+    GK_CUDA(cudaGetDeviceCount(&count));
+    need(device >= 0 && device < count, GK_ERR_INVALID_ARGUMENT, "gk_ctx_create: no such device");
+    GK_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    GK_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      gk::fail(GK_ERR_RUNTIME, "gk_ctx_create: libgk is built for sm_100a (B200); device is sm_" +
+                                   std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* c = new gk_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    cudaMemPool_t pool;
+    GK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    GK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    try {
+      GK_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+      c->stream = c->own;
+      GK_CUDA(cudaEventCreate(&c->ev0));
+      GK_CUDA(cudaEventCreate(&c->ev1));
+      c->scratch.alloc(64, c->stream);
+      GK_CUDA(cudaMemsetAsync(c->scratch.p, 0, c->scratch.bytes(), c->stream));
+      gk::init_phase_table(c);
+      GK_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+      gk_ctx_destroy(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+gk_status gk_ctx_destroy(gk_ctx* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    c->scratch.reset();
+    c->phase.reset();
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->own) cudaStreamDestroy(c->own);
+    delete c;
+  });
+}
+
+gk_status gk_ctx_set_stream(gk_ctx* c, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    c->stream = static_cast<cudaStream_t>(s);
+  });
+}
+
+gk_status gk_ctx_use_own_stream(gk_ctx* c) {
+  return guarded([&] {
+    check_ctx(c);
+    c->stream = c->own;
+  });
+}
+
+gk_status gk_ctx_synchronize(gk_ctx* c) {
+  return guarded([&] {
+    check_ctx(c);
+    use_device(c);
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+gk_status gk_wavenumber(const gk_medium* m, double* k_re, double* k_im) {
+  return guarded([&] {
+    need(m && k_re && k_im, GK_ERR_INVALID_ARGUMENT, "null argument");
+    wavenumber(*m, *k_re, *k_im);
+  });
+}
+
+gk_status gk_table_build(gk_ctx* c, const gk_sampling_config* cfg, const gk_medium* med,
+                         int degree, gk_table** out) {
+  return guarded([&] {
+    check_ctx(c);
+    need(cfg && med && out, GK_ERR_INVALID_ARGUMENT, "null argument");
+    validate_cfg(*cfg);  // build_plan validates before the medium (sampling.hpp:213)
+    double k_re, k_im;
+    wavenumber(*med, k_re, k_im);
+    need(degree >= 1, GK_ERR_INVALID_ARGUMENT, "KernelEvaluator: lagrange_degree must be >= 1");
+    need(degree <= 7, GK_ERR_INVALID_ARGUMENT, "device tables support lagrange_degree <= 7");
+    const double t_nominal = base_interval(*med, cfg->samples_per_wavelength);
+    use_device(c);
+    auto* t = new gk_table();
+    t->ctx = c;
+    try {
+      gk::build_table_device(c, t, *cfg, k_re, t_nominal, k_re, k_im, degree);
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+gk_status gk_table_info_get(const gk_table* t, gk_table_info* info) {
+  return guarded([&] {
+    need(t && info, GK_ERR_INVALID_ARGUMENT, "null argument");
+    *info = t->info;
+  });
+}
+
+gk_status gk_table_download(const gk_table* t, double* absc, double* zeros, gk_c128* ev,
+                            gk_c128* gv, uint32_t* buckets) {
+  return guarded([&] {
+    need(t != nullptr, GK_ERR_INVALID_ARGUMENT, "null table");
+    use_device(t->ctx);
+    cudaStream_t s = t->ctx->stream;
+    const size_t n = t->info.nodes;
+    if (absc) GK_CUDA(cudaMemcpyAsync(absc, t->absc.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (ev) GK_CUDA(cudaMemcpyAsync(ev, t->exp_vals.p, n * 16, cudaMemcpyDeviceToHost, s));
+    if (gv) GK_CUDA(cudaMemcpyAsync(gv, t->green_vals.p, n * 16, cudaMemcpyDeviceToHost, s));
+    if (buckets)
+      GK_CUDA(cudaMemcpyAsync(buckets, t->hash.p, t->info.hash_buckets * 4, cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+    if (zeros && !t->zeros.empty()) std::memcpy(zeros, t->zeros.data(), t->zeros.size() * 8);
+  });
+}
+
+gk_status gk_table_destroy(gk_table* t) {
+  return guarded([&] {
+    if (!t) return;
+    cudaSetDevice(t->ctx->device);
+    cudaStreamSynchronize(t->ctx->stream);
+    delete t;
+  });
+}
+
+gk_status gk_eval_batch(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re, double k_im,
+                        const double* radii, size_t n, gk_c128* out, uint64_t* fallbacks) {
+  return guarded([&] {
+    check_ctx(c);
+    need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
+    if (t) {
+      k_re = t->dev.k_re;
+      k_im = t->dev.k_im;
+    }
+    need(k_re >= 0.0, GK_ERR_INVALID_ARGUMENT, "eval_analytic: k must be >= 0");
+    if (fallbacks) *fallbacks = 0;
+    if (n == 0) return;
+    need(radii && out, GK_ERR_INVALID_ARGUMENT, "null buffer");
+    use_device(c);
+    unsigned long long* w = c->scratch.p;  // [0] fallbacks, [1] first bad (index<<3 | code)
+    const unsigned long long init[2] = {0ull, ~0ull};
+    GK_CUDA(cudaMemcpyAsync(w, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    gk::launch_eval_batch(c, t, kind, k_re, k_im, radii, n, out, w);
+    unsigned long long res[2];
+    GK_CUDA(cudaMemcpyAsync(res, w, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    if (fallbacks) *fallbacks = res[0];
+    if (res[1] != ~0ull) {
+      const size_t idx = static_cast<size_t>(res[1] >> 3);
+      const unsigned code = static_cast<unsigned>(res[1] & 7u);
+      double r = 0.0;
+      GK_CUDA(cudaMemcpy(&r, radii + idx, sizeof(double), cudaMemcpyDeviceToHost));
+      const char* why = code == 2 ? "exp(-jkr)/r is singular at r = 0"
+                      : code == 3 ? "r outside the tabulated range"
+                                  : "r must be >= 0 (Exp) / > 0 (Green)";
+      gk::fail(GK_ERR_INVALID_ARGUMENT, "eval_batch: radius [" + std::to_string(idx) + "] = " +
+                                            std::to_string(r) + ": " + why);
+    }
+  });
+}
+
+gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32_t* tris,
+                         size_t nt, int m, int n, gk_mesh** out) {
+  return guarded([&] {
+    check_ctx(c);
+    need(out != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");
+    validate_spec(m, n);  // fill_matrix validates the spec first (matfill.hpp:148)
+    need(nv == 0 || verts, GK_ERR_INVALID_ARGUMENT, "null vertices");
+    need(nt == 0 || tris, GK_ERR_INVALID_ARGUMENT, "null triangles");
+    gk::validate_mesh(verts, nv, tris, nt);
+    need(nt >= 1, GK_ERR_INVALID_ARGUMENT, "gk_mesh_create: empty mesh");
+    use_device(c);
+    auto* mesh = new gk_mesh();
+    try {
+      mesh->ctx = c;
+      mesh->N = nt;
+      mesh->nv = nv;
+      mesh->m = m;
+      mesh->n = n;
+      mesh->outer.alloc(nt * m, c->stream);
+      mesh->inner.alloc(nt * 3 * static_cast<size_t>(n), c->stream);
+      mesh->bounds.alloc(nt, c->stream);
+      mesh->binner.alloc(nt, c->stream);
+      gk::DevBuf<double> dv;
+      gk::DevBuf<uint32_t> dt;
+      dv.alloc(3 * nv, c->stream);
+      dt.alloc(3 * nt, c->stream);
+      GK_CUDA(cudaMemcpyAsync(dv.p, verts, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      GK_CUDA(cudaMemcpyAsync(dt.p, tris, 3 * nt * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+      gk::launch_points(mesh, dv.p, dt.p, c->stream);
+      GK_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+      delete mesh;
+      throw;
+    }
+    *out = mesh;
+  });
+}
+
+gk_status gk_mesh_points_download(const gk_mesh* mesh, double* outer, double* inner) {
+  return guarded([&] {
+    need(mesh != nullptr, GK_ERR_INVALID_ARGUMENT, "null mesh");
+    use_device(mesh->ctx);
+    cudaStream_t s = mesh->ctx->stream;
+    const size_t no = mesh->N * mesh->m, ni = mesh->N * 3 * static_cast<size_t>(mesh->n);
+    std::vector<double4> ho(no), hi(ni);
+    GK_CUDA(cudaMemcpyAsync(ho.data(), mesh->outer.p, no * sizeof(double4), cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaMemcpyAsync(hi.data(), mesh->inner.p, ni * sizeof(double4), cudaMemcpyDeviceToHost, s));
+    GK_CUDA(cudaStreamSynchronize(s));
+    if (outer)
+      for (size_t k = 0; k < no; ++k) {
+        outer[k] = ho[k].x;
+        outer[no + k] = ho[k].y;
+        outer[2 * no + k] = ho[k].z;
+        outer[3 * no + k] = ho[k].w;
+      }
+    if (inner) {
+      // device planes are [3n][N]; the reference order is q * 3n + i
+      const size_t N = mesh->N, ipt = 3 * static_cast<size_t>(mesh->n);
+      for (size_t i = 0; i < ipt; ++i)
+        for (size_t q = 0; q < N; ++q) {
+          const double4& v = hi[i * N + q];
+          const size_t k = q * ipt + i;
+          inner[k] = v.x;
+          inner[ni + k] = v.y;
+          inner[2 * ni + k] = v.z;
+          inner[3 * ni + k] = v.w;
+        }
+    }
+  });
+}
+
+gk_status gk_mesh_destroy(gk_mesh* mesh) {
+  return guarded([&] {
+    if (!mesh) return;
+    cudaSetDevice(mesh->ctx->device);
+    cudaStreamSynchronize(mesh->ctx->stream);
+    delete mesh;
+  });
+}
+
+gk_status gk_distance_range(gk_ctx* c, const gk_mesh* mesh, size_t row_begin, size_t row_end,
+                            double* r_min, double* r_max) {
+  return guarded([&] {
+    check_ctx(c);
+    need(mesh && r_min && r_max, GK_ERR_INVALID_ARGUMENT, "null argument");
+    need(mesh->N >= 2, GK_ERR_INVALID_ARGUMENT, "gk_distance_range: need at least two triangles");
+    need(row_begin < row_end && row_end <= mesh->N, GK_ERR_INVALID_ARGUMENT,
+         "gk_distance_range: bad row range");
+    use_device(c);
+    double d2min = 0.0, d2max = 0.0;
+    gk::launch_range(c, mesh, row_begin, row_end, &d2min, &d2max);
+    *r_min = std::sqrt(d2min) * (1.0 - 0x1p-49);
+    *r_max = std::sqrt(d2max) * (1.0 + 0x1p-49);
+  });
+}
+
+gk_status gk_fill_rows(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t,
+                       gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
+                       gk_c128* z, size_t ldz, gk_fill_report* report) {
+  return guarded([&] {
+    check_ctx(c);
+    need(mesh != nullptr, GK_ERR_INVALID_ARGUMENT, "null mesh");
+    need(mode == GK_MODE_DIRECT || mode == GK_MODE_TABLE, GK_ERR_INVALID_ARGUMENT, "bad mode");
+    need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
+    need(row_begin <= row_end && row_end <= mesh->N, GK_ERR_INVALID_ARGUMENT,
+         "gk_fill_rows: bad row range");
+    need(ldz >= mesh->N, GK_ERR_INVALID_ARGUMENT, "gk_fill_rows: ldz < N");
+    need(row_begin == row_end || z, GK_ERR_INVALID_ARGUMENT, "null z");
+    if (mode == GK_MODE_TABLE) {
+      need(t != nullptr, GK_ERR_INVALID_ARGUMENT, "TABLE mode needs a table");
+      k_re = t->dev.k_re;
+      k_im = t->dev.k_im;
+    }
+    need(k_re >= 0.0, GK_ERR_INVALID_ARGUMENT, "eval_analytic: k must be >= 0");
+    const uint64_t pred = predicted(mesh->N, mesh->m, mesh->n);
+    use_device(c);
+    unsigned long long* cnt = c->scratch.p + 16;
+    if (report) {
+      GK_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
+      GK_CUDA(cudaEventRecord(c->ev0, c->stream));
+    }
+    gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, ldz, cnt);
+    if (!report) return;
+    GK_CUDA(cudaEventRecord(c->ev1, c->stream));
+    unsigned long long h[2];
+    GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    GK_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    report->N = mesh->N;
+    report->m = mesh->m;
+    report->n = mesh->n;
+    report->predicted_calls = pred;
+    const size_t rows = row_end - row_begin;
+    report->actual_calls = 3ull * mesh->m * mesh->n * rows * (mesh->N - 1);
+    report->fallback_calls = h[0] + h[1];
+    report->wall_time_s = ms * 1e-3;
+    if (h[1])
+      gk::fail(GK_ERR_OUT_OF_RANGE,
+               "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
+  });
+}
+
+gk_status gk_fill_matrix_host(gk_ctx* c, const double* verts, size_t nv, const uint32_t* tris,
+                              size_t nt, int m, int n, gk_mode mode,
+                              const gk_sampling_config* cfg, const gk_medium* med, gk_kind kind,
+                              gk_c128* z_host, gk_fill_report* report) {
+  gk_mesh* mesh = nullptr;
+  gk_table* table = nullptr;
+  gk_c128* dz[2] = {nullptr, nullptr};
+  cudaStream_t copy = nullptr;
+  cudaEvent_t filled[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+  gk_status st = guarded([&] {
+    check_ctx(c);
+    need(med && z_host, GK_ERR_INVALID_ARGUMENT, "null argument");
+    need(mode != GK_MODE_TABLE || cfg, GK_ERR_INVALID_ARGUMENT, "TABLE mode needs a config");
+    double k_re, k_im;
+    wavenumber(*med, k_re, k_im);
+    if (gk_mesh_create(c, verts, nv, tris, nt, m, n, &mesh) != GK_OK)
+      gk::fail(GK_ERR_INVALID_ARGUMENT, g_last_error);
+    if (mode == GK_MODE_TABLE) {
+      gk_sampling_config cc = *cfg;
+      if (cc.r_min <= 0.0 || cc.r_max <= 0.0) {
+        double lo, hi;
+        const gk_status s = gk_distance_range(c, mesh, 0, nt, &lo, &hi);
+        if (s != GK_OK) gk::fail(s, g_last_error);
+        if (cc.r_min <= 0.0) cc.r_min = lo;
+        if (cc.r_max <= 0.0) cc.r_max = hi;
+      }
+      const gk_status s = gk_table_build(c, &cc, med, 3, &table);
+      if (s != GK_OK) gk::fail(s, g_last_error);
+    }
+    use_device(c);
+    // row chunks of <= 1 GiB, double-buffered: the fill of chunk i+1 overlaps
+    // the device->host copy of chunk i (second stream + events)
+    const size_t row_bytes = nt * sizeof(gk_c128);
+    size_t chunk = (size_t(1) << 30) / row_bytes;
+    if (chunk < 8) chunk = 8;
+    if (chunk > nt) chunk = nt;
+    GK_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      GK_CUDA(cudaMalloc(reinterpret_cast<void**>(&dz[b]), chunk * row_bytes));
+      GK_CUDA(cudaEventCreateWithFlags(&filled[b], cudaEventDisableTiming));
+      GK_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+    }
+    gk_fill_report rep{};
+    rep.N = nt;
+    rep.m = m;
+    rep.n = n;
+    rep.predicted_calls = predicted(nt, m, n);
+    unsigned long long* cnt = c->scratch.p + 16;
+    GK_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
+    GK_CUDA(cudaEventRecord(c->ev0, c->stream));
+    size_t idx = 0;
+    for (size_t rb = 0; rb < nt; rb += chunk, ++idx) {
+      const size_t re = rb + chunk < nt ? rb + chunk : nt;
+      const int b = static_cast<int>(idx & 1);
+      if (idx >= 2) GK_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
+      gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nt, cnt);
+      GK_CUDA(cudaEventRecord(filled[b], c->stream));
+      GK_CUDA(cudaStreamWaitEvent(copy, filled[b], 0));
+      GK_CUDA(cudaMemcpyAsync(z_host + rb * nt, dz[b], (re - rb) * row_bytes,
+                              cudaMemcpyDeviceToHost, copy));
+      GK_CUDA(cudaEventRecord(copied[b], copy));
+    }
+    GK_CUDA(cudaEventRecord(c->ev1, c->stream));
+    unsigned long long h[2];
+    GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(copy));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    GK_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    rep.actual_calls = 3ull * m * n * nt * (nt - 1);
+    rep.fallback_calls = h[0] + h[1];
+    rep.wall_time_s = ms * 1e-3;
+    if (h[1])
+      gk::fail(GK_ERR_OUT_OF_RANGE,
+               "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
+    if (report) *report = rep;
+  });
+  if (copy) cudaStreamSynchronize(copy);
+  for (int b = 0; b < 2; ++b) {
+    if (dz[b]) cudaFree(dz[b]);
+    if (filled[b]) cudaEventDestroy(filled[b]);
+    if (copied[b]) cudaEventDestroy(copied[b]);
+  }
+  if (copy) cudaStreamDestroy(copy);
+  gk_table_destroy(table);
+  gk_mesh_destroy(mesh);
+  return st;
+}
+
+gk_status gk_predicted_calls(uint64_t N, uint64_t m, uint64_t n, uint64_t* out) {
+  return guarded([&] {
+    need(out != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");
+    *out = predicted(N, m, n);
+  });
+}
+
+gk_status gk_sphere_mesh(double radius, int subdivisions, double* verts, size_t* nv,
+                         uint32_t* tris, size_t* nt) {
+  return guarded([&] {
+    need(nv && nt, GK_ERR_INVALID_ARGUMENT, "null counts");
+    std::vector<double> v;
+    std::vector<uint32_t> t;
+    gk::sphere_mesh(radius, subdivisions, v, t);
+    gk::validate_mesh(v.data(), v.size() / 3, t.data(), t.size() / 3);
+    *nv = v.size() / 3;
+    *nt = t.size() / 3;
+    if (verts) std::memcpy(verts, v.data(), v.size() * sizeof(double));
+    if (tris) std::memcpy(tris, t.data(), t.size() * sizeof(uint32_t));
+  });
+}
+
+gk_status gk_plate_mesh(double side, int cells, double* verts, size_t* nv, uint32_t* tris,
+                        size_t* nt) {
+  return guarded([&] {
+    need(nv && nt, GK_ERR_INVALID_ARGUMENT, "null counts");
+    std::vector<double> v;
+    std::vector<uint32_t> t;
+    gk::plate_mesh(side, cells, v, t);
+    *nv = v.size() / 3;
+    *nt = t.size() / 3;
+    if (verts) std::memcpy(verts, v.data(), v.size() * sizeof(double));
+    if (tris) std::memcpy(tris, t.data(), t.size() * sizeof(uint32_t));
+  });
+}
+
+gk_status gk_jitter(double* verts, size_t nv, uint64_t seed, double amp) {
+  return guarded([&] {
+    need(nv == 0 || verts, GK_ERR_INVALID_ARGUMENT, "null vertices");
+    gk::jitter(verts, nv, seed, amp);
+  });
+}
+
+gk_status gk_bench_fp64_peak(gk_ctx* c, double* tflops) {
+  return guarded([&] {
+    check_ctx(c);
+    need(tflops != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");
+    use_device(c);
+    *tflops = gk::run_fp64_peak(c);
+  });
+}
+
+gk_status gk_device_info(gk_ctx* c, int* sm_count, int* clock_khz, int* major, int* minor) {
+  return guarded([&] {
+    check_ctx(c);
+    cudaDeviceProp p{};
+    GK_CUDA(cudaGetDeviceProperties(&p, c->device));
+    if (sm_count) *sm_count = p.multiProcessorCount;
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, c->device);
+    if (clock_khz) *clock_khz = clk;
+    if (major) *major = p.major;
+    if (minor) *minor = p.minor;
+  });
+}
+
+}  // extern "C"

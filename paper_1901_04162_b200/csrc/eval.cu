@@ -1,0 +1,123 @@
+// eval.cu -- K5 standalone evaluation (KernelEvaluator::eval_batch,
+// evaluator.hpp:209-221, and eval_analytic, kernel.hpp:48-61) and the FP64
+// peak microbenchmark used as the fill's roofline denominator.
+#include <cstdint>
+
+#include "gk_internal.h"
+
+namespace gk {
+
+// validation outcome of one radius, in the reference's order
+// (eval_kernel -> eval_exp/eval_green or eval_analytic, evaluator.hpp:199-205)
+enum : unsigned { V_OK = 0, V_INVALID = 1, V_DOMAIN = 2, V_RANGE = 3 };
+
+template <int KIND, bool TABLE, int DEG>
+__global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
+                                  double2* __restrict__ out, TableDev T, double k_re,
+                                  double k_im, unsigned long long* w) {
+  unsigned long long fb = 0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const double r = radii[i];
+    unsigned bad = V_OK;
+    double2 v = make_double2(0.0, 0.0);
+    if (TABLE && r >= T.r_min) {
+      if (!(r <= T.r_max)) {
+        bad = V_RANGE;
+      } else if (KIND == GK_KIND_EXP) {
+        v = exp_table(r, T);
+      } else {
+        v = DEG == 3 ? green_table<3>(r, T) : green_table_any(r, T);
+      }
+    } else {
+      if (KIND == GK_KIND_GREEN) {
+        if (r == 0.0) bad = V_DOMAIN;
+        else if (!(r > 0.0)) bad = V_INVALID;
+      } else if (!(r >= 0.0)) {
+        bad = V_INVALID;
+      }
+      if (bad == V_OK) {
+        v = analytic_sincos(KIND, k_re, k_im, r);
+        if (TABLE) ++fb;
+      }
+    }
+    if (bad) atomicMin(w + 1, (static_cast<unsigned long long>(i) << 3) | bad);
+    out[i] = v;
+  }
+  if (TABLE) {
+    for (int o = 16; o; o >>= 1) fb += __shfl_xor_sync(0xffffffffu, fb, o);
+    if ((threadIdx.x & 31) == 0 && fb) atomicAdd(w, fb);
+  }
+}
+
+template <int KIND>
+void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, double2* out,
+                      double k_re, double k_im, unsigned long long* w) {
+  size_t grid = (n + 255) / 256;
+  const size_t cap = static_cast<size_t>(ctx->sm_count) * 32;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  const unsigned g = static_cast<unsigned>(grid);
+  TableDev T{};
+  if (t) T = t->dev;
+  if (!t)
+    eval_batch_kernel<KIND, false, 0><<<g, 256, 0, ctx->stream>>>(r, n, out, T, k_re, k_im, w);
+  else if (KIND == GK_KIND_GREEN && T.degree == 3)
+    eval_batch_kernel<KIND, true, 3><<<g, 256, 0, ctx->stream>>>(r, n, out, T, k_re, k_im, w);
+  else
+    eval_batch_kernel<KIND, true, 0><<<g, 256, 0, ctx->stream>>>(r, n, out, T, k_re, k_im, w);
+  GK_CUDA(cudaGetLastError());
+}
+
+void launch_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re, double k_im,
+                       const double* r, size_t n, gk_c128* out, unsigned long long* w) {
+  double2* o = reinterpret_cast<double2*>(out);
+  if (kind == GK_KIND_GREEN) launch_eval_kind<GK_KIND_GREEN>(ctx, table, r, n, o, k_re, k_im, w);
+  else launch_eval_kind<GK_KIND_EXP>(ctx, table, r, n, o, k_re, k_im, w);
+}
+
+// ------------------------------------------------------------- FP64 peak
+
+constexpr int kChains = 8;
+
+__global__ void __launch_bounds__(256) fp64_peak_kernel(double* sink, int iters, double b, double c) {
+  double a[kChains];
+#pragma unroll
+  for (int k = 0; k < kChains; ++k) a[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int k = 0; k < kChains; ++k) a[k] = __fma_rn(a[k], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kChains; ++k) s += a[k];
+  if (s == 1234.5678) sink[0] = s;  // keeps the chains live
+}
+
+double run_fp64_peak(gk_ctx* ctx) {
+  int per_sm = 0;
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fp64_peak_kernel, 256, 0));
+  const unsigned grid = static_cast<unsigned>(ctx->sm_count * (per_sm > 0 ? per_sm : 1));
+  const int iters = 4096;
+  DevBuf<double> sink;
+  sink.alloc(1, ctx->stream);
+  // warm-up, then the best of 5 timed launches
+  fp64_peak_kernel<<<grid, 256, 0, ctx->stream>>>(sink.p, iters / 8, 0.9999999, 1e-7);
+  GK_CUDA(cudaGetLastError());
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    GK_CUDA(cudaEventRecord(ctx->ev0, ctx->stream));
+    fp64_peak_kernel<<<grid, 256, 0, ctx->stream>>>(sink.p, iters, 0.9999999, 1e-7);
+    GK_CUDA(cudaEventRecord(ctx->ev1, ctx->stream));
+    GK_CUDA(cudaEventSynchronize(ctx->ev1));
+    float ms = 0.f;
+    GK_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    best = ms < best ? ms : best;
+  }
+  const double fmas = static_cast<double>(grid) * 256.0 * iters * 16.0 * kChains;
+  return 2.0 * fmas / (best * 1e-3) / 1e12;
+}
+
+}  // namespace gk

@@ -1,0 +1,331 @@
+// fill.cu -- K1 distance range, K3 table fill, K4 direct fill.
+//
+// The fill replaces fill_matrix's fill_rows loop (matfill.hpp:169-203) with
+// AnalyticKernel::accumulate (DIRECT, kernel.hpp:48-61) or
+// TableKernel::accumulate -> accumulate_green (TABLE, evaluator.hpp:150-194).
+//
+// Work decomposition: a CTA of 8 warps owns a tile of 8 observation rows x
+// 128 source columns; warp w takes row p = tile_row*8 + w, lane l takes the
+// columns q = tile_col*128 + 32 b + l (b = 0..3), so every warp store is one
+// coalesced 512-byte complex128 row segment.  The m outer points of p live in
+// registers; the 3n inner points of q stream from a [3n][N] plane layout
+// (coalesced 32-byte loads, L1/L2 resident).  Each lane keeps one complex
+// accumulator per outer point (sum_i w_i K(r_oi)) and finishes the entry with
+// sum_o w_o acc_o -- the reference's double sum regrouped (same terms).
+#include <cstdint>
+#include <cstring>
+#include <math_constants.h>
+
+#include "gk_internal.h"
+
+namespace gk {
+
+constexpr int kRowsPerTile = 8;  // one row per warp
+constexpr int kColBlocks = 4;    // 32-column blocks per tile
+constexpr int kThreads = 32 * kRowsPerTile;
+
+struct FillArgs {
+  const double4* outer;
+  const double4* inner;
+  size_t N;
+  int ipt;
+  size_t row_begin, row_end;
+  size_t ncb, ntiles;
+  double2* z;
+  size_t ldz;
+  TableDev T;
+  const double2* phase;
+  double K1, k_re, k_im;
+  unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max
+};
+
+template <int MODE>
+struct PhaseSmem {
+  __device__ static const double2* get(const double2*) { return nullptr; }
+};
+template <>
+struct PhaseSmem<GK_MODE_DIRECT> {
+  __device__ static const double2* get(const double2* g) {
+    __shared__ double2 tab[kPhaseM];
+    for (int i = threadIdx.x; i < kPhaseM; i += blockDim.x) tab[i] = g[i];
+    __syncthreads();
+    return tab;
+  }
+};
+
+template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
+__global__ void __launch_bounds__(kThreads, 2) fill_kernel(const FillArgs A) {
+  const double2* tab = PhaseSmem<MODE>::get(A.phase);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t N = A.N;
+  unsigned long long n_low = 0, n_high = 0;
+
+  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
+    const size_t p = A.row_begin + tr * kRowsPerTile + warp;
+    if (p >= A.row_end) continue;  // warp-uniform
+    double ox[MO], oy[MO], oz[MO];
+#pragma unroll
+    for (int o = 0; o < MO; ++o) {
+      const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
+      const double2 zw = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o) + 1);
+      ox[o] = xy.x;
+      oy[o] = xy.y;
+      oz[o] = zw.x;
+    }
+    for (int cb = 0; cb < kColBlocks; ++cb) {
+      const size_t q0 = tc * (32 * kColBlocks) + 32 * cb;
+      if (q0 >= N) break;  // warp-uniform
+      const size_t q_raw = q0 + lane;
+      const bool valid = q_raw < N;
+      const size_t q = valid ? q_raw : N - 1;
+      const bool self = q == p;
+      double2 acc[MO];
+#pragma unroll
+      for (int o = 0; o < MO; ++o) acc[o] = make_double2(0.0, 0.0);
+
+      for (int i = 0; i < A.ipt; ++i) {
+        const double2* ip = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
+        const double2 pxy = __ldg(ip), pzw = __ldg(ip + 1);
+#pragma unroll
+        for (int o = 0; o < MO; ++o) {
+          const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
+          const double y = rsqrt_fast(d2);
+          const double r = __dmul_rn(d2, y);
+          if constexpr (MODE == GK_MODE_DIRECT) {
+            double2 e = expmjkr_phase(r, A.K1, tab);
+            if constexpr (LOSSY) {
+              const double a = exp(A.k_im * r);
+              e.x *= a;
+              e.y *= a;
+            }
+            const double wgt = KIND == GK_KIND_GREEN ? __dmul_rn(pzw.y, y) : pzw.y;
+            acc[o].x = __fma_rn(wgt, e.x, acc[o].x);
+            acc[o].y = __fma_rn(wgt, e.y, acc[o].y);
+          } else {
+            double2 v;
+            if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, A.T);
+            else if constexpr (DEG == 3) v = green_table<3>(r, A.T);
+            else v = green_table_any(r, A.T);
+            const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
+            if (__any_sync(0xffffffffu, oob)) {
+              if (oob) {
+                if (!self && valid) {
+                  // the reference's eval_kernel fallback (evaluator.hpp:199-205)
+                  v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
+                  if (r > A.T.r_max) ++n_high; else ++n_low;
+                } else {
+                  v = make_double2(0.0, 0.0);
+                }
+              }
+            }
+            acc[o].x = __fma_rn(pzw.y, v.x, acc[o].x);
+            acc[o].y = __fma_rn(pzw.y, v.y, acc[o].y);
+          }
+        }
+      }
+      double2 res = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int o = 0; o < MO; ++o) {
+        const double wo = __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3);
+        res.x = __fma_rn(wo, acc[o].x, res.x);
+        res.y = __fma_rn(wo, acc[o].y, res.y);
+      }
+      if (self) res = make_double2(0.0, 0.0);  // self pairs stay zero (matfill.hpp:178)
+      if (valid) __stcs(A.z + (p - A.row_begin) * A.ldz + q, res);
+    }
+  }
+  if constexpr (MODE == GK_MODE_TABLE) {
+    for (int o = 16; o; o >>= 1) {
+      n_low += __shfl_xor_sync(0xffffffffu, n_low, o);
+      n_high += __shfl_xor_sync(0xffffffffu, n_high, o);
+    }
+    if (lane == 0 && n_low) atomicAdd(A.counters, n_low);
+    if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
+  }
+}
+
+template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
+void launch_one(gk_ctx* ctx, const FillArgs& a) {
+  auto k = fill_kernel<MO, MODE, KIND, DEG, LOSSY>;
+  int per_sm = 0;
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0));
+  if (per_sm < 1) per_sm = 1;
+  size_t grid = static_cast<size_t>(ctx->sm_count) * per_sm;
+  if (grid > a.ntiles) grid = a.ntiles;
+  if (grid < 1) grid = 1;
+  k<<<static_cast<unsigned>(grid), kThreads, 0, ctx->stream>>>(a);
+  GK_CUDA(cudaGetLastError());
+}
+
+template <int MO>
+void dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, gk_kind kind, int degree,
+                 bool lossy) {
+  if (mode == GK_MODE_DIRECT) {
+    if (kind == GK_KIND_GREEN) {
+      if (lossy) launch_one<MO, GK_MODE_DIRECT, GK_KIND_GREEN, 0, true>(ctx, a);
+      else launch_one<MO, GK_MODE_DIRECT, GK_KIND_GREEN, 0, false>(ctx, a);
+    } else {
+      if (lossy) launch_one<MO, GK_MODE_DIRECT, GK_KIND_EXP, 0, true>(ctx, a);
+      else launch_one<MO, GK_MODE_DIRECT, GK_KIND_EXP, 0, false>(ctx, a);
+    }
+  } else {
+    if (kind == GK_KIND_EXP) launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, false>(ctx, a);
+    else if (degree == 3) launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, false>(ctx, a);
+    else launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, false>(ctx, a);
+  }
+}
+
+void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
+                 gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
+                 gk_c128* z, size_t ldz, unsigned long long* counters) {
+  FillArgs a{};
+  a.outer = mesh->outer.p;
+  a.inner = mesh->inner.p;
+  a.N = mesh->N;
+  a.ipt = 3 * mesh->n;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  a.ncb = (mesh->N + 32 * kColBlocks - 1) / (32 * kColBlocks);
+  a.ntiles = ((row_end - row_begin + kRowsPerTile - 1) / kRowsPerTile) * a.ncb;
+  a.z = reinterpret_cast<double2*>(z);
+  a.ldz = ldz;
+  if (table) a.T = table->dev;
+  a.phase = ctx->phase.p;
+  a.K1 = k_re * kPhaseM / (2.0 * kPi);
+  a.k_re = k_re;
+  a.k_im = k_im;
+  a.counters = counters;
+  if (a.ntiles == 0) return;
+  const int degree = table ? table->dev.degree : 3;
+  const bool lossy = k_im != 0.0;
+  switch (mesh->m) {
+    case 1: dispatch_mo<1>(ctx, a, mode, kind, degree, lossy); break;
+    case 3: dispatch_mo<3>(ctx, a, mode, kind, degree, lossy); break;
+    case 4: dispatch_mo<4>(ctx, a, mode, kind, degree, lossy); break;
+    case 6: dispatch_mo<6>(ctx, a, mode, kind, degree, lossy); break;
+    case 7: dispatch_mo<7>(ctx, a, mode, kind, degree, lossy); break;
+    default: fail(GK_ERR_INVALID_ARGUMENT, "QuadratureSpec: outer_points must be one of 1, 3, 4, 6, 7");
+  }
+}
+
+// ------------------------------------------------------------------- K1
+
+__device__ __forceinline__ unsigned long long bits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+__device__ __forceinline__ double unbits(unsigned long long b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+__device__ __forceinline__ void reduce_minmax(double lo, double hi, unsigned long long* wmin,
+                                              unsigned long long* wmax) {
+  unsigned long long l = bits(lo), h = bits(hi);  // non-negative: bit order == value order
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, l, o);
+    const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, h, o);
+    l = l2 < l ? l2 : l;
+    h = h2 > h ? h2 : h;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(wmin, l);
+    atomicMax(wmax, h);
+  }
+}
+
+// pass 1: one sample pair distance (outer 0, inner 0) per (p, q): an upper
+// bound of the true min and a lower bound of the true max
+__global__ void range_sample_kernel(const double4* outer, const double4* inner, int m, size_t N,
+                                    size_t row_begin, size_t row_end, unsigned long long* w) {
+  double lo = CUDART_INF, hi = 0.0;
+  for (size_t p = row_begin + blockIdx.x; p < row_end; p += gridDim.x) {
+    const double4 o = outer[p * m];
+    for (size_t q = threadIdx.x; q < N; q += blockDim.x) {
+      if (q == p) continue;
+      const double4 I = inner[q];
+      const double d2 = dist2(o.x, o.y, o.z, I.x, I.y, I.z);
+      lo = fmin(lo, d2);
+      hi = fmax(hi, d2);
+    }
+  }
+  reduce_minmax(lo, hi, w + 0, w + 1);
+}
+
+// pass 2: exact min/max over the pairs whose centroid bounds can beat the
+// samples: |c_p - c_q| - rho_p - rho_q <= m0  or  |c_p - c_q| + rho_p + rho_q >= M0
+__global__ void range_exact_kernel(const double4* outer, const double4* inner,
+                                   const double4* bounds, const double* binner, int m, int ipt,
+                                   size_t N, size_t row_begin, size_t row_end,
+                                   unsigned long long* w) {
+  const double m0 = sqrt(unbits(w[0])), M0 = sqrt(unbits(w[1]));
+  double lo = CUDART_INF, hi = 0.0;
+  for (size_t p = row_begin + blockIdx.x; p < row_end; p += gridDim.x) {
+    const double4 bp = bounds[p];
+    for (size_t q = threadIdx.x; q < N; q += blockDim.x) {
+      if (q == p) continue;
+      const double4 bq = bounds[q];
+      const double dx = bp.x - bq.x, dy = bp.y - bq.y, dz = bp.z - bq.z;
+      const double dc2 = dx * dx + dy * dy + dz * dz;
+      const double rho = bp.w + binner[q];
+      const double a = m0 + rho, b = M0 - rho;
+      const bool cmin = dc2 <= a * a * (1.0 + 1e-12);
+      const bool cmax = b <= 0.0 || dc2 >= b * b * (1.0 - 1e-12);
+      if (!(cmin || cmax)) continue;
+      for (int o = 0; o < m; ++o) {
+        const double4 O = outer[p * m + o];
+        for (int i = 0; i < ipt; ++i) {
+          const double4 I = inner[static_cast<size_t>(i) * N + q];
+          const double d2 = dist2(O.x, O.y, O.z, I.x, I.y, I.z);
+          lo = fmin(lo, d2);
+          hi = fmax(hi, d2);
+        }
+      }
+    }
+  }
+  reduce_minmax(lo, hi, w + 2, w + 3);
+}
+
+void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,
+                  double* d2min, double* d2max) {
+  cudaStream_t st = ctx->stream;
+  unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+  unsigned long long* w = ctx->scratch.p + 8;
+  GK_CUDA(cudaMemcpyAsync(w, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  const size_t rows = row_end - row_begin;
+  const unsigned grid = static_cast<unsigned>(rows < 65535 ? rows : 65535);
+  range_sample_kernel<<<grid, 256, 0, st>>>(mesh->outer.p, mesh->inner.p, mesh->m, mesh->N,
+                                            row_begin, row_end, w);
+  GK_CUDA(cudaGetLastError());
+  range_exact_kernel<<<grid, 256, 0, st>>>(mesh->outer.p, mesh->inner.p, mesh->bounds.p,
+                                           mesh->binner.p, mesh->m, 3 * mesh->n, mesh->N,
+                                           row_begin, row_end, w);
+  GK_CUDA(cudaGetLastError());
+  unsigned long long out[4];
+  GK_CUDA(cudaMemcpyAsync(out, w, sizeof(out), cudaMemcpyDeviceToHost, st));
+  GK_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long lo = out[0] < out[2] ? out[0] : out[2];
+  const unsigned long long hi = out[1] > out[3] ? out[1] : out[3];
+  double a, b;
+  std::memcpy(&a, &lo, 8);
+  std::memcpy(&b, &hi, 8);
+  *d2min = a;
+  *d2max = b;
+}
+
+// ------------------------------------------------------- phase table
+
+__global__ void phase_kernel(double2* tab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kPhaseM) return;
+  double s, c;
+  sincospi(2.0 * i / kPhaseM, &s, &c);
+  tab[i] = make_double2(c, s);
+}
+
+void init_phase_table(gk_ctx* ctx) {
+  ctx->phase.alloc(kPhaseM, ctx->stream);
+  phase_kernel<<<(kPhaseM + 255) / 256, 256, 0, ctx->stream>>>(ctx->phase.p);
+  GK_CUDA(cudaGetLastError());
+}
+
+}  // namespace gk

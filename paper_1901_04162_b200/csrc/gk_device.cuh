@@ -1,0 +1,177 @@
+// gk_device.cuh -- device data layout and FP64 math shared by the sm_100a
+// kernels of libgk (table build, fill, standalone evaluation).
+//
+// Layout in HBM:
+//   Green interval records, one per plan interval j = 0..n-2 plus a sentinel
+//   record n-1 for r = r_max, stride 2 + 2(d+1) doubles:
+//     { a_j, a_{j+1}, c0.re, c0.im, c1.re, c1.im, ..., cd.re, cd.im }
+//   where P_j(u) = sum_k c_k u^k, u = r - a_j, is the degree-d Lagrange
+//   interpolant through the reference's stencil for interval j
+//   (evaluator.hpp:40-95, 237-272; same nodes, so the same polynomial up to
+//   rounding) and c0 is the node value itself (exact node reproduction).
+//   Exp interval records (linear, evaluator.hpp:22-30), 6 doubles:
+//     { a_j, a_{j+1}, e_j.re, e_j.im, slope.re, slope.im }.
+//   Lookup buckets (uint32, width dr_min/2, so at most one node per bucket):
+//     lk[b] = max(0, #{nodes with bucket < b} - 1); the interval holding r is
+//     j = lk[b] + (r >= a_{lk[b]+1}), exactly the reference's locate()
+//     (table.hpp:87-102) without clamping: r = r_max lands on the sentinel.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gk {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kMagic52 = 4503599627370496.0;   // 2^52
+constexpr double kMagicRint = 6755399441055744.0; // 1.5 * 2^52
+
+// Direct-mode phase table size: e^{-j theta} = e^{-j 2pi idx/M} e^{-j delta},
+// |delta| <= pi/M.  M = 2048 keeps the Taylor tail below 2^-60.
+constexpr int kPhaseM = 2048;
+
+struct TableDev {
+  const double* grec;  // Green interval records
+  const double* erec;  // Exp interval records
+  const uint32_t* lk;  // lookup buckets
+  double r_min, r_max;
+  double inv_w, bias;  // bucket map: x = fma(r, inv_w, bias), b = floor(x)
+  uint32_t nlk;
+  int degree;
+  int grs;  // Green record stride in doubles = 2 + 2 (degree + 1)
+  double k_re, k_im;
+};
+
+struct PhaseDev {
+  double K1;        // k * M / (2 pi)
+  double k_im;      // attenuation exponent (lossy medium), 0 for real k
+};
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ double ld_nc(const double* p) { return __ldg(p); }
+
+// squared distance; FMA form (pinned: all kernels share this one function so
+// K1's range and the fills see bit-identical radii)
+__device__ __forceinline__ double dist2(double ox, double oy, double oz, double ix, double iy,
+                                        double iz) {
+  const double dx = ox - ix, dy = oy - iy, dz = oz - iz;
+  return __fma_rn(dz, dz, __fma_rn(dy, dy, __dmul_rn(dx, dx)));
+}
+
+// 1/sqrt(x) to ~1 ulp: MUFU.RSQ64H seed + one third-order correction
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = __fma_rn(-x, __dmul_rn(y, y), 1.0);
+  const double ye = __dmul_rn(y, e);
+  return __fma_rn(ye, __fma_rn(0.375, e, 0.5), y);
+}
+
+// bucket of r in the lookup hash (r >= r_min gives x >= 0); clamped so any
+// input (out of range, NaN) yields a readable bucket
+__device__ __forceinline__ uint32_t lookup_bucket(double r, const TableDev& t) {
+  const double x = __fma_rn(r, t.inv_w, t.bias);
+  const double y = __dadd_rd(x, kMagic52);
+  const uint32_t b = static_cast<uint32_t>(__double2loint(y));
+  return b < t.nlk ? b : t.nlk - 1;
+}
+
+// interval index of r (table.hpp:87-102 semantics, sentinel at r_max)
+__device__ __forceinline__ uint32_t locate_interval(double r, const TableDev& t,
+                                                    const double* grec, int grs, double& aj) {
+  const uint32_t base = __ldg(t.lk + lookup_bucket(r, t));
+  const double2 ab = __ldg(reinterpret_cast<const double2*>(grec + static_cast<size_t>(base) * grs));
+  const bool hi = r >= ab.y;
+  aj = hi ? ab.y : ab.x;
+  return base + (hi ? 1u : 0u);
+}
+
+// Green kernel by table: degree-3 fast path
+template <int DEG>
+__device__ __forceinline__ double2 green_table(double r, const TableDev& t) {
+  constexpr int RS = 2 + 2 * (DEG + 1);
+  double aj;
+  const uint32_t j = locate_interval(r, t, t.grec, RS, aj);
+  const double2* c = reinterpret_cast<const double2*>(t.grec + static_cast<size_t>(j) * RS + 2);
+  const double u = r - aj;
+  double2 acc = __ldg(c + DEG);
+#pragma unroll
+  for (int k = DEG - 1; k >= 0; --k) {
+    const double2 ck = __ldg(c + k);
+    acc.x = __fma_rn(acc.x, u, ck.x);
+    acc.y = __fma_rn(acc.y, u, ck.y);
+  }
+  return acc;
+}
+
+// runtime-degree variant (degrees other than the instantiated fast paths)
+__device__ __forceinline__ double2 green_table_any(double r, const TableDev& t) {
+  double aj;
+  const uint32_t j = locate_interval(r, t, t.grec, t.grs, aj);
+  const double2* c = reinterpret_cast<const double2*>(t.grec + static_cast<size_t>(j) * t.grs + 2);
+  const double u = r - aj;
+  double2 acc = __ldg(c + t.degree);
+  for (int k = t.degree - 1; k >= 0; --k) {
+    const double2 ck = __ldg(c + k);
+    acc.x = __fma_rn(acc.x, u, ck.x);
+    acc.y = __fma_rn(acc.y, u, ck.y);
+  }
+  return acc;
+}
+
+// Exp kernel by table (linear, evaluator.hpp:22-30)
+__device__ __forceinline__ double2 exp_table(double r, const TableDev& t) {
+  double aj;
+  // Exp records carry the same {a_j, a_{j+1}} header as the Green records
+  const uint32_t j = locate_interval(r, t, t.erec, 6, aj);
+  const double2* c = reinterpret_cast<const double2*>(t.erec + static_cast<size_t>(j) * 6 + 2);
+  const double u = r - aj;
+  const double2 e0 = __ldg(c), s = __ldg(c + 1);
+  return make_double2(__fma_rn(s.x, u, e0.x), __fma_rn(s.y, u, e0.y));
+}
+
+// ------------------------------------------------------------ direct math
+
+// exp(-j k r) from a phase table tab[M] = (cos 2pi i/M, sin 2pi i/M) in
+// shared memory: phi = r K1, n = rint(phi), f = phi - n, delta = 2pi f/M,
+// e^{-j delta} by Taylor to delta^6 / delta^5.
+__device__ __forceinline__ double2 expmjkr_phase(double r, double K1, const double2* tab) {
+  constexpr double C = 2.0 * kPi / kPhaseM;
+  constexpr double a1 = -C * C / 2.0;
+  constexpr double a2 = C * C * C * C / 24.0;
+  constexpr double a3 = -C * C * C * C * C * C / 720.0;
+  constexpr double s1 = C;
+  constexpr double s3 = -C * C * C / 6.0;
+  constexpr double s5 = C * C * C * C * C / 120.0;
+  const double t = __fma_rn(r, K1, kMagicRint);
+  const double nf = t - kMagicRint;
+  const double f = __fma_rn(r, K1, -nf);
+  const int idx = __double2loint(t) & (kPhaseM - 1);
+  const double g = __dmul_rn(f, f);
+  const double c = __fma_rn(__fma_rn(__fma_rn(a3, g, a2), g, a1), g, 1.0);
+  const double s = __dmul_rn(f, __fma_rn(__fma_rn(s5, g, s3), g, s1));
+  const double2 T = tab[idx];
+  // (C0 - j S0)(c - j s) = (C0 c - S0 s) - j (S0 c + C0 s)
+  return make_double2(__fma_rn(-T.y, s, __dmul_rn(T.x, c)), -__fma_rn(T.x, s, __dmul_rn(T.y, c)));
+}
+
+// reference-accuracy direct kernel via libdevice sincos (the accuracy oracle
+// on the device side and the fallback of the table path, evaluator.hpp:199-205)
+__device__ __forceinline__ double2 analytic_sincos(int kind, double k_re, double k_im, double r) {
+  double s, c;
+  sincos(k_re * r, &s, &c);
+  double re = c, im = -s;
+  if (k_im != 0.0) {
+    const double a = exp(k_im * r);
+    re *= a;
+    im *= a;
+  }
+  if (kind == 1) {
+    re = re / r;
+    im = im / r;
+  }
+  return make_double2(re, im);
+}
+
+}  // namespace gk

@@ -1,0 +1,118 @@
+// gk_internal.h -- host-side objects behind the C ABI (include/gk/gk.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gk/gk.h"
+#include "gk_device.cuh"
+
+namespace gk {
+
+struct Error {
+  gk_status status;
+  std::string what;
+};
+
+[[noreturn]] inline void fail(gk_status s, const std::string& what) { throw Error{s, what}; }
+
+#define GK_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t gk_e_ = (call);                                                         \
+    if (gk_e_ != cudaSuccess)                                                           \
+      ::gk::fail(GK_ERR_RUNTIME, std::string(#call) + ": " + cudaGetErrorString(gk_e_)); \
+  } while (0)
+
+// device buffer owned by a gk object.  Allocated stream-ordered from the
+// device's default memory pool (release threshold = max, set at context
+// creation) so the temporaries of a table build cost no device-wide syncs.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count, cudaStream_t stream = nullptr) {
+    reset();
+    if (count == 0) count = 1;
+    s = stream;
+    GK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+    n = count;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+}  // namespace gk
+
+struct gk_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int sm_count = 0;
+  gk::DevBuf<unsigned long long> scratch;  // counters / reductions (64 words)
+  gk::DevBuf<double2> phase;               // direct-mode phase table (kPhaseM)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+struct gk_table {
+  gk_ctx* ctx = nullptr;
+  gk_table_info info{};
+  gk::TableDev dev{};
+  gk::DevBuf<double> absc;
+  gk::DevBuf<double2> exp_vals, green_vals;
+  gk::DevBuf<uint32_t> hash;  // reference-format buckets (table.hpp:40-82)
+  gk::DevBuf<double> grec, erec;
+  gk::DevBuf<uint32_t> lk;
+  std::vector<double> zeros;  // zero_locations (host copy)
+};
+
+struct gk_mesh {
+  gk_ctx* ctx = nullptr;
+  size_t N = 0, nv = 0;
+  int m = 0, n = 0;
+  gk::DevBuf<double4> outer;  // [N * m]    (x, y, z, w)
+  gk::DevBuf<double4> inner;  // [3n][N]    (x, y, z, w), column-major in q
+  gk::DevBuf<double4> bounds; // [N]        (cx, cy, cz, rho_outer), rho_inner in binner
+  gk::DevBuf<double> binner;  // [N]
+};
+
+namespace gk {
+
+// host-side quadrature rules (quadrature.hpp:35-110), bit-identical
+void triangle_rule(int m, double* b0, double* b1, double* b2, double* w);
+void gauss_legendre_unit(int n, double* x, double* w);
+void sphere_mesh(double radius, int subdivisions, std::vector<double>& verts,
+                 std::vector<uint32_t>& tris);
+void plate_mesh(double side, int cells, std::vector<double>& verts, std::vector<uint32_t>& tris);
+void jitter(double* v, size_t nv, uint64_t seed, double amp);
+void validate_mesh(const double* v, size_t nv, const uint32_t* t, size_t nt);
+
+// kernels launched by abi.cu (defined in build.cu / fill.cu / eval.cu)
+void launch_points(gk_mesh* mesh, const double* d_verts, const uint32_t* d_tris,
+                   cudaStream_t s);
+void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg, double k_zero,
+                        double t_nominal, double k_re, double k_im, int degree);
+void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
+                 gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
+                 gk_c128* z, size_t ldz, unsigned long long* d_fallbacks);
+void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,
+                  double* d2min, double* d2max);
+void launch_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,
+                       double k_im, const double* r, size_t n, gk_c128* out,
+                       unsigned long long* d_scratch);
+double run_fp64_peak(gk_ctx* ctx);
+void init_phase_table(gk_ctx* ctx);
+
+}  // namespace gk

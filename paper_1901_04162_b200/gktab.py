@@ -1,0 +1,382 @@
+"""Python mirror of the reference's operator surface for the fill hot path.
+
+The names, argument meaning and error behaviour follow ``gktab``
+(/root/reference/proj/include/gktab/): ``Medium``, ``SamplingConfig``,
+``QuadratureSpec``, ``KernelKind``, ``wavenumber``, ``generate_sphere_mesh``,
+``KernelEvaluator`` (here ``DeviceTable``: built on the GPU), ``eval_batch``,
+``fill_matrix`` and ``FillReport``.  All compute runs in libgk.so (sm_100a
+CUDA); torch supplies device memory and the current CUDA stream only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import FillReportC, Medium as _MediumC, SamplingConfigC, TableInfoC, check, lib
+
+
+class KernelKind(enum.IntEnum):
+    """gktab::KernelKind (kernel.hpp:14-17)"""
+
+    PlainExp = 0
+    GreenOverR = 1
+
+
+class Mode(enum.IntEnum):
+    """AnalyticKernel (DIRECT) vs TableKernel (TABLE), matfill.hpp:59-87"""
+
+    DIRECT = 0
+    TABLE = 1
+
+
+@dataclass
+class Medium:
+    """gktab::Medium (kernel.hpp:25-38); eps_r_im < 0 = lossy extension."""
+
+    lambda0: float = 1.0
+    eps_r: float = 1.0
+    mu_r: float = 1.0
+    eps_r_im: float = 0.0
+
+    def c(self) -> _MediumC:
+        return _MediumC(self.lambda0, self.eps_r, self.mu_r, self.eps_r_im)
+
+
+@dataclass
+class SamplingConfig:
+    """gktab::SamplingConfig (sampling.hpp:18-45), same defaults."""
+
+    r_min: float = 1e-4
+    r_max: float = 1.0
+    samples_per_wavelength: int = 1000
+    refine_interval_divisor: int = 2
+    refine_halfwidth_in_t: float = 2.0
+    dedup_fraction: float = 0.5
+    refine: bool = True
+
+    def c(self) -> SamplingConfigC:
+        return SamplingConfigC(self.r_min, self.r_max, int(self.samples_per_wavelength),
+                               int(self.refine_interval_divisor), self.refine_halfwidth_in_t,
+                               self.dedup_fraction, int(bool(self.refine)))
+
+
+@dataclass
+class QuadratureSpec:
+    """gktab::QuadratureSpec (quadrature.hpp:15-26)"""
+
+    outer_points: int = 4
+    inner_points_per_edge: int = 3
+
+
+@dataclass
+class TriangleMesh:
+    """gktab::TriangleMesh (mesh.hpp:33-58): vertices (nv,3) f64, triangles (nt,3) u32"""
+
+    vertices: np.ndarray
+    triangles: np.ndarray
+
+    def __post_init__(self):
+        self.vertices = np.ascontiguousarray(self.vertices, np.float64).reshape(-1, 3)
+        self.triangles = np.ascontiguousarray(self.triangles, np.uint32).reshape(-1, 3)
+
+    def triangle_count(self) -> int:
+        return self.triangles.shape[0]
+
+
+@dataclass
+class FillReport:
+    """gktab::FillReport (matfill.hpp:33-47), the fields fill_matrix sets."""
+
+    N: int = 0
+    m: int = 0
+    n: int = 0
+    predicted_calls: int = 0
+    actual_calls: int = 0
+    fallback_calls: int = 0
+    wall_time_s: float = 0.0
+
+    @classmethod
+    def from_c(cls, r: FillReportC) -> "FillReport":
+        return cls(r.N, r.m, r.n, r.predicted_calls, r.actual_calls, r.fallback_calls,
+                   r.wall_time_s)
+
+
+def wavenumber(medium: Medium) -> complex:
+    """k = 2 pi sqrt(eps_r mu_r) / lambda0 (kernel.hpp:41-44); complex if lossy"""
+    kr, ki = C.c_double(), C.c_double()
+    check(lib().gk_wavenumber(C.byref(medium.c()), C.byref(kr), C.byref(ki)), "wavenumber")
+    return complex(kr.value, ki.value) if ki.value else kr.value
+
+
+def predicted_calls(N: int, m: int, n: int) -> int:
+    out = C.c_uint64()
+    check(lib().gk_predicted_calls(N, m, n, C.byref(out)), "predicted_calls")
+    return out.value
+
+
+def _mesh_from(fn, *args) -> TriangleMesh:
+    nv, nt = C.c_size_t(), C.c_size_t()
+    check(fn(*args, None, C.byref(nv), None, C.byref(nt)), fn.__name__)
+    v = np.zeros((nv.value, 3), np.float64)
+    t = np.zeros((nt.value, 3), np.uint32)
+    check(fn(*args, v.ctypes.data, C.byref(nv), t.ctypes.data, C.byref(nt)), fn.__name__)
+    return TriangleMesh(v, t)
+
+
+def generate_sphere_mesh(radius: float, subdivisions: int) -> TriangleMesh:
+    """generate_sphere_mesh (mesh.hpp:154-202), bit-identical"""
+    return _mesh_from(lib().gk_sphere_mesh, C.c_double(radius), C.c_int(subdivisions))
+
+
+def generate_plate_mesh(side: float, cells: int) -> TriangleMesh:
+    """flat side x side plate, cells x cells grid, two right triangles per cell"""
+    return _mesh_from(lib().gk_plate_mesh, C.c_double(side), C.c_int(cells))
+
+
+def jitter(mesh: TriangleMesh, seed: int, amp: float) -> TriangleMesh:
+    """splitmix64(seed) per coordinate, U(-amp, amp)"""
+    v = mesh.vertices.copy()
+    check(lib().gk_jitter(v.ctypes.data, v.shape[0], seed, amp), "jitter")
+    return TriangleMesh(v, mesh.triangles.copy())
+
+
+def _torch():
+    import torch  # plumbing only: device memory + streams
+
+    return torch
+
+
+class Context:
+    """One gk_ctx per CUDA device, running on torch's current stream."""
+
+    _cache: dict[int, "Context"] = {}
+
+    def __init__(self, device: int = 0):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise _lib.RuntimeErrorGk("no CUDA device: libgk has no CPU fallback")
+        self.device = device
+        h = C.c_void_p()
+        check(lib().gk_ctx_create(device, C.byref(h)), "gk_ctx_create")
+        self.h = h
+
+    @classmethod
+    def get(cls, device: int = 0) -> "Context":
+        if device not in cls._cache:
+            cls._cache[device] = cls(device)
+        ctx = cls._cache[device]
+        ctx.bind_stream()
+        return ctx
+
+    def bind_stream(self, stream=None) -> None:
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().gk_ctx_set_stream(self.h, C.c_void_p(s.cuda_stream)), "set_stream")
+
+    def synchronize(self) -> None:
+        check(lib().gk_ctx_synchronize(self.h), "synchronize")
+
+    def fp64_peak_tflops(self) -> float:
+        out = C.c_double()
+        check(lib().gk_bench_fp64_peak(self.h, C.byref(out)), "fp64_peak")
+        return out.value
+
+    def device_info(self) -> dict:
+        sm, clk, ma, mi = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        check(lib().gk_device_info(self.h, C.byref(sm), C.byref(clk), C.byref(ma),
+                                   C.byref(mi)), "device_info")
+        return {"sm_count": sm.value, "clock_khz": clk.value, "cc": f"{ma.value}.{mi.value}"}
+
+
+@dataclass
+class TableInfo:
+    nodes: int
+    zeros: int
+    hash_buckets: int
+    lookup_buckets: int
+    r_min: float
+    r_max: float
+    t: float
+    dr_min: float
+    inv_dr_min: float
+    k: complex
+    degree: int
+    device_bytes: int
+    build_ms: float
+
+
+class DeviceTable:
+    """gktab::KernelEvaluator built on the device (evaluator.hpp:102-309).
+
+    Plan and reference-format hash are bit-identical to build_plan /
+    build_hash; Exp uses linear and Green degree-d Lagrange interpolation on
+    the reference's stencils; r < r_min falls back to direct evaluation and
+    is counted.
+    """
+
+    def __init__(self, cfg: SamplingConfig, medium: Medium = Medium(), lagrange_degree: int = 3,
+                 ctx: Context | None = None):
+        self.ctx = ctx or Context.get()
+        self.cfg, self.medium = cfg, medium
+        h = C.c_void_p()
+        check(lib().gk_table_build(self.ctx.h, C.byref(cfg.c()), C.byref(medium.c()),
+                                   lagrange_degree, C.byref(h)), "KernelEvaluator")
+        self.h = h
+        ic = TableInfoC()
+        check(lib().gk_table_info_get(self.h, C.byref(ic)), "table_info")
+        self.info = TableInfo(ic.nodes, ic.zeros, ic.hash_buckets, ic.lookup_buckets, ic.r_min,
+                              ic.r_max, ic.t, ic.dr_min, ic.inv_dr_min,
+                              complex(ic.k_re, ic.k_im) if ic.k_im else ic.k_re, ic.degree,
+                              ic.device_bytes, ic.build_ms)
+        self.fallbacks = 0
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().gk_table_destroy(h)
+            self.h = None
+
+    @property
+    def k(self):
+        return self.info.k
+
+    def download(self) -> dict:
+        """Host copies: abscissae, zero_locations, exp/green node values, buckets."""
+        n, nz, nb = self.info.nodes, self.info.zeros, self.info.hash_buckets
+        a = np.zeros(n, np.float64)
+        z = np.zeros(max(nz, 1), np.float64)
+        e = np.zeros(n, np.complex128)
+        g = np.zeros(n, np.complex128)
+        b = np.zeros(nb, np.uint32)
+        check(lib().gk_table_download(self.h, a.ctypes.data, z.ctypes.data, e.ctypes.data,
+                                      g.ctypes.data, b.ctypes.data), "download")
+        return {"abscissae": a, "zeros": z[:nz], "exp": e, "green": g, "buckets": b,
+                "t": self.info.t, "dr_min": self.info.dr_min}
+
+    def eval_batch(self, kind: KernelKind, radii):
+        """KernelEvaluator::eval_batch (evaluator.hpp:209-221) on the device.
+
+        ``radii``: torch CUDA float64 tensor (stays on device) or array-like
+        (copied).  Returns a complex128 tensor on the device.
+        """
+        return eval_batch(kind, radii, table=self, ctx=self.ctx)
+
+    def eval_exp(self, r: float) -> complex:
+        return complex(self.eval_batch(KernelKind.PlainExp, [r]).cpu()[0])
+
+    def eval_green(self, r: float) -> complex:
+        return complex(self.eval_batch(KernelKind.GreenOverR, [r]).cpu()[0])
+
+
+def _as_device_f64(x, device: int):
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=f"cuda:{device}", dtype=torch.float64)
+    else:
+        t = torch.as_tensor(np.ascontiguousarray(x, np.float64), device=f"cuda:{device}")
+    return t.contiguous()
+
+
+def eval_batch(kind: KernelKind, radii, table: DeviceTable | None = None, k: complex = 0.0,
+               ctx: Context | None = None):
+    """eval_batch with a table, or eval_analytic elementwise (table=None)."""
+    torch = _torch()
+    ctx = ctx or (table.ctx if table else Context.get())
+    r = _as_device_f64(radii, ctx.device)
+    out = torch.empty(r.numel(), dtype=torch.complex128, device=r.device)
+    fb = C.c_uint64()
+    kc = complex(k)
+    check(lib().gk_eval_batch(ctx.h, table.h if table else None, int(kind), kc.real, kc.imag,
+                              r.data_ptr() if r.numel() else None, r.numel(),
+                              out.data_ptr() if r.numel() else None, C.byref(fb)), "eval_batch")
+    if table is not None:
+        table.fallbacks += fb.value
+    return out
+
+
+class DeviceMesh:
+    """A mesh resident on the device with its quadrature points (K0)."""
+
+    def __init__(self, mesh: TriangleMesh, spec: QuadratureSpec, ctx: Context | None = None):
+        self.ctx = ctx or Context.get()
+        self.mesh, self.spec = mesh, spec
+        h = C.c_void_p()
+        check(lib().gk_mesh_create(self.ctx.h, mesh.vertices.ctypes.data, mesh.vertices.shape[0],
+                                   mesh.triangles.ctypes.data, mesh.triangles.shape[0],
+                                   spec.outer_points, spec.inner_points_per_edge, C.byref(h)),
+              "fill_matrix")
+        self.h = h
+        self.N = mesh.triangle_count()
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            lib().gk_mesh_destroy(h)
+            self.h = None
+
+    def points(self):
+        """(outer[4][N m], inner[4][N 3n]) in the reference's SoA order"""
+        m, n = self.spec.outer_points, self.spec.inner_points_per_edge
+        o = np.zeros((4, self.N * m), np.float64)
+        i = np.zeros((4, self.N * 3 * n), np.float64)
+        check(lib().gk_mesh_points_download(self.h, o.ctypes.data, i.ctypes.data), "points")
+        return o, i
+
+    def distance_range(self, row_begin: int = 0, row_end: int | None = None):
+        """K1: min/max quadrature pair distance over rows x all q != p"""
+        row_end = self.N if row_end is None else row_end
+        lo, hi = C.c_double(), C.c_double()
+        check(lib().gk_distance_range(self.ctx.h, self.h, row_begin, row_end, C.byref(lo),
+                                      C.byref(hi)), "distance_range")
+        return lo.value, hi.value
+
+
+def fill_rows(dmesh: DeviceMesh, mode: Mode, kind: KernelKind = KernelKind.GreenOverR,
+              table: DeviceTable | None = None, k: complex = 0.0, row_begin: int = 0,
+              row_end: int | None = None, out=None, report: bool = True):
+    """fill_rows (matfill.hpp:169-203) for rows [row_begin,row_end) on the device.
+
+    Returns (Z, FillReport | None); Z is a (rows, N) complex128 CUDA tensor.
+    ``report=False`` launches asynchronously on the current stream.
+    """
+    torch = _torch()
+    ctx = dmesh.ctx
+    N = dmesh.N
+    row_end = N if row_end is None else row_end
+    rows = row_end - row_begin
+    if out is None:
+        out = torch.empty((rows, N), dtype=torch.complex128, device=f"cuda:{ctx.device}")
+    assert out.dtype == torch.complex128 and out.is_cuda and out.stride(1) == 1
+    kc = complex(k)
+    rep = FillReportC()
+    check(lib().gk_fill_rows(ctx.h, dmesh.h, int(mode), table.h if table else None, int(kind),
+                             kc.real, kc.imag, row_begin, row_end,
+                             out.data_ptr() if rows else None, out.stride(0) if rows else N,
+                             C.byref(rep) if report else None), "fill_matrix")
+    return out, (FillReport.from_c(rep) if report else None)
+
+
+def fill_matrix(mesh: TriangleMesh, spec: QuadratureSpec, mode: Mode, medium: Medium = Medium(),
+                cfg: SamplingConfig | None = None, kind: KernelKind = KernelKind.GreenOverR,
+                ctx: Context | None = None, out: np.ndarray | None = None):
+    """fill_matrix<Kernel> (matfill.hpp:144-228) end to end from host buffers.
+
+    TABLE mode: ``cfg.r_min/r_max <= 0`` selects the device-computed pair
+    distance range (K1).  Returns (Z as a host complex128 (N,N) array, report).
+    """
+    ctx = ctx or Context.get()
+    N = mesh.triangle_count()
+    z = out if out is not None else np.empty((N, N), np.complex128)
+    assert z.dtype == np.complex128 and z.flags.c_contiguous and z.shape == (N, N)
+    rep = FillReportC()
+    cfg_c = (cfg or SamplingConfig(r_min=0.0, r_max=0.0)).c()
+    check(lib().gk_fill_matrix_host(ctx.h, mesh.vertices.ctypes.data, mesh.vertices.shape[0],
+                                    mesh.triangles.ctypes.data, N, spec.outer_points,
+                                    spec.inner_points_per_edge, int(mode), C.byref(cfg_c),
+                                    C.byref(medium.c()), int(kind), z.ctypes.data,
+                                    C.byref(rep)), "fill_matrix")
+    return z, FillReport.from_c(rep)

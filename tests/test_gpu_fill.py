@@ -1,0 +1,188 @@
+"""K0 points, K1 range, K3/K4 fills vs the oracle (parity tests proper).
+
+Tolerance (stated here in code): for each entry
+  |Z_gpu - Z_cpu_direct| <= B_pq = sum_{o,i} |w_o w_i| (pw(r_oi) + 64 2^-53 (1 + |k| r) / r)
+with pw = pointwise_bound(ev, Green, Lagrange, r) (bounds.hpp:97-111) for the
+table mode and 0 for the direct mode; the (1 + |k| r) factor is the rounding
+of the phase k r, which the reference itself carries.
+"""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import DIRECT, EXP, GREEN, TABLE, SamplingConfig as OCfg
+
+pytestmark = pytest.mark.gpu
+
+ULPS = 64.0
+
+
+def sphere(gk, level, radius=1.0, seed=1901, amp=1e-3):
+    return gk.jitter(gk.generate_sphere_mesh(radius, level), seed, amp)
+
+
+def test_points_bit_exact(gk, oracle):
+    for mesh, m, n in [(sphere(gk, 2), 6, 4), (sphere(gk, 1, 0.5), 7, 5),
+                       (gk.generate_plate_mesh(1.0, 10), 4, 3), (sphere(gk, 0), 1, 1)]:
+        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+        go, gi = dm.points()
+        oo, oi = oracle.points(mesh.vertices, mesh.triangles, m, n)
+        assert np.array_equal(go, oo) and np.array_equal(gi, oi)
+
+
+def test_distance_range_brackets_exact(gk, oracle):
+    mesh = sphere(gk, 2)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    for rb, re in [(0, 320), (0, 160), (160, 320), (17, 18)]:
+        lo, hi = dm.distance_range(rb, re)
+        olo, ohi = oracle.distance_range(mesh.vertices, mesh.triangles, 6, 4, rb, re)
+        assert lo <= olo <= lo * (1 + 2.0 ** -47)
+        assert hi * (1 - 2.0 ** -47) <= ohi <= hi
+
+
+def _fill_case(gk, oracle, mesh, m, n, k, S=1000):
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+    lo, hi = dm.distance_range()
+    med = gk.Medium(lambda0=2 * np.pi / k)
+    cfg = gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S)
+    t = gk.DeviceTable(cfg, med)
+    plan = oracle.make_plan(t.download()["abscissae"], t.download()["zeros"])
+    ev = oracle.evaluator(plan, t.k)
+    return dm, t, ev
+
+
+@pytest.mark.parametrize("level,m,n,S", [(1, 6, 4, 1000), (2, 6, 4, 1000), (2, 4, 3, 10000),
+                                         (1, 7, 5, 1000), (1, 1, 1, 1000), (1, 3, 2, 10000)])
+def test_fill_parity_sphere(gk, oracle, level, m, n, S):
+    mesh = sphere(gk, level)
+    k = 2 * np.pi
+    dm, t, ev = _fill_case(gk, oracle, mesh, m, n, k, S)
+    zd, rd = gk.fill_rows(dm, gk.Mode.DIRECT, k=k)
+    zt, rt = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+    zd, zt = zd.cpu().numpy(), zt.cpu().numpy()
+    ref_d, rep = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, DIRECT, k, threads=8)
+    ref_t, rep_t = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, TABLE, k, ev=ev,
+                                    threads=8)
+    B_d = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, None, k, ULPS)
+    B_t = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, ev, k, ULPS)
+    assert np.all(np.abs(zd - ref_d) <= B_d), np.max(np.abs(zd - ref_d) / np.maximum(B_d, 1e-300))
+    assert np.all(np.abs(zt - ref_d) <= B_t), np.max(np.abs(zt - ref_d) / np.maximum(B_t, 1e-300))
+    # same plan on both sides: only rounding separates GPU-table and CPU-table
+    assert np.all(np.abs(zt - ref_t) <= B_d)
+    N = mesh.triangle_count()
+    assert rd.actual_calls == rt.actual_calls == rep.actual_calls == 3 * m * n * N * (N - 1)
+    assert rd.predicted_calls == 3 * m * n * N * N
+    assert rt.fallback_calls == 0 == rep_t.fallback_calls
+    assert np.all(np.diag(zd) == 0) and np.all(np.diag(zt) == 0)
+
+
+def test_fill_exp_kind(gk, oracle):
+    mesh = sphere(gk, 1, 0.5)
+    k = 2 * np.pi
+    dm, t, ev = _fill_case(gk, oracle, mesh, 4, 3, k)
+    zd, _ = gk.fill_rows(dm, gk.Mode.DIRECT, kind=gk.KernelKind.PlainExp, k=k)
+    zt, _ = gk.fill_rows(dm, gk.Mode.TABLE, kind=gk.KernelKind.PlainExp, table=t)
+    ref_d, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, 4, 3, DIRECT, k, kind=EXP)
+    ref_t, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, 4, 3, TABLE, k, ev=ev, kind=EXP)
+    scale = np.abs(ref_d).max()
+    assert np.max(np.abs(zd.cpu().numpy() - ref_d)) <= 1e-13 * scale * 80
+    assert np.max(np.abs(zt.cpu().numpy() - ref_t)) <= 1e-12 * scale * 80
+
+
+def test_fallback_routing_below_rmin(gk, oracle):
+    """test_matfill.cpp:152-165: r_min = 0.3 forces a fat near-field region."""
+    mesh = gk.generate_sphere_mesh(0.5, 1)
+    k = 2 * np.pi
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(1, 1))
+    hi = oracle.max_vertex_distance(mesh.vertices) * 1.01
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=0.3, r_max=hi))
+    zt, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+    d = t.download()
+    ev = oracle.evaluator(oracle.make_plan(d["abscissae"], d["zeros"]), k)
+    ref, orep = oracle.fill_rows(mesh.vertices, mesh.triangles, 1, 1, TABLE, k, ev=ev)
+    assert 0 < rep.fallback_calls < rep.actual_calls
+    assert rep.fallback_calls == orep.fallback_calls
+    B = oracle.entry_bounds(mesh.vertices, mesh.triangles, 1, 1, None, k, ULPS)
+    assert np.all(np.abs(zt.cpu().numpy() - ref) <= B + np.abs(ref) * 1e-12)
+
+
+def test_above_rmax_is_out_of_range(gk):
+    mesh = gk.generate_sphere_mesh(0.5, 1)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(1, 1))
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=1e-3, r_max=0.5))
+    with pytest.raises(gk.OutOfRange):
+        gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+
+
+def test_row_blocks_union_bit_exact(gk):
+    """test_matfill.cpp:98-105 (threads) mirrored as row blocks (GPU shards)."""
+    mesh = sphere(gk, 2)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi))
+    for mode, kw in ((gk.Mode.DIRECT, dict(k=2 * np.pi)), (gk.Mode.TABLE, dict(table=t))):
+        full, _ = gk.fill_rows(dm, mode, **kw)
+        N = dm.N
+        parts = []
+        for w in range(3):
+            chunk = (N + 2) // 3
+            b, e = w * chunk, min(N, (w + 1) * chunk)
+            z, rep = gk.fill_rows(dm, mode, row_begin=b, row_end=e, **kw)
+            assert rep.actual_calls == 3 * 6 * 4 * (e - b) * (N - 1)
+            parts.append(z)
+        import torch
+        assert torch.equal(torch.cat(parts), full)
+
+
+def test_lossy_plate_parity(gk, oracle):
+    """C4 shape at small N: complex k, direct and table vs the complex-k oracle."""
+    mesh = gk.generate_plate_mesh(1.0, 8)
+    med = gk.Medium(lambda0=1.0, eps_r=4.0, eps_r_im=-0.4)
+    k = gk.wavenumber(med)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi), med)
+    d = t.download()
+    ev = oracle.evaluator(oracle.make_plan(d["abscissae"], d["zeros"]), k.real, k_im=k.imag)
+    zd, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k)
+    zt, _ = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+    ref, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, 6, 4, DIRECT, k.real, k_im=k.imag,
+                              threads=8)
+    B_d = oracle.entry_bounds(mesh.vertices, mesh.triangles, 6, 4, None, abs(k), ULPS)
+    B_t = oracle.entry_bounds(mesh.vertices, mesh.triangles, 6, 4, ev, abs(k), ULPS)
+    assert np.all(np.abs(zd.cpu().numpy() - ref) <= B_d)
+    assert np.all(np.abs(zt.cpu().numpy() - ref) <= B_t)
+
+
+def test_fill_matrix_host_end_to_end(gk, oracle):
+    mesh = sphere(gk, 1)
+    k = 2 * np.pi
+    z, rep = gk.fill_matrix(mesh, gk.QuadratureSpec(4, 3), gk.Mode.TABLE, gk.Medium())
+    ref, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, 4, 3, DIRECT, k)
+    assert rep.actual_calls == 3 * 4 * 3 * 80 * 79 and rep.fallback_calls == 0
+    re, im = oracle.compare_fills(z, ref)
+    assert max(re, im) <= 1e-4   # acceptance criterion 5 gate
+
+
+def test_hand_summed_static_kernel(gk):
+    """test_matfill.cpp:38-59: m = n = 1, k = 0, hand sum of 1/r."""
+    mesh = gk.TriangleMesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 0, 1],
+                                     [0, 1, 1]], float), np.array([[0, 1, 2], [3, 4, 5]]))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(1, 1))
+    z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=0.0)
+    z = z.cpu().numpy()
+    c = np.array([1 / 3, 1 / 3, 0.0])
+    mids = np.array([[0.5, 0, 1], [0.5, 0.5, 1], [0, 0.5, 1]])
+    lens = [1.0, np.sqrt(2.0), 1.0]
+    expect = sum(0.5 * lens[e] / np.linalg.norm(c - mids[e]) for e in range(3))
+    assert abs(z[0, 1].real - expect) <= expect * 1e-14
+    assert z[0, 1].imag == 0.0 and z[0, 0] == 0 and z[1, 1] == 0
+    assert rep.actual_calls == 6 and rep.predicted_calls == 12
+
+
+def test_mesh_validation(gk):
+    mesh = gk.generate_sphere_mesh(0.5, 0)
+    with pytest.raises(gk.InvalidArgument):
+        gk.DeviceMesh(mesh, gk.QuadratureSpec(5, 1))
+    bad = gk.TriangleMesh(mesh.vertices, np.array([[0, 1, 99]]))
+    with pytest.raises(gk.InvalidArgument):
+        gk.DeviceMesh(bad, gk.QuadratureSpec(4, 3))

@@ -1,0 +1,176 @@
+"""K2 device table build and K5 evaluation vs the oracle (parity tests proper).
+
+Plan and reference-format hash: bit-exact vs the oracle's build_plan /
+build_hash (which is pinned bitwise to the reference, test_oracle_vs_ref.py).
+Node values: device sincos vs glibc, <= 4 ulp.  Interpolated values: GPU table
+vs CPU table on the same plan, rounding-level; vs direct evaluation, within
+the reference's own per-probe bound (bounds.hpp:97-111) plus FP64 rounding.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.pyoracle import EXP, GREEN, SamplingConfig as OCfg, splitmix64_uniform
+
+pytestmark = pytest.mark.gpu
+
+ULP = 2.0 ** -52
+
+
+def _cfg(g, **kw):
+    return g.SamplingConfig(**kw)
+
+
+def _ocfg(c):
+    return OCfg(c.r_min, c.r_max, c.samples_per_wavelength, c.refine_interval_divisor,
+                c.refine_halfwidth_in_t, c.dedup_fraction, c.refine)
+
+
+def _oracle_plan(oracle, c, med):
+    if med.eps_r_im == 0.0:
+        return oracle.build_plan(_ocfg(c), med.lambda0, med.eps_r, med.mu_r)
+    n = np.sqrt(complex(med.eps_r * med.mu_r, med.eps_r_im * med.mu_r))
+    k = 2.0 * math.pi * n / med.lambda0
+    t = med.lambda0 / (c.samples_per_wavelength * n.real)
+    return oracle.build_plan_core(_ocfg(c), k.real, t)
+
+
+def _random_configs(n, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        lam = float(rng.uniform(0.3, 3.0))
+        out.append((dict(r_min=1e-4 * lam, r_max=lam * 1.3,
+                         samples_per_wavelength=int(rng.integers(40, 4001)),
+                         refine_interval_divisor=int(rng.integers(2, 5)),
+                         refine_halfwidth_in_t=float(rng.uniform(1.0, 3.0)),
+                         dedup_fraction=float(rng.uniform(0.25, 1.0))),
+                    dict(lambda0=lam)))
+    return out
+
+
+FIXED = [
+    (dict(), dict()),                                            # reference default config
+    (dict(refine=False), dict()),                                # plain grid, 1001 nodes
+    (dict(r_min=1e-3, r_max=2.0), dict(lambda0=0.5)),            # C1, S = 1e3
+    (dict(r_min=1e-3, r_max=2.0, samples_per_wavelength=10000), dict(lambda0=0.5)),  # C1 1e4
+    (dict(r_min=0.0118, r_max=1.9997), dict()),                  # C2-like range
+    (dict(r_min=1.4e-3, r_max=2.0, samples_per_wavelength=10000), dict(lambda0=0.15)),  # C5
+    (dict(r_min=0.26, r_max=0.49), dict()),                      # no zero in range
+    (dict(r_min=0.25, r_max=1.0), dict()),                       # zeros on both endpoints
+    (dict(r_min=1e-4, r_max=1.0, samples_per_wavelength=20, refine_halfwidth_in_t=3.0),
+     dict()),                                                    # overlapping windows
+    (dict(r_min=1e-3, r_max=1.5, samples_per_wavelength=1000), dict(eps_r=4.0, eps_r_im=-0.4)),
+]
+
+
+@pytest.mark.parametrize("cfg_kw,med_kw", FIXED + _random_configs(24, 991))
+def test_plan_and_hash_bit_exact(gk, oracle, cfg_kw, med_kw):
+    c = gk.SamplingConfig(**cfg_kw)
+    med = gk.Medium(**med_kw)
+    t = gk.DeviceTable(c, med)
+    d = t.download()
+    p = _oracle_plan(oracle, c, med)
+    assert d["abscissae"].size == p.abscissae.size
+    assert np.array_equal(d["abscissae"], p.abscissae)
+    assert np.array_equal(d["zeros"], p.zeros)
+    assert d["t"] == p.t and d["dr_min"] == p.dr_min
+    b, dr, inv = oracle.build_hash(p.abscissae, p.zeros)
+    assert np.array_equal(d["buckets"], b)
+    assert t.info.inv_dr_min == inv
+
+
+def test_refine_off_plan_size(gk):
+    t = gk.DeviceTable(gk.SamplingConfig(refine=False))
+    assert t.info.nodes == 1001 and t.info.zeros == 0   # test_sampling.cpp:122-129
+
+
+def test_zero_locations_quarter_period(gk):
+    t = gk.DeviceTable(gk.SamplingConfig())
+    assert list(t.download()["zeros"]) == [0.25, 0.5, 0.75, 1.0]  # test_sampling.cpp:42-49
+
+
+@pytest.mark.parametrize("S", [1000, 10000])
+def test_node_values_vs_glibc(gk, oracle, S):
+    c = gk.SamplingConfig(r_min=1e-3, r_max=2.0, samples_per_wavelength=S)
+    med = gk.Medium(lambda0=0.5)
+    t = gk.DeviceTable(c, med)
+    d = t.download()
+    p = _oracle_plan(oracle, c, med)
+    ev = oracle.evaluator(p, oracle.wavenumber(0.5))
+    e, g = ev.tables()
+    assert np.all(np.abs(d["exp"] - e) <= 4 * ULP * np.abs(e))
+    assert np.all(np.abs(d["green"] - g) <= 4 * ULP * np.abs(g))
+
+
+def _c1(gk, oracle, S, n=1 << 20, lo=1e-3, seed=1901):
+    c = gk.SamplingConfig(r_min=1e-3, r_max=2.0, samples_per_wavelength=S)
+    med = gk.Medium(lambda0=0.5)
+    t = gk.DeviceTable(c, med)
+    p = _oracle_plan(oracle, c, med)
+    ev = oracle.evaluator(p, oracle.wavenumber(0.5))
+    r = splitmix64_uniform(seed, n, lo, 2.0)
+    return t, ev, r
+
+
+@pytest.mark.parametrize("S", [1000, 10000])
+def test_eval_batch_table_vs_cpu_table(gk, oracle, S):
+    """C1 (2^20 seeded radii): same plan, GPU vs CPU interpolation."""
+    t, ev, r = _c1(gk, oracle, S, lo=1e-4)  # straddles r_min: fallbacks exercised
+    for kind in (EXP, GREEN):
+        got = t.eval_batch(gk.KernelKind(kind), r).cpu().numpy()
+        ref = ev.eval_batch(kind, r)
+        scale = np.abs(ref) + (1.0 if kind == EXP else 1.0 / r)
+        err = np.abs(got - ref) / scale
+        assert err.max() <= 1e-11, (kind, err.max(), r[err.argmax()])
+    assert t.fallbacks == ev.fallbacks and ev.fallbacks > 0
+
+
+@pytest.mark.parametrize("S", [1000, 10000])
+def test_eval_batch_green_within_pointwise_bound(gk, oracle, S):
+    t, ev, r = _c1(gk, oracle, S, n=1 << 16)
+    got = t.eval_batch(gk.KernelKind.GreenOverR, r).cpu().numpy()
+    k = oracle.wavenumber(0.5)
+    exact = np.array([oracle.eval_analytic(GREEN, k, x) for x in r])
+    bound = np.array([ev.pointwise_bound(GREEN, 1, x) for x in r])
+    tol = bound + 64 * 2.0 ** -53 * (1 + k * r) / r
+    assert np.all(np.abs(got - exact) <= tol)
+
+
+def test_nodes_reproduced_exactly(gk):
+    t = gk.DeviceTable(gk.SamplingConfig())
+    d = t.download()
+    a = d["abscissae"]
+    assert np.array_equal(t.eval_batch(gk.KernelKind.GreenOverR, a).cpu().numpy(), d["green"])
+    assert np.array_equal(t.eval_batch(gk.KernelKind.PlainExp, a).cpu().numpy(), d["exp"])
+
+
+def test_eval_batch_direct_vs_glibc(gk, oracle):
+    r = splitmix64_uniform(7, 1 << 16, 1e-3, 2.0)
+    k = 4.0 * math.pi
+    for kind in (EXP, GREEN):
+        got = gk.eval_batch(gk.KernelKind(kind), r, k=k).cpu().numpy()
+        ref = np.array([oracle.eval_analytic(kind, k, x) for x in r])
+        assert np.all(np.abs(got - ref) <= 8 * ULP * (1 + k * r) * np.abs(ref))
+
+
+def test_eval_batch_errors_carry_index(gk):
+    t = gk.DeviceTable(gk.SamplingConfig())
+    with pytest.raises(gk.InvalidArgument, match=r"\[2\]"):
+        t.eval_batch(gk.KernelKind.PlainExp, [0.2, 0.3, -1.0, 0.4])
+    with pytest.raises(gk.InvalidArgument, match=r"\[1\]"):
+        t.eval_batch(gk.KernelKind.GreenOverR, [0.2, 1.5])          # above r_max
+    with pytest.raises(gk.InvalidArgument, match=r"\[0\]"):
+        gk.eval_batch(gk.KernelKind.GreenOverR, [0.0], k=1.0)      # singular
+    assert gk.eval_batch(gk.KernelKind.PlainExp, [], k=1.0).numel() == 0
+    assert complex(gk.eval_batch(gk.KernelKind.PlainExp, [0.0], k=7.3).cpu()[0]) == 1.0
+
+
+def test_config_validation(gk):
+    with pytest.raises(gk.InvalidArgument):
+        gk.DeviceTable(gk.SamplingConfig(r_min=-1.0))
+    with pytest.raises(gk.InvalidArgument):
+        gk.DeviceTable(gk.SamplingConfig(r_min=0.1, r_max=0.1 + 1.5e-3))  # < two intervals
+    with pytest.raises(gk.InvalidArgument):
+        gk.DeviceTable(gk.SamplingConfig(), gk.Medium(lambda0=0.0))
