@@ -13,6 +13,7 @@
 // accumulator per outer point (sum_i w_i K(r_oi)) and finishes the entry with
 // sum_o w_o acc_o -- the reference's double sum regrouped (same terms).
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <math_constants.h>
 
@@ -21,7 +22,7 @@
 namespace gk {
 
 constexpr int kRowsPerTile = 8;  // one row per warp
-constexpr int kColBlocks = 4;    // 32-column blocks per tile
+constexpr int kMaxColBlocks = 32;  // 32-column blocks per tile (adaptive, see launch_fill)
 constexpr int kThreads = 32 * kRowsPerTile;
 
 struct FillArgs {
@@ -31,6 +32,7 @@ struct FillArgs {
   int ipt;
   size_t row_begin, row_end;
   size_t ncb, ntiles;
+  int cpt;  // column blocks per tile
   double2* z;
   size_t ldz;
   TableDev T;
@@ -39,23 +41,107 @@ struct FillArgs {
   unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max
 };
 
-template <int MODE>
-struct PhaseSmem {
-  __device__ static const double2* get(const double2*) { return nullptr; }
-};
-template <>
-struct PhaseSmem<GK_MODE_DIRECT> {
-  __device__ static const double2* get(const double2* g) {
-    __shared__ double2 tab[kPhaseM];
-    for (int i = threadIdx.x; i < kPhaseM; i += blockDim.x) tab[i] = g[i];
-    __syncthreads();
-    return tab;
+// Column-block walk shared by both kernels: the (column block, inner point)
+// iterations of a tile are flattened into one loop so the next inner point is
+// always in flight (register double buffer) while the current one is used.
+struct InnerWalk {
+  const double4* inner;
+  size_t N, q0base;
+  int ipt, ncb;
+  __device__ __forceinline__ void load(int cb, int i, int lane, double2& xy, double2& zw,
+                                       size_t& q, bool& valid) const {
+    const size_t qr = q0base + 32 * static_cast<size_t>(cb) + lane;
+    valid = qr < N;
+    q = valid ? qr : N - 1;
+    const double2* p = reinterpret_cast<const double2*>(inner + static_cast<size_t>(i) * N + q);
+    xy = __ldg(p);
+    zw = __ldg(p + 1);
   }
 };
 
-template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
-__global__ void __launch_bounds__(kThreads, 2) fill_kernel(const FillArgs A) {
-  const double2* tab = PhaseSmem<MODE>::get(A.phase);
+// K4: direct evaluation.  Per eval: 6 (r^2) + 6 (rsqrt, r) + 12 (phase,
+// table lookup, complex combine) + 3 (weight, accumulate) = 27 FP64 ops.
+// The warp's outer points sit in shared memory (broadcast loads, one
+// wavefront each) instead of registers, so ~80 registers per thread allow 3
+// CTAs (24 warps) per SM to hide the FP64 dependency latency.
+template <int MO, int KIND, bool LOSSY, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A) {
+  extern __shared__ double2 tab[];  // kPhaseM phase entries (64 KB)
+  __shared__ double so[kRowsPerTile][MO][4];
+  for (int i = threadIdx.x; i < kPhaseM; i += blockDim.x) tab[i] = A.phase[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t N = A.N;
+  double (*my)[4] = so[warp];
+
+  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
+    const size_t p = A.row_begin + tr * kRowsPerTile + warp;
+    if (p >= A.row_end) continue;  // warp-uniform
+    __syncwarp();
+    if (lane < MO) {
+      const double4 P = A.outer[p * MO + lane];
+      my[lane][0] = P.x;
+      my[lane][1] = P.y;
+      my[lane][2] = P.z;
+      my[lane][3] = P.w;
+    }
+    __syncwarp();
+    const size_t q0base = tc * (32 * static_cast<size_t>(A.cpt));
+    int ncb = static_cast<int>((N - q0base + 31) / 32);
+    if (ncb > A.cpt) ncb = A.cpt;
+    const InnerWalk W{A.inner, N, q0base, A.ipt, ncb};
+    const int iters = ncb * A.ipt;
+    double2 nxy, nzw;
+    size_t q;
+    bool valid;
+    W.load(0, 0, lane, nxy, nzw, q, valid);
+    double2 acc[MO];
+#pragma unroll
+    for (int o = 0; o < MO; ++o) acc[o] = make_double2(0.0, 0.0);
+    int ncb_next = 0, ni = 0;  // (column block, inner point) of the prefetch
+    for (int it = 0; it < iters; ++it) {
+      const double2 pxy = nxy, pzw = nzw;
+      const size_t qc = q;
+      const bool vc = valid;
+      if (++ni == A.ipt) {
+        ni = 0;
+        ++ncb_next;
+      }
+      const bool block_done = ni == 0;
+      if (it + 1 < iters) W.load(ncb_next, ni, lane, nxy, nzw, q, valid);
+#pragma unroll
+      for (int o = 0; o < MO; ++o) {
+        const double2 oxy = *reinterpret_cast<const double2*>(&my[o][0]);
+        const double oz = my[o][2];
+        const double d2 = dist2(oxy.x, oxy.y, oz, pxy.x, pxy.y, pzw.x);
+        const double y = rsqrt_fast(d2);
+        const double r = __dmul_rn(d2, y);
+        const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
+        double wgt = KIND == GK_KIND_GREEN ? __dmul_rn(pzw.y, y) : pzw.y;
+        if constexpr (LOSSY) wgt *= exp(A.k_im * r);
+        acc[o].x = __fma_rn(wgt, cs.x, acc[o].x);
+        acc[o].y = __fma_rn(-wgt, cs.y, acc[o].y);
+      }
+      if (block_done) {  // column block complete: finish the entry
+        double2 res = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int o = 0; o < MO; ++o) {
+          const double wo = my[o][3];
+          res.x = __fma_rn(wo, acc[o].x, res.x);
+          res.y = __fma_rn(wo, acc[o].y, res.y);
+          acc[o] = make_double2(0.0, 0.0);
+        }
+        if (qc == p) res = make_double2(0.0, 0.0);  // self pairs stay zero (matfill.hpp:178)
+        if (vc) __stcs(A.z + (p - A.row_begin) * A.ldz + qc, res);
+      }
+    }
+  }
+}
+
+// K3: table evaluation (the paper's method) with the reference's fallback.
+template <int MO, int KIND, int DEG>
+__global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t N = A.N;
   unsigned long long n_low = 0, n_high = 0;
@@ -68,94 +154,111 @@ __global__ void __launch_bounds__(kThreads, 2) fill_kernel(const FillArgs A) {
 #pragma unroll
     for (int o = 0; o < MO; ++o) {
       const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
-      const double2 zw = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o) + 1);
+      const double zz = __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 2);
       ox[o] = xy.x;
       oy[o] = xy.y;
-      oz[o] = zw.x;
+      oz[o] = zz;
     }
-    for (int cb = 0; cb < kColBlocks; ++cb) {
-      const size_t q0 = tc * (32 * kColBlocks) + 32 * cb;
-      if (q0 >= N) break;  // warp-uniform
-      const size_t q_raw = q0 + lane;
-      const bool valid = q_raw < N;
-      const size_t q = valid ? q_raw : N - 1;
-      const bool self = q == p;
-      double2 acc[MO];
+    const size_t q0base = tc * (32 * static_cast<size_t>(A.cpt));
+    int ncb = static_cast<int>((N - q0base + 31) / 32);
+    if (ncb > A.cpt) ncb = A.cpt;
+    const InnerWalk W{A.inner, N, q0base, A.ipt, ncb};
+    const int iters = ncb * A.ipt;
+    double2 nxy, nzw;
+    size_t q;
+    bool valid;
+    W.load(0, 0, lane, nxy, nzw, q, valid);
+    double2 acc[MO];
 #pragma unroll
-      for (int o = 0; o < MO; ++o) acc[o] = make_double2(0.0, 0.0);
-
-      for (int i = 0; i < A.ipt; ++i) {
-        const double2* ip = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
-        const double2 pxy = __ldg(ip), pzw = __ldg(ip + 1);
-#pragma unroll
-        for (int o = 0; o < MO; ++o) {
-          const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-          const double y = rsqrt_fast(d2);
-          const double r = __dmul_rn(d2, y);
-          if constexpr (MODE == GK_MODE_DIRECT) {
-            double2 e = expmjkr_phase(r, A.K1, tab);
-            if constexpr (LOSSY) {
-              const double a = exp(A.k_im * r);
-              e.x *= a;
-              e.y *= a;
-            }
-            const double wgt = KIND == GK_KIND_GREEN ? __dmul_rn(pzw.y, y) : pzw.y;
-            acc[o].x = __fma_rn(wgt, e.x, acc[o].x);
-            acc[o].y = __fma_rn(wgt, e.y, acc[o].y);
-          } else {
-            double2 v;
-            if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, A.T);
-            else if constexpr (DEG == 3) v = green_table<3>(r, A.T);
-            else v = green_table_any(r, A.T);
-            const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
-            if (__any_sync(0xffffffffu, oob)) {
-              if (oob) {
-                if (!self && valid) {
-                  // the reference's eval_kernel fallback (evaluator.hpp:199-205)
-                  v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
-                  if (r > A.T.r_max) ++n_high; else ++n_low;
-                } else {
-                  v = make_double2(0.0, 0.0);
-                }
-              }
-            }
-            acc[o].x = __fma_rn(pzw.y, v.x, acc[o].x);
-            acc[o].y = __fma_rn(pzw.y, v.y, acc[o].y);
-          }
-        }
+    for (int o = 0; o < MO; ++o) acc[o] = make_double2(0.0, 0.0);
+    int ncb_next = 0, ni = 0;  // (column block, inner point) of the prefetch
+    for (int it = 0; it < iters; ++it) {
+      const double2 pxy = nxy, pzw = nzw;
+      const size_t qc = q;
+      const bool vc = valid;
+      if (++ni == A.ipt) {
+        ni = 0;
+        ++ncb_next;
       }
-      double2 res = make_double2(0.0, 0.0);
+      const bool block_done = ni == 0;
+      const bool self = qc == p;
+      if (it + 1 < iters) W.load(ncb_next, ni, lane, nxy, nzw, q, valid);
 #pragma unroll
       for (int o = 0; o < MO; ++o) {
-        const double wo = __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3);
-        res.x = __fma_rn(wo, acc[o].x, res.x);
-        res.y = __fma_rn(wo, acc[o].y, res.y);
+        const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
+        const double r = __dmul_rn(d2, rsqrt_fast(d2));
+        double2 v;
+        if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, A.T);
+        else if constexpr (DEG == 3) v = green_table<3>(r, A.T);
+        else v = green_table_any(r, A.T);
+        const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
+        if (__any_sync(0xffffffffu, oob)) {
+          if (oob) {
+            if (!self && vc) {
+              // the reference's eval_kernel fallback (evaluator.hpp:199-205)
+              v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
+              if (r > A.T.r_max) ++n_high; else ++n_low;
+            } else {
+              v = make_double2(0.0, 0.0);
+            }
+          }
+        }
+        acc[o].x = __fma_rn(pzw.y, v.x, acc[o].x);
+        acc[o].y = __fma_rn(pzw.y, v.y, acc[o].y);
       }
-      if (self) res = make_double2(0.0, 0.0);  // self pairs stay zero (matfill.hpp:178)
-      if (valid) __stcs(A.z + (p - A.row_begin) * A.ldz + q, res);
+      if (block_done) {
+        double2 res = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int o = 0; o < MO; ++o) {
+          const double wo = __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3);
+          res.x = __fma_rn(wo, acc[o].x, res.x);
+          res.y = __fma_rn(wo, acc[o].y, res.y);
+          acc[o] = make_double2(0.0, 0.0);
+        }
+        if (self) res = make_double2(0.0, 0.0);
+        if (vc) __stcs(A.z + (p - A.row_begin) * A.ldz + qc, res);
+      }
     }
   }
-  if constexpr (MODE == GK_MODE_TABLE) {
-    for (int o = 16; o; o >>= 1) {
-      n_low += __shfl_xor_sync(0xffffffffu, n_low, o);
-      n_high += __shfl_xor_sync(0xffffffffu, n_high, o);
-    }
-    if (lane == 0 && n_low) atomicAdd(A.counters, n_low);
-    if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
+  for (int o = 16; o; o >>= 1) {
+    n_low += __shfl_xor_sync(0xffffffffu, n_low, o);
+    n_high += __shfl_xor_sync(0xffffffffu, n_high, o);
   }
+  if (lane == 0 && n_low) atomicAdd(A.counters, n_low);
+  if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
 }
 
-template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
-void launch_one(gk_ctx* ctx, const FillArgs& a) {
-  auto k = fill_kernel<MO, MODE, KIND, DEG, LOSSY>;
+template <class K>
+void launch_kernel(gk_ctx* ctx, K kernel, const FillArgs& a, size_t smem) {
+  if (smem > 48 * 1024)
+    GK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
   int per_sm = 0;
-  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0));
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
   if (per_sm < 1) per_sm = 1;
   size_t grid = static_cast<size_t>(ctx->sm_count) * per_sm;
   if (grid > a.ntiles) grid = a.ntiles;
   if (grid < 1) grid = 1;
-  k<<<static_cast<unsigned>(grid), kThreads, 0, ctx->stream>>>(a);
+  kernel<<<static_cast<unsigned>(grid), kThreads, smem, ctx->stream>>>(a);
   GK_CUDA(cudaGetLastError());
+}
+
+template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
+void launch_one(gk_ctx* ctx, const FillArgs& a) {
+  if constexpr (MODE == GK_MODE_DIRECT)
+  {
+    // occupancy variant (tuning knob; default from the r1 ncu measurements)
+    static const int minb = [] {
+      const char* e = std::getenv("GK_DIRECT_MINB");
+      return e ? std::atoi(e) : 2;
+    }();
+    if (minb == 2)
+      launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 2>, a, kPhaseM * sizeof(double2));
+    else
+      launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 3>, a, kPhaseM * sizeof(double2));
+  }
+  else
+    launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
 }
 
 template <int MO>
@@ -186,8 +289,16 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.ipt = 3 * mesh->n;
   a.row_begin = row_begin;
   a.row_end = row_end;
-  a.ncb = (mesh->N + 32 * kColBlocks - 1) / (32 * kColBlocks);
-  a.ntiles = ((row_end - row_begin + kRowsPerTile - 1) / kRowsPerTile) * a.ncb;
+  // widest tiles (fewest cold starts) that still leave >= 16 tiles per
+  // resident CTA for load balance
+  const size_t row_blocks = (row_end - row_begin + kRowsPerTile - 1) / kRowsPerTile;
+  const size_t col_blocks = (mesh->N + 31) / 32;
+  const size_t want = static_cast<size_t>(ctx->sm_count) * 2 * 16;
+  int cpt = kMaxColBlocks;
+  while (cpt > 1 && row_blocks * ((col_blocks + cpt - 1) / cpt) < want) cpt /= 2;
+  a.cpt = cpt;
+  a.ncb = (col_blocks + cpt - 1) / cpt;
+  a.ntiles = row_blocks * a.ncb;
   a.z = reinterpret_cast<double2*>(z);
   a.ldz = ldz;
   if (table) a.T = table->dev;

@@ -27,8 +27,9 @@ constexpr double kMagic52 = 4503599627370496.0;   // 2^52
 constexpr double kMagicRint = 6755399441055744.0; // 1.5 * 2^52
 
 // Direct-mode phase table size: e^{-j theta} = e^{-j 2pi idx/M} e^{-j delta},
-// |delta| <= pi/M.  M = 2048 keeps the Taylor tail below 2^-60.
-constexpr int kPhaseM = 2048;
+// |delta| <= pi/M = 7.7e-4.  The dropped Taylor terms (delta^6/720 in cos,
+// delta^5/120 in sin) stay below 2.2e-18, i.e. < 0.02 ulp of the result.
+constexpr int kPhaseM = 4096;
 
 struct TableDev {
   const double* grec;  // Green interval records
@@ -134,26 +135,34 @@ __device__ __forceinline__ double2 exp_table(double r, const TableDev& t) {
 // ------------------------------------------------------------ direct math
 
 // exp(-j k r) from a phase table tab[M] = (cos 2pi i/M, sin 2pi i/M) in
-// shared memory: phi = r K1, n = rint(phi), f = phi - n, delta = 2pi f/M,
-// e^{-j delta} by Taylor to delta^6 / delta^5.
-__device__ __forceinline__ double2 expmjkr_phase(double r, double K1, const double2* tab) {
+// shared memory: phi = r K1 (K1 = k M / 2pi), n = rint(phi) (1.5 2^52 magic
+// add), f = phi - n in [-1/2, 1/2], delta = 2pi f / M;
+//   cos(theta0 + delta) = C0 (1 + v) - S0 s,  sin(theta0 + delta) = S0 (1 + v) + C0 s
+// with v = cos(delta) - 1 = -delta^2/2 + delta^4/24 and s = delta - delta^3/6.
+// Returns (Re, -Im) of exp(-j k r) = (cos kr, sin kr): 12 FP64 ops + 1 LDS.128.
+__device__ __forceinline__ double2 cis_phase(double r, double K1, const double2* tab) {
   constexpr double C = 2.0 * kPi / kPhaseM;
   constexpr double a1 = -C * C / 2.0;
   constexpr double a2 = C * C * C * C / 24.0;
-  constexpr double a3 = -C * C * C * C * C * C / 720.0;
   constexpr double s1 = C;
   constexpr double s3 = -C * C * C / 6.0;
-  constexpr double s5 = C * C * C * C * C / 120.0;
   const double t = __fma_rn(r, K1, kMagicRint);
   const double nf = t - kMagicRint;
   const double f = __fma_rn(r, K1, -nf);
   const int idx = __double2loint(t) & (kPhaseM - 1);
   const double g = __dmul_rn(f, f);
-  const double c = __fma_rn(__fma_rn(__fma_rn(a3, g, a2), g, a1), g, 1.0);
-  const double s = __dmul_rn(f, __fma_rn(__fma_rn(s5, g, s3), g, s1));
+  const double v = __dmul_rn(g, __fma_rn(a2, g, a1));
+  const double s = __dmul_rn(f, __fma_rn(s3, g, s1));
   const double2 T = tab[idx];
-  // (C0 - j S0)(c - j s) = (C0 c - S0 s) - j (S0 c + C0 s)
-  return make_double2(__fma_rn(-T.y, s, __dmul_rn(T.x, c)), -__fma_rn(T.x, s, __dmul_rn(T.y, c)));
+  const double c = __fma_rn(-T.y, s, __fma_rn(T.x, v, T.x));
+  const double sn = __fma_rn(T.x, s, __fma_rn(T.y, v, T.y));
+  return make_double2(c, sn);
+}
+
+// exp(-j k r) as (re, im)
+__device__ __forceinline__ double2 expmjkr_phase(double r, double K1, const double2* tab) {
+  const double2 cs = cis_phase(r, K1, tab);
+  return make_double2(cs.x, -cs.y);
 }
 
 // reference-accuracy direct kernel via libdevice sincos (the accuracy oracle

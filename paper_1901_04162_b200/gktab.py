@@ -236,8 +236,11 @@ class DeviceTable:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h:
-            lib().gk_table_destroy(h)
+        if h and _lib._lib is not None:
+            try:
+                _lib._lib.gk_table_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self.h = None
 
     @property
@@ -314,8 +317,11 @@ class DeviceMesh:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h:
-            lib().gk_mesh_destroy(h)
+        if h and _lib._lib is not None:
+            try:
+                _lib._lib.gk_mesh_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self.h = None
 
     def points(self):
