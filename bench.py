@@ -399,29 +399,55 @@ def main():
 
 
 def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals):
-    """Host mesh in, host Z out, through gk_fill_matrix_host (the C-ABI drop-in)."""
+    """End to end through the C-ABI host-buffer entry points: each step uploads
+    the host mesh (H2D), generates quadrature points, (TABLE) computes the
+    range and builds the table, fills, and copies every byte of Z to pinned
+    host memory (D2H).  Z fits host RAM up to C3/C4 (gk_fill_matrix_host into
+    a full host matrix); C5's 107 GB is streamed with gk_fill_rows_host into a
+    reused 4 GiB pinned host window (the full matrix does not fit this host's
+    RAM twice, nor the reference's)."""
     import torch
     N = mesh.triangle_count()
     nbytes = N * N * 16
+    full = nbytes <= (16 << 30)
+    rows_win = N if full else max(1, (4 << 30) // (N * 16))
     try:
-        zh = torch.empty((N, N), dtype=torch.complex128, pin_memory=True)
+        zh = torch.empty((rows_win, N), dtype=torch.complex128, pin_memory=True)
     except RuntimeError as exc:
         return {"value": None, "unit": "evals/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": nbytes, "note": f"pinned host Z unavailable: {exc}"}
+                "d2h_bytes_per_step": nbytes, "note": f"pinned host buffer unavailable: {exc}"}
     z = zh.numpy()
-    cfgs = gk.SamplingConfig(r_min=0.0, r_max=0.0, samples_per_wavelength=args.S)
     m = gk.Mode.TABLE if mode == "table" else gk.Mode.DIRECT
-    gk.fill_matrix(mesh, spec, m, medium, cfgs, ctx=ctx, out=z)  # warm-up
-    steps = max(1, min(args.steps, 3))
+    k = gk.wavenumber(medium)
+
+    def step():
+        if full:
+            cfgs = gk.SamplingConfig(r_min=0.0, r_max=0.0, samples_per_wavelength=args.S)
+            gk.fill_matrix(mesh, spec, m, medium, cfgs, ctx=ctx, out=z)
+            return
+        dm = gk.DeviceMesh(mesh, spec, ctx)
+        t = None
+        if m == gk.Mode.TABLE:
+            lo, hi = dm.distance_range()
+            t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
+                                                 samples_per_wavelength=args.S), medium, ctx=ctx)
+        for rb in range(0, N, rows_win):
+            re = min(N, rb + rows_win)
+            gk.fill_rows_host(dm, m, z, table=t, k=k, row_begin=rb, row_end=re)
+
+    step()  # warm-up
+    steps = max(1, min(args.steps, 2 if not full else 3))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(steps):
-        gk.fill_matrix(mesh, spec, m, medium, cfgs, ctx=ctx, out=z)
+        step()
     dt = (time.perf_counter() - t0) / steps
     h2d = mesh.vertices.nbytes + mesh.triangles.nbytes
     return {"value": total_evals / dt, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(nbytes), "ms_per_step": dt * 1e3,
-            "api": "gk_fill_matrix_host (pinned host Z)"}
+            "api": ("gk_fill_matrix_host -> full pinned host Z" if full else
+                    f"gk_mesh_create + gk_fill_rows_host x{(N + rows_win - 1) // rows_win} "
+                    f"-> {rows_win}-row pinned host window")}
 
 
 def run_vs_n(gk, ctx, mode, args):

@@ -169,6 +169,16 @@ gk_status gk_fill_matrix_host(gk_ctx* ctx, const double* vertices, size_t nv,
                               const gk_sampling_config* cfg, const gk_medium* medium,
                               gk_kind kind, gk_c128* z_host, gk_fill_report* report);
 
+/* fill_rows into HOST memory: rows [row_begin,row_end) land in
+   z_host[(p-row_begin)*ldz_host + q], computed in <= 1 GiB row chunks whose
+   device->host copies overlap the fill of the next chunk (double buffer, a
+   second stream).  Pinned z_host gets full PCIe bandwidth.  For fills larger
+   than host RAM (C5: 107 GB) call it per row range into a reused buffer. */
+gk_status gk_fill_rows_host(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode,
+                            const gk_table* table, gk_kind kind, double k_re, double k_im,
+                            size_t row_begin, size_t row_end, gk_c128* z_host, size_t ldz_host,
+                            gk_fill_report* report);
+
 /* predicted_calls (matfill.hpp:50-56): 3 m n N^2 with the overflow guard */
 gk_status gk_predicted_calls(uint64_t N, uint64_t m, uint64_t n, uint64_t* out);
 

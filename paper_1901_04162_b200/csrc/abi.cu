@@ -429,15 +429,107 @@ gk_status gk_fill_rows(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
   });
 }
 
+namespace {
+
+// chunked, double-buffered device fill + D2H into host memory
+void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
+                       gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
+                       gk_c128* z_host, size_t ldz, gk_fill_report* report) {
+  const size_t nt = mesh->N;
+  need(ldz >= nt, GK_ERR_INVALID_ARGUMENT, "ldz_host < N");
+  need(row_begin <= row_end && row_end <= nt, GK_ERR_INVALID_ARGUMENT, "bad row range");
+  need(row_begin == row_end || z_host, GK_ERR_INVALID_ARGUMENT, "null z_host");
+  if (mode == GK_MODE_TABLE) {
+    need(table != nullptr, GK_ERR_INVALID_ARGUMENT, "TABLE mode needs a table");
+    k_re = table->dev.k_re;
+    k_im = table->dev.k_im;
+  }
+  const size_t row_bytes = nt * sizeof(gk_c128);
+  size_t chunk = (size_t(1) << 30) / row_bytes;
+  if (chunk < 8) chunk = 8;
+  if (chunk > row_end - row_begin) chunk = row_end - row_begin;
+  if (chunk == 0) chunk = 1;
+  cudaStream_t copy = nullptr;
+  gk_c128* dz[2] = {nullptr, nullptr};
+  cudaEvent_t filled[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+  auto cleanup = [&] {
+    if (copy) cudaStreamSynchronize(copy);
+    cudaStreamSynchronize(c->stream);
+    for (int b = 0; b < 2; ++b) {
+      if (dz[b]) cudaFreeAsync(dz[b], c->stream);
+      if (filled[b]) cudaEventDestroy(filled[b]);
+      if (copied[b]) cudaEventDestroy(copied[b]);
+    }
+    if (copy) cudaStreamDestroy(copy);
+  };
+  try {
+    GK_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      GK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dz[b]), chunk * row_bytes, c->stream));
+      GK_CUDA(cudaEventCreateWithFlags(&filled[b], cudaEventDisableTiming));
+      GK_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+    }
+    unsigned long long* cnt = c->scratch.p + 16;
+    GK_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
+    GK_CUDA(cudaEventRecord(c->ev0, c->stream));
+    size_t idx = 0;
+    for (size_t rb = row_begin; rb < row_end; rb += chunk, ++idx) {
+      const size_t re = rb + chunk < row_end ? rb + chunk : row_end;
+      const int b = static_cast<int>(idx & 1);
+      if (idx >= 2) GK_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
+      gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nt, cnt);
+      GK_CUDA(cudaEventRecord(filled[b], c->stream));
+      GK_CUDA(cudaStreamWaitEvent(copy, filled[b], 0));
+      GK_CUDA(cudaMemcpy2DAsync(z_host + (rb - row_begin) * ldz, ldz * sizeof(gk_c128), dz[b],
+                                row_bytes, row_bytes, re - rb, cudaMemcpyDeviceToHost, copy));
+      GK_CUDA(cudaEventRecord(copied[b], copy));
+    }
+    GK_CUDA(cudaEventRecord(c->ev1, c->stream));
+    unsigned long long h[2];
+    GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(copy));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    GK_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (report) {
+      report->N = nt;
+      report->m = mesh->m;
+      report->n = mesh->n;
+      report->predicted_calls = predicted(nt, mesh->m, mesh->n);
+      report->actual_calls = 3ull * mesh->m * mesh->n * (row_end - row_begin) * (nt - 1);
+      report->fallback_calls = h[0] + h[1];
+      report->wall_time_s = ms * 1e-3;
+    }
+    if (h[1])
+      gk::fail(GK_ERR_OUT_OF_RANGE,
+               "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
+}  // namespace
+
+gk_status gk_fill_rows_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t,
+                            gk_kind kind, double k_re, double k_im, size_t row_begin,
+                            size_t row_end, gk_c128* z_host, size_t ldz, gk_fill_report* report) {
+  return guarded([&] {
+    check_ctx(c);
+    need(mesh != nullptr, GK_ERR_INVALID_ARGUMENT, "null mesh");
+    need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
+    use_device(c);
+    fill_rows_to_host(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z_host, ldz, report);
+  });
+}
+
 gk_status gk_fill_matrix_host(gk_ctx* c, const double* verts, size_t nv, const uint32_t* tris,
                               size_t nt, int m, int n, gk_mode mode,
                               const gk_sampling_config* cfg, const gk_medium* med, gk_kind kind,
                               gk_c128* z_host, gk_fill_report* report) {
   gk_mesh* mesh = nullptr;
   gk_table* table = nullptr;
-  gk_c128* dz[2] = {nullptr, nullptr};
-  cudaStream_t copy = nullptr;
-  cudaEvent_t filled[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
   gk_status st = guarded([&] {
     check_ctx(c);
     need(med && z_host, GK_ERR_INVALID_ARGUMENT, "null argument");
@@ -459,60 +551,8 @@ gk_status gk_fill_matrix_host(gk_ctx* c, const double* verts, size_t nv, const u
       if (s != GK_OK) gk::fail(s, g_last_error);
     }
     use_device(c);
-    // row chunks of <= 1 GiB, double-buffered: the fill of chunk i+1 overlaps
-    // the device->host copy of chunk i (second stream + events)
-    const size_t row_bytes = nt * sizeof(gk_c128);
-    size_t chunk = (size_t(1) << 30) / row_bytes;
-    if (chunk < 8) chunk = 8;
-    if (chunk > nt) chunk = nt;
-    GK_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
-      GK_CUDA(cudaMalloc(reinterpret_cast<void**>(&dz[b]), chunk * row_bytes));
-      GK_CUDA(cudaEventCreateWithFlags(&filled[b], cudaEventDisableTiming));
-      GK_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
-    }
-    gk_fill_report rep{};
-    rep.N = nt;
-    rep.m = m;
-    rep.n = n;
-    rep.predicted_calls = predicted(nt, m, n);
-    unsigned long long* cnt = c->scratch.p + 16;
-    GK_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
-    GK_CUDA(cudaEventRecord(c->ev0, c->stream));
-    size_t idx = 0;
-    for (size_t rb = 0; rb < nt; rb += chunk, ++idx) {
-      const size_t re = rb + chunk < nt ? rb + chunk : nt;
-      const int b = static_cast<int>(idx & 1);
-      if (idx >= 2) GK_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
-      gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nt, cnt);
-      GK_CUDA(cudaEventRecord(filled[b], c->stream));
-      GK_CUDA(cudaStreamWaitEvent(copy, filled[b], 0));
-      GK_CUDA(cudaMemcpyAsync(z_host + rb * nt, dz[b], (re - rb) * row_bytes,
-                              cudaMemcpyDeviceToHost, copy));
-      GK_CUDA(cudaEventRecord(copied[b], copy));
-    }
-    GK_CUDA(cudaEventRecord(c->ev1, c->stream));
-    unsigned long long h[2];
-    GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    GK_CUDA(cudaStreamSynchronize(copy));
-    GK_CUDA(cudaStreamSynchronize(c->stream));
-    float ms = 0.f;
-    GK_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    rep.actual_calls = 3ull * m * n * nt * (nt - 1);
-    rep.fallback_calls = h[0] + h[1];
-    rep.wall_time_s = ms * 1e-3;
-    if (h[1])
-      gk::fail(GK_ERR_OUT_OF_RANGE,
-               "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
-    if (report) *report = rep;
+    fill_rows_to_host(c, mesh, mode, table, kind, k_re, k_im, 0, nt, z_host, nt, report);
   });
-  if (copy) cudaStreamSynchronize(copy);
-  for (int b = 0; b < 2; ++b) {
-    if (dz[b]) cudaFree(dz[b]);
-    if (filled[b]) cudaEventDestroy(filled[b]);
-    if (copied[b]) cudaEventDestroy(copied[b]);
-  }
-  if (copy) cudaStreamDestroy(copy);
   gk_table_destroy(table);
   gk_mesh_destroy(mesh);
   return st;

@@ -366,6 +366,24 @@ def fill_rows(dmesh: DeviceMesh, mode: Mode, kind: KernelKind = KernelKind.Green
     return out, (FillReport.from_c(rep) if report else None)
 
 
+def fill_rows_host(dmesh: DeviceMesh, mode: Mode, out: np.ndarray,
+                   kind: KernelKind = KernelKind.GreenOverR, table: DeviceTable | None = None,
+                   k: complex = 0.0, row_begin: int = 0, row_end: int | None = None) -> FillReport:
+    """fill_rows straight into host memory (``out``: (rows, N) complex128, C order;
+    pinned memory gets full PCIe bandwidth).  Chunked + double-buffered."""
+    ctx = dmesh.ctx
+    N = dmesh.N
+    row_end = N if row_end is None else row_end
+    assert out.dtype == np.complex128 and out.flags.c_contiguous and out.shape[1] == N
+    assert out.shape[0] >= row_end - row_begin
+    kc = complex(k)
+    rep = FillReportC()
+    check(lib().gk_fill_rows_host(ctx.h, dmesh.h, int(mode), table.h if table else None,
+                                  int(kind), kc.real, kc.imag, row_begin, row_end,
+                                  out.ctypes.data, N, C.byref(rep)), "fill_matrix")
+    return FillReport.from_c(rep)
+
+
 def fill_matrix(mesh: TriangleMesh, spec: QuadratureSpec, mode: Mode, medium: Medium = Medium(),
                 cfg: SamplingConfig | None = None, kind: KernelKind = KernelKind.GreenOverR,
                 ctx: Context | None = None, out: np.ndarray | None = None):

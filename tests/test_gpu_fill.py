@@ -186,3 +186,13 @@ def test_mesh_validation(gk):
     bad = gk.TriangleMesh(mesh.vertices, np.array([[0, 1, 99]]))
     with pytest.raises(gk.InvalidArgument):
         gk.DeviceMesh(bad, gk.QuadratureSpec(4, 3))
+
+
+def test_fill_rows_host_matches_device(gk):
+    mesh = sphere(gk, 2)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    zd, rep_d = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi, row_begin=5, row_end=301)
+    zh = np.zeros((296, dm.N), np.complex128)
+    rep_h = gk.fill_rows_host(dm, gk.Mode.DIRECT, zh, k=2 * np.pi, row_begin=5, row_end=301)
+    assert np.array_equal(zh, zd.cpu().numpy())
+    assert rep_h.actual_calls == rep_d.actual_calls

@@ -1,0 +1,90 @@
+"""The N > 1 path of bench.py on CPU (gloo, world_size 2), with the oracle as
+the per-rank compute: each rank takes bench.rows_of(rank, world, N), computes
+its K1 distance range, one 16-byte all-reduce (MIN of {r_min, -r_max}) gives
+the global range, every rank builds the identical plan from it, fills its own
+rows, and the union of the row blocks equals the single-process fill bit for
+bit (the GPU-side union property is tests/test_gpu_fill.py)."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from oracle.pyoracle import DIRECT, TABLE, Oracle, SamplingConfig
+    o = Oracle()
+    v, t = o.sphere_mesh(1.0, 1)
+    v = o.jitter(v, 1901, 1e-3)
+    N = t.shape[0]
+    rb, re = bench.rows_of(rank, world, N)
+    lo, hi = o.distance_range(v, t, 6, 4, rb, re)
+    rng = torch.tensor([lo, -hi], dtype=torch.float64)
+    dist.all_reduce(rng, op=dist.ReduceOp.MIN)
+    glo, ghi = float(rng[0]), -float(rng[1])
+    plan = o.build_plan(SamplingConfig(r_min=glo, r_max=ghi, samples_per_wavelength=2000))
+    digest = torch.tensor([float(plan.abscissae.size), float(plan.abscissae.sum())],
+                          dtype=torch.float64)
+    digests = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(digests, digest)
+    ev = o.evaluator(plan, 2 * math.pi)
+    zt, rept = o.fill_rows(v, t, 6, 4, TABLE, 2 * math.pi, ev=ev, row_begin=rb, row_end=re)
+    zd, repd = o.fill_rows(v, t, 6, 4, DIRECT, 2 * math.pi, row_begin=rb, row_end=re)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), zt=zt, zd=zd, rb=rb, re=re, lo=glo, hi=ghi,
+             digests=torch.stack(digests).numpy(), calls=rept.actual_calls,
+             fb=rept.fallback_calls)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_row_sharding_matches_single_process(tmp_path, oracle):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    parts = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    v, t = oracle.sphere_mesh(1.0, 1)
+    v = oracle.jitter(v, 1901, 1e-3)
+    N = t.shape[0]
+    lo, hi = oracle.distance_range(v, t, 6, 4)
+    for p in parts:   # the all-reduced range is the global one, on every rank
+        assert float(p["lo"]) == lo and float(p["hi"]) == hi
+        assert np.array_equal(p["digests"][0], p["digests"][1])  # identical tables
+    assert int(parts[0]["rb"]) == 0 and int(parts[0]["re"]) == int(parts[1]["rb"])
+    assert int(parts[1]["re"]) == N
+    from oracle.pyoracle import DIRECT, TABLE, SamplingConfig
+    plan = oracle.build_plan(SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=2000))
+    ev = oracle.evaluator(plan, 2 * math.pi)
+    zt, _ = oracle.fill_rows(v, t, 6, 4, TABLE, 2 * math.pi, ev=ev, threads=4)
+    zd, _ = oracle.fill_rows(v, t, 6, 4, DIRECT, 2 * math.pi, threads=4)
+    assert np.array_equal(np.concatenate([p["zt"] for p in parts]), zt)
+    assert np.array_equal(np.concatenate([p["zd"] for p in parts]), zd)
+    assert sum(int(p["calls"]) for p in parts) == 3 * 6 * 4 * N * (N - 1)
+    assert all(int(p["fb"]) == 0 for p in parts)
+
+
+@pytest.mark.parametrize("world,N", [(1, 1280), (2, 1280), (8, 81920), (3, 80), (8, 20)])
+def test_rows_of_partitions_exactly(world, N):
+    import bench
+    blocks = [bench.rows_of(r, world, N) for r in range(world)]
+    covered = [i for b, e in blocks for i in range(b, e)]
+    assert covered == list(range(N))
+    chunk = (N + world - 1) // world    # matfill.hpp:211-215
+    assert all(e - b <= chunk for b, e in blocks)
