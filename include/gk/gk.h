@@ -126,6 +126,12 @@ gk_status gk_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double
                         double k_im, const double* radii, size_t n, gk_c128* out,
                         uint64_t* fallbacks);
 
+/* gk_eval_batch from HOST buffers (radii[n] in, out[n] back): the FFI-friendly
+   form of KernelEvaluator::eval_batch; copies through device memory. */
+gk_status gk_eval_batch_host(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,
+                             double k_im, const double* radii, size_t n, gk_c128* out,
+                             uint64_t* fallbacks);
+
 /* ------------------------------------------------------------------- mesh */
 /* Uploads a triangle mesh (host arrays: xyz-interleaved vertices[3 nv],
    triangles[3 nt]) and generates its quadrature points on the device:

@@ -1,0 +1,219 @@
+// gk.hpp -- header-only C++20 adapter over the C ABI (gk.h), shaped like the
+// reference library `gktab` (/root/reference/proj/include/gktab/) so code
+// written against it switches by changing the namespace and the evaluator:
+//
+//   gktab::KernelEvaluator ev(build_plan(cfg, medium), k);      // CPU tables
+//   auto [Z, rep] = gktab::fill_matrix(mesh, spec, gktab::TableKernel{&ev}, kind);
+// becomes
+//   gk::Context ctx;                                            // one B200
+//   gk::DeviceEvaluator ev(ctx, cfg, medium);                   // tables built on the GPU
+//   auto [Z, rep] = gk::fill_matrix(ctx, mesh, spec, gk::Mode::Table, medium, cfg, kind);
+//
+// Status codes are rethrown as the reference's exception types
+// (std::invalid_argument, std::domain_error, std::out_of_range,
+// std::overflow_error, std::runtime_error).  Link with -lgk.
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gk/gk.h"
+
+namespace gk {
+
+using Complex = std::complex<double>;
+static_assert(sizeof(Complex) == sizeof(gk_c128), "gk_c128 must match std::complex<double>");
+
+enum class KernelKind : std::uint8_t { PlainExp = GK_KIND_EXP, GreenOverR = GK_KIND_GREEN };
+enum class Mode { Direct = GK_MODE_DIRECT, Table = GK_MODE_TABLE };
+
+inline void check(gk_status s) {
+  switch (s) {
+    case GK_OK: return;
+    case GK_ERR_INVALID_ARGUMENT: throw std::invalid_argument(gk_last_error());
+    case GK_ERR_DOMAIN: throw std::domain_error(gk_last_error());
+    case GK_ERR_OUT_OF_RANGE: throw std::out_of_range(gk_last_error());
+    case GK_ERR_OVERFLOW: throw std::overflow_error(gk_last_error());
+    default: throw std::runtime_error(gk_last_error());
+  }
+}
+
+// gktab::Medium (kernel.hpp:25-38) + lossy extension
+struct Medium {
+  double lambda0 = 1.0, eps_r = 1.0, mu_r = 1.0, eps_r_im = 0.0;
+  gk_medium c() const { return {lambda0, eps_r, mu_r, eps_r_im}; }
+};
+
+// gktab::SamplingConfig (sampling.hpp:18-45), same defaults
+struct SamplingConfig {
+  double r_min = 1e-4, r_max = 1.0;
+  int samples_per_wavelength = 1000;
+  int refine_interval_divisor = 2;
+  double refine_halfwidth_in_t = 2.0;
+  double dedup_fraction = 0.5;
+  bool refine = true;
+  gk_sampling_config c() const {
+    return {r_min, r_max, samples_per_wavelength, refine_interval_divisor, refine_halfwidth_in_t,
+            dedup_fraction, refine ? 1 : 0};
+  }
+};
+
+// gktab::QuadratureSpec (quadrature.hpp:15-26)
+struct QuadratureSpec {
+  int outer_points = 4;
+  int inner_points_per_edge = 3;
+};
+
+// gktab::TriangleMesh (mesh.hpp:33-58), flattened xyz / index triples
+struct TriangleMesh {
+  std::vector<double> vertices;
+  std::vector<std::uint32_t> triangles;
+  std::size_t triangle_count() const { return triangles.size() / 3; }
+};
+
+// gktab::KernelMatrix (matfill.hpp:24-31)
+struct KernelMatrix {
+  std::size_t n = 0;
+  std::vector<Complex> z;
+  explicit KernelMatrix(std::size_t size = 0) : n(size), z(size * size) {}
+  Complex& at(std::size_t p, std::size_t q) { return z[p * n + q]; }
+  const Complex& at(std::size_t p, std::size_t q) const { return z[p * n + q]; }
+};
+
+// gktab::FillReport (matfill.hpp:33-47), the fields fill_matrix sets
+struct FillReport {
+  std::size_t N = 0;
+  int m = 0, n = 0;
+  std::uint64_t predicted_calls = 0, actual_calls = 0, fallback_calls = 0;
+  double wall_time_s = 0.0;
+  static FillReport from(const gk_fill_report& r) {
+    return {static_cast<std::size_t>(r.N), r.m, r.n, r.predicted_calls, r.actual_calls,
+            r.fallback_calls, r.wall_time_s};
+  }
+};
+
+inline double wavenumber(const Medium& m) {
+  double re = 0, im = 0;
+  const gk_medium c = m.c();
+  check(gk_wavenumber(&c, &re, &im));
+  return re;
+}
+
+inline std::uint64_t predicted_calls(std::uint64_t N, std::uint64_t m, std::uint64_t n) {
+  std::uint64_t out = 0;
+  check(gk_predicted_calls(N, m, n, &out));
+  return out;
+}
+
+// generate_sphere_mesh (mesh.hpp:154-202), bit-identical
+inline TriangleMesh generate_sphere_mesh(double radius, int subdivisions) {
+  std::size_t nv = 0, nt = 0;
+  check(gk_sphere_mesh(radius, subdivisions, nullptr, &nv, nullptr, &nt));
+  TriangleMesh m;
+  m.vertices.resize(3 * nv);
+  m.triangles.resize(3 * nt);
+  check(gk_sphere_mesh(radius, subdivisions, m.vertices.data(), &nv, m.triangles.data(), &nt));
+  return m;
+}
+
+// one B200 (RAII over gk_ctx)
+class Context {
+ public:
+  explicit Context(int device = 0) { check(gk_ctx_create(device, &h_)); }
+  ~Context() { gk_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  gk_ctx* get() const { return h_; }
+  void set_stream(void* cuda_stream) { check(gk_ctx_set_stream(h_, cuda_stream)); }
+
+ private:
+  gk_ctx* h_ = nullptr;
+};
+
+// gktab::KernelEvaluator (evaluator.hpp:102-309) with its tables on the GPU
+class DeviceEvaluator {
+ public:
+  DeviceEvaluator(Context& ctx, const SamplingConfig& cfg, const Medium& medium = {},
+                  int lagrange_degree = 3)
+      : ctx_(&ctx) {
+    const gk_sampling_config c = cfg.c();
+    const gk_medium m = medium.c();
+    check(gk_table_build(ctx.get(), &c, &m, lagrange_degree, &h_));
+    check(gk_table_info_get(h_, &info_));
+  }
+  ~DeviceEvaluator() { gk_table_destroy(h_); }
+  DeviceEvaluator(const DeviceEvaluator&) = delete;
+  DeviceEvaluator& operator=(const DeviceEvaluator&) = delete;
+
+  const gk_table_info& info() const { return info_; }
+  gk_table* get() const { return h_; }
+  double k() const { return info_.k_re; }
+  int lagrange_degree() const { return info_.degree; }
+  std::uint64_t fallback_count() const { return fallbacks_; }
+
+  // eval_batch (evaluator.hpp:209-221): host in, host out
+  std::vector<Complex> eval_batch(KernelKind kind, std::span<const double> radii) const {
+    std::vector<Complex> out(radii.size());
+    std::uint64_t fb = 0;
+    check(gk_eval_batch_host(ctx_->get(), h_, static_cast<gk_kind>(kind), 0.0, 0.0,
+                             radii.data(), radii.size(), reinterpret_cast<gk_c128*>(out.data()),
+                             &fb));
+    fallbacks_ += fb;
+    return out;
+  }
+  Complex eval_kernel(KernelKind kind, double r) const {
+    return eval_batch(kind, std::span<const double>(&r, 1))[0];
+  }
+  Complex eval_exp(double r) const { return eval_kernel(KernelKind::PlainExp, r); }
+  Complex eval_green(double r) const { return eval_kernel(KernelKind::GreenOverR, r); }
+
+  std::vector<double> abscissae() const {
+    std::vector<double> a(info_.nodes);
+    check(gk_table_download(h_, a.data(), nullptr, nullptr, nullptr, nullptr));
+    return a;
+  }
+  std::vector<double> zero_locations() const {
+    std::vector<double> z(info_.zeros);
+    check(gk_table_download(h_, nullptr, z.data(), nullptr, nullptr, nullptr));
+    return z;
+  }
+  std::vector<Complex> green_values() const {
+    std::vector<Complex> g(info_.nodes);
+    check(gk_table_download(h_, nullptr, nullptr, nullptr, reinterpret_cast<gk_c128*>(g.data()),
+                            nullptr));
+    return g;
+  }
+
+ private:
+  Context* ctx_;
+  gk_table* h_ = nullptr;
+  gk_table_info info_{};
+  mutable std::uint64_t fallbacks_ = 0;
+};
+
+// fill_matrix<Kernel> (matfill.hpp:144-228) on the GPU, host mesh in, host
+// matrix out.  Table mode: cfg.r_min / r_max <= 0 selects the device-computed
+// quadrature-pair distance range.
+inline std::pair<KernelMatrix, FillReport> fill_matrix(
+    Context& ctx, const TriangleMesh& mesh, const QuadratureSpec& spec, Mode mode,
+    const Medium& medium = {}, SamplingConfig cfg = SamplingConfig{0.0, 0.0},
+    KernelKind kind = KernelKind::GreenOverR) {
+  const std::size_t N = mesh.triangle_count();
+  KernelMatrix z(N);
+  gk_fill_report rep{};
+  const gk_sampling_config c = cfg.c();
+  const gk_medium m = medium.c();
+  check(gk_fill_matrix_host(ctx.get(), mesh.vertices.data(), mesh.vertices.size() / 3,
+                            mesh.triangles.data(), N, spec.outer_points,
+                            spec.inner_points_per_edge, static_cast<gk_mode>(mode), &c, &m,
+                            static_cast<gk_kind>(kind), reinterpret_cast<gk_c128*>(z.z.data()),
+                            &rep));
+  return {std::move(z), FillReport::from(rep)};
+}
+
+}  // namespace gk

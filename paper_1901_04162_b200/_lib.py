@@ -100,6 +100,8 @@ PROTOTYPES = {
     "gk_table_download": [_vp, _vp, _vp, _vp, _vp, _vp],
     "gk_table_destroy": [_vp],
     "gk_eval_batch": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp, _u64p],
+    "gk_eval_batch_host": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp,
+                           _u64p],
     "gk_mesh_create": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.POINTER(_vp)],
     "gk_mesh_points_download": [_vp, _vp, _vp],
     "gk_mesh_destroy": [_vp],

@@ -74,7 +74,24 @@ def build(verbose: bool = False, force: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    build_cpp_test()
     return LIB
+
+
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_adapter.cpp")
+CPP_TEST_BIN = os.path.join(OBJ, "test_adapter")
+
+
+def build_cpp_test() -> str:
+    """The C++ adapter test (include/gk/gk.hpp over libgk.so), host g++ only."""
+    deps = [CPP_TEST_SRC, LIB, os.path.join(ROOT, "include", "gk", "gk.hpp")]
+    if _newer(deps, CPP_TEST_BIN):
+        cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), CPP_TEST_SRC,
+               "-o", CPP_TEST_BIN, "-L", PKG, "-lgk", "-Wl,-rpath,$ORIGIN/.."]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed for test_adapter:\n{r.stderr}")
+    return CPP_TEST_BIN
 
 
 if __name__ == "__main__":

@@ -286,6 +286,34 @@ gk_status gk_eval_batch(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
   });
 }
 
+gk_status gk_eval_batch_host(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
+                             double k_im, const double* radii, size_t n, gk_c128* out,
+                             uint64_t* fallbacks) {
+  double* dr = nullptr;
+  gk_c128* dout = nullptr;
+  gk_status st = guarded([&] {
+    check_ctx(c);
+    if (fallbacks) *fallbacks = 0;
+    if (n == 0) return;
+    need(radii && out, GK_ERR_INVALID_ARGUMENT, "null buffer");
+    use_device(c);
+    GK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dr), n * sizeof(double), c->stream));
+    GK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), n * sizeof(gk_c128), c->stream));
+    GK_CUDA(cudaMemcpyAsync(dr, radii, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  });
+  if (st == GK_OK && n) {
+    st = gk_eval_batch(c, t, kind, k_re, k_im, dr, n, dout, fallbacks);
+    if (st == GK_OK)
+      st = guarded([&] {
+        GK_CUDA(cudaMemcpyAsync(out, dout, n * sizeof(gk_c128), cudaMemcpyDeviceToHost, c->stream));
+        GK_CUDA(cudaStreamSynchronize(c->stream));
+      });
+  }
+  if (dr) cudaFreeAsync(dr, c->stream);
+  if (dout) cudaFreeAsync(dout, c->stream);
+  return st;
+}
+
 gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32_t* tris,
                          size_t nt, int m, int n, gk_mesh** out) {
   return guarded([&] {

@@ -1,0 +1,110 @@
+// FP64 issue-ceiling microbenchmarks on B200 (standalone; not part of libgk).
+//   A: DFMA chains with constant operands (gk_bench_fp64_peak style)
+//   B: DFMA chains with 3 distinct register operands
+//   C: the fill's mix per "eval": 16 DFMA + 8 DMUL + 3 DADD, register operands
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_mix fp64_mix.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int K = 8;
+
+__global__ void __launch_bounds__(256) kA(double* sink, int iters, double b, double c) {
+  double a[K];
+  for (int k = 0; k < K; ++k) a[k] = 1.0 + 1e-9 * (threadIdx.x + k);
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int k = 0; k < K; ++k) a[k] = __fma_rn(a[k], b, c);
+  double s = 0;
+  for (int k = 0; k < K; ++k) s += a[k];
+  if (s == 1234.5) sink[0] = s;
+}
+
+__global__ void __launch_bounds__(256) kB(double* sink, int iters, const double* in) {
+  double a[K], b[K], c[K];
+  for (int k = 0; k < K; ++k) {
+    a[k] = in[threadIdx.x % 32 + k];
+    b[k] = in[threadIdx.x % 32 + k + 8] * 1e-9 + 0.9999999;
+    c[k] = in[threadIdx.x % 32 + k + 16] * 1e-12;
+  }
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int k = 0; k < K; ++k) a[k] = __fma_rn(a[k], b[(k + u) % K], c[(k + 3 * u) % K]);
+  double s = 0;
+  for (int k = 0; k < K; ++k) s += a[k];
+  if (s == 1234.5) sink[0] = s;
+}
+
+// 27 FP64 ops shaped like one direct eval, 6 independent "evals" per iteration
+__global__ void __launch_bounds__(256, 2) kC(double* sink, int iters, const double* in) {
+  double x[6], acc[6];
+  for (int k = 0; k < 6; ++k) { x[k] = in[threadIdx.x % 32 + k] * 1e-3 + 0.5; acc[k] = 0; }
+  double px = in[1], py = in[2], pz = in[3], w = in[4];
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int o = 0; o < 6; ++o) {
+      double dx = x[o] - px, dy = x[(o + 1) % 6] - py, dz = x[(o + 2) % 6] - pz;   // 3 DADD
+      double d2 = __fma_rn(dz, dz, __fma_rn(dy, dy, __dmul_rn(dx, dx)));          // 3
+      double y = d2 * 0.7;                                                         // 1
+      double e = __fma_rn(-d2, __dmul_rn(y, y), 1.0);                              // 2
+      double ye = __dmul_rn(y, e);                                                 // 1
+      y = __fma_rn(ye, __fma_rn(0.375, e, 0.5), y);                                // 2
+      double r = __dmul_rn(d2, y);                                                 // 1
+      double t = __fma_rn(r, 13.7, 6755399441055744.0);                            // 1
+      double nf = t - 6755399441055744.0;                                          // 1
+      double f = __fma_rn(r, 13.7, -nf);                                           // 1
+      double g = __dmul_rn(f, f);                                                  // 1
+      double v = __dmul_rn(g, __fma_rn(1e-9, g, -1e-6));                           // 2
+      double s = __dmul_rn(f, __fma_rn(-1e-10, g, 1.5e-3));                        // 2
+      double c = __fma_rn(-y, s, __fma_rn(x[o], v, x[o]));                         // 2
+      double sn = __fma_rn(x[o], s, __fma_rn(y, v, y));                            // 2
+      double wg = __dmul_rn(w, y);                                                 // 1
+      acc[o] = __fma_rn(wg, c, acc[o]);                                            // 1
+      acc[(o + 3) % 6] = __fma_rn(-wg, sn, acc[(o + 3) % 6]);                      // 1
+    }
+    px += 1e-12; py -= 1e-12;
+  }
+  double s = 0;
+  for (int k = 0; k < 6; ++k) s += acc[k];
+  if (s == 1234.5) sink[0] = s;
+}
+
+int main() {
+  double *sink, *in;
+  cudaMalloc(&sink, 8);
+  cudaMalloc(&in, 64 * 8);
+  double h[64];
+  for (int i = 0; i < 64; ++i) h[i] = 0.1 + 0.01 * i;
+  cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+  int sm = 0;
+  cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto run = [&](const char* name, auto launch, double ops_per_thread_iter, int blocks_per_sm, int iters) {
+    launch(sm * blocks_per_sm, iters / 4);
+    cudaEventRecord(e0);
+    launch(sm * blocks_per_sm, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double lane_ops = double(sm) * blocks_per_sm * 256 * double(iters) * ops_per_thread_iter;
+    std::printf("%s: %.2f ms, %.1f FP64 lane-ops/clk/SM @ 1.965 GHz (%.1f%% of 64)\n", name, ms,
+                lane_ops / (ms * 1e-3) / sm / 1.965e9, 100.0 * lane_ops / (ms * 1e-3) / sm / 1.965e9 / 64);
+  };
+  for (int bps : {2, 4, 8}) {
+    char nm[64];
+    std::snprintf(nm, 64, "A const-operand DFMA  (%d CTA/SM)", bps);
+    run(nm, [&](int g, int it) { kA<<<g, 256>>>(sink, it, 0.9999999, 1e-7); }, 16.0 * K, bps, 2048);
+    std::snprintf(nm, 64, "B 3-register DFMA     (%d CTA/SM)", bps);
+    run(nm, [&](int g, int it) { kB<<<g, 256>>>(sink, it, in); }, 16.0 * K, bps, 2048);
+  }
+  run("C fill-shaped mix 27 ops (2 CTA/SM)", [&](int g, int it) { kC<<<g, 256>>>(sink, it, in); }, 6 * 27.0 + 2, 2, 8192);
+  cudaDeviceSynchronize();
+  std::printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

@@ -1,0 +1,98 @@
+// C++ host-side test of the drop-in adapter (include/gk/gk.hpp) on a B200.
+// Mirrors reference tests through the C ABI:
+//   * CLI bench row prefix "20,4,3,14400,13680,0" (test_cli.cpp:176-189),
+//   * reference-config zeros {0.25, 0.5, 0.75, 1} (test_sampling.cpp:42-49),
+//   * node reproduction (test_evaluator.cpp:24-31),
+//   * exception types (test_evaluator.cpp:83-91, test_matfill.cpp:23-26, 183-191),
+//   * table fill vs direct fill agreement (acceptance criterion 5 gate, 1e-4).
+// Built by __graft_entry__.build(); run by tests/test_gpu_cpp.py.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "gk/gk.hpp"
+
+static int failures = 0;
+#define CHECK(c)                                                        \
+  do {                                                                  \
+    if (!(c)) {                                                         \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);          \
+      ++failures;                                                       \
+    }                                                                   \
+  } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+int main() {
+  gk::Context ctx(0);
+
+  // bench row prefix on the 20-triangle icosphere, m = 4, n = 3
+  const auto mesh20 = gk::generate_sphere_mesh(0.5, 0);
+  {
+    auto [z, rep] = gk::fill_matrix(ctx, mesh20, {4, 3}, gk::Mode::Table, gk::Medium{});
+    CHECK(rep.N == 20 && rep.m == 4 && rep.n == 3);
+    CHECK(rep.predicted_calls == 14400 && rep.actual_calls == 13680 && rep.fallback_calls == 0);
+    CHECK(z.at(0, 0) == gk::Complex(0.0, 0.0));
+  }
+
+  // reference configuration: forced zeros and node reproduction
+  gk::DeviceEvaluator ev(ctx, gk::SamplingConfig{});
+  {
+    const auto z = ev.zero_locations();
+    CHECK(z.size() == 4 && z[0] == 0.25 && z[1] == 0.5 && z[2] == 0.75 && z[3] == 1.0);
+    const auto a = ev.abscissae();
+    const auto g = ev.green_values();
+    const auto v = ev.eval_batch(gk::KernelKind::GreenOverR, a);
+    bool exact = true;
+    for (std::size_t j = 0; j < a.size(); ++j) exact = exact && v[j] == g[j];
+    CHECK(exact);
+    CHECK(ev.eval_kernel(gk::KernelKind::GreenOverR, 5e-5) != gk::Complex(0, 0));
+    CHECK(ev.fallback_count() == 1);  // r < r_min: analytic fallback, counted
+  }
+
+  // exception types
+  CHECK(throws<std::invalid_argument>([&] { ev.eval_green(1.5); }));  // eval_batch rethrows
+  CHECK(throws<std::overflow_error>([] { gk::predicted_calls(1ull << 32, 1ull << 16, 1ull << 16); }));
+  CHECK(throws<std::invalid_argument>(
+      [&] { gk::fill_matrix(ctx, mesh20, {5, 1}, gk::Mode::Direct, gk::Medium{}); }));
+  CHECK(throws<std::invalid_argument>([] { gk::generate_sphere_mesh(1.0, 7); }));
+  CHECK(throws<std::invalid_argument>([&] {
+    gk::SamplingConfig bad;
+    bad.r_min = 0.1;
+    bad.r_max = 0.1 + 1.5e-3;
+    gk::DeviceEvaluator e2(ctx, bad);
+  }));
+
+  // table fill vs direct fill, N = 320 (acceptance criterion 5 shape)
+  {
+    const auto mesh = gk::generate_sphere_mesh(0.5, 2);
+    gk::SamplingConfig cfg{0.0, 0.0};
+    cfg.samples_per_wavelength = 10000;
+    auto [zt, rt] = gk::fill_matrix(ctx, mesh, {4, 3}, gk::Mode::Table, gk::Medium{}, cfg);
+    auto [zd, rd] = gk::fill_matrix(ctx, mesh, {4, 3}, gk::Mode::Direct, gk::Medium{});
+    double worst = 0.0;
+    for (std::size_t p = 0; p < zt.n; ++p)
+      for (std::size_t q = 0; q < zt.n; ++q) {
+        if (p == q) continue;
+        const gk::Complex a = zd.at(p, q), b = zt.at(p, q);
+        if (a.real() != 0) worst = std::fmax(worst, std::fabs(b.real() - a.real()) / std::fabs(a.real()));
+        if (a.imag() != 0) worst = std::fmax(worst, std::fabs(b.imag() - a.imag()) / std::fabs(a.imag()));
+      }
+    CHECK(worst <= 1e-4);
+    CHECK(rt.actual_calls == 3ull * 4 * 3 * 320 * 319 && rd.actual_calls == rt.actual_calls);
+    std::printf("N=320 table vs direct: max elementwise relative error %.3g\n", worst);
+  }
+  std::printf("%s (%d failure(s))\n", failures ? "FAILED" : "ALL OK", failures);
+  return failures ? 1 : 0;
+}
