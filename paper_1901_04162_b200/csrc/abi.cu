@@ -332,6 +332,14 @@ gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32
       mesh->nv = nv;
       mesh->m = m;
       mesh->n = n;
+      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (size_t i = 0; i < nv; ++i)
+        for (int c3 = 0; c3 < 3; ++c3) {
+          lo[c3] = std::fmin(lo[c3], verts[3 * i + c3]);
+          hi[c3] = std::fmax(hi[c3], verts[3 * i + c3]);
+        }
+      mesh->diameter = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                                 (hi[2] - lo[2]) * (hi[2] - lo[2])) * (1.0 + 1e-12);
       mesh->outer.alloc(nt * m, c->stream);
       mesh->inner.alloc(nt * 3 * static_cast<size_t>(n), c->stream);
       mesh->bounds.alloc(nt, c->stream);

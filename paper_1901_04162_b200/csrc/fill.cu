@@ -25,6 +25,8 @@ constexpr int kRowsPerTile = 8;  // one row per warp
 constexpr int kMaxColBlocks = 32;  // 32-column blocks per tile (adaptive, see launch_fill)
 constexpr int kThreads = 32 * kRowsPerTile;
 
+__global__ void atten_kernel(double* E, int n);
+
 struct FillArgs {
   const double4* outer;
   const double4* inner;
@@ -38,6 +40,9 @@ struct FillArgs {
   TableDev T;
   const double2* phase;
   double K1, k_re, k_im;
+  const double* atten;  // lossy: exp(-n / 512), n < natten
+  int natten;
+  double KA;            // -k_im * 512
   unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max
 };
 
@@ -66,9 +71,12 @@ struct InnerWalk {
 // CTAs (24 warps) per SM to hide the FP64 dependency latency.
 template <int MO, int KIND, bool LOSSY, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A) {
-  extern __shared__ double2 tab[];  // kPhaseM phase entries (64 KB)
+  extern __shared__ double2 tab[];  // kPhaseM phase entries (64 KB) [+ attenuation table]
   __shared__ double so[kRowsPerTile][MO][4];
   for (int i = threadIdx.x; i < kPhaseM; i += blockDim.x) tab[i] = A.phase[i];
+  double* att = reinterpret_cast<double*>(tab + kPhaseM);
+  if constexpr (LOSSY)
+    for (int i = threadIdx.x; i < A.natten; i += blockDim.x) att[i] = A.atten[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t N = A.N;
@@ -119,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
         const double r = __dmul_rn(d2, y);
         const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
         double wgt = KIND == GK_KIND_GREEN ? __dmul_rn(pzw.y, y) : pzw.y;
-        if constexpr (LOSSY) wgt *= exp(A.k_im * r);
+        if constexpr (LOSSY) wgt = __dmul_rn(wgt, atten_table(r, A.KA, att, A.natten));
         acc[o].x = __fma_rn(wgt, cs.x, acc[o].x);
         acc[o].y = __fma_rn(-wgt, cs.y, acc[o].y);
       }
@@ -252,10 +260,11 @@ void launch_one(gk_ctx* ctx, const FillArgs& a) {
       const char* e = std::getenv("GK_DIRECT_MINB");
       return e ? std::atoi(e) : 2;
     }();
+    const size_t smem = kPhaseM * sizeof(double2) + (LOSSY ? a.natten * sizeof(double) : 0);
     if (minb == 2)
-      launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 2>, a, kPhaseM * sizeof(double2));
+      launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 2>, a, smem);
     else
-      launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 3>, a, kPhaseM * sizeof(double2));
+      launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 3>, a, smem);
   }
   else
     launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
@@ -308,6 +317,20 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.k_im = k_im;
   a.counters = counters;
   if (a.ntiles == 0) return;
+  DevBuf<double> atten;
+  if (mode == GK_MODE_DIRECT && k_im != 0.0) {
+    if (!(k_im < 0.0)) fail(GK_ERR_INVALID_ARGUMENT, "lossy medium needs Im k < 0 (attenuation)");
+    // radii are bounded by the mesh's bounding-box diagonal
+    const double xmax = -k_im * mesh->diameter * kAttenScale;
+    if (!(xmax < 8000.0))
+      fail(GK_ERR_INVALID_ARGUMENT, "lossy fill: attenuation exp(Im k r) range too large for the device table");
+    a.natten = static_cast<int>(xmax) + 3;
+    a.KA = -k_im * kAttenScale;
+    atten.alloc(a.natten, ctx->stream);
+    atten_kernel<<<(a.natten + 255) / 256, 256, 0, ctx->stream>>>(atten.p, a.natten);
+    GK_CUDA(cudaGetLastError());
+    a.atten = atten.p;
+  }
   const int degree = table ? table->dev.degree : 3;
   const bool lossy = k_im != 0.0;
   switch (mesh->m) {
@@ -318,6 +341,11 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
     case 7: dispatch_mo<7>(ctx, a, mode, kind, degree, lossy); break;
     default: fail(GK_ERR_INVALID_ARGUMENT, "QuadratureSpec: outer_points must be one of 1, 3, 4, 6, 7");
   }
+}
+
+__global__ void atten_kernel(double* E, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) E[i] = exp(-static_cast<double>(i) / kAttenScale);
 }
 
 // ------------------------------------------------------------------- K1

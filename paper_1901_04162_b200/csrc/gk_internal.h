@@ -82,6 +82,7 @@ struct gk_mesh {
   gk_ctx* ctx = nullptr;
   size_t N = 0, nv = 0;
   int m = 0, n = 0;
+  double diameter = 0.0;  // bounding-box diagonal of the vertices (bounds every pair distance)
   gk::DevBuf<double4> outer;  // [N * m]    (x, y, z, w)
   gk::DevBuf<double4> inner;  // [3n][N]    (x, y, z, w), column-major in q
   gk::DevBuf<double4> bounds; // [N]        (cx, cy, cz, rho_outer), rho_inner in binner
