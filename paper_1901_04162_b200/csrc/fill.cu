@@ -147,6 +147,92 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
   }
 }
 
+// K4 fast path (IPT = 3n known at compile time, n = 1..5): the inner-point
+// loop of a column block is fully unrolled with a one-point register
+// prefetch, the outer points live in registers and 12 warps x 1 CTA per SM
+// (~160 registers each) keep the FP64 pipe fed.  Non-FP64 instructions cost
+// an issue cycle each while an FP64 warp instruction holds the 16-lane pipe
+// for two, so this variant's ~9 non-FP64 instructions/eval (vs ~16 in the
+// runtime-IPT kernel) are worth ~12% (ablations: scripts/direct_variants.cu).
+constexpr int kWarpsV4 = 12;
+
+template <int MO, int IPT, int KIND, bool LOSSY>
+__global__ void __launch_bounds__(32 * kWarpsV4, 1) direct_kernel_v4(const FillArgs A) {
+  extern __shared__ double2 tab[];  // kPhaseM phase entries (64 KB) [+ attenuation table]
+  __shared__ double sw[kWarpsV4][MO];
+  for (int i = threadIdx.x; i < kPhaseM; i += blockDim.x) tab[i] = A.phase[i];
+  double* att = reinterpret_cast<double*>(tab + kPhaseM);
+  if constexpr (LOSSY)
+    for (int i = threadIdx.x; i < A.natten; i += blockDim.x) att[i] = A.atten[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t N = A.N;
+  const double4* last = A.inner + (N - 1);
+
+  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
+    const size_t p = A.row_begin + tr * kWarpsV4 + warp;
+    if (p >= A.row_end) continue;  // warp-uniform
+    double ox[MO], oy[MO], oz[MO];
+#pragma unroll
+    for (int o = 0; o < MO; ++o) {
+      const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
+      const double2 zw = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o) + 1);
+      ox[o] = xy.x;
+      oy[o] = xy.y;
+      oz[o] = zw.x;
+      if (lane == 0) sw[warp][o] = zw.y;
+    }
+    __syncwarp();
+    const size_t q0 = tc * (32 * static_cast<size_t>(A.cpt));
+    int nblk = static_cast<int>((N - q0 + 31) / 32);
+    if (nblk > A.cpt) nblk = A.cpt;
+    const double4* colp = A.inner + q0 + lane;  // column block 0, inner point 0
+    double2 cxy, czw;
+    {
+      const double2* ptr = reinterpret_cast<const double2*>(colp <= last ? colp : last);
+      cxy = __ldg(ptr);
+      czw = __ldg(ptr + 1);
+    }
+    for (int cb = 0; cb < nblk; ++cb) {
+      const double4* cp = colp <= last ? colp : last;
+      double2 acc[MO];
+#pragma unroll
+      for (int o = 0; o < MO; ++o) acc[o] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const double2 pxy = cxy, pzw = czw;
+        const double4* np = (i + 1 < IPT) ? cp + (i + 1) * N : (colp + 32 <= last ? colp + 32 : last);
+        cxy = __ldg(reinterpret_cast<const double2*>(np));
+        czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
+#pragma unroll
+        for (int o = 0; o < MO; ++o) {
+          const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
+          const double y = rsqrt_fast(d2);
+          const double r = __dmul_rn(d2, y);
+          const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
+          double wgt = KIND == GK_KIND_GREEN ? __dmul_rn(pzw.y, y) : pzw.y;
+          if constexpr (LOSSY) wgt = __dmul_rn(wgt, atten_table(r, A.KA, att, A.natten));
+          acc[o].x = __fma_rn(wgt, cs.x, acc[o].x);
+          acc[o].y = __fma_rn(-wgt, cs.y, acc[o].y);
+        }
+      }
+      double2 res = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int o = 0; o < MO; ++o) {
+        const double wo = sw[warp][o];
+        res.x = __fma_rn(wo, acc[o].x, res.x);
+        res.y = __fma_rn(wo, acc[o].y, res.y);
+      }
+      const size_t q = q0 + 32 * static_cast<size_t>(cb) + lane;
+      if (q == p) res = make_double2(0.0, 0.0);  // self pairs stay zero (matfill.hpp:178)
+      if (q < N) __stcs(A.z + (p - A.row_begin) * A.ldz + q, res);
+      colp += 32;
+    }
+    __syncwarp();
+  }
+}
+
 // K3: table evaluation (the paper's method) with the reference's fallback.
 template <int MO, int KIND, int DEG>
 __global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
@@ -237,37 +323,63 @@ __global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
 }
 
 template <class K>
-void launch_kernel(gk_ctx* ctx, K kernel, const FillArgs& a, size_t smem) {
+void launch_kernel(gk_ctx* ctx, K kernel, const FillArgs& a, size_t smem, int threads = kThreads) {
   if (smem > 48 * 1024)
     GK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   int per_sm = 0;
-  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
+  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
   if (per_sm < 1) per_sm = 1;
   size_t grid = static_cast<size_t>(ctx->sm_count) * per_sm;
   if (grid > a.ntiles) grid = a.ntiles;
   if (grid < 1) grid = 1;
-  kernel<<<static_cast<unsigned>(grid), kThreads, smem, ctx->stream>>>(a);
+  kernel<<<static_cast<unsigned>(grid), threads, smem, ctx->stream>>>(a);
   GK_CUDA(cudaGetLastError());
 }
 
+// widest tiles (fewest cold starts) that still leave >= 16 tiles per
+// resident CTA for load balance
+void set_tiling(const gk_ctx* ctx, FillArgs& a, int rows_per_tile, int ctas_per_sm) {
+  const size_t row_blocks = (a.row_end - a.row_begin + rows_per_tile - 1) / rows_per_tile;
+  const size_t col_blocks = (a.N + 31) / 32;
+  const size_t want = static_cast<size_t>(ctx->sm_count) * ctas_per_sm * 16;
+  int cpt = kMaxColBlocks;
+  while (cpt > 1 && row_blocks * ((col_blocks + cpt - 1) / cpt) < want) cpt /= 2;
+  a.cpt = cpt;
+  a.ncb = (col_blocks + cpt - 1) / cpt;
+  a.ntiles = row_blocks * a.ncb;
+}
+
+template <int MO, int IPT, int KIND, bool LOSSY>
+void launch_v4(gk_ctx* ctx, FillArgs a, size_t smem) {
+  set_tiling(ctx, a, kWarpsV4, 1);
+  launch_kernel(ctx, direct_kernel_v4<MO, IPT, KIND, LOSSY>, a, smem, 32 * kWarpsV4);
+}
+
 template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
-void launch_one(gk_ctx* ctx, const FillArgs& a) {
-  if constexpr (MODE == GK_MODE_DIRECT)
-  {
-    // occupancy variant (tuning knob; default from the r1 ncu measurements)
-    static const int minb = [] {
-      const char* e = std::getenv("GK_DIRECT_MINB");
-      return e ? std::atoi(e) : 2;
-    }();
+void launch_one(gk_ctx* ctx, FillArgs a) {
+  if constexpr (MODE == GK_MODE_DIRECT) {
     const size_t smem = kPhaseM * sizeof(double2) + (LOSSY ? a.natten * sizeof(double) : 0);
-    if (minb == 2)
-      launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 2>, a, smem);
-    else
-      launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 3>, a, smem);
-  }
-  else
+    static const bool use_v4 = [] {
+      const char* e = std::getenv("GK_DIRECT_V4");
+      return !(e && e[0] == '0');
+    }();
+    if (use_v4) {
+      switch (a.ipt) {  // n = 1..5 Gauss points per edge: fully unrolled fast path
+        case 3: return launch_v4<MO, 3, KIND, LOSSY>(ctx, a, smem);
+        case 6: return launch_v4<MO, 6, KIND, LOSSY>(ctx, a, smem);
+        case 9: return launch_v4<MO, 9, KIND, LOSSY>(ctx, a, smem);
+        case 12: return launch_v4<MO, 12, KIND, LOSSY>(ctx, a, smem);
+        case 15: return launch_v4<MO, 15, KIND, LOSSY>(ctx, a, smem);
+        default: break;
+      }
+    }
+    set_tiling(ctx, a, kRowsPerTile, 2);
+    launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 2>, a, smem);
+  } else {
+    set_tiling(ctx, a, kRowsPerTile, 2);
     launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
+  }
 }
 
 template <int MO>
@@ -298,16 +410,6 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.ipt = 3 * mesh->n;
   a.row_begin = row_begin;
   a.row_end = row_end;
-  // widest tiles (fewest cold starts) that still leave >= 16 tiles per
-  // resident CTA for load balance
-  const size_t row_blocks = (row_end - row_begin + kRowsPerTile - 1) / kRowsPerTile;
-  const size_t col_blocks = (mesh->N + 31) / 32;
-  const size_t want = static_cast<size_t>(ctx->sm_count) * 2 * 16;
-  int cpt = kMaxColBlocks;
-  while (cpt > 1 && row_blocks * ((col_blocks + cpt - 1) / cpt) < want) cpt /= 2;
-  a.cpt = cpt;
-  a.ncb = (col_blocks + cpt - 1) / cpt;
-  a.ntiles = row_blocks * a.ncb;
   a.z = reinterpret_cast<double2*>(z);
   a.ldz = ldz;
   if (table) a.T = table->dev;
@@ -316,7 +418,7 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.k_re = k_re;
   a.k_im = k_im;
   a.counters = counters;
-  if (a.ntiles == 0) return;
+  if (row_end <= row_begin || mesh->N == 0) return;
   DevBuf<double> atten;
   if (mode == GK_MODE_DIRECT && k_im != 0.0) {
     if (!(k_im < 0.0)) fail(GK_ERR_INVALID_ARGUMENT, "lossy medium needs Im k < 0 (attenuation)");
