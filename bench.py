@@ -227,6 +227,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     import paper_1901_04162_b200 as gk
+    from paper_1901_04162_b200._lib import lib as _gk_lib
+    gk_lib = _gk_lib()
 
     ctx = gk.Context.get(local)
     mesh = make_mesh(gk, cfg)
@@ -269,6 +271,8 @@ def main():
         fill_ev.append((e0, e1))
         return table
 
+    launches = {}
+
     def timed(mode, steps, warmup):
         for _ in range(warmup):
             step(mode)
@@ -277,6 +281,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         fill_ev.clear()
+        l0 = gk_lib.gk_launch_count()
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record()
@@ -284,6 +289,7 @@ def main():
             step(mode)
         s1.record()
         torch.cuda.synchronize()
+        launches[mode] = gk_lib.gk_launch_count() - l0
         if world > 1:
             dist.barrier()
         ms = s0.elapsed_time(s1) / steps
@@ -317,15 +323,12 @@ def main():
     chosen = args.mode if args.mode != "auto" else min(results, key=lambda x: results[x]["ms_per_step"])
     main_res = results[chosen]
 
-    # launches in the timed region (this library's kernels only)
-    launches_per_step = 1 if chosen == "direct" else None
-    if chosen == "table":
-        launches_per_step = 2 + 14 + 1  # K1 (2) + K2 build (~14 incl. CUB) + K3
 
     # e2e through the host-buffer C-ABI entry point (gk_fill_matrix_host), rank-local rows
     e2e = None
-    if args.e2e and rank == 0 and world == 1:
-        e2e = run_e2e(gk, ctx, cfg, mesh, spec, medium, chosen, args, total_evals)
+    if args.e2e:
+        e2e = run_e2e(gk, ctx, cfg, mesh, spec, medium, chosen, args, total_evals, rank, world,
+                      rb, re, dist if world > 1 else None)
 
     cpu = None
     if args.cpu_baseline and rank == 0 and world == 1:
@@ -386,7 +389,7 @@ def main():
                      "hbm_write_gbs": fill_bytes / (main_res["fill_kernel_ms"] * 1e-3) / 1e9},
         "modes": results,
         "clocks": clocks,
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches[chosen],
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
@@ -398,24 +401,28 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals):
-    """End to end through the C-ABI host-buffer entry points: each step uploads
-    the host mesh (H2D), generates quadrature points, (TABLE) computes the
-    range and builds the table, fills, and copies every byte of Z to pinned
-    host memory (D2H).  Z fits host RAM up to C3/C4 (gk_fill_matrix_host into
-    a full host matrix); C5's 107 GB is streamed with gk_fill_rows_host into a
-    reused 4 GiB pinned host window (the full matrix does not fit this host's
-    RAM twice, nor the reference's)."""
+def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals, rank, world, rb, re,
+            dist=None):
+    """End to end through the C-ABI host-buffer entry points, at N ranks: each
+    step every rank uploads the host mesh (H2D), generates its quadrature
+    points, (TABLE) computes its range, all-reduces it and builds the table,
+    fills its row block and copies every byte of it to pinned host memory
+    (D2H).  At N = 1 a Z that fits host RAM (C2-C4) goes through
+    gk_fill_matrix_host into a full host matrix; larger row blocks (C5: 107 GB
+    / N) are streamed with gk_fill_rows_host into a reused 4 GiB pinned host
+    window (the full matrix does not fit this host's RAM twice, nor the
+    reference's).  Time = max over ranks."""
     import torch
     N = mesh.triangle_count()
-    nbytes = N * N * 16
-    full = nbytes <= (16 << 30)
-    rows_win = N if full else max(1, (4 << 30) // (N * 16))
+    rows = re - rb
+    nbytes = rows * N * 16
+    full = world == 1 and nbytes <= (16 << 30)
+    rows_win = max(1, min(rows, (4 << 30) // (N * 16)))
     try:
-        zh = torch.empty((rows_win, N), dtype=torch.complex128, pin_memory=True)
+        zh = torch.empty((rows_win if not full else N, N), dtype=torch.complex128, pin_memory=True)
     except RuntimeError as exc:
         return {"value": None, "unit": "evals/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": nbytes, "note": f"pinned host buffer unavailable: {exc}"}
+                "d2h_bytes_per_step": N * N * 16, "note": f"pinned host buffer unavailable: {exc}"}
     z = zh.numpy()
     m = gk.Mode.TABLE if mode == "table" else gk.Mode.DIRECT
     k = gk.wavenumber(medium)
@@ -428,26 +435,36 @@ def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals):
         dm = gk.DeviceMesh(mesh, spec, ctx)
         t = None
         if m == gk.Mode.TABLE:
-            lo, hi = dm.distance_range()
+            lo, hi = dm.distance_range(rb, re) if rows else (math.inf, 0.0)
+            if world > 1:
+                tt = torch.tensor([lo, -hi], dtype=torch.float64, device=f"cuda:{ctx.device}")
+                dist.all_reduce(tt, op=dist.ReduceOp.MIN)
+                lo, hi = float(tt[0]), -float(tt[1])
             t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
                                                  samples_per_wavelength=args.S), medium, ctx=ctx)
-        for rb in range(0, N, rows_win):
-            re = min(N, rb + rows_win)
-            gk.fill_rows_host(dm, m, z, table=t, k=k, row_begin=rb, row_end=re)
+        for b in range(rb, re, rows_win):
+            gk.fill_rows_host(dm, m, z, table=t, k=k, row_begin=b, row_end=min(re, b + rows_win))
 
     step()  # warm-up
-    steps = max(1, min(args.steps, 2 if not full else 3))
+    steps = max(1, min(args.steps, 3))
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
     dt = (time.perf_counter() - t0) / steps
-    h2d = mesh.vertices.nbytes + mesh.triangles.nbytes
+    if world > 1:
+        tt = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{ctx.device}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt[0])
+    h2d = (mesh.vertices.nbytes + mesh.triangles.nbytes) * world
     return {"value": total_evals / dt, "unit": "evals/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(nbytes), "ms_per_step": dt * 1e3,
+            "d2h_bytes_per_step": int(N * N * 16), "ms_per_step": dt * 1e3,
             "api": ("gk_fill_matrix_host -> full pinned host Z" if full else
-                    f"gk_mesh_create + gk_fill_rows_host x{(N + rows_win - 1) // rows_win} "
-                    f"-> {rows_win}-row pinned host window")}
+                    f"per rank: gk_mesh_create + gk_fill_rows_host x{(rows + rows_win - 1) // rows_win}"
+                    f" -> {rows_win}-row pinned host window"),
+            "timing": "host wall clock per step, max over ranks"}
 
 
 def run_vs_n(gk, ctx, mode, args):

@@ -126,6 +126,13 @@ gk_status gk_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double
                         double k_im, const double* radii, size_t n, gk_c128* out,
                         uint64_t* fallbacks);
 
+/* locate (table.hpp:87-102) on the device: for each radius the bracketing
+   interval j with a_j <= r < a_{j+1} (r = r_max maps to nodes-2).  radii and
+   out are device pointers; a radius outside [r_min, r_max] fails with
+   GK_ERR_OUT_OF_RANGE naming the first such index. */
+gk_status gk_locate(gk_ctx* ctx, const gk_table* table, const double* radii, size_t n,
+                    uint32_t* out);
+
 /* gk_eval_batch from HOST buffers (radii[n] in, out[n] back): the FFI-friendly
    form of KernelEvaluator::eval_batch; copies through device memory. */
 gk_status gk_eval_batch_host(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,
@@ -203,6 +210,9 @@ gk_status gk_jitter(double* vertices, size_t nv, uint64_t seed, double amp);
 /* DFMA throughput microbenchmark on the context's device: FP64 TFLOP/s with
    an FMA counted as 2 flops (the fill's roofline denominator). */
 gk_status gk_bench_fp64_peak(gk_ctx* ctx, double* tflops);
+/* Number of kernels this library has launched in this process (its own
+   kernels plus the CUB kernels of the table build), for launch accounting. */
+uint64_t gk_launch_count(void);
 /* SM count and clock of the context's device */
 gk_status gk_device_info(gk_ctx* ctx, int* sm_count, int* sm_clock_khz, int* cc_major,
                          int* cc_minor);

@@ -81,6 +81,15 @@ int go_eval_analytic_ck(int kind, double k_re, double k_im, double r, go_c128* o
   return GO_OK;
 }
 
+int go_eval_analytic_batch(int kind, double k, double k_im, const double* r, size_t n,
+                           go_c128* out) {
+  for (size_t i = 0; i < n; ++i) {
+    int s = go_eval_analytic_ck(kind, k, k_im, r[i], &out[i]);
+    if (s) return s;
+  }
+  return GO_OK;
+}
+
 /* ---------------------------------------------------------------- sampling */
 
 /* sampling.hpp:18-45 */

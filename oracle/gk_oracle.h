@@ -39,6 +39,10 @@ int go_eval_analytic(int kind, double k, double r, go_c128* out);
 /* complex-k extension (C4; no reference counterpart): exp(-jkr), k = k_re + j k_im */
 int go_eval_analytic_ck(int kind, double k_re, double k_im, double r, go_c128* out);
 
+/* eval_analytic elementwise (test sweeps): status of the first failure */
+int go_eval_analytic_batch(int kind, double k, double k_im, const double* r, size_t n,
+                           go_c128* out);
+
 /* sampling.hpp:18-45 */
 typedef struct {
   double r_min, r_max;

@@ -150,6 +150,18 @@ class Oracle:
                                         C.c_double(r), out), "eval_analytic")
         return complex(out[0], out[1])
 
+    def eval_analytic_batch(self, kind: int, k: float, radii, k_im: float = 0.0) -> np.ndarray:
+        r = np.ascontiguousarray(radii, np.float64)
+        out = np.zeros(r.size, np.complex128)
+        _chk(self.L.go_eval_analytic_batch(C.c_int(kind), C.c_double(k), C.c_double(k_im),
+                                           dptr(r), C.c_size_t(r.size),
+                                           out.ctypes.data_as(C.c_void_p)), "eval_analytic")
+        return out
+
+    def pointwise_bounds(self, ev, kind: int, method: int, radii) -> np.ndarray:
+        r = np.ascontiguousarray(radii, np.float64)
+        return np.array([ev.pointwise_bound(kind, method, x) for x in r])
+
     # -- sampling.hpp
     def zero_crossings(self, k: float, r_min: float, r_max: float) -> np.ndarray:
         cnt = C.c_size_t()

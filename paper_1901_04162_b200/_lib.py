@@ -100,6 +100,7 @@ PROTOTYPES = {
     "gk_table_download": [_vp, _vp, _vp, _vp, _vp, _vp],
     "gk_table_destroy": [_vp],
     "gk_eval_batch": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp, _u64p],
+    "gk_locate": [_vp, _vp, _vp, C.c_size_t, _vp],
     "gk_eval_batch_host": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp,
                            _u64p],
     "gk_mesh_create": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.POINTER(_vp)],
@@ -121,7 +122,7 @@ PROTOTYPES = {
     "gk_device_info": [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                        C.POINTER(C.c_int)],
 }
-EXPORTS = sorted(PROTOTYPES) + ["gk_abi_version", "gk_last_error"]
+EXPORTS = sorted(PROTOTYPES) + ["gk_abi_version", "gk_last_error", "gk_launch_count"]
 
 _lib = None
 
@@ -140,6 +141,8 @@ def lib() -> C.CDLL:
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = C.c_int
+    L.gk_launch_count.restype = C.c_uint64
+    L.gk_launch_count.argtypes = []
     L.gk_abi_version.restype = C.c_int
     L.gk_abi_version.argtypes = []
     L.gk_last_error.restype = C.c_char_p

@@ -2,6 +2,7 @@
 // orchestration behind it.  Every entry point converts exceptions into
 // gk_status codes that mirror the reference's exception types; the message
 // is kept in a thread-local buffer for gk_last_error().
+#include <atomic>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -108,7 +109,14 @@ void use_device(const gk_ctx* c) { GK_CUDA(cudaSetDevice(c->device)); }
 
 }  // namespace
 
+namespace gk {
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace gk
+
 extern "C" {
+
+uint64_t gk_launch_count(void) { return gk::g_launches.load(std::memory_order_relaxed); }
 
 int gk_abi_version(void) { return GK_ABI_VERSION; }
 
@@ -283,6 +291,26 @@ gk_status gk_eval_batch(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
       gk::fail(GK_ERR_INVALID_ARGUMENT, "eval_batch: radius [" + std::to_string(idx) + "] = " +
                                             std::to_string(r) + ": " + why);
     }
+  });
+}
+
+gk_status gk_locate(gk_ctx* c, const gk_table* t, const double* radii, size_t n, uint32_t* out) {
+  return guarded([&] {
+    check_ctx(c);
+    need(t != nullptr, GK_ERR_INVALID_ARGUMENT, "locate needs a table");
+    if (n == 0) return;
+    need(radii && out, GK_ERR_INVALID_ARGUMENT, "null buffer");
+    use_device(c);
+    unsigned long long* w = c->scratch.p;
+    const unsigned long long init[2] = {0ull, ~0ull};
+    GK_CUDA(cudaMemcpyAsync(w, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    gk::launch_locate(c, t, radii, n, out, w);
+    unsigned long long res[2];
+    GK_CUDA(cudaMemcpyAsync(res, w, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    if (res[1] != ~0ull)
+      gk::fail(GK_ERR_OUT_OF_RANGE,
+               "locate: radius [" + std::to_string(res[1]) + "] outside the tabulated range");
   });
 }
 

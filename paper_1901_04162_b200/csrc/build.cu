@@ -90,6 +90,7 @@ void launch_points(gk_mesh* mesh, const double* d_verts, const uint32_t* d_tris,
   const unsigned blocks = static_cast<unsigned>((mesh->N + threads - 1) / threads);
   points_kernel<<<blocks, threads, 0, s>>>(d_verts, d_tris, mesh->N, q, mesh->outer.p,
                                            mesh->inner.p, mesh->bounds.p, mesh->binner.p);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
 }
 
@@ -463,7 +464,10 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
   DevBuf<double> zeros, kz;
   zeros.alloc(static_cast<size_t>(S.ncand) + 1, st);
   kz.alloc(static_cast<size_t>(S.ncand) + 1, st);
-  if (S.refine) zeros_kernel<<<1, 1, 0, st>>>(S, zeros.p, kz.p, w.p);
+  if (S.refine) {
+    zeros_kernel<<<1, 1, 0, st>>>(S, zeros.p, kz.p, w.p);
+    count_launches(1);
+  }
   GK_CUDA(cudaGetLastError());
   unsigned long long hw[W_COUNT];
   GK_CUDA(cudaMemcpyAsync(hw, w.p, sizeof(hw), cudaMemcpyDeviceToHost, st));
@@ -502,10 +506,13 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     uint8_t* bkeep = flags.p + 2 + nkz;
     GK_CUDA(cudaMemsetAsync(bkeep, 0, 1, st));  // index 0 is not a base point
     base_kernel<<<grid_for(nbase), 256, 0, st>>>(S, kz.p, w.p, bvals, bkeep);
+    count_launches(1);
     GK_CUDA(cudaGetLastError());
-    if (nref)
+    if (nref) {
       refined_kernel<<<grid_for(nref), 256, 0, st>>>(S, zeros.p, kz.p, w.p, bkeep,
                                                      bvals + nbase, bkeep + nbase);
+      count_launches(1);
+    }
     GK_CUDA(cudaGetLastError());
     // compact + sort (all values positive: uint64 order == double order)
     DevBuf<double> sel;
@@ -519,6 +526,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     tmp.alloc(tmp_bytes, st);
     GK_CUDA(cub::DeviceSelect::Flagged(tmp.p, tmp_bytes, cand.p, flags.p, sel.p, nsel.p,
                                        static_cast<int>(ncand_total), st));
+    count_launches(2);  // compact-init + select-sweep
     int nh = 0;
     GK_CUDA(cudaMemcpyAsync(&nh, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     GK_CUDA(cudaStreamSynchronize(st));
@@ -533,6 +541,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     tmp2.alloc(sort_bytes, st);
     GK_CUDA(cub::DeviceRadixSort::SortKeys(tmp2.p, sort_bytes, kin, kout, static_cast<int>(n), 0,
                                            64, st));
+    count_launches(10);  // histogram + exclusive-sum + 8 onesweep passes (64-bit keys)
   } else {
     const long long cap = 2 + nz + S.steps + nz * 2LL * S.side_steps;
     DevBuf<double> kept;
@@ -542,6 +551,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     isz.alloc(static_cast<size_t>(cap), st);
     nout.alloc(1, st);
     plan_sequential_kernel<<<1, 1, 0, st>>>(S, zeros.p, w.p, kept.p, isz.p, nout.p);
+    count_launches(1);
     GK_CUDA(cudaGetLastError());
     unsigned long long nh = 0;
     GK_CUDA(cudaMemcpyAsync(&nh, nout.p, 8, cudaMemcpyDeviceToHost, st));
@@ -576,6 +586,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     fail(GK_ERR_INVALID_ARGUMENT, "KernelEvaluator: table smaller than the Lagrange stencil");
 
   gaps_kernel<<<grid_for(n), 256, 0, st>>>(absc.p, n, w.p);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
   GK_CUDA(cudaMemcpyAsync(hw, w.p, sizeof(hw), cudaMemcpyDeviceToHost, st));
   GK_CUDA(cudaStreamSynchronize(st));
@@ -592,6 +603,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
   GK_CUDA(cudaMemsetAsync(t->hash.p, 0, t->hash.bytes(), st));
   hash_seed_kernel<<<grid_for(n), 256, 0, st>>>(absc.p, n, cfg.r_min, dr_min, inv_dr_min, nb,
                                                 t->hash.p);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
   {
     DevBuf<uint32_t> seeds;
@@ -604,6 +616,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     tmp.alloc(bytes, st);
     GK_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, bytes, seeds.p, t->hash.p, MaxU32(),
                                            static_cast<int>(nb), st));
+    count_launches(2);  // scan-init + scan
   }
 
   // node values and interval records
@@ -611,12 +624,14 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
   t->green_vals.alloc(static_cast<size_t>(n), st);
   values_kernel<<<grid_for(n), 256, 0, st>>>(absc.p, n, k_re, k_im, t->exp_vals.p,
                                              t->green_vals.p);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
   const int grs = 2 + 2 * (degree + 1);
   t->grec.alloc(static_cast<size_t>(n) * grs, st);
   t->erec.alloc(static_cast<size_t>(n) * 6, st);
   records_kernel<<<grid_for(n, 128), 128, 0, st>>>(absc.p, n, t->exp_vals.p, t->green_vals.p,
                                                     degree, t->grec.p, t->erec.p);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
 
   // lookup buckets of width dr_min / 2
@@ -634,6 +649,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     cnt.alloc(d.nlk, st);
     GK_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes(), st));
     lookup_count_kernel<<<grid_for(n), 256, 0, st>>>(absc.p, n, d, cnt.p, w.p);
+    count_launches(1);
     GK_CUDA(cudaGetLastError());
     size_t bytes = 0;
     GK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, t->lk.p, static_cast<int>(d.nlk),
@@ -642,7 +658,9 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     tmp.alloc(bytes, st);
     GK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, t->lk.p, static_cast<int>(d.nlk),
                                           st));
+    count_launches(2);  // scan-init + scan
     lookup_finish_kernel<<<grid_for(d.nlk), 256, 0, st>>>(t->lk.p, d.nlk, t->lk.p);
+    count_launches(1);
     GK_CUDA(cudaGetLastError());
     GK_CUDA(cudaMemcpyAsync(hw, w.p, sizeof(hw), cudaMemcpyDeviceToHost, st));
     GK_CUDA(cudaEventRecord(ctx->ev1, st));

@@ -334,6 +334,7 @@ void launch_kernel(gk_ctx* ctx, K kernel, const FillArgs& a, size_t smem, int th
   if (grid > a.ntiles) grid = a.ntiles;
   if (grid < 1) grid = 1;
   kernel<<<static_cast<unsigned>(grid), threads, smem, ctx->stream>>>(a);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
 }
 
@@ -430,6 +431,7 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
     a.KA = -k_im * kAttenScale;
     atten.alloc(a.natten, ctx->stream);
     atten_kernel<<<(a.natten + 255) / 256, 256, 0, ctx->stream>>>(atten.p, a.natten);
+    count_launches(1);
     GK_CUDA(cudaGetLastError());
     a.atten = atten.p;
   }
@@ -536,10 +538,12 @@ void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row
   const unsigned grid = static_cast<unsigned>(rows < 65535 ? rows : 65535);
   range_sample_kernel<<<grid, 256, 0, st>>>(mesh->outer.p, mesh->inner.p, mesh->m, mesh->N,
                                             row_begin, row_end, w);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
   range_exact_kernel<<<grid, 256, 0, st>>>(mesh->outer.p, mesh->inner.p, mesh->bounds.p,
                                            mesh->binner.p, mesh->m, 3 * mesh->n, mesh->N,
                                            row_begin, row_end, w);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
   unsigned long long out[4];
   GK_CUDA(cudaMemcpyAsync(out, w, sizeof(out), cudaMemcpyDeviceToHost, st));
@@ -566,6 +570,7 @@ __global__ void phase_kernel(double2* tab) {
 void init_phase_table(gk_ctx* ctx) {
   ctx->phase.alloc(kPhaseM, ctx->stream);
   phase_kernel<<<(kPhaseM + 255) / 256, 256, 0, ctx->stream>>>(ctx->phase.p);
+  count_launches(1);
   GK_CUDA(cudaGetLastError());
 }
 

@@ -91,6 +91,9 @@ struct gk_mesh {
 
 namespace gk {
 
+// launch accounting (gk_launch_count)
+void count_launches(unsigned long long n);
+
 // host-side quadrature rules (quadrature.hpp:35-110), bit-identical
 void triangle_rule(int m, double* b0, double* b1, double* b2, double* w);
 void gauss_legendre_unit(int n, double* x, double* w);
@@ -113,6 +116,8 @@ void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row
 void launch_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,
                        double k_im, const double* r, size_t n, gk_c128* out,
                        unsigned long long* d_scratch);
+void launch_locate(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, uint32_t* out,
+                   unsigned long long* w);
 double run_fp64_peak(gk_ctx* ctx);
 void init_phase_table(gk_ctx* ctx);
 

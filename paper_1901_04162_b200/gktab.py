@@ -268,6 +268,15 @@ class DeviceTable:
         """
         return eval_batch(kind, radii, table=self, ctx=self.ctx)
 
+    def locate(self, radii):
+        """locate (table.hpp:87-102): bracketing interval index per radius (device)."""
+        torch = _torch()
+        r = _as_device_f64(radii, self.ctx.device)
+        out = torch.empty(r.numel(), dtype=torch.int32, device=r.device)
+        check(lib().gk_locate(self.ctx.h, self.h, r.data_ptr() if r.numel() else None, r.numel(),
+                              out.data_ptr() if r.numel() else None), "locate")
+        return out
+
     def eval_exp(self, r: float) -> complex:
         return complex(self.eval_batch(KernelKind.PlainExp, [r]).cpu()[0])
 

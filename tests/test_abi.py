@@ -23,8 +23,8 @@ def libgk():
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:gk_status|int|const char\*)\s+(gk_\w+)\s*\(", text,
-                                 re.M)))
+    return sorted(set(re.findall(r"^\s*(?:gk_status|int|uint64_t|const char\*)\s+(gk_\w+)\s*\(",
+                                 text, re.M)))
 
 
 def test_header_declares_the_boundary():
