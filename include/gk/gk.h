@@ -172,6 +172,16 @@ gk_status gk_fill_rows(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_
                        gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
                        gk_c128* z, size_t ldz, gk_fill_report* report);
 
+/* Fused Exp + Green fill sharing every radius (and, in TABLE mode, every
+   lookup): z_exp gets the PlainExp matrix, z_green the GreenOverR matrix, each
+   bit-identical to the separate gk_fill_rows result.  The EFIE-type use the
+   paper's "several tables" serve.  Reported calls count
+   both kernels. */
+gk_status gk_fill_rows_pair(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode,
+                            const gk_table* table, double k_re, double k_im, size_t row_begin,
+                            size_t row_end, gk_c128* z_exp, gk_c128* z_green, size_t ldz,
+                            gk_fill_report* report);
+
 /* fill_matrix<Kernel> (matfill.hpp:144-228) end to end from HOST buffers:
    upload mesh, quadrature points, (TABLE) K1 range when cfg->r_min <= 0 or
    cfg->r_max <= 0, table build, fill, copy Z (nt x nt, row-major) back into

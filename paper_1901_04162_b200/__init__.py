@@ -6,7 +6,7 @@ all in hand-written CUDA (libgk.so, C ABI in include/gk/gk.h).
 """
 from .gktab import (Context, DeviceMesh, DeviceTable, FillReport, KernelKind, Medium, Mode,
                     QuadratureSpec, SamplingConfig, TriangleMesh, eval_batch, fill_matrix,
-                    fill_rows, fill_rows_host, generate_plate_mesh, generate_sphere_mesh, jitter,
+                    fill_rows, fill_rows_host, fill_rows_pair, generate_plate_mesh, generate_sphere_mesh, jitter,
                     predicted_calls, wavenumber)
 from ._lib import (DomainError, GkError, InvalidArgument, OutOfRange, OverflowErrorGk,
                    RuntimeErrorGk, LIB_PATH)
@@ -14,7 +14,7 @@ from ._lib import (DomainError, GkError, InvalidArgument, OutOfRange, OverflowEr
 __all__ = [
     "Context", "DeviceMesh", "DeviceTable", "FillReport", "KernelKind", "Medium", "Mode",
     "QuadratureSpec", "SamplingConfig", "TriangleMesh", "eval_batch", "fill_matrix",
-    "fill_rows", "fill_rows_host", "generate_plate_mesh", "generate_sphere_mesh", "jitter", "predicted_calls",
+    "fill_rows", "fill_rows_host", "fill_rows_pair", "generate_plate_mesh", "generate_sphere_mesh", "jitter", "predicted_calls",
     "wavenumber", "DomainError", "GkError", "InvalidArgument", "OutOfRange", "OverflowErrorGk",
     "RuntimeErrorGk", "LIB_PATH",
 ]

@@ -109,6 +109,8 @@ PROTOTYPES = {
     "gk_distance_range": [_vp, _vp, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_fill_rows": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_double, C.c_size_t,
                      C.c_size_t, _vp, C.c_size_t, C.POINTER(FillReportC)],
+    "gk_fill_rows_pair": [_vp, _vp, C.c_int, _vp, C.c_double, C.c_double, C.c_size_t,
+                          C.c_size_t, _vp, _vp, C.c_size_t, C.POINTER(FillReportC)],
     "gk_fill_matrix_host": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.c_int,
                             C.POINTER(SamplingConfigC), C.POINTER(Medium), C.c_int, _vp,
                             C.POINTER(FillReportC)],

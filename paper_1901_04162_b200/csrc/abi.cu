@@ -446,50 +446,73 @@ gk_status gk_distance_range(gk_ctx* c, const gk_mesh* mesh, size_t row_begin, si
   });
 }
 
+namespace {
+
+// fill_rows on the device for kind EXP / GREEN, or 2 = the fused pair (z: Exp, z2: Green)
+void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t, int kind,
+                    double k_re, double k_im, size_t row_begin, size_t row_end, gk_c128* z,
+                    gk_c128* z2, size_t ldz, gk_fill_report* report) {
+  check_ctx(c);
+  need(mesh != nullptr, GK_ERR_INVALID_ARGUMENT, "null mesh");
+  need(mode == GK_MODE_DIRECT || mode == GK_MODE_TABLE, GK_ERR_INVALID_ARGUMENT, "bad mode");
+  need(row_begin <= row_end && row_end <= mesh->N, GK_ERR_INVALID_ARGUMENT,
+       "gk_fill_rows: bad row range");
+  need(ldz >= mesh->N, GK_ERR_INVALID_ARGUMENT, "gk_fill_rows: ldz < N");
+  need(row_begin == row_end || (z && (kind != 2 || z2)), GK_ERR_INVALID_ARGUMENT, "null z");
+  if (mode == GK_MODE_TABLE) {
+    need(t != nullptr, GK_ERR_INVALID_ARGUMENT, "TABLE mode needs a table");
+    k_re = t->dev.k_re;
+    k_im = t->dev.k_im;
+  }
+  need(k_re >= 0.0, GK_ERR_INVALID_ARGUMENT, "eval_analytic: k must be >= 0");
+  const uint64_t kinds = kind == 2 ? 2 : 1;
+  const uint64_t pred = predicted(mesh->N, mesh->m, mesh->n);
+  use_device(c);
+  unsigned long long* cnt = c->scratch.p + 16;
+  if (report) {
+    GK_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
+    GK_CUDA(cudaEventRecord(c->ev0, c->stream));
+  }
+  gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, z2, ldz, cnt);
+  if (!report) return;
+  GK_CUDA(cudaEventRecord(c->ev1, c->stream));
+  unsigned long long h[2];
+  GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  GK_CUDA(cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  GK_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  report->N = mesh->N;
+  report->m = mesh->m;
+  report->n = mesh->n;
+  report->predicted_calls = kinds * pred;
+  const size_t rows = row_end - row_begin;
+  report->actual_calls = kinds * 3ull * mesh->m * mesh->n * rows * (mesh->N - 1);
+  report->fallback_calls = h[0] + h[1];
+  report->wall_time_s = ms * 1e-3;
+  if (h[1])
+    gk::fail(GK_ERR_OUT_OF_RANGE,
+             "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
+}
+
+}  // namespace
+
 gk_status gk_fill_rows(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t,
                        gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
                        gk_c128* z, size_t ldz, gk_fill_report* report) {
   return guarded([&] {
-    check_ctx(c);
-    need(mesh != nullptr, GK_ERR_INVALID_ARGUMENT, "null mesh");
-    need(mode == GK_MODE_DIRECT || mode == GK_MODE_TABLE, GK_ERR_INVALID_ARGUMENT, "bad mode");
     need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
-    need(row_begin <= row_end && row_end <= mesh->N, GK_ERR_INVALID_ARGUMENT,
-         "gk_fill_rows: bad row range");
-    need(ldz >= mesh->N, GK_ERR_INVALID_ARGUMENT, "gk_fill_rows: ldz < N");
-    need(row_begin == row_end || z, GK_ERR_INVALID_ARGUMENT, "null z");
-    if (mode == GK_MODE_TABLE) {
-      need(t != nullptr, GK_ERR_INVALID_ARGUMENT, "TABLE mode needs a table");
-      k_re = t->dev.k_re;
-      k_im = t->dev.k_im;
-    }
-    need(k_re >= 0.0, GK_ERR_INVALID_ARGUMENT, "eval_analytic: k must be >= 0");
-    const uint64_t pred = predicted(mesh->N, mesh->m, mesh->n);
-    use_device(c);
-    unsigned long long* cnt = c->scratch.p + 16;
-    if (report) {
-      GK_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
-      GK_CUDA(cudaEventRecord(c->ev0, c->stream));
-    }
-    gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, ldz, cnt);
-    if (!report) return;
-    GK_CUDA(cudaEventRecord(c->ev1, c->stream));
-    unsigned long long h[2];
-    GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    GK_CUDA(cudaStreamSynchronize(c->stream));
-    float ms = 0.f;
-    GK_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-    report->N = mesh->N;
-    report->m = mesh->m;
-    report->n = mesh->n;
-    report->predicted_calls = pred;
-    const size_t rows = row_end - row_begin;
-    report->actual_calls = 3ull * mesh->m * mesh->n * rows * (mesh->N - 1);
-    report->fallback_calls = h[0] + h[1];
-    report->wall_time_s = ms * 1e-3;
-    if (h[1])
-      gk::fail(GK_ERR_OUT_OF_RANGE,
-               "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
+    fill_rows_impl(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, nullptr, ldz,
+                   report);
+  });
+}
+
+gk_status gk_fill_rows_pair(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t,
+                            double k_re, double k_im, size_t row_begin, size_t row_end,
+                            gk_c128* z_exp, gk_c128* z_green, size_t ldz,
+                            gk_fill_report* report) {
+  return guarded([&] {
+    fill_rows_impl(c, mesh, mode, t, 2, k_re, k_im, row_begin, row_end, z_exp, z_green, ldz,
+                   report);
   });
 }
 
@@ -541,7 +564,7 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       const size_t re = rb + chunk < row_end ? rb + chunk : row_end;
       const int b = static_cast<int>(idx & 1);
       if (idx >= 2) GK_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
-      gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nt, cnt);
+      gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt, cnt);
       GK_CUDA(cudaEventRecord(filled[b], c->stream));
       GK_CUDA(cudaStreamWaitEvent(copy, filled[b], 0));
       GK_CUDA(cudaMemcpy2DAsync(z_host + (rb - row_begin) * ldz, ldz * sizeof(gk_c128), dz[b],

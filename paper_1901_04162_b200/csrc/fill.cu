@@ -24,6 +24,65 @@ namespace gk {
 constexpr int kRowsPerTile = 8;  // one row per warp
 constexpr int kMaxColBlocks = 32;  // 32-column blocks per tile (adaptive, see launch_fill)
 constexpr int kThreads = 32 * kRowsPerTile;
+constexpr int kKindPair = 2;  // fused Exp + Green fill sharing r
+
+// per-entry accumulators: one complex per outer point, two for the fused pair
+template <int MO, bool PAIR>
+struct Acc {
+  double2 e[MO], g[PAIR ? MO : 1];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int o = 0; o < MO; ++o) {
+      e[o] = make_double2(0.0, 0.0);
+      if constexpr (PAIR) g[o] = make_double2(0.0, 0.0);
+    }
+  }
+  // acc += w * (c - j s) for kind KIND; y = 1/r for the Green weight
+  template <int KIND>
+  __device__ __forceinline__ void add(int o, double w, double y, double2 cs) {
+    if constexpr (KIND == kKindPair) {
+      e[o].x = __fma_rn(w, cs.x, e[o].x);
+      e[o].y = __fma_rn(-w, cs.y, e[o].y);
+      const double wg = __dmul_rn(w, y);
+      g[o].x = __fma_rn(wg, cs.x, g[o].x);
+      g[o].y = __fma_rn(-wg, cs.y, g[o].y);
+    } else {
+      const double wk = KIND == GK_KIND_GREEN ? __dmul_rn(w, y) : w;
+      e[o].x = __fma_rn(wk, cs.x, e[o].x);
+      e[o].y = __fma_rn(-wk, cs.y, e[o].y);
+    }
+  }
+  // acc += w * v (table values: v = K(r) for the kind, vg = Green for the pair)
+  __device__ __forceinline__ void add_values(int o, double w, double2 v, double2 vg) {
+    e[o].x = __fma_rn(w, v.x, e[o].x);
+    e[o].y = __fma_rn(w, v.y, e[o].y);
+    if constexpr (PAIR) {
+      g[o].x = __fma_rn(w, vg.x, g[o].x);
+      g[o].y = __fma_rn(w, vg.y, g[o].y);
+    }
+  }
+  // finish sum_o w_o acc_o and store (self pairs stay zero, matfill.hpp:178)
+  template <class W>
+  __device__ __forceinline__ void finish(const W& wo, bool self, bool valid, double2* z,
+                                         double2* z2, size_t off) {
+    double2 re = make_double2(0.0, 0.0), rg = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int o = 0; o < MO; ++o) {
+      const double w = wo(o);
+      re.x = __fma_rn(w, e[o].x, re.x);
+      re.y = __fma_rn(w, e[o].y, re.y);
+      if constexpr (PAIR) {
+        rg.x = __fma_rn(w, g[o].x, rg.x);
+        rg.y = __fma_rn(w, g[o].y, rg.y);
+      }
+    }
+    if (self) re = rg = make_double2(0.0, 0.0);
+    if (valid) {
+      __stcs(z + off, re);
+      if constexpr (PAIR) __stcs(z2 + off, rg);
+    }
+  }
+};
 
 __global__ void atten_kernel(double* E, int n);
 
@@ -35,7 +94,8 @@ struct FillArgs {
   size_t row_begin, row_end;
   size_t ncb, ntiles;
   int cpt;  // column blocks per tile
-  double2* z;
+  double2* z;   // Exp or Green (or Exp for the fused pair fill)
+  double2* z2;  // fused pair fill: Green
   size_t ldz;
   TableDev T;
   const double2* phase;
@@ -104,9 +164,8 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
     size_t q;
     bool valid;
     W.load(0, 0, lane, nxy, nzw, q, valid);
-    double2 acc[MO];
-#pragma unroll
-    for (int o = 0; o < MO; ++o) acc[o] = make_double2(0.0, 0.0);
+    Acc<MO, KIND == kKindPair> acc;
+    acc.zero();
     int ncb_next = 0, ni = 0;  // (column block, inner point) of the prefetch
     for (int it = 0; it < iters; ++it) {
       const double2 pxy = nxy, pzw = nzw;
@@ -126,22 +185,14 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
         const double y = rsqrt_fast(d2);
         const double r = __dmul_rn(d2, y);
         const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
-        double wgt = KIND == GK_KIND_GREEN ? __dmul_rn(pzw.y, y) : pzw.y;
-        if constexpr (LOSSY) wgt = __dmul_rn(wgt, atten_table(r, A.KA, att, A.natten));
-        acc[o].x = __fma_rn(wgt, cs.x, acc[o].x);
-        acc[o].y = __fma_rn(-wgt, cs.y, acc[o].y);
+        double w = pzw.y;
+        if constexpr (LOSSY) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
+        acc.template add<KIND>(o, w, y, cs);
       }
       if (block_done) {  // column block complete: finish the entry
-        double2 res = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int o = 0; o < MO; ++o) {
-          const double wo = my[o][3];
-          res.x = __fma_rn(wo, acc[o].x, res.x);
-          res.y = __fma_rn(wo, acc[o].y, res.y);
-          acc[o] = make_double2(0.0, 0.0);
-        }
-        if (qc == p) res = make_double2(0.0, 0.0);  // self pairs stay zero (matfill.hpp:178)
-        if (vc) __stcs(A.z + (p - A.row_begin) * A.ldz + qc, res);
+        acc.finish([&](int o) { return my[o][3]; }, qc == p, vc, A.z, A.z2,
+                   (p - A.row_begin) * A.ldz + qc);
+        acc.zero();
       }
     }
   }
@@ -154,10 +205,13 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
 // an issue cycle each while an FP64 warp instruction holds the 16-lane pipe
 // for two, so this variant's ~9 non-FP64 instructions/eval (vs ~16 in the
 // runtime-IPT kernel) are worth ~12% (ablations: scripts/direct_variants.cu).
-constexpr int kWarpsV4 = 12;
+// (The fused pair fill carries twice the accumulators: 8 warps, ~200 registers.)
+template <int KIND>
+__host__ __device__ constexpr int warps_v4() { return KIND == kKindPair ? 8 : 12; }
 
 template <int MO, int IPT, int KIND, bool LOSSY>
-__global__ void __launch_bounds__(32 * kWarpsV4, 1) direct_kernel_v4(const FillArgs A) {
+__global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(const FillArgs A) {
+  constexpr int kWarpsV4 = warps_v4<KIND>();
   extern __shared__ double2 tab[];  // kPhaseM phase entries (64 KB) [+ attenuation table]
   __shared__ double sw[kWarpsV4][MO];
   for (int i = threadIdx.x; i < kPhaseM; i += blockDim.x) tab[i] = A.phase[i];
@@ -196,9 +250,8 @@ __global__ void __launch_bounds__(32 * kWarpsV4, 1) direct_kernel_v4(const FillA
     }
     for (int cb = 0; cb < nblk; ++cb) {
       const double4* cp = colp <= last ? colp : last;
-      double2 acc[MO];
-#pragma unroll
-      for (int o = 0; o < MO; ++o) acc[o] = make_double2(0.0, 0.0);
+      Acc<MO, KIND == kKindPair> acc;
+      acc.zero();
 #pragma unroll
       for (int i = 0; i < IPT; ++i) {
         const double2 pxy = cxy, pzw = czw;
@@ -211,22 +264,14 @@ __global__ void __launch_bounds__(32 * kWarpsV4, 1) direct_kernel_v4(const FillA
           const double y = rsqrt_fast(d2);
           const double r = __dmul_rn(d2, y);
           const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
-          double wgt = KIND == GK_KIND_GREEN ? __dmul_rn(pzw.y, y) : pzw.y;
-          if constexpr (LOSSY) wgt = __dmul_rn(wgt, atten_table(r, A.KA, att, A.natten));
-          acc[o].x = __fma_rn(wgt, cs.x, acc[o].x);
-          acc[o].y = __fma_rn(-wgt, cs.y, acc[o].y);
+          double w = pzw.y;
+          if constexpr (LOSSY) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
+          acc.template add<KIND>(o, w, y, cs);
         }
       }
-      double2 res = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int o = 0; o < MO; ++o) {
-        const double wo = sw[warp][o];
-        res.x = __fma_rn(wo, acc[o].x, res.x);
-        res.y = __fma_rn(wo, acc[o].y, res.y);
-      }
       const size_t q = q0 + 32 * static_cast<size_t>(cb) + lane;
-      if (q == p) res = make_double2(0.0, 0.0);  // self pairs stay zero (matfill.hpp:178)
-      if (q < N) __stcs(A.z + (p - A.row_begin) * A.ldz + q, res);
+      acc.finish([&](int o) { return sw[warp][o]; }, q == p, q < N, A.z, A.z2,
+                 (p - A.row_begin) * A.ldz + q);
       colp += 32;
     }
     __syncwarp();
@@ -262,9 +307,8 @@ __global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
     size_t q;
     bool valid;
     W.load(0, 0, lane, nxy, nzw, q, valid);
-    double2 acc[MO];
-#pragma unroll
-    for (int o = 0; o < MO; ++o) acc[o] = make_double2(0.0, 0.0);
+    Acc<MO, KIND == kKindPair> acc;
+    acc.zero();
     int ncb_next = 0, ni = 0;  // (column block, inner point) of the prefetch
     for (int it = 0; it < iters; ++it) {
       const double2 pxy = nxy, pzw = nzw;
@@ -281,8 +325,9 @@ __global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
       for (int o = 0; o < MO; ++o) {
         const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
         const double r = __dmul_rn(d2, rsqrt_fast(d2));
-        double2 v;
-        if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, A.T);
+        double2 v, vg = make_double2(0.0, 0.0);
+        if constexpr (KIND == kKindPair) pair_table<DEG>(r, A.T, v, vg);
+        else if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, A.T);
         else if constexpr (DEG == 3) v = green_table<3>(r, A.T);
         else v = green_table_any(r, A.T);
         const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
@@ -290,27 +335,25 @@ __global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
           if (oob) {
             if (!self && vc) {
               // the reference's eval_kernel fallback (evaluator.hpp:199-205)
-              v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
-              if (r > A.T.r_max) ++n_high; else ++n_low;
+              const unsigned calls = KIND == kKindPair ? 2u : 1u;
+              if constexpr (KIND == kKindPair) {
+                v = analytic_sincos(GK_KIND_EXP, A.T.k_re, A.T.k_im, r);
+                vg = analytic_sincos(GK_KIND_GREEN, A.T.k_re, A.T.k_im, r);
+              } else {
+                v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
+              }
+              if (r > A.T.r_max) n_high += calls; else n_low += calls;
             } else {
-              v = make_double2(0.0, 0.0);
+              v = vg = make_double2(0.0, 0.0);
             }
           }
         }
-        acc[o].x = __fma_rn(pzw.y, v.x, acc[o].x);
-        acc[o].y = __fma_rn(pzw.y, v.y, acc[o].y);
+        acc.add_values(o, pzw.y, v, vg);
       }
       if (block_done) {
-        double2 res = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int o = 0; o < MO; ++o) {
-          const double wo = __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3);
-          res.x = __fma_rn(wo, acc[o].x, res.x);
-          res.y = __fma_rn(wo, acc[o].y, res.y);
-          acc[o] = make_double2(0.0, 0.0);
-        }
-        if (self) res = make_double2(0.0, 0.0);
-        if (vc) __stcs(A.z + (p - A.row_begin) * A.ldz + qc, res);
+        acc.finish([&](int o) { return __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3); },
+                   self, vc, A.z, A.z2, (p - A.row_begin) * A.ldz + qc);
+        acc.zero();
       }
     }
   }
@@ -353,8 +396,8 @@ void set_tiling(const gk_ctx* ctx, FillArgs& a, int rows_per_tile, int ctas_per_
 
 template <int MO, int IPT, int KIND, bool LOSSY>
 void launch_v4(gk_ctx* ctx, FillArgs a, size_t smem) {
-  set_tiling(ctx, a, kWarpsV4, 1);
-  launch_kernel(ctx, direct_kernel_v4<MO, IPT, KIND, LOSSY>, a, smem, 32 * kWarpsV4);
+  set_tiling(ctx, a, warps_v4<KIND>(), 1);
+  launch_kernel(ctx, direct_kernel_v4<MO, IPT, KIND, LOSSY>, a, smem, 32 * warps_v4<KIND>());
 }
 
 template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
@@ -384,26 +427,31 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
 }
 
 template <int MO>
-void dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, gk_kind kind, int degree,
-                 bool lossy) {
+void dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, bool lossy) {
   if (mode == GK_MODE_DIRECT) {
     if (kind == GK_KIND_GREEN) {
       if (lossy) launch_one<MO, GK_MODE_DIRECT, GK_KIND_GREEN, 0, true>(ctx, a);
       else launch_one<MO, GK_MODE_DIRECT, GK_KIND_GREEN, 0, false>(ctx, a);
-    } else {
+    } else if (kind == GK_KIND_EXP) {
       if (lossy) launch_one<MO, GK_MODE_DIRECT, GK_KIND_EXP, 0, true>(ctx, a);
       else launch_one<MO, GK_MODE_DIRECT, GK_KIND_EXP, 0, false>(ctx, a);
+    } else {
+      if (lossy) launch_one<MO, GK_MODE_DIRECT, kKindPair, 0, true>(ctx, a);
+      else launch_one<MO, GK_MODE_DIRECT, kKindPair, 0, false>(ctx, a);
     }
   } else {
     if (kind == GK_KIND_EXP) launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, false>(ctx, a);
-    else if (degree == 3) launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, false>(ctx, a);
-    else launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, false>(ctx, a);
+    else if (kind == GK_KIND_GREEN && degree == 3)
+      launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, false>(ctx, a);
+    else if (kind == GK_KIND_GREEN) launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, false>(ctx, a);
+    else if (degree == 3) launch_one<MO, GK_MODE_TABLE, kKindPair, 3, false>(ctx, a);
+    else launch_one<MO, GK_MODE_TABLE, kKindPair, 0, false>(ctx, a);
   }
 }
 
 void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
-                 gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
-                 gk_c128* z, size_t ldz, unsigned long long* counters) {
+                 int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
+                 gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* counters) {
   FillArgs a{};
   a.outer = mesh->outer.p;
   a.inner = mesh->inner.p;
@@ -412,6 +460,7 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.row_begin = row_begin;
   a.row_end = row_end;
   a.z = reinterpret_cast<double2*>(z);
+  a.z2 = reinterpret_cast<double2*>(z2);
   a.ldz = ldz;
   if (table) a.T = table->dev;
   a.phase = ctx->phase.p;

@@ -132,6 +132,29 @@ __device__ __forceinline__ double2 exp_table(double r, const TableDev& t) {
   return make_double2(__fma_rn(s.x, u, e0.x), __fma_rn(s.y, u, e0.y));
 }
 
+// Exp (linear) and Green (Lagrange) sharing one lookup: the Exp and Green
+// records carry the same {a_j, a_{j+1}} header (fused pair fill)
+template <int DEG>
+__device__ __forceinline__ void pair_table(double r, const TableDev& t, double2& e, double2& g) {
+  const int grs = DEG > 0 ? 2 + 2 * (DEG + 1) : t.grs;
+  const int deg = DEG > 0 ? DEG : t.degree;
+  double aj;
+  const uint32_t j = locate_interval(r, t, t.grec, grs, aj);
+  const double u = r - aj;
+  const double2* ce = reinterpret_cast<const double2*>(t.erec + static_cast<size_t>(j) * 6 + 2);
+  const double2 e0 = __ldg(ce), sl = __ldg(ce + 1);
+  e = make_double2(__fma_rn(sl.x, u, e0.x), __fma_rn(sl.y, u, e0.y));
+  const double2* c = reinterpret_cast<const double2*>(t.grec + static_cast<size_t>(j) * grs + 2);
+  double2 acc = __ldg(c + deg);
+#pragma unroll
+  for (int k = deg - 1; k >= 0; --k) {
+    const double2 ck = __ldg(c + k);
+    acc.x = __fma_rn(acc.x, u, ck.x);
+    acc.y = __fma_rn(acc.y, u, ck.y);
+  }
+  g = acc;
+}
+
 // ------------------------------------------------------------ direct math
 
 // exp(-j k r) from a phase table tab[M] = (cos 2pi i/M, sin 2pi i/M) in

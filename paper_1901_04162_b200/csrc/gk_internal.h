@@ -108,9 +108,10 @@ void launch_points(gk_mesh* mesh, const double* d_verts, const uint32_t* d_tris,
                    cudaStream_t s);
 void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg, double k_zero,
                         double t_nominal, double k_re, double k_im, int degree);
+// kind: GK_KIND_EXP, GK_KIND_GREEN, or 2 = fused pair (z = Exp, z2 = Green)
 void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
-                 gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
-                 gk_c128* z, size_t ldz, unsigned long long* d_fallbacks);
+                 int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
+                 gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* d_fallbacks);
 void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,
                   double* d2min, double* d2max);
 void launch_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,

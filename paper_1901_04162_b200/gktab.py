@@ -375,6 +375,27 @@ def fill_rows(dmesh: DeviceMesh, mode: Mode, kind: KernelKind = KernelKind.Green
     return out, (FillReport.from_c(rep) if report else None)
 
 
+def fill_rows_pair(dmesh: DeviceMesh, mode: Mode, table: DeviceTable | None = None,
+                   k: complex = 0.0, row_begin: int = 0, row_end: int | None = None,
+                   report: bool = True):
+    """Fused Exp + Green fill sharing r (and the table lookup): returns
+    (Z_exp, Z_green, FillReport) with each matrix identical to its separate fill."""
+    torch = _torch()
+    ctx = dmesh.ctx
+    N = dmesh.N
+    row_end = N if row_end is None else row_end
+    rows = row_end - row_begin
+    ze = torch.empty((rows, N), dtype=torch.complex128, device=f"cuda:{ctx.device}")
+    zg = torch.empty_like(ze)
+    kc = complex(k)
+    rep = FillReportC()
+    check(lib().gk_fill_rows_pair(ctx.h, dmesh.h, int(mode), table.h if table else None, kc.real,
+                                  kc.imag, row_begin, row_end, ze.data_ptr() if rows else None,
+                                  zg.data_ptr() if rows else None, N,
+                                  C.byref(rep) if report else None), "fill_matrix")
+    return ze, zg, (FillReport.from_c(rep) if report else None)
+
+
 def fill_rows_host(dmesh: DeviceMesh, mode: Mode, out: np.ndarray,
                    kind: KernelKind = KernelKind.GreenOverR, table: DeviceTable | None = None,
                    k: complex = 0.0, row_begin: int = 0, row_end: int | None = None) -> FillReport:

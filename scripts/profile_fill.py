@@ -26,7 +26,12 @@ if mode == "table":
     t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S), med)
 Z = torch.empty((rows, N), dtype=torch.complex128, device="cuda")
 for _ in range(2):
-    z, rep = gk.fill_rows(dm, gk.Mode.TABLE if t else gk.Mode.DIRECT, table=t, k=k, row_end=rows,
-                          out=Z)
+    if mode == "pair":
+        del Z
+        _, _, rep = gk.fill_rows_pair(dm, gk.Mode.DIRECT, k=k, row_end=rows)
+        Z = None
+    else:
+        z, rep = gk.fill_rows(dm, gk.Mode.TABLE if t else gk.Mode.DIRECT, table=t, k=k,
+                              row_end=rows, out=Z)
 print(f"{sys.argv[1]} {mode} rows={rows} N={N} fill {rep.wall_time_s*1e3:.3f} ms "
       f"{rep.actual_calls / rep.wall_time_s:.3e} evals/s fallbacks={rep.fallback_calls}")

@@ -196,3 +196,23 @@ def test_fill_rows_host_matches_device(gk):
     rep_h = gk.fill_rows_host(dm, gk.Mode.DIRECT, zh, k=2 * np.pi, row_begin=5, row_end=301)
     assert np.array_equal(zh, zd.cpu().numpy())
     assert rep_h.actual_calls == rep_d.actual_calls
+
+
+@pytest.mark.parametrize("mode", ["direct", "table"])
+@pytest.mark.parametrize("m,n", [(6, 4), (7, 5), (3, 7)])
+def test_fused_pair_fill_equals_separate_fills(gk, mode, m, n):
+    """gk_fill_rows_pair: Exp and Green from one pass, bitwise equal to two fills."""
+    import torch
+    mesh = sphere(gk, 2)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+    k = 2 * np.pi
+    kw = dict(k=k)
+    if mode == "table":
+        lo, hi = dm.distance_range()
+        kw = dict(table=gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi)))
+    md = gk.Mode.DIRECT if mode == "direct" else gk.Mode.TABLE
+    ze, zg, rep = gk.fill_rows_pair(dm, md, **kw)
+    e, _ = gk.fill_rows(dm, md, kind=gk.KernelKind.PlainExp, **kw)
+    g, rg = gk.fill_rows(dm, md, kind=gk.KernelKind.GreenOverR, **kw)
+    assert torch.equal(ze, e) and torch.equal(zg, g)
+    assert rep.actual_calls == 2 * rg.actual_calls and rep.fallback_calls == 0
