@@ -116,6 +116,13 @@ gk_status gk_table_info_get(const gk_table* table, gk_table_info* info);
 gk_status gk_table_download(const gk_table* table, double* abscissae, double* zeros,
                             gk_c128* exp_values, gk_c128* green_values, uint32_t* buckets);
 gk_status gk_table_destroy(gk_table* table);
+/* Wire formats of the reference, written from a device table:
+   dump_table_binary (io.hpp:77-96): "GKTB", u32 version 1, u32 count, f64 k,
+   u8 kind, count x (f64 r, f64 re, f64 im), little-endian -- readable by the
+   reference's load_table_binary (io.hpp:105-132);
+   dump_plan_csv (io.hpp:60-74): "index,r,is_zero,gap_to_next", %.17g. */
+gk_status gk_table_dump_binary(const gk_table* table, gk_kind kind, const char* path);
+gk_status gk_plan_dump_csv(const gk_table* table, const char* path);
 
 /* KernelEvaluator::eval_batch (evaluator.hpp:209-221) when table != NULL
    (Exp: linear, Green: Lagrange; r < r_min -> analytic fallback, counted),

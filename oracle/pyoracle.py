@@ -546,6 +546,22 @@ class Ref:
                                                C.c_int(threads)), "analytic_batch")
         return out
 
+    def dump_plan_csv(self, plan: Plan, path: str) -> None:
+        a, z = plan.abscissae, plan.zeros
+        _chk(self.L.gr_dump_plan_csv(dptr(a), C.c_size_t(a.size), dptr(z) if z.size else None,
+                                     C.c_size_t(z.size), path.encode()), "dump_plan_csv")
+
+    def load_table_binary(self, path: str):
+        kind, k, cnt = C.c_int(), C.c_double(), C.c_size_t()
+        _chk(self.L.gr_load_table_binary(path.encode(), C.byref(kind), C.byref(k), C.byref(cnt),
+                                         None, None), "load_table_binary")
+        r = np.zeros(cnt.value, np.float64)
+        v = np.zeros(cnt.value, np.complex128)
+        _chk(self.L.gr_load_table_binary(path.encode(), C.byref(kind), C.byref(k), C.byref(cnt),
+                                         dptr(r), v.ctypes.data_as(C.c_void_p)),
+             "load_table_binary")
+        return kind.value, k.value, r, v
+
     def compare_fills(self, test, ref):
         a = np.ascontiguousarray(test, np.complex128)
         b = np.ascontiguousarray(ref, np.complex128)

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <stdexcept>
 #include <thread>
 #include <vector>
@@ -413,6 +414,40 @@ int gr_fill_sampled_rows(const double* v, size_t nv, const uint32_t* t, size_t n
     *wall_s = std::chrono::duration<double>(t1 - t0).count();
     *calls = 0;
     for (auto c : per) *calls += c;
+  });
+}
+
+// io.hpp wire formats through the reference's own writers / reader
+int gr_dump_plan_csv(const double* absc, size_t n, const double* zeros, size_t nz,
+                     const char* path) {
+  return guarded([&] {
+    const SamplingPlan plan = make_plan(std::vector<double>(absc, absc + n),
+                                        std::vector<double>(zeros, zeros + nz));
+    std::ofstream out(path);
+    dump_plan_csv(plan, out);
+  });
+}
+
+int gr_dump_table_binary(void* h, int kind, const char* path) {
+  return guarded([&] {
+    const auto* ev = static_cast<const KernelEvaluator*>(h);
+    std::ofstream out(path, std::ios::binary);
+    dump_table_binary(kind == 0 ? ev->exp_table() : ev->green_table(), ev->plan(), out);
+  });
+}
+
+// load_table_binary (io.hpp:105-132): counts first (radii == nullptr), then data
+int gr_load_table_binary(const char* path, int* kind, double* k, size_t* count, double* radii,
+                         double* values) {
+  return guarded([&] {
+    std::ifstream in(path, std::ios::binary);
+    const TableDump d = load_table_binary(in);
+    *kind = static_cast<int>(d.kind);
+    *k = d.k;
+    *count = d.radii.size();
+    if (!radii) return;
+    std::copy(d.radii.begin(), d.radii.end(), radii);
+    std::memcpy(values, d.values.data(), d.values.size() * sizeof(Complex));
   });
 }
 

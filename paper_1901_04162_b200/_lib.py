@@ -99,6 +99,8 @@ PROTOTYPES = {
     "gk_table_info_get": [_vp, C.POINTER(TableInfoC)],
     "gk_table_download": [_vp, _vp, _vp, _vp, _vp, _vp],
     "gk_table_destroy": [_vp],
+    "gk_table_dump_binary": [_vp, C.c_int, C.c_char_p],
+    "gk_plan_dump_csv": [_vp, C.c_char_p],
     "gk_eval_batch": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp, _u64p],
     "gk_locate": [_vp, _vp, _vp, C.c_size_t, _vp],
     "gk_eval_batch_host": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp,

@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -246,6 +247,85 @@ gk_status gk_table_download(const gk_table* t, double* absc, double* zeros, gk_c
       GK_CUDA(cudaMemcpyAsync(buckets, t->hash.p, t->info.hash_buckets * 4, cudaMemcpyDeviceToHost, s));
     GK_CUDA(cudaStreamSynchronize(s));
     if (zeros && !t->zeros.empty()) std::memcpy(zeros, t->zeros.data(), t->zeros.size() * 8);
+  });
+}
+
+namespace {
+
+void put_u32(std::FILE* f, uint32_t v) {
+  unsigned char b[4];
+  for (int i = 0; i < 4; ++i) b[i] = static_cast<unsigned char>((v >> (8 * i)) & 0xff);
+  std::fwrite(b, 1, 4, f);
+}
+
+void put_f64(std::FILE* f, double v) {
+  uint64_t bits;
+  std::memcpy(&bits, &v, 8);
+  unsigned char b[8];
+  for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>((bits >> (8 * i)) & 0xff);
+  std::fwrite(b, 1, 8, f);
+}
+
+std::string g17(double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+
+}  // namespace
+
+gk_status gk_table_dump_binary(const gk_table* t, gk_kind kind, const char* path) {
+  return guarded([&] {
+    need(t && path, GK_ERR_INVALID_ARGUMENT, "null argument");
+    need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
+    const size_t n = t->info.nodes;
+    std::vector<double> a(n);
+    std::vector<gk_c128> v(n);
+    const gk_status s = gk_table_download(t, a.data(), nullptr,
+                                          kind == GK_KIND_EXP ? v.data() : nullptr,
+                                          kind == GK_KIND_GREEN ? v.data() : nullptr, nullptr);
+    if (s != GK_OK) gk::fail(s, g_last_error);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) gk::fail(GK_ERR_RUNTIME, std::string("dump_table_binary: cannot open '") + path + "'");
+    std::fwrite("GKTB", 1, 4, f);
+    put_u32(f, 1u);
+    put_u32(f, static_cast<uint32_t>(n));
+    put_f64(f, t->info.k_re);
+    const unsigned char kb = static_cast<unsigned char>(kind);
+    std::fwrite(&kb, 1, 1, f);
+    for (size_t i = 0; i < n; ++i) {
+      put_f64(f, a[i]);
+      put_f64(f, v[i].re);
+      put_f64(f, v[i].im);
+    }
+    const bool ok = std::ferror(f) == 0;
+    std::fclose(f);
+    if (!ok) gk::fail(GK_ERR_RUNTIME, "dump_table_binary: write failed");
+  });
+}
+
+gk_status gk_plan_dump_csv(const gk_table* t, const char* path) {
+  return guarded([&] {
+    need(t && path, GK_ERR_INVALID_ARGUMENT, "null argument");
+    const size_t n = t->info.nodes;
+    std::vector<double> a(n);
+    const gk_status s = gk_table_download(t, a.data(), nullptr, nullptr, nullptr, nullptr);
+    if (s != GK_OK) gk::fail(s, g_last_error);
+    std::FILE* f = std::fopen(path, "w");
+    if (!f) gk::fail(GK_ERR_RUNTIME, std::string("dump_plan_csv: cannot open '") + path + "'");
+    std::fputs("index,r,is_zero,gap_to_next\n", f);
+    size_t zi = 0;
+    const std::vector<double>& z = t->zeros;
+    for (size_t i = 0; i < n; ++i) {
+      const double r = a[i];
+      while (zi < z.size() && z[zi] < r) ++zi;
+      const bool is_zero = zi < z.size() && z[zi] == r;
+      const double gap = i + 1 < n ? a[i + 1] - r : 0.0;
+      std::fprintf(f, "%zu,%s,%d,%s\n", i, g17(r).c_str(), is_zero ? 1 : 0, g17(gap).c_str());
+    }
+    const bool ok = std::ferror(f) == 0;
+    std::fclose(f);
+    if (!ok) gk::fail(GK_ERR_RUNTIME, "dump_plan_csv: write failed");
   });
 }
 

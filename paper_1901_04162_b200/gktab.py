@@ -260,6 +260,14 @@ class DeviceTable:
         return {"abscissae": a, "zeros": z[:nz], "exp": e, "green": g, "buckets": b,
                 "t": self.info.t, "dr_min": self.info.dr_min}
 
+    def dump_table_binary(self, kind: KernelKind, path: str) -> None:
+        """The reference's GKTB table dump (io.hpp:77-96) of this device table."""
+        check(lib().gk_table_dump_binary(self.h, int(kind), path.encode()), "dump_table_binary")
+
+    def dump_plan_csv(self, path: str) -> None:
+        """The reference's plan CSV (io.hpp:60-74) of this device table's plan."""
+        check(lib().gk_plan_dump_csv(self.h, path.encode()), "dump_plan_csv")
+
     def eval_batch(self, kind: KernelKind, radii):
         """KernelEvaluator::eval_batch (evaluator.hpp:209-221) on the device.
 

@@ -174,3 +174,26 @@ def test_config_validation(gk):
         gk.DeviceTable(gk.SamplingConfig(r_min=0.1, r_max=0.1 + 1.5e-3))  # < two intervals
     with pytest.raises(gk.InvalidArgument):
         gk.DeviceTable(gk.SamplingConfig(), gk.Medium(lambda0=0.0))
+
+
+def test_wire_formats_readable_by_reference(gk, oracle, ref, tmp_path):
+    """io.hpp formats written from a DEVICE table: the plan CSV is byte-identical
+    to the reference's dump_plan_csv, and the reference's load_table_binary reads
+    the GKTB dump (radii bitwise, values within 4 ulp of glibc)."""
+    c = gk.SamplingConfig(r_min=1e-3, r_max=2.0)
+    t = gk.DeviceTable(c, gk.Medium(lambda0=0.5))
+    d = t.download()
+    t.dump_plan_csv(str(tmp_path / "gpu.csv"))
+    p = oracle.build_plan(_ocfg(c), 0.5)
+    ref.dump_plan_csv(p, str(tmp_path / "ref.csv"))
+    assert (tmp_path / "gpu.csv").read_bytes() == (tmp_path / "ref.csv").read_bytes()
+    for kind in (EXP, GREEN):
+        path = str(tmp_path / f"t{kind}.gktb")
+        t.dump_table_binary(gk.KernelKind(kind), path)
+        k_kind, k, r, v = ref.load_table_binary(path)
+        assert k_kind == kind and k == t.k
+        assert np.array_equal(r, p.abscissae)
+        e, g = oracle.evaluator(p, oracle.wavenumber(0.5)).tables()
+        want = e if kind == EXP else g
+        assert np.all(np.abs(v - want) <= 4 * ULP * np.abs(want))
+        assert np.array_equal(v, d["exp"] if kind == EXP else d["green"])
