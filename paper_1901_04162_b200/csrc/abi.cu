@@ -550,13 +550,13 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
   use_device(c);
   unsigned long long* cnt = c->scratch.p + 16;
   if (report) {
-    GK_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
+    GK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
   }
   gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, z2, ldz, cnt);
   if (!report) return;
   GK_CUDA(cudaEventRecord(c->ev1, c->stream));
-  unsigned long long h[2];
+  unsigned long long h[3];
   GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   GK_CUDA(cudaStreamSynchronize(c->stream));
   float ms = 0.f;
@@ -572,6 +572,9 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
   if (h[1])
     gk::fail(GK_ERR_OUT_OF_RANGE,
              "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
+  if (h[2])
+    gk::fail(GK_ERR_DOMAIN, "eval_analytic: exp(-jkr)/r is singular at r = 0 (" +
+                                std::to_string(h[2]) + " entries meet a zero-distance point pair)");
 }
 
 }  // namespace
@@ -637,7 +640,7 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       GK_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
     }
     unsigned long long* cnt = c->scratch.p + 16;
-    GK_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned long long), c->stream));
+    GK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
     size_t idx = 0;
     for (size_t rb = row_begin; rb < row_end; rb += chunk, ++idx) {
@@ -652,7 +655,7 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       GK_CUDA(cudaEventRecord(copied[b], copy));
     }
     GK_CUDA(cudaEventRecord(c->ev1, c->stream));
-    unsigned long long h[2];
+    unsigned long long h[3];
     GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     GK_CUDA(cudaStreamSynchronize(copy));
     GK_CUDA(cudaStreamSynchronize(c->stream));
@@ -670,6 +673,9 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
     if (h[1])
       gk::fail(GK_ERR_OUT_OF_RANGE,
                "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
+    if (h[2])
+      gk::fail(GK_ERR_DOMAIN, "eval_analytic: exp(-jkr)/r is singular at r = 0 (" +
+                                  std::to_string(h[2]) + " entries meet a zero-distance point pair)");
   } catch (...) {
     cleanup();
     throw;

@@ -61,10 +61,12 @@ struct Acc {
       g[o].y = __fma_rn(w, vg.y, g[o].y);
     }
   }
-  // finish sum_o w_o acc_o and store (self pairs stay zero, matfill.hpp:178)
+  // finish sum_o w_o acc_o and store (self pairs stay zero, matfill.hpp:178).
+  // A non-finite entry can only come from a zero-distance point pair, which
+  // the reference rejects (eval_analytic, kernel.hpp:51-53): counted in *bad.
   template <class W>
   __device__ __forceinline__ void finish(const W& wo, bool self, bool valid, double2* z,
-                                         double2* z2, size_t off) {
+                                         double2* z2, size_t off, unsigned long long* bad) {
     double2 re = make_double2(0.0, 0.0), rg = make_double2(0.0, 0.0);
 #pragma unroll
     for (int o = 0; o < MO; ++o) {
@@ -77,6 +79,8 @@ struct Acc {
       }
     }
     if (self) re = rg = make_double2(0.0, 0.0);
+    if (valid && !(isfinite(re.x) && isfinite(re.y) && isfinite(rg.x) && isfinite(rg.y)))
+      atomicAdd(bad, 1ull);
     if (valid) {
       __stcs(z + off, re);
       if constexpr (PAIR) __stcs(z2 + off, rg);
@@ -103,7 +107,7 @@ struct FillArgs {
   const double* atten;  // lossy: exp(-n / 512), n < natten
   int natten;
   double KA;            // -k_im * 512
-  unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max
+  unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max, [2] non-finite entries
 };
 
 // Column-block walk shared by both kernels: the (column block, inner point)
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
       }
       if (block_done) {  // column block complete: finish the entry
         acc.finish([&](int o) { return my[o][3]; }, qc == p, vc, A.z, A.z2,
-                   (p - A.row_begin) * A.ldz + qc);
+                   (p - A.row_begin) * A.ldz + qc, A.counters + 2);
         acc.zero();
       }
     }
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
       }
       const size_t q = q0 + 32 * static_cast<size_t>(cb) + lane;
       acc.finish([&](int o) { return sw[warp][o]; }, q == p, q < N, A.z, A.z2,
-                 (p - A.row_begin) * A.ldz + q);
+                 (p - A.row_begin) * A.ldz + q, A.counters + 2);
       colp += 32;
     }
     __syncwarp();
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
       }
       if (block_done) {
         acc.finish([&](int o) { return __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3); },
-                   self, vc, A.z, A.z2, (p - A.row_begin) * A.ldz + qc);
+                   self, vc, A.z, A.z2, (p - A.row_begin) * A.ldz + qc, A.counters + 2);
         acc.zero();
       }
     }

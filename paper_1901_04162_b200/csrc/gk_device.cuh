@@ -43,14 +43,7 @@ struct TableDev {
   double k_re, k_im;
 };
 
-struct PhaseDev {
-  double K1;        // k * M / (2 pi)
-  double k_im;      // attenuation exponent (lossy medium), 0 for real k
-};
-
 // ---------------------------------------------------------------- helpers
-
-__device__ __forceinline__ double ld_nc(const double* p) { return __ldg(p); }
 
 // squared distance; FMA form (pinned: all kernels share this one function so
 // K1's range and the fills see bit-identical radii)
@@ -192,8 +185,8 @@ __device__ __forceinline__ double atten_table(double r, double KA, const double*
   const double t = __fma_rn(r, KA, kMagicRint);
   const double nf = t - kMagicRint;
   const double f = __fma_rn(r, KA, -nf);
-  int idx = __double2loint(t);
-  idx = idx < nE ? idx : nE - 1;
+  unsigned idx = static_cast<unsigned>(__double2loint(t));
+  idx = idx < static_cast<unsigned>(nE) ? idx : static_cast<unsigned>(nE - 1);
   const double p = __fma_rn(__fma_rn(__fma_rn(__fma_rn(c4, f, c3), f, c2), f, c1), f, 1.0);
   return __dmul_rn(E[idx], p);
 }

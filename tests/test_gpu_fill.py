@@ -216,3 +216,21 @@ def test_fused_pair_fill_equals_separate_fills(gk, mode, m, n):
     g, rg = gk.fill_rows(dm, md, kind=gk.KernelKind.GreenOverR, **kw)
     assert torch.equal(ze, e) and torch.equal(zg, g)
     assert rep.actual_calls == 2 * rg.actual_calls and rep.fallback_calls == 0
+
+
+def test_zero_distance_pair_is_domain_error(gk, oracle):
+    """A source edge through an observation quadrature point: r = 0 exactly.
+    The reference throws domain_error (kernel.hpp:51-53); so does the device fill."""
+    v = np.array([[0, 0, 0], [3, 0, 0], [0, 3, 0],          # p: centroid (1, 1, 0)
+                  [0.5, 1, 0], [1.5, 1, 0], [1, 1, 1]], float)  # q: edge midpoint (1, 1, 0)
+    t = np.array([[0, 1, 2], [3, 4, 5]])
+    mesh = gk.TriangleMesh(v, t)
+    from oracle.pyoracle import OracleError
+    with pytest.raises(OracleError) as e:
+        oracle.fill_rows(mesh.vertices, mesh.triangles, 1, 1, DIRECT, 2 * np.pi)
+    assert e.value.status == 2
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(1, 1))
+    with pytest.raises(gk.DomainError):
+        gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    with pytest.raises(gk.DomainError):
+        gk.fill_matrix(mesh, gk.QuadratureSpec(1, 1), gk.Mode.DIRECT, gk.Medium())
