@@ -446,6 +446,17 @@ gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32
           lo[c3] = std::fmin(lo[c3], verts[3 * i + c3]);
           hi[c3] = std::fmax(hi[c3], verts[3 * i + c3]);
         }
+      double area = 0.0;
+      for (size_t i = 0; i < nt; ++i) {
+        const double* a = verts + 3 * static_cast<size_t>(tris[3 * i]);
+        const double* b = verts + 3 * static_cast<size_t>(tris[3 * i + 1]);
+        const double* c3v = verts + 3 * static_cast<size_t>(tris[3 * i + 2]);
+        const double e1x = b[0] - a[0], e1y = b[1] - a[1], e1z = b[2] - a[2];
+        const double e2x = c3v[0] - a[0], e2y = c3v[1] - a[1], e2z = c3v[2] - a[2];
+        const double cx = e1y * e2z - e1z * e2y, cy = e1z * e2x - e1x * e2z, cz = e1x * e2y - e1y * e2x;
+        area += 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
+      }
+      mesh->mean_edge = std::sqrt(4.0 * (area / static_cast<double>(nt)) / std::sqrt(3.0));
       mesh->diameter = std::sqrt((hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
                                  (hi[2] - lo[2]) * (hi[2] - lo[2])) * (1.0 + 1e-12);
       mesh->outer.alloc(nt * m, c->stream);

@@ -643,7 +643,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
   const double xmax = std::fma(cfg.r_max, d.inv_w, d.bias);
   if (!(xmax < 2.0e9)) fail(GK_ERR_INVALID_ARGUMENT, "lookup hash too large");
   d.nlk = static_cast<uint32_t>(std::floor(xmax)) + 2u;
-  t->lk.alloc(d.nlk, st);
+  t->lk.alloc(d.nlk + 4, st);  // +4: 16-byte-granular TMA windows may read past nlk
   {
     DevBuf<uint32_t> cnt;
     cnt.alloc(d.nlk, st);
@@ -681,6 +681,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
   d.erec = t->erec.p;
   d.lk = t->lk.p;
   d.degree = degree;
+  d.nrec = static_cast<uint32_t>(n);
   d.grs = grs;
   d.k_re = k_re;
   d.k_im = k_im;

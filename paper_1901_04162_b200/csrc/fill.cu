@@ -104,6 +104,9 @@ struct FillArgs {
   TableDev T;
   const double2* phase;
   double K1, k_re, k_im;
+  const double4* bounds;  // per-triangle (centroid, rho_outer), for tile radius bounds
+  const double* binner;   // per-triangle rho_inner
+  double window_est;      // estimated radius spread of a 16 x 64 tile (staging heuristic)
   const double* atten;  // lossy: exp(-n / 512), n < natten
   int natten;
   double KA;            // -k_im * 512
@@ -369,6 +372,253 @@ __global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
   if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
 }
 
+// ------------------------------------------------ K3 with a shared-memory table
+//
+// North star part (2): the table a tile needs is held in shared memory.  Per
+// tile (16 rows x 32 cpt columns) the CTA bounds the tile's radii from the
+// per-triangle centroids and radii (as K1 does), maps [r_lo, r_hi] to the
+// lookup-bucket and record ranges it can touch, and stages exactly those
+// slices with TMA bulk copies (cp.async.bulk + mbarrier).  A table that fits
+// whole is staged once per CTA; a tile whose window exceeds the budget reads
+// the global table through L1 instead (correct either way: same code path,
+// different TableWin).
+
+constexpr int kStagedWarps = 16;
+
+struct StageArgs {
+  uint32_t lk_cap, j_cap;  // shared-memory capacity in buckets / records
+  int whole;               // the whole table fits: stage once
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// the fill of one tile through a table window (shared or global)
+template <bool SMEM, int MO, int KIND, int DEG>
+__device__ __forceinline__ void table_tile(const FillArgs& A, const TableWin& win, size_t p0,
+                                           size_t tc, unsigned long long& n_low,
+                                           unsigned long long& n_high) {
+  constexpr bool WANT_E = KIND == GK_KIND_EXP || KIND == kKindPair;
+  constexpr bool WANT_G = KIND == GK_KIND_GREEN || KIND == kKindPair;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t N = A.N;
+  const size_t p = p0 + warp;
+  if (p >= A.row_end) return;  // warp-uniform
+  double ox[MO], oy[MO], oz[MO];
+#pragma unroll
+  for (int o = 0; o < MO; ++o) {
+    const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
+    const double zz = __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 2);
+    ox[o] = xy.x;
+    oy[o] = xy.y;
+    oz[o] = zz;
+  }
+  const size_t q0base = tc * (32 * static_cast<size_t>(A.cpt));
+  int ncb = static_cast<int>((N - q0base + 31) / 32);
+  if (ncb > A.cpt) ncb = A.cpt;
+  const InnerWalk W{A.inner, N, q0base, A.ipt, ncb};
+  const int iters = ncb * A.ipt;
+  double2 nxy, nzw;
+  size_t q;
+  bool valid;
+  W.load(0, 0, lane, nxy, nzw, q, valid);
+  Acc<MO, KIND == kKindPair> acc;
+  acc.zero();
+  int ncb_next = 0, ni = 0;
+  for (int it = 0; it < iters; ++it) {
+    const double2 pxy = nxy, pzw = nzw;
+    const size_t qc = q;
+    const bool vc = valid;
+    if (++ni == A.ipt) {
+      ni = 0;
+      ++ncb_next;
+    }
+    const bool block_done = ni == 0;
+    const bool self = qc == p;
+    if (it + 1 < iters) W.load(ncb_next, ni, lane, nxy, nzw, q, valid);
+#pragma unroll
+    for (int o = 0; o < MO; ++o) {
+      const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
+      const double r = __dmul_rn(d2, rsqrt_fast(d2));
+      double2 ve = make_double2(0.0, 0.0), vg = make_double2(0.0, 0.0);
+      win_eval<SMEM, DEG, WANT_E, WANT_G>(r, A.T, win, ve, vg);
+      const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
+      if (__any_sync(0xffffffffu, oob)) {
+        if (oob) {
+          if (!self && vc) {
+            // the reference's eval_kernel fallback (evaluator.hpp:199-205)
+            if constexpr (WANT_E) ve = analytic_sincos(GK_KIND_EXP, A.T.k_re, A.T.k_im, r);
+            if constexpr (WANT_G) vg = analytic_sincos(GK_KIND_GREEN, A.T.k_re, A.T.k_im, r);
+            const unsigned calls = KIND == kKindPair ? 2u : 1u;
+            if (r > A.T.r_max) n_high += calls; else n_low += calls;
+          } else {
+            ve = vg = make_double2(0.0, 0.0);
+          }
+        }
+      }
+      if constexpr (KIND == kKindPair) acc.add_values(o, pzw.y, ve, vg);
+      else acc.add_values(o, pzw.y, KIND == GK_KIND_EXP ? ve : vg, vg);
+    }
+    if (block_done) {
+      acc.finish([&](int o) { return __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3); },
+                 self, vc, A.z, A.z2, (p - A.row_begin) * A.ldz + qc, A.counters + 2);
+      acc.zero();
+    }
+  }
+}
+
+template <int MO, int KIND, int DEG>
+__global__ void __launch_bounds__(32 * kStagedWarps, 1)
+    table_staged_kernel(const FillArgs A, const StageArgs S) {
+  constexpr bool WANT_E = KIND == GK_KIND_EXP || KIND == kKindPair;
+  const int grs = DEG > 0 ? 2 + 2 * (DEG + 1) : A.T.grs;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_lk = reinterpret_cast<uint32_t*>(smem);
+  double* s_grec = reinterpret_cast<double*>(smem + static_cast<size_t>(S.lk_cap) * 4);
+  double* s_erec = s_grec + static_cast<size_t>(S.j_cap) * grs;
+  __shared__ uint64_t bar;
+  __shared__ double red_lo[kStagedWarps], red_hi[kStagedWarps];
+  __shared__ uint32_t cur[4];   // staged window: b0, nb, j0, nj (nb = 0: none)
+  __shared__ uint32_t want[4];  // window this tile needs
+  __shared__ int mode;          // 0: shared window, 1: global table
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n = static_cast<uint32_t>(A.T.nrec);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar);
+    cur[1] = 0;
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  unsigned long long n_low = 0, n_high = 0;
+  const TableWin gwin{A.T.grec, A.T.erec, A.T.lk, 0u, A.T.nlk, 0u, n};
+  const size_t N = A.N;
+
+  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
+    const size_t p0 = A.row_begin + tr * kStagedWarps;
+    if (!S.whole) {
+      // conservative radius range of the tile's pairs (centroid +- radii)
+      const size_t q0 = tc * (32 * static_cast<size_t>(A.cpt));
+      const size_t ncols = (N - q0) < 32 * static_cast<size_t>(A.cpt) ? N - q0 : 32 * static_cast<size_t>(A.cpt);
+      double lo = CUDART_INF, hi = 0.0;
+      for (size_t k = threadIdx.x; k < kStagedWarps * ncols; k += blockDim.x) {
+        const size_t pp = p0 + k / ncols, qq = q0 + k % ncols;
+        if (pp >= A.row_end || qq == pp) continue;
+        const double4 bp = A.bounds[pp];
+        const double4 bq = A.bounds[qq];
+        const double dx = bp.x - bq.x, dy = bp.y - bq.y, dz = bp.z - bq.z;
+        const double dc = sqrt(dx * dx + dy * dy + dz * dz);
+        const double rho = bp.w + __ldg(A.binner + qq);
+        lo = fmin(lo, (dc - rho) * (1.0 - 1e-12));
+        hi = fmax(hi, (dc + rho) * (1.0 + 1e-12));
+      }
+      for (int o = 16; o; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if (lane == 0) {
+        red_lo[warp] = lo;
+        red_hi[warp] = hi;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int w = 1; w < kStagedWarps; ++w) {
+          lo = fmin(lo, red_lo[w]);
+          hi = fmax(hi, red_hi[w]);
+        }
+        lo = fmax(lo, A.T.r_min);
+        hi = fmin(hi, A.T.r_max);
+        if (!(lo <= hi)) lo = hi = A.T.r_min;  // no in-range pair: any valid window
+        const uint32_t b_lo = lookup_bucket(lo, A.T), b_hi = lookup_bucket(hi, A.T);
+        const uint32_t b0 = b_lo & ~3u;
+        const uint32_t nb = (b_hi + 1 - b0 + 3) & ~3u;
+        const uint32_t j_lo = __ldg(A.T.lk + b_lo);
+        uint32_t j_hi = __ldg(A.T.lk + b_hi) + 1;
+        if (j_hi > n - 1) j_hi = n - 1;
+        want[0] = b0;
+        want[1] = nb;
+        want[2] = j_lo;
+        want[3] = j_hi - j_lo + 1;
+        const bool covered = cur[1] != 0 && b0 >= cur[0] && b0 + nb <= cur[0] + cur[1] &&
+                             j_lo >= cur[2] && j_hi < cur[2] + cur[3];
+        mode = covered ? 0 : (nb <= S.lk_cap && want[3] <= S.j_cap ? 2 : 1);
+      }
+    } else if (threadIdx.x == 0) {
+      want[0] = 0;
+      want[1] = (A.T.nlk + 3) & ~3u;
+      want[2] = 0;
+      want[3] = n;
+      mode = cur[1] != 0 ? 0 : 2;
+    }
+    __syncthreads();
+    if (mode == 2) {  // stage the window with TMA bulk copies
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        cur[0] = want[0];
+        cur[1] = want[1];
+        cur[2] = want[2];
+        cur[3] = want[3];
+        const uint32_t lk_bytes = want[1] * 4;
+        const uint32_t g_bytes = want[3] * grs * 8;
+        const uint32_t e_bytes = WANT_E ? want[3] * 6 * 8 : 0;
+        mbar_expect_tx(&bar, lk_bytes + g_bytes + e_bytes);
+        tma_load_1d(s_lk, A.T.lk + want[0], lk_bytes, &bar);
+        tma_load_1d(s_grec, A.T.grec + static_cast<size_t>(want[2]) * grs, g_bytes, &bar);
+        if (WANT_E) tma_load_1d(s_erec, A.T.erec + static_cast<size_t>(want[2]) * 6, e_bytes, &bar);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      __syncthreads();
+    }
+    if (mode != 1) {
+      const TableWin swin{s_grec, s_erec, s_lk, cur[0], cur[1], cur[2], cur[3]};
+      table_tile<true, MO, KIND, DEG>(A, swin, p0, tc, n_low, n_high);
+    } else {
+      table_tile<false, MO, KIND, DEG>(A, gwin, p0, tc, n_low, n_high);
+    }
+    __syncthreads();  // the window may be restaged for the next tile
+  }
+  for (int o = 16; o; o >>= 1) {
+    n_low += __shfl_xor_sync(0xffffffffu, n_low, o);
+    n_high += __shfl_xor_sync(0xffffffffu, n_high, o);
+  }
+  if (lane == 0 && n_low) atomicAdd(A.counters, n_low);
+  if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
+}
+
 template <class K>
 void launch_kernel(gk_ctx* ctx, K kernel, const FillArgs& a, size_t smem, int threads = kThreads) {
   if (smem > 48 * 1024)
@@ -425,8 +675,61 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
     set_tiling(ctx, a, kRowsPerTile, 2);
     launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 2>, a, smem);
   } else {
-    set_tiling(ctx, a, kRowsPerTile, 2);
-    launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
+    // GK_TABLE_SMEM: 0 = L1 kernel, 2 = always stage (tests), unset/1 = auto.
+    // GK_TABLE_SMEM_BUDGET (bytes) shrinks the window budget (tests).  Read per
+    // launch so a test can exercise every path in one process.
+    const char* env = std::getenv("GK_TABLE_SMEM");
+    const int staging = env ? std::atoi(env) : 1;
+    if (staging == 0) {
+      set_tiling(ctx, a, kRowsPerTile, 2);
+      launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
+      return;
+    }
+    // shared-memory window sizing: whole table if it fits, else proportional caps
+    constexpr bool want_e = KIND == GK_KIND_EXP || KIND == kKindPair;
+    const size_t rec_bytes = static_cast<size_t>(a.T.grs) * 8 + (want_e ? 48 : 0);
+    size_t budget = 200 * 1024;
+    if (const char* b = std::getenv("GK_TABLE_SMEM_BUDGET")) {
+      const long v = std::atol(b);
+      if (v >= 4096 && static_cast<size_t>(v) < budget) budget = static_cast<size_t>(v);
+    }
+    StageArgs S{};
+    const size_t nlk4 = (static_cast<size_t>(a.T.nlk) + 3) & ~size_t(3);
+    if (nlk4 * 4 + a.T.nrec * rec_bytes <= budget) {
+      S.whole = 1;
+      S.lk_cap = static_cast<uint32_t>(nlk4);
+      S.j_cap = a.T.nrec;
+      set_tiling(ctx, a, kStagedWarps, 1);
+    } else {
+      const double per_rec = static_cast<double>(a.T.nlk) / a.T.nrec;  // buckets per record
+      const size_t j_cap = static_cast<size_t>(budget / (rec_bytes + 4.0 * per_rec * 1.5));
+      // records a typical tile window spans; when it clearly exceeds the
+      // capacity (dense tables, e.g. S = 1e4 on large meshes) every tile would
+      // fall back to global reads: use the L1 kernel with its wider tiles
+      const double est = a.T.nrec * a.window_est / (a.T.r_max - a.T.r_min);
+      if (staging != 2 && est > 2.0 * static_cast<double>(j_cap)) {
+        set_tiling(ctx, a, kRowsPerTile, 2);
+        launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
+        return;
+      }
+      S.j_cap = static_cast<uint32_t>(j_cap);
+      S.lk_cap = static_cast<uint32_t>(((budget - j_cap * rec_bytes) / 4) & ~size_t(3));
+      set_tiling(ctx, a, kStagedWarps, 1);
+      // narrow tiles keep each tile's radius window small
+      a.cpt = 2;
+      a.ncb = (a.N + 63) / 64;
+      a.ntiles = ((a.row_end - a.row_begin + kStagedWarps - 1) / kStagedWarps) * a.ncb;
+    }
+    const size_t smem = static_cast<size_t>(S.lk_cap) * 4 + static_cast<size_t>(S.j_cap) * rec_bytes;
+    auto k = table_staged_kernel<MO, KIND, DEG>;
+    GK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    size_t grid = static_cast<size_t>(ctx->sm_count);
+    if (grid > a.ntiles) grid = a.ntiles;
+    if (grid < 1) grid = 1;
+    k<<<static_cast<unsigned>(grid), 32 * kStagedWarps, smem, ctx->stream>>>(a, S);
+    count_launches(1);
+    GK_CUDA(cudaGetLastError());
   }
 }
 
@@ -459,6 +762,10 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   FillArgs a{};
   a.outer = mesh->outer.p;
   a.inner = mesh->inner.p;
+  a.bounds = mesh->bounds.p;
+  a.binner = mesh->binner.p;
+  // 16 rows x 64 columns of spatially ordered triangles span ~ (4 + 8) edges each way
+  a.window_est = 18.0 * mesh->mean_edge;
   a.N = mesh->N;
   a.ipt = 3 * mesh->n;
   a.row_begin = row_begin;

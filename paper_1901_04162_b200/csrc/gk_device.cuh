@@ -38,6 +38,7 @@ struct TableDev {
   double r_min, r_max;
   double inv_w, bias;  // bucket map: x = fma(r, inv_w, bias), b = floor(x)
   uint32_t nlk;
+  uint32_t nrec;  // interval records (= plan nodes; record n-1 is the r_max sentinel)
   int degree;
   int grs;  // Green record stride in doubles = 2 + 2 (degree + 1)
   double k_re, k_im;
@@ -146,6 +147,69 @@ __device__ __forceinline__ void pair_table(double r, const TableDev& t, double2&
     acc.y = __fma_rn(acc.y, u, ck.y);
   }
   g = acc;
+}
+
+// ------------------------------------------- table window (shared memory)
+//
+// The fill's table path evaluates through a TableWin: a contiguous window of
+// lookup buckets [b0, b0 + nb) and interval records [j0, j0 + nj), either the
+// whole table in global memory (SMEM = false, read through L1 with __ldg) or
+// the slice a tile needs, staged into shared memory by a TMA bulk copy
+// (SMEM = true).  Indices are clamped into the window, so any input (out of
+// range, NaN) reads valid memory; in-range radii of the tile are inside the
+// window by construction (monotone bucket map, conservative tile bounds).
+struct TableWin {
+  const double* grec;
+  const double* erec;
+  const uint32_t* lk;
+  uint32_t b0, nb, j0, nj;
+};
+
+template <bool SMEM, class T>
+__device__ __forceinline__ T win_ld(const T* p) {
+  if constexpr (SMEM) return *p;
+  else return __ldg(p);
+}
+
+template <bool SMEM>
+__device__ __forceinline__ uint32_t win_locate(double r, const TableDev& t, const TableWin& w,
+                                               int grs, double& aj) {
+  uint32_t b = lookup_bucket(r, t) - w.b0;
+  b = b < w.nb ? b : w.nb - 1;
+  uint32_t base = win_ld<SMEM>(w.lk + b) - w.j0;
+  base = base < w.nj ? base : w.nj - 1;
+  const double2 ab = win_ld<SMEM>(reinterpret_cast<const double2*>(w.grec + static_cast<size_t>(base) * grs));
+  const bool hi = r >= ab.y;
+  aj = hi ? ab.y : ab.x;
+  const uint32_t j = base + (hi ? 1u : 0u);
+  return j < w.nj ? j : w.nj - 1;
+}
+
+// Green (degree DEG, or runtime degree for DEG = 0), Exp, or both for one r
+template <bool SMEM, int DEG, bool WANT_E, bool WANT_G>
+__device__ __forceinline__ void win_eval(double r, const TableDev& t, const TableWin& w,
+                                         double2& e, double2& g) {
+  const int grs = DEG > 0 ? 2 + 2 * (DEG + 1) : t.grs;
+  const int deg = DEG > 0 ? DEG : t.degree;
+  double aj;
+  const uint32_t j = win_locate<SMEM>(r, t, w, grs, aj);
+  const double u = r - aj;
+  if constexpr (WANT_E) {
+    const double2* ce = reinterpret_cast<const double2*>(w.erec + static_cast<size_t>(j) * 6 + 2);
+    const double2 e0 = win_ld<SMEM>(ce), sl = win_ld<SMEM>(ce + 1);
+    e = make_double2(__fma_rn(sl.x, u, e0.x), __fma_rn(sl.y, u, e0.y));
+  }
+  if constexpr (WANT_G) {
+    const double2* c = reinterpret_cast<const double2*>(w.grec + static_cast<size_t>(j) * grs + 2);
+    double2 acc = win_ld<SMEM>(c + deg);
+#pragma unroll
+    for (int k = deg - 1; k >= 0; --k) {
+      const double2 ck = win_ld<SMEM>(c + k);
+      acc.x = __fma_rn(acc.x, u, ck.x);
+      acc.y = __fma_rn(acc.y, u, ck.y);
+    }
+    g = acc;
+  }
 }
 
 // ------------------------------------------------------------ direct math

@@ -83,6 +83,7 @@ struct gk_mesh {
   size_t N = 0, nv = 0;
   int m = 0, n = 0;
   double diameter = 0.0;  // bounding-box diagonal of the vertices (bounds every pair distance)
+  double mean_edge = 0.0; // edge of the mean-area equilateral triangle (tile window estimate)
   gk::DevBuf<double4> outer;  // [N * m]    (x, y, z, w)
   gk::DevBuf<double4> inner;  // [3n][N]    (x, y, z, w), column-major in q
   gk::DevBuf<double4> bounds; // [N]        (cx, cy, cz, rho_outer), rho_inner in binner

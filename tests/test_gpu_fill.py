@@ -234,3 +234,30 @@ def test_zero_distance_pair_is_domain_error(gk, oracle):
         gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
     with pytest.raises(gk.DomainError):
         gk.fill_matrix(mesh, gk.QuadratureSpec(1, 1), gk.Mode.DIRECT, gk.Medium())
+
+
+@pytest.mark.parametrize("level,S,r_min", [(2, 1000, None), (3, 10000, None), (2, 1000, 0.3)])
+def test_table_staging_paths_bit_identical(gk, monkeypatch, level, S, r_min):
+    """The L1 table kernel, the shared-memory kernel with the whole table staged,
+    with per-tile TMA windows, and with windows overflowing a small budget (global
+    reads inside the staged kernel) all give the same bits, fallbacks included."""
+    import torch
+    mesh = sphere(gk, level)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=r_min or lo, r_max=hi, samples_per_wavelength=S))
+    settings = [("0", None), ("2", None), ("2", "65536"), ("2", "8192")]
+    outs = []
+    for smem, budget in settings:
+        monkeypatch.setenv("GK_TABLE_SMEM", smem)
+        if budget:
+            monkeypatch.setenv("GK_TABLE_SMEM_BUDGET", budget)
+        else:
+            monkeypatch.delenv("GK_TABLE_SMEM_BUDGET", raising=False)
+        ze, zg, rep = gk.fill_rows_pair(dm, gk.Mode.TABLE, table=t)
+        g, rg = gk.fill_rows(dm, gk.Mode.TABLE, table=t, row_begin=7, row_end=dm.N - 3)
+        outs.append((ze, zg, g, rep.fallback_calls, rg.fallback_calls))
+    for o in outs[1:]:
+        assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
+        assert torch.equal(o[2], outs[0][2]) and o[3:] == outs[0][3:]
+    assert (outs[0][3] > 0) == (r_min is not None)
