@@ -133,6 +133,19 @@ gk_status gk_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double
                         double k_im, const double* radii, size_t n, gk_c128* out,
                         uint64_t* fallbacks);
 
+/* Stream-ordered form of gk_eval_batch for pipelines that launch many batches
+   back to back (no host synchronisation per call).  `status` is a DEVICE
+   array of 2 words that accumulates over calls: status[0] += fallbacks,
+   status[1] = min over failing radii of (index << 3 | code).  Initialise it
+   with gk_eval_status_reset and read it with gk_eval_status_read, which
+   synchronises the context stream and fails like gk_eval_batch would have
+   (the index is within the batch that failed). */
+gk_status gk_eval_batch_async(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,
+                              double k_im, const double* radii, size_t n, gk_c128* out,
+                              uint64_t* status);
+gk_status gk_eval_status_reset(gk_ctx* ctx, uint64_t* status);
+gk_status gk_eval_status_read(gk_ctx* ctx, const uint64_t* status, uint64_t* fallbacks);
+
 /* locate (table.hpp:87-102) on the device: for each radius the bracketing
    interval j with a_j <= r < a_{j+1} (r = r_max maps to nodes-2).  radii and
    out are device pointers; a radius outside [r_min, r_max] fails with

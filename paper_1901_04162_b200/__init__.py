@@ -4,17 +4,19 @@ Drop-in for the reference ``gktab`` fill hot path: device table build,
 table lookup/evaluation, direct evaluation and the triangle-pair fill driver,
 all in hand-written CUDA (libgk.so, C ABI in include/gk/gk.h).
 """
-from .gktab import (Context, DeviceMesh, DeviceTable, FillReport, KernelKind, Medium, Mode,
-                    QuadratureSpec, SamplingConfig, TriangleMesh, eval_batch, fill_matrix,
-                    fill_rows, fill_rows_host, fill_rows_pair, generate_plate_mesh, generate_sphere_mesh, jitter,
-                    predicted_calls, wavenumber)
+from .gktab import (Context, DeviceMesh, DeviceTable, EvalStatus, FillReport, KernelKind, Medium,
+                    Mode, QuadratureSpec, SamplingConfig, TriangleMesh, eval_batch,
+                    eval_batch_async, fill_matrix, fill_rows, fill_rows_host, fill_rows_pair,
+                    generate_plate_mesh, generate_sphere_mesh, jitter, predicted_calls,
+                    wavenumber)
 from ._lib import (DomainError, GkError, InvalidArgument, OutOfRange, OverflowErrorGk,
                    RuntimeErrorGk, LIB_PATH)
 
 __all__ = [
-    "Context", "DeviceMesh", "DeviceTable", "FillReport", "KernelKind", "Medium", "Mode",
-    "QuadratureSpec", "SamplingConfig", "TriangleMesh", "eval_batch", "fill_matrix",
-    "fill_rows", "fill_rows_host", "fill_rows_pair", "generate_plate_mesh", "generate_sphere_mesh", "jitter", "predicted_calls",
+    "Context", "DeviceMesh", "DeviceTable", "EvalStatus", "FillReport", "KernelKind", "Medium",
+    "Mode", "QuadratureSpec", "SamplingConfig", "TriangleMesh", "eval_batch", "eval_batch_async",
+    "fill_matrix", "fill_rows", "fill_rows_host", "fill_rows_pair", "generate_plate_mesh",
+    "generate_sphere_mesh", "jitter", "predicted_calls",
     "wavenumber", "DomainError", "GkError", "InvalidArgument", "OutOfRange", "OverflowErrorGk",
     "RuntimeErrorGk", "LIB_PATH",
 ]

@@ -102,6 +102,9 @@ PROTOTYPES = {
     "gk_table_dump_binary": [_vp, C.c_int, C.c_char_p],
     "gk_plan_dump_csv": [_vp, C.c_char_p],
     "gk_eval_batch": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp, _u64p],
+    "gk_eval_batch_async": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp, _vp],
+    "gk_eval_status_reset": [_vp, _vp],
+    "gk_eval_status_read": [_vp, _vp, _u64p],
     "gk_locate": [_vp, _vp, _vp, C.c_size_t, _vp],
     "gk_eval_batch_host": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp,
                            _u64p],

@@ -338,39 +338,92 @@ gk_status gk_table_destroy(gk_table* t) {
   });
 }
 
+namespace {
+
+// validates and enqueues one eval_batch launch accumulating into w[2]
+void enqueue_eval_batch(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re, double k_im,
+                        const double* radii, size_t n, gk_c128* out, unsigned long long* w) {
+  need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
+  if (t) {
+    k_re = t->dev.k_re;
+    k_im = t->dev.k_im;
+  }
+  need(k_re >= 0.0, GK_ERR_INVALID_ARGUMENT, "eval_analytic: k must be >= 0");
+  if (n == 0) return;
+  need(radii && out, GK_ERR_INVALID_ARGUMENT, "null buffer");
+  use_device(c);
+  gk::launch_eval_batch(c, t, kind, k_re, k_im, radii, n, out, w);
+}
+
+// raises the reference's exception for a failing radius recorded in `word`
+void raise_bad_radius(unsigned long long word, const double* radii) {
+  if (word == ~0ull) return;
+  const size_t idx = static_cast<size_t>(word >> 3);
+  const unsigned code = static_cast<unsigned>(word & 7u);
+  double r = 0.0;
+  if (radii) GK_CUDA(cudaMemcpy(&r, radii + idx, sizeof(double), cudaMemcpyDeviceToHost));
+  const char* why = code == 2 ? "exp(-jkr)/r is singular at r = 0"
+                  : code == 3 ? "r outside the tabulated range"
+                              : "r must be >= 0 (Exp) / > 0 (Green)";
+  gk::fail(GK_ERR_INVALID_ARGUMENT, "eval_batch: radius [" + std::to_string(idx) + "]" +
+                                        (radii ? " = " + std::to_string(r) : std::string()) +
+                                        ": " + why);
+}
+
+}  // namespace
+
 gk_status gk_eval_batch(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re, double k_im,
                         const double* radii, size_t n, gk_c128* out, uint64_t* fallbacks) {
   return guarded([&] {
     check_ctx(c);
-    need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
-    if (t) {
-      k_re = t->dev.k_re;
-      k_im = t->dev.k_im;
-    }
-    need(k_re >= 0.0, GK_ERR_INVALID_ARGUMENT, "eval_analytic: k must be >= 0");
     if (fallbacks) *fallbacks = 0;
-    if (n == 0) return;
-    need(radii && out, GK_ERR_INVALID_ARGUMENT, "null buffer");
-    use_device(c);
     unsigned long long* w = c->scratch.p;  // [0] fallbacks, [1] first bad (index<<3 | code)
-    const unsigned long long init[2] = {0ull, ~0ull};
-    GK_CUDA(cudaMemcpyAsync(w, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-    gk::launch_eval_batch(c, t, kind, k_re, k_im, radii, n, out, w);
+    if (n) {
+      use_device(c);
+      const unsigned long long init[2] = {0ull, ~0ull};
+      GK_CUDA(cudaMemcpyAsync(w, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    }
+    enqueue_eval_batch(c, t, kind, k_re, k_im, radii, n, out, w);
+    if (n == 0) return;
     unsigned long long res[2];
     GK_CUDA(cudaMemcpyAsync(res, w, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
     GK_CUDA(cudaStreamSynchronize(c->stream));
     if (fallbacks) *fallbacks = res[0];
-    if (res[1] != ~0ull) {
-      const size_t idx = static_cast<size_t>(res[1] >> 3);
-      const unsigned code = static_cast<unsigned>(res[1] & 7u);
-      double r = 0.0;
-      GK_CUDA(cudaMemcpy(&r, radii + idx, sizeof(double), cudaMemcpyDeviceToHost));
-      const char* why = code == 2 ? "exp(-jkr)/r is singular at r = 0"
-                      : code == 3 ? "r outside the tabulated range"
-                                  : "r must be >= 0 (Exp) / > 0 (Green)";
-      gk::fail(GK_ERR_INVALID_ARGUMENT, "eval_batch: radius [" + std::to_string(idx) + "] = " +
-                                            std::to_string(r) + ": " + why);
-    }
+    raise_bad_radius(res[1], radii);
+  });
+}
+
+gk_status gk_eval_batch_async(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
+                              double k_im, const double* radii, size_t n, gk_c128* out,
+                              uint64_t* status) {
+  return guarded([&] {
+    check_ctx(c);
+    need(status != nullptr, GK_ERR_INVALID_ARGUMENT, "null status");
+    enqueue_eval_batch(c, t, kind, k_re, k_im, radii, n, out,
+                       reinterpret_cast<unsigned long long*>(status));
+  });
+}
+
+gk_status gk_eval_status_reset(gk_ctx* c, uint64_t* status) {
+  return guarded([&] {
+    check_ctx(c);
+    need(status != nullptr, GK_ERR_INVALID_ARGUMENT, "null status");
+    use_device(c);
+    GK_CUDA(cudaMemsetAsync(status, 0, sizeof(uint64_t), c->stream));
+    GK_CUDA(cudaMemsetAsync(status + 1, 0xff, sizeof(uint64_t), c->stream));
+  });
+}
+
+gk_status gk_eval_status_read(gk_ctx* c, const uint64_t* status, uint64_t* fallbacks) {
+  return guarded([&] {
+    check_ctx(c);
+    need(status != nullptr, GK_ERR_INVALID_ARGUMENT, "null status");
+    use_device(c);
+    uint64_t res[2];
+    GK_CUDA(cudaMemcpyAsync(res, status, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    if (fallbacks) *fallbacks = res[0];
+    raise_bad_radius(res[1], nullptr);
   });
 }
 

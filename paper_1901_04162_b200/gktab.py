@@ -318,6 +318,42 @@ def eval_batch(kind: KernelKind, radii, table: DeviceTable | None = None, k: com
     return out
 
 
+class EvalStatus:
+    """Device-resident status of stream-ordered eval_batch calls
+    (gk_eval_batch_async): fallback count and the first failing radius."""
+
+    def __init__(self, ctx: Context | None = None):
+        torch = _torch()
+        self.ctx = ctx or Context.get()
+        self.words = torch.empty(2, dtype=torch.int64, device=f"cuda:{self.ctx.device}")
+        self.reset()
+
+    def reset(self) -> None:
+        check(lib().gk_eval_status_reset(self.ctx.h, self.words.data_ptr()), "eval_status")
+
+    def read(self) -> int:
+        """Synchronises; raises like eval_batch if any radius was invalid; returns fallbacks."""
+        fb = C.c_uint64()
+        check(lib().gk_eval_status_read(self.ctx.h, self.words.data_ptr(), C.byref(fb)),
+              "eval_batch")
+        return fb.value
+
+
+def eval_batch_async(kind: KernelKind, radii, out, status: EvalStatus,
+                     table: DeviceTable | None = None, k: complex = 0.0) -> None:
+    """Stream-ordered eval_batch into a preallocated complex128 ``out``; errors
+    and fallbacks accumulate in ``status`` (no host synchronisation)."""
+    ctx = status.ctx
+    kc = complex(k)
+    n = radii.numel()
+    if out.numel() < n or out.dtype != _torch().complex128 or radii.dtype != _torch().float64:
+        raise _lib.InvalidArgument("eval_batch_async: float64 radii and complex128 out[n]")
+    check(lib().gk_eval_batch_async(ctx.h, table.h if table else None, int(kind), kc.real, kc.imag,
+                                    radii.data_ptr() if n else None, n,
+                                    out.data_ptr() if n else None, status.words.data_ptr()),
+          "eval_batch")
+
+
 class DeviceMesh:
     """A mesh resident on the device with its quadrature points (K0)."""
 

@@ -197,3 +197,30 @@ def test_wire_formats_readable_by_reference(gk, oracle, ref, tmp_path):
         want = e if kind == EXP else g
         assert np.all(np.abs(v - want) <= 4 * ULP * np.abs(want))
         assert np.array_equal(v, d["exp"] if kind == EXP else d["green"])
+
+
+def test_eval_batch_async_matches_sync_and_reports(gk, oracle):
+    """gk_eval_batch_async: same bits as gk_eval_batch; fallbacks and the first
+    bad radius accumulate in the device status and raise at read()."""
+    import torch
+    t, ev, r = _c1(gk, oracle, 1000, n=1 << 16, lo=1e-4)
+    rd = torch.as_tensor(r, device="cuda:0")
+    st = gk.EvalStatus(t.ctx)
+    f0 = t.fallbacks
+    for kind in (gk.KernelKind.PlainExp, gk.KernelKind.GreenOverR):
+        out = torch.empty(r.size, dtype=torch.complex128, device="cuda:0")
+        gk.eval_batch_async(kind, rd, out, st, table=t)
+        assert torch.equal(out, t.eval_batch(kind, rd))
+    fb_sync = t.fallbacks - f0
+    assert fb_sync > 0 and st.read() == fb_sync
+    bad = rd.clone()
+    bad[9] = 3.0     # above r_max
+    bad[5] = -1.0
+    st.reset()
+    out = torch.empty(r.size, dtype=torch.complex128, device="cuda:0")
+    gk.eval_batch_async(gk.KernelKind.GreenOverR, bad, out, st, table=t)
+    with pytest.raises(gk.InvalidArgument, match=r"\[5\]"):
+        st.read()
+    st.reset()
+    gk.eval_batch_async(gk.KernelKind.PlainExp, rd, out, st, k=2.0)  # direct: no fallbacks
+    assert st.read() == 0
