@@ -131,16 +131,68 @@ struct InnerWalk {
   }
 };
 
-// K4: direct evaluation.  Per eval: 6 (r^2) + 6 (rsqrt, r) + 12 (phase,
-// table lookup, complex combine) + 3 (weight, accumulate) = 27 FP64 ops.
+// --------------------------------------------------- TMA bulk-copy helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// one-shot copy of `bytes` (multiple of 16, 16 B aligned) global -> shared,
+// issued by thread 0 as a TMA bulk copy; every thread waits on the mbarrier
+__device__ __forceinline__ void stage_bulk(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    mbar_init(bar);
+    mbar_expect_tx(bar, bytes);
+    tma_load_1d(dst, src, bytes, bar);
+  }
+  __syncthreads();  // barrier initialised before anyone polls it
+  mbar_wait(bar, 0);
+}
+
+// K4: direct evaluation.  Per eval: 6 (r^2) + 6 (rsqrt, r) + 11 (phase,
+// table lookup, complex combine) + 3 (weight, accumulate) = 26 FP64 ops.
 // The warp's outer points sit in shared memory (broadcast loads, one
 // wavefront each) instead of registers, so ~80 registers per thread allow 3
 // CTAs (24 warps) per SM to hide the FP64 dependency latency.
 template <int MO, int KIND, bool LOSSY, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A) {
-  extern __shared__ double2 tab[];  // kPhaseM phase entries (64 KB) [+ attenuation table]
+  extern __shared__ double2 tab[];  // kPhaseM phase entries (128 KB) [+ attenuation table]
   __shared__ double so[kRowsPerTile][MO][4];
-  for (int i = threadIdx.x; i < kPhaseM; i += blockDim.x) tab[i] = A.phase[i];
+  __shared__ uint64_t bar;
+  stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
   double* att = reinterpret_cast<double*>(tab + kPhaseM);
   if constexpr (LOSSY)
     for (int i = threadIdx.x; i < A.natten; i += blockDim.x) att[i] = A.atten[i];
@@ -219,9 +271,10 @@ __host__ __device__ constexpr int warps_v4() { return KIND == kKindPair ? 8 : 12
 template <int MO, int IPT, int KIND, bool LOSSY>
 __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(const FillArgs A) {
   constexpr int kWarpsV4 = warps_v4<KIND>();
-  extern __shared__ double2 tab[];  // kPhaseM phase entries (64 KB) [+ attenuation table]
+  extern __shared__ double2 tab[];  // kPhaseM phase entries (128 KB) [+ attenuation table]
   __shared__ double sw[kWarpsV4][MO];
-  for (int i = threadIdx.x; i < kPhaseM; i += blockDim.x) tab[i] = A.phase[i];
+  __shared__ uint64_t bar;
+  stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
   double* att = reinterpret_cast<double*>(tab + kPhaseM);
   if constexpr (LOSSY)
     for (int i = threadIdx.x; i < A.natten; i += blockDim.x) att[i] = A.atten[i];
@@ -390,41 +443,6 @@ struct StageArgs {
   int whole;               // the whole table fits: stage once
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
 
 // the fill of one tile through a table window (shared or global)
 template <bool SMEM, int MO, int KIND, int DEG>

@@ -27,9 +27,15 @@ constexpr double kMagic52 = 4503599627370496.0;   // 2^52
 constexpr double kMagicRint = 6755399441055744.0; // 1.5 * 2^52
 
 // Direct-mode phase table size: e^{-j theta} = e^{-j 2pi idx/M} e^{-j delta},
-// |delta| <= pi/M = 7.7e-4.  The dropped Taylor terms (delta^6/720 in cos,
-// delta^5/120 in sin) stay below 2.2e-18, i.e. < 0.02 ulp of the result.
-constexpr int kPhaseM = 4096;
+// |delta| <= D = pi/M = 3.8e-4 (128 KB of shared memory).  sin delta =
+// delta - delta^3/6 (dropped delta^5/120 < 7e-20); cos delta - 1 = c delta^2
+// with c the minimax constant on [0, D^2] (kCosMinimax): max error
+// 0.00715 D^4 = 1.5e-16 (0.7 ulp of 1) for one DMUL instead of FMA + DMUL.
+constexpr int kPhaseM = 8192;
+// c = -1/2 + b D^2, b = (sqrt 2 - 1)/12: the error x(-1/2 - c) + x^2/24,
+// x = delta^2, equioscillates at x = D^2 and x = -12(-1/2 - c)
+constexpr double kPhaseD = kPi / kPhaseM;
+constexpr double kCosMinimax = -0.5 + (1.4142135623730951 - 1.0) / 12.0 * kPhaseD * kPhaseD;
 
 struct TableDev {
   const double* grec;  // Green interval records
@@ -218,12 +224,11 @@ __device__ __forceinline__ void win_eval(double r, const TableDev& t, const Tabl
 // shared memory: phi = r K1 (K1 = k M / 2pi), n = rint(phi) (1.5 2^52 magic
 // add), f = phi - n in [-1/2, 1/2], delta = 2pi f / M;
 //   cos(theta0 + delta) = C0 (1 + v) - S0 s,  sin(theta0 + delta) = S0 (1 + v) + C0 s
-// with v = cos(delta) - 1 = -delta^2/2 + delta^4/24 and s = delta - delta^3/6.
-// Returns (Re, -Im) of exp(-j k r) = (cos kr, sin kr): 12 FP64 ops + 1 LDS.128.
+// with v = cos(delta) - 1 = kCosMinimax delta^2 and s = delta - delta^3/6.
+// Returns (Re, -Im) of exp(-j k r) = (cos kr, sin kr): 11 FP64 ops + 1 LDS.128.
 __device__ __forceinline__ double2 cis_phase(double r, double K1, const double2* tab) {
   constexpr double C = 2.0 * kPi / kPhaseM;
-  constexpr double a1 = -C * C / 2.0;
-  constexpr double a2 = C * C * C * C / 24.0;
+  constexpr double a1 = kCosMinimax * C * C;
   constexpr double s1 = C;
   constexpr double s3 = -C * C * C / 6.0;
   const double t = __fma_rn(r, K1, kMagicRint);
@@ -231,7 +236,7 @@ __device__ __forceinline__ double2 cis_phase(double r, double K1, const double2*
   const double f = __fma_rn(r, K1, -nf);
   const int idx = __double2loint(t) & (kPhaseM - 1);
   const double g = __dmul_rn(f, f);
-  const double v = __dmul_rn(g, __fma_rn(a2, g, a1));
+  const double v = __dmul_rn(a1, g);
   const double s = __dmul_rn(f, __fma_rn(s3, g, s1));
   const double2 T = tab[idx];
   const double c = __fma_rn(-T.y, s, __fma_rn(T.x, v, T.x));
