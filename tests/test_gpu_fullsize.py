@@ -1,0 +1,116 @@
+"""Parity at BASELINE.json's full sizes (C2-C5), on sampled row blocks.
+
+A full C5 matrix is 107 GB and ~4.8e11 evaluations: too large for a CPU
+check, but every row is independent (matfill.hpp:169-203).  So each config
+is filled on the device for three 2-row blocks (first, middle and last rows)
+against the FULL mesh.  The same rows are computed on the CPU by
+ * the reference itself (oracle/_ref, AnalyticKernel through the reference's
+   own staging loop: gr_fill_sampled_rows) for direct mode, real k;
+ * the oracle (pinned bitwise to the reference, test_oracle_vs_ref.py) for
+   complex k (C4) and for table mode on the device table's own plan.
+Tolerance: the per-entry bound B_pq of tests/test_gpu_fill.py.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.pyoracle import DIRECT, TABLE
+
+pytestmark = pytest.mark.gpu
+ULPS = 64.0
+
+CONFIGS = {  # BASELINE.json configs[1..4]
+    "c2": dict(level=3, m=6, n=4, lambda0=1.0),
+    "c3": dict(level=5, m=7, n=5, lambda0=0.3),
+    "c4": dict(plate=100, m=6, n=4, lambda0=1.0, eps_r=4.0, eps_r_im=-0.4),
+    "c5": dict(level=6, m=6, n=4, lambda0=0.15),
+}
+
+
+def _mesh(gk, c):
+    if "plate" in c:
+        return gk.generate_plate_mesh(1.0, c["plate"])
+    return gk.jitter(gk.generate_sphere_mesh(1.0, c["level"]), 1901, 1e-3)
+
+
+def _row_blocks(N):
+    return [(0, 2), (N // 2, N // 2 + 2), (N - 2, N)]
+
+
+@pytest.fixture(scope="module", params=sorted(CONFIGS))
+def case(request, gk):
+    c = CONFIGS[request.param]
+    mesh = _mesh(gk, c)
+    med = gk.Medium(lambda0=c["lambda0"], eps_r=c.get("eps_r", 1.0),
+                    eps_r_im=c.get("eps_r_im", 0.0))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(c["m"], c["n"]))
+    return request.param, c, mesh, med, dm
+
+
+def test_direct_fullsize_vs_reference(gk, oracle, ref, case):
+    name, c, mesh, med, dm = case
+    k = gk.wavenumber(med)
+    kc = complex(k)
+    m, n, N = c["m"], c["n"], mesh.triangle_count()
+    for rb, re in _row_blocks(N):
+        z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, row_begin=rb, row_end=re)
+        z = z.cpu().numpy()
+        if kc.imag == 0.0:   # the reference itself
+            want, calls, _ = ref.fill_sampled_rows(mesh.vertices, mesh.triangles, m, n, DIRECT,
+                                                   kc.real, np.arange(rb, re), threads=8)
+            assert calls == rep.actual_calls
+        else:                # complex k: the oracle restatement (no reference path)
+            want, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, DIRECT, kc.real,
+                                       k_im=kc.imag, threads=8, row_begin=rb, row_end=re)
+        B = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, None, abs(kc), ULPS,
+                                row_begin=rb, row_end=re)
+        err = np.abs(z - want)
+        assert np.all(err <= B), (name, rb, float(np.max(err / np.maximum(B, 1e-300))))
+        assert rep.actual_calls == 3 * m * n * (re - rb) * (N - 1)
+        for r in range(rb, re):
+            assert z[r - rb, r] == 0
+
+
+@pytest.mark.parametrize("S", [1000, 10000])
+def test_table_fullsize_vs_oracle(gk, oracle, case, S):
+    name, c, mesh, med, dm = case
+    m, n, N = c["m"], c["n"], mesh.triangle_count()
+    lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S), med)
+    d = t.download()
+    kc = complex(t.k)
+    ev = oracle.evaluator(oracle.make_plan(d["abscissae"], d["zeros"]), kc.real, k_im=kc.imag)
+    for rb, re in _row_blocks(N):
+        z, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t, row_begin=rb, row_end=re)
+        z = z.cpu().numpy()
+        ref_d, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, DIRECT, kc.real,
+                                    k_im=kc.imag, threads=8, row_begin=rb, row_end=re)
+        ref_t, orep = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, TABLE, kc.real,
+                                       ev=ev, k_im=kc.imag, threads=8, row_begin=rb, row_end=re)
+        B_t = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, ev, abs(kc), ULPS,
+                                  row_begin=rb, row_end=re)
+        B_d = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, None, abs(kc), ULPS,
+                                  row_begin=rb, row_end=re)
+        assert np.all(np.abs(z - ref_d) <= B_t), (name, S, rb)
+        assert np.all(np.abs(z - ref_t) <= B_d), (name, S, rb)   # same plan: rounding only
+        assert rep.fallback_calls == orep.fallback_calls == 0   # K1 range is exact
+
+
+def test_row_blocks_tile_the_full_matrix_checksum(gk, case):
+    """Size-independent property at full size: filling [0, N) in one call and
+    in 3 uneven row blocks gives bitwise the same rows (sum of |Z| checked
+    block by block, plus the full row equality of the block seams)."""
+    import torch
+    name, c, mesh, med, dm = case
+    if name == "c5":
+        pytest.skip("C5 full Z is 107 GB; covered by the sampled-row tests and bench")
+    k = gk.wavenumber(med)
+    N = dm.N
+    full, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k)
+    cuts = [0, N // 3 + 1, (2 * N) // 3 - 5, N]
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        part, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, row_begin=b, row_end=e)
+        assert torch.equal(part, full[b:e])
+    assert torch.all(torch.diagonal(full) == 0)
+    assert math.isfinite(float(full.abs().sum()))
