@@ -2,6 +2,7 @@
 // orchestration behind it.  Every entry point converts exceptions into
 // gk_status codes that mirror the reference's exception types; the message
 // is kept in a thread-local buffer for gk_last_error().
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <complex>
@@ -679,10 +680,16 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
     k_im = table->dev.k_im;
   }
   const size_t row_bytes = nt * sizeof(gk_c128);
+  // chunk sizes grow geometrically from ~32 MB to 1 GiB: the copy engine
+  // starts after a sub-millisecond first fill instead of a 1 GiB one, then
+  // every copy overlaps the (faster) fill of the next chunk
   size_t chunk = (size_t(1) << 30) / row_bytes;
   if (chunk < 8) chunk = 8;
   if (chunk > row_end - row_begin) chunk = row_end - row_begin;
   if (chunk == 0) chunk = 1;
+  size_t first = (size_t(32) << 20) / row_bytes;
+  if (first < 8) first = 8;
+  if (first > chunk) first = chunk;
   cudaStream_t copy = nullptr;
   gk_c128* dz[2] = {nullptr, nullptr};
   cudaEvent_t filled[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
@@ -706,9 +713,9 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
     unsigned long long* cnt = c->scratch.p + 16;
     GK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
-    size_t idx = 0;
-    for (size_t rb = row_begin; rb < row_end; rb += chunk, ++idx) {
-      const size_t re = rb + chunk < row_end ? rb + chunk : row_end;
+    size_t idx = 0, step = first;
+    for (size_t rb = row_begin; rb < row_end; rb += step, step = std::min(chunk, 2 * step), ++idx) {
+      const size_t re = rb + step < row_end ? rb + step : row_end;
       const int b = static_cast<int>(idx & 1);
       if (idx >= 2) GK_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
       gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt, cnt);
