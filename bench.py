@@ -60,9 +60,8 @@ def make_mesh(gk, cfg):
 
 def rows_of(rank, world, N):
     """contiguous row blocks, chunk = ceil(N / world) (matfill.hpp:211-215)"""
-    chunk = (N + world - 1) // world
-    b = min(N, rank * chunk)
-    return b, min(N, b + chunk)
+    from paper_1901_04162_b200.sharding import rows_of as _rows_of
+    return _rows_of(rank, world, N)
 
 
 class ClockSampler:
@@ -218,6 +217,8 @@ def main():
     ap.add_argument("--e2e", type=int, default=1)
     ap.add_argument("--vs-n", type=int, default=1, help="also time C2/C3 fills (rank 0, N=1)")
     ap.add_argument("--c1", type=int, default=1, help="also time standalone eval_batch (C1)")
+    ap.add_argument("--gather", type=int, default=1,
+                    help="N > 1: also time the gather of Z to rank 0 (reported apart)")
     ap.add_argument("--S-alt", type=int, default=1000,
                     help="also time the table mode at this S (0 = off)")
     args = ap.parse_args()
@@ -239,6 +240,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     import paper_1901_04162_b200 as gk
+    from paper_1901_04162_b200 import sharding
     from paper_1901_04162_b200._lib import lib as _gk_lib
     gk_lib = _gk_lib()
 
@@ -258,11 +260,7 @@ def main():
 
     def global_range():
         lo, hi = dmesh.distance_range(rb, re) if rows else (math.inf, 0.0)
-        if world > 1:
-            t = torch.tensor([lo, -hi], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MIN)   # C1: one 16-byte all-reduce
-            lo, hi = float(t[0]), -float(t[1])
-        return lo, hi
+        return sharding.global_distance_range(lo, hi, device=f"cuda:{local}")
 
     fill_ev = []
 
@@ -375,6 +373,10 @@ def main():
     if args.vs_n and rank == 0 and world == 1 and args.config == "c5":
         vs_n = run_vs_n(gk, ctx, chosen, args)
 
+    gather = None
+    if world > 1 and args.gather:
+        gather = run_gather(sharding, Z, N, rows, local, dist)
+
     c1 = None
     if args.c1 and rank == 0 and world == 1:
         c1 = run_c1(gk, ctx)
@@ -423,6 +425,8 @@ def main():
         line["vs_N"] = vs_n
     if c1:
         line["c1_eval_batch"] = c1
+    if gather:
+        line["gather"] = gather
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -464,10 +468,8 @@ def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals, rank, wor
         t = None
         if m == gk.Mode.TABLE:
             lo, hi = dm.distance_range(rb, re) if rows else (math.inf, 0.0)
-            if world > 1:
-                tt = torch.tensor([lo, -hi], dtype=torch.float64, device=f"cuda:{ctx.device}")
-                dist.all_reduce(tt, op=dist.ReduceOp.MIN)
-                lo, hi = float(tt[0]), -float(tt[1])
+            from paper_1901_04162_b200.sharding import global_distance_range
+            lo, hi = global_distance_range(lo, hi, device=f"cuda:{ctx.device}")
             t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
                                                  samples_per_wavelength=args.S), medium, ctx=ctx)
         for b in range(rb, re, rows_win):
@@ -493,6 +495,34 @@ def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals, rank, wor
                     f"per rank: gk_mesh_create + gk_fill_rows_host x{(rows + rows_win - 1) // rows_win}"
                     f" -> {rows_win}-row pinned host window"),
             "timing": "host wall clock per step, max over ranks"}
+
+
+def run_gather(sharding, Z, N, rows, local, dist):
+    """Optional gather of all row blocks of Z to rank 0 (NCCL send/recv over
+    NVLink), timed apart from the fill.  Skipped when the
+    full matrix does not fit next to rank 0's own block."""
+    import torch
+    need = N * N * 16
+    ok = torch.tensor([1.0 if torch.cuda.mem_get_info(local)[0] > need + (4 << 30) else 0.0],
+                      device=f"cuda:{local}")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() == 0:
+        return {"skipped": f"full Z ({need / 1e9:.1f} GB) does not fit rank 0's free memory"}
+    out = torch.empty((N, N), dtype=torch.complex128, device=f"cuda:{local}") \
+        if dist.get_rank() == 0 else None
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sharding.gather_rows(Z[:rows] if rows else Z[:0], N, dst=0, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    del out
+    return {"ms": ms, "bytes": need, "gbs": need / (ms * 1e-3) / 1e9,
+            "how": "row blocks sent to rank 0 (torch.distributed send/irecv over NCCL)"}
 
 
 def hbm_peak_gbs():

@@ -1,9 +1,10 @@
-"""The N > 1 path of bench.py on CPU (gloo, world_size 2), with the oracle as
-the per-rank compute: each rank takes bench.rows_of(rank, world, N), computes
-its K1 distance range, one 16-byte all-reduce (MIN of {r_min, -r_max}) gives
-the global range, every rank builds the identical plan from it, fills its own
-rows, and the union of the row blocks equals the single-process fill bit for
-bit (the GPU-side union property is tests/test_gpu_fill.py)."""
+"""The N > 1 path (paper_1901_04162_b200.sharding, used by bench.py) on CPU
+(gloo, world_size 2 and 3), with the oracle as the per-rank compute: each rank
+takes rows_of(rank, world, N), computes its K1 distance range, one 16-byte
+all-reduce (global_distance_range) gives the global range, every rank builds
+the identical plan from it, fills its own rows, gather_rows collects the
+blocks on rank 0, and the result equals the single-process fill bit for bit
+(the GPU-side union property is tests/test_gpu_fill.py)."""
 import math
 import os
 import socket
@@ -30,17 +31,15 @@ def _worker(rank, world, port, out_dir):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    import bench
+    from paper_1901_04162_b200 import sharding
     from oracle.pyoracle import DIRECT, TABLE, Oracle, SamplingConfig
     o = Oracle()
     v, t = o.sphere_mesh(1.0, 1)
     v = o.jitter(v, 1901, 1e-3)
     N = t.shape[0]
-    rb, re = bench.rows_of(rank, world, N)
+    rb, re = sharding.rows_of(rank, world, N)
     lo, hi = o.distance_range(v, t, 6, 4, rb, re)
-    rng = torch.tensor([lo, -hi], dtype=torch.float64)
-    dist.all_reduce(rng, op=dist.ReduceOp.MIN)
-    glo, ghi = float(rng[0]), -float(rng[1])
+    glo, ghi = sharding.global_distance_range(lo, hi)
     plan = o.build_plan(SamplingConfig(r_min=glo, r_max=ghi, samples_per_wavelength=2000))
     digest = torch.tensor([float(plan.abscissae.size), float(plan.abscissae.sum())],
                           dtype=torch.float64)
@@ -49,6 +48,11 @@ def _worker(rank, world, port, out_dir):
     ev = o.evaluator(plan, 2 * math.pi)
     zt, rept = o.fill_rows(v, t, 6, 4, TABLE, 2 * math.pi, ev=ev, row_begin=rb, row_end=re)
     zd, repd = o.fill_rows(v, t, 6, 4, DIRECT, 2 * math.pi, row_begin=rb, row_end=re)
+    full = sharding.gather_rows(torch.from_numpy(zd), N, dst=0)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "gathered.npy"), full.numpy())
+    else:
+        assert full is None
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), zt=zt, zd=zd, rb=rb, re=re, lo=glo, hi=ghi,
              digests=torch.stack(digests).numpy(), calls=rept.actual_calls,
              fb=rept.fallback_calls)
@@ -56,8 +60,8 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_two_rank_row_sharding_matches_single_process(tmp_path, oracle):
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharding_matches_single_process(tmp_path, oracle, world):
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     parts = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
     v, t = oracle.sphere_mesh(1.0, 1)
@@ -67,8 +71,9 @@ def test_two_rank_row_sharding_matches_single_process(tmp_path, oracle):
     for p in parts:   # the all-reduced range is the global one, on every rank
         assert float(p["lo"]) == lo and float(p["hi"]) == hi
         assert np.array_equal(p["digests"][0], p["digests"][1])  # identical tables
-    assert int(parts[0]["rb"]) == 0 and int(parts[0]["re"]) == int(parts[1]["rb"])
-    assert int(parts[1]["re"]) == N
+    assert int(parts[0]["rb"]) == 0 and int(parts[-1]["re"]) == N
+    for a, b in zip(parts[:-1], parts[1:]):
+        assert int(a["re"]) == int(b["rb"])
     from oracle.pyoracle import DIRECT, TABLE, SamplingConfig
     plan = oracle.build_plan(SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=2000))
     ev = oracle.evaluator(plan, 2 * math.pi)
@@ -76,6 +81,7 @@ def test_two_rank_row_sharding_matches_single_process(tmp_path, oracle):
     zd, _ = oracle.fill_rows(v, t, 6, 4, DIRECT, 2 * math.pi, threads=4)
     assert np.array_equal(np.concatenate([p["zt"] for p in parts]), zt)
     assert np.array_equal(np.concatenate([p["zd"] for p in parts]), zd)
+    assert np.array_equal(np.load(tmp_path / "gathered.npy"), zd)   # gather_rows on rank 0
     assert sum(int(p["calls"]) for p in parts) == 3 * 6 * 4 * N * (N - 1)
     assert all(int(p["fb"]) == 0 for p in parts)
 
