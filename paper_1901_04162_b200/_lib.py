@@ -9,7 +9,10 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgk.so")
+# GK_LIB: an alternative in-tree build of the same library (kernel A/B
+# experiments, scripts/build_variant.sh); default: the package's libgk.so
+LIB_PATH = os.environ.get("GK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                    "libgk.so")
 
 GK_OK = 0
 

@@ -265,8 +265,11 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
 // for two, so this variant's ~9 non-FP64 instructions/eval (vs ~16 in the
 // runtime-IPT kernel) are worth ~12% (ablations: scripts/direct_variants.cu).
 // (The fused pair fill carries twice the accumulators: 8 warps, ~200 registers.)
+#ifndef GK_WARPS_V4
+#define GK_WARPS_V4 12  // scripts/build_variant.sh experiments override it
+#endif
 template <int KIND>
-__host__ __device__ constexpr int warps_v4() { return KIND == kKindPair ? 8 : 12; }
+__host__ __device__ constexpr int warps_v4() { return KIND == kKindPair ? 8 : GK_WARPS_V4; }
 
 template <int MO, int IPT, int KIND, bool LOSSY>
 __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(const FillArgs A) {

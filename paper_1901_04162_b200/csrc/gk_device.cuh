@@ -37,6 +37,13 @@ constexpr int kPhaseM = 8192;
 constexpr double kPhaseD = kPi / kPhaseM;
 constexpr double kCosMinimax = -0.5 + (1.4142135623730951 - 1.0) / 12.0 * kPhaseD * kPhaseD;
 
+// read-only double4 load (two 16 B loads; __ldg has no double4 overload)
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
 struct TableDev {
   const double* grec;  // Green interval records
   const double* erec;  // Exp interval records
