@@ -222,6 +222,20 @@ gk_status gk_fill_rows_host(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode,
                             size_t row_begin, size_t row_end, gk_c128* z_host, size_t ldz_host,
                             gk_fill_report* report);
 
+/* compare_fills (matfill.hpp:237-254) on DEVICE matrices: componentwise max
+   relative error of test against ref over `rows` rows of an N-column block
+   whose first row is matrix row row_begin (leading dimension ld), skipping
+   the diagonal (p == q) and exactly-zero ref components, like the reference
+   (NaN errors are ignored as std::max ignores them). */
+gk_status gk_compare_fills(gk_ctx* ctx, const gk_c128* test, const gk_c128* ref, size_t rows,
+                           size_t N, size_t row_begin, size_t ld, double* max_rel_re,
+                           double* max_rel_im);
+
+/* max_vertex_distance (mesh.hpp:62-68) of a device mesh: exact O(V^2) scan,
+   bit-identical to the reference (its r_max convention in bench_compare,
+   matfill.hpp:270, is 1.01 x this). */
+gk_status gk_max_vertex_distance(gk_ctx* ctx, const gk_mesh* mesh, double* out);
+
 /* predicted_calls (matfill.hpp:50-56): 3 m n N^2 with the overflow guard */
 gk_status gk_predicted_calls(uint64_t N, uint64_t m, uint64_t n, uint64_t* out);
 

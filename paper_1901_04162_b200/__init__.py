@@ -5,7 +5,8 @@ table lookup/evaluation, direct evaluation and the triangle-pair fill driver,
 all in hand-written CUDA (libgk.so, C ABI in include/gk/gk.h).
 """
 from .gktab import (Context, DeviceMesh, DeviceTable, EvalStatus, FillReport, KernelKind, Medium,
-                    Mode, QuadratureSpec, SamplingConfig, TriangleMesh, eval_batch,
+                    Mode, QuadratureSpec, SamplingConfig, TriangleMesh, bench_compare,
+                    compare_fills, eval_batch,
                     eval_batch_async, fill_matrix, fill_rows, fill_rows_host, fill_rows_pair,
                     generate_plate_mesh, generate_sphere_mesh, jitter, predicted_calls,
                     wavenumber)
@@ -14,7 +15,8 @@ from ._lib import (DomainError, GkError, InvalidArgument, OutOfRange, OverflowEr
 
 __all__ = [
     "Context", "DeviceMesh", "DeviceTable", "EvalStatus", "FillReport", "KernelKind", "Medium",
-    "Mode", "QuadratureSpec", "SamplingConfig", "TriangleMesh", "eval_batch", "eval_batch_async",
+    "Mode", "QuadratureSpec", "SamplingConfig", "TriangleMesh", "bench_compare", "compare_fills",
+    "eval_batch", "eval_batch_async",
     "fill_matrix", "fill_rows", "fill_rows_host", "fill_rows_pair", "generate_plate_mesh",
     "generate_sphere_mesh", "jitter", "predicted_calls",
     "wavenumber", "DomainError", "GkError", "InvalidArgument", "OutOfRange", "OverflowErrorGk",

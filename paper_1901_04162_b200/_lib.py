@@ -125,6 +125,8 @@ PROTOTYPES = {
     "gk_fill_rows_host": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_double, C.c_size_t,
                           C.c_size_t, _vp, C.c_size_t, C.POINTER(FillReportC)],
     "gk_predicted_calls": [C.c_uint64, C.c_uint64, C.c_uint64, _u64p],
+    "gk_compare_fills": [_vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp],
+    "gk_max_vertex_distance": [_vp, _vp, _dp],
     "gk_sphere_mesh": [C.c_double, C.c_int, _vp, _szp, _vp, _szp],
     "gk_plate_mesh": [C.c_double, C.c_int, _vp, _szp, _vp, _szp],
     "gk_jitter": [_vp, C.c_size_t, C.c_uint64, C.c_double],

@@ -394,6 +394,47 @@ gk_status gk_eval_batch(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
   });
 }
 
+gk_status gk_compare_fills(gk_ctx* c, const gk_c128* test, const gk_c128* ref, size_t rows,
+                           size_t N, size_t row_begin, size_t ld, double* max_rel_re,
+                           double* max_rel_im) {
+  return guarded([&] {
+    check_ctx(c);
+    need(ld >= N, GK_ERR_INVALID_ARGUMENT, "compare_fills: ld < N");
+    need(rows == 0 || N == 0 || (test && ref), GK_ERR_INVALID_ARGUMENT, "null matrix");
+    double re = 0.0, im = 0.0;
+    if (rows && N) {
+      use_device(c);
+      unsigned long long* w = c->scratch.p + 24;
+      GK_CUDA(cudaMemsetAsync(w, 0, 2 * sizeof(unsigned long long), c->stream));
+      gk::launch_compare(c, test, ref, rows, N, row_begin, ld, w);
+      unsigned long long h[2];
+      GK_CUDA(cudaMemcpyAsync(h, w, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+      GK_CUDA(cudaStreamSynchronize(c->stream));
+      std::memcpy(&re, &h[0], sizeof(double));
+      std::memcpy(&im, &h[1], sizeof(double));
+    }
+    if (max_rel_re) *max_rel_re = re;
+    if (max_rel_im) *max_rel_im = im;
+  });
+}
+
+gk_status gk_max_vertex_distance(gk_ctx* c, const gk_mesh* mesh, double* out) {
+  return guarded([&] {
+    check_ctx(c);
+    need(mesh != nullptr && out != nullptr, GK_ERR_INVALID_ARGUMENT, "null argument");
+    use_device(c);
+    unsigned long long* w = c->scratch.p + 26;
+    GK_CUDA(cudaMemsetAsync(w, 0, sizeof(unsigned long long), c->stream));
+    gk::launch_max_vertex_d2(mesh->verts.p, mesh->nv, w, c->stream);
+    unsigned long long h = 0;
+    GK_CUDA(cudaMemcpyAsync(&h, w, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    double d2 = 0.0;
+    std::memcpy(&d2, &h, sizeof(double));
+    *out = std::sqrt(d2);
+  });
+}
+
 gk_status gk_eval_batch_async(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
                               double k_im, const double* radii, size_t n, gk_c128* out,
                               uint64_t* status) {
@@ -517,13 +558,12 @@ gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32
       mesh->inner.alloc(nt * 3 * static_cast<size_t>(n), c->stream);
       mesh->bounds.alloc(nt, c->stream);
       mesh->binner.alloc(nt, c->stream);
-      gk::DevBuf<double> dv;
       gk::DevBuf<uint32_t> dt;
-      dv.alloc(3 * nv, c->stream);
+      mesh->verts.alloc(3 * nv, c->stream);
       dt.alloc(3 * nt, c->stream);
-      GK_CUDA(cudaMemcpyAsync(dv.p, verts, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      GK_CUDA(cudaMemcpyAsync(mesh->verts.p, verts, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, c->stream));
       GK_CUDA(cudaMemcpyAsync(dt.p, tris, 3 * nt * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
-      gk::launch_points(mesh, dv.p, dt.p, c->stream);
+      gk::launch_points(mesh, mesh->verts.p, dt.p, c->stream);
       GK_CUDA(cudaStreamSynchronize(c->stream));
     } catch (...) {
       delete mesh;

@@ -94,6 +94,58 @@ void launch_points(gk_mesh* mesh, const double* d_verts, const uint32_t* d_tris,
   GK_CUDA(cudaGetLastError());
 }
 
+// max_vertex_distance (mesh.hpp:62-68): thread i scans j > i; |a - b|^2 in the
+// reference's order (dot(a - b, a - b), no contraction: this unit is built
+// with -fmad=false) and one correctly rounded sqrt of the maximum on the host
+// side reproduce max_ij sqrt(.) exactly (sqrt is monotone).  Vertices j are
+// staged through shared memory in tiles.
+__global__ void max_vertex_d2_kernel(const double* __restrict__ V, size_t nv,
+                                     unsigned long long* __restrict__ out) {
+  __shared__ double tx[256], ty[256], tz[256];
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  double ax = 0.0, ay = 0.0, az = 0.0;
+  if (i < nv) {
+    ax = V[3 * i];
+    ay = V[3 * i + 1];
+    az = V[3 * i + 2];
+  }
+  double best = 0.0;
+  const size_t first = blockIdx.x * static_cast<size_t>(blockDim.x);  // j > i >= first
+  for (size_t j0 = first; j0 < nv; j0 += 256) {
+    __syncthreads();
+    const size_t jl = j0 + threadIdx.x;
+    if (jl < nv) {
+      tx[threadIdx.x] = V[3 * jl];
+      ty[threadIdx.x] = V[3 * jl + 1];
+      tz[threadIdx.x] = V[3 * jl + 2];
+    }
+    __syncthreads();
+    const size_t cnt = nv - j0 < 256 ? nv - j0 : 256;
+    if (i < nv)
+      for (size_t t = 0; t < cnt; ++t) {
+        if (j0 + t <= i) continue;
+        const double dx = ax - tx[t], dy = ay - ty[t], dz = az - tz[t];
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        best = best < d2 ? d2 : best;
+      }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double v = __shfl_xor_sync(0xffffffffu, best, o);
+    best = best < v ? v : best;
+  }
+  if ((threadIdx.x & 31) == 0 && best > 0.0)
+    atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(best)));
+}
+
+void launch_max_vertex_d2(const double* verts, size_t nv, unsigned long long* d2_bits,
+                          cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>((nv + 255) / 256);
+  if (blocks == 0) return;
+  max_vertex_d2_kernel<<<blocks, 256, 0, s>>>(verts, nv, d2_bits);
+  count_launches(1);
+  GK_CUDA(cudaGetLastError());
+}
+
 // ---------------------------------------------------------- plan (K2)
 
 struct PlanScalars {

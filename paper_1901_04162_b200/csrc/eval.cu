@@ -108,6 +108,45 @@ void launch_locate(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, ui
   GK_CUDA(cudaGetLastError());
 }
 
+// ---------------------------------------------------------- compare_fills
+
+__global__ void compare_kernel(const double2* __restrict__ test, const double2* __restrict__ ref,
+                               size_t rows, size_t N, size_t row_begin, size_t ld,
+                               unsigned long long* w) {
+  double mre = 0.0, mim = 0.0;
+  const size_t total = rows * N;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = e / N, q = e - r * N;
+    if (row_begin + r == q) continue;  // the excluded diagonal
+    const double2 a = ref[r * ld + q], b = test[r * ld + q];
+    // std::max(stats, x) keeps stats when x is NaN: so does fmax
+    if (a.x != 0.0) mre = fmax(mre, fabs(b.x - a.x) / fabs(a.x));
+    if (a.y != 0.0) mim = fmax(mim, fabs(b.y - a.y) / fabs(a.y));
+  }
+  for (int o = 16; o; o >>= 1) {
+    mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+    mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mre > 0.0) atomicMax(w, static_cast<unsigned long long>(__double_as_longlong(mre)));
+    if (mim > 0.0) atomicMax(w + 1, static_cast<unsigned long long>(__double_as_longlong(mim)));
+  }
+}
+
+void launch_compare(gk_ctx* ctx, const gk_c128* test, const gk_c128* ref, size_t rows, size_t N,
+                    size_t row_begin, size_t ld, unsigned long long* w) {
+  size_t grid = (rows * N + 255) / 256;
+  const size_t cap = static_cast<size_t>(ctx->sm_count) * 16;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  compare_kernel<<<static_cast<unsigned>(grid), 256, 0, ctx->stream>>>(
+      reinterpret_cast<const double2*>(test), reinterpret_cast<const double2*>(ref), rows, N,
+      row_begin, ld, w);
+  count_launches(1);
+  GK_CUDA(cudaGetLastError());
+}
+
 // ------------------------------------------------------------- FP64 peak
 
 constexpr int kChains = 8;

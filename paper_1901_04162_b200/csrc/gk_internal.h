@@ -88,6 +88,7 @@ struct gk_mesh {
   gk::DevBuf<double4> inner;  // [3n][N]    (x, y, z, w), column-major in q
   gk::DevBuf<double4> bounds; // [N]        (cx, cy, cz, rho_outer), rho_inner in binner
   gk::DevBuf<double> binner;  // [N]
+  gk::DevBuf<double> verts;   // [3 nv] vertices (max_vertex_distance)
 };
 
 namespace gk {
@@ -107,6 +108,12 @@ void validate_mesh(const double* v, size_t nv, const uint32_t* t, size_t nt);
 // kernels launched by abi.cu (defined in build.cu / fill.cu / eval.cu)
 void launch_points(gk_mesh* mesh, const double* d_verts, const uint32_t* d_tris,
                    cudaStream_t s);
+// max over vertex pairs of |a - b|^2 (reference summation order) -> *d2_bits
+void launch_max_vertex_d2(const double* verts, size_t nv, unsigned long long* d2_bits,
+                          cudaStream_t s);
+// compare_fills partial maxima (as non-negative double bits) -> w[0] (re), w[1] (im)
+void launch_compare(gk_ctx* ctx, const gk_c128* test, const gk_c128* ref, size_t rows, size_t N,
+                    size_t row_begin, size_t ld, unsigned long long* w);
 void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg, double k_zero,
                         double t_nominal, double k_re, double k_im, int degree);
 // kind: GK_KIND_EXP, GK_KIND_GREEN, or 2 = fused pair (z = Exp, z2 = Green)

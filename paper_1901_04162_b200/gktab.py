@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import dataclasses
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -98,6 +99,13 @@ class FillReport:
     actual_calls: int = 0
     fallback_calls: int = 0
     wall_time_s: float = 0.0
+    # set by bench_compare (matfill.hpp:41-46)
+    max_rel_re: float = 0.0
+    max_rel_im: float = 0.0
+    speedup: float = 0.0
+    analytic_time_s: float = 0.0
+    interp_time_s: float = 0.0
+    table_build_s: float = 0.0
 
     @classmethod
     def from_c(cls, r: FillReportC) -> "FillReport":
@@ -385,6 +393,13 @@ class DeviceMesh:
         check(lib().gk_mesh_points_download(self.h, o.ctypes.data, i.ctypes.data), "points")
         return o, i
 
+    def max_vertex_distance(self) -> float:
+        """max_vertex_distance (mesh.hpp:62-68), exact, on the device."""
+        out = C.c_double()
+        check(lib().gk_max_vertex_distance(self.ctx.h, self.h, C.byref(out)),
+              "max_vertex_distance")
+        return out.value
+
     def distance_range(self, row_begin: int = 0, row_end: int | None = None):
         """K1: min/max quadrature pair distance over rows x all q != p"""
         row_end = self.N if row_end is None else row_end
@@ -417,6 +432,57 @@ def fill_rows(dmesh: DeviceMesh, mode: Mode, kind: KernelKind = KernelKind.Green
                              out.data_ptr() if rows else None, out.stride(0) if rows else N,
                              C.byref(rep) if report else None), "fill_matrix")
     return out, (FillReport.from_c(rep) if report else None)
+
+
+def compare_fills(test, ref, row_begin: int = 0, ctx: Context | None = None):
+    """compare_fills (matfill.hpp:237-254) on device matrices: (max_rel_re,
+    max_rel_im) over the rows given, skipping the diagonal (row index
+    row_begin + r == column) and exactly-zero reference components."""
+    torch = _torch()
+    if test.shape != ref.shape:
+        raise _lib.InvalidArgument("compare_fills: size mismatch")
+    ctx = ctx or Context.get(test.device.index or 0)
+    t = test.contiguous()
+    r = ref.contiguous()
+    rows, N = (t.shape[0], t.shape[1]) if t.dim() == 2 else (0, 0)
+    assert t.dtype == r.dtype == torch.complex128 and t.is_cuda and r.is_cuda
+    re, im = C.c_double(), C.c_double()
+    check(lib().gk_compare_fills(ctx.h, t.data_ptr() if t.numel() else None,
+                                 r.data_ptr() if r.numel() else None, rows, N, row_begin,
+                                 max(N, 1), C.byref(re), C.byref(im)), "compare_fills")
+    return re.value, im.value
+
+
+def bench_compare(mesh: TriangleMesh, spec: QuadratureSpec, medium: Medium = Medium(),
+                  cfg: SamplingConfig | None = None, lagrange_degree: int = 3,
+                  kind: KernelKind = KernelKind.GreenOverR, repeats: int = 1,
+                  ctx: Context | None = None) -> FillReport:
+    """bench_compare (matfill.hpp:262-294) on the device: direct fill, then the
+    table fill over a plan with r_max = 1.01 x max_vertex_distance (cfg.r_min
+    kept), the table build charged to the table side; with repeats > 1 the two
+    fills interleave and the fastest device time per side counts.  Times are
+    CUDA-event device times (fills) and the device build time (table)."""
+    if repeats < 1:
+        raise _lib.InvalidArgument("bench_compare: repeats must be >= 1")
+    cfg = dataclasses.replace(cfg or SamplingConfig())
+    ctx = ctx or Context.get()
+    dm = DeviceMesh(mesh, spec, ctx)
+    k = wavenumber(medium)
+    cfg.r_max = dm.max_vertex_distance() * 1.01
+    table = DeviceTable(cfg, medium, lagrange_degree, ctx=ctx)
+    za, ra = fill_rows(dm, Mode.DIRECT, kind=kind, k=k)
+    zi, rep = fill_rows(dm, Mode.TABLE, kind=kind, table=table)
+    for _ in range(1, repeats):
+        _, r2 = fill_rows(dm, Mode.DIRECT, kind=kind, k=k, out=za)
+        ra.wall_time_s = min(ra.wall_time_s, r2.wall_time_s)
+        _, r3 = fill_rows(dm, Mode.TABLE, kind=kind, table=table, out=zi)
+        rep.wall_time_s = min(rep.wall_time_s, r3.wall_time_s)
+    rep.max_rel_re, rep.max_rel_im = compare_fills(zi, za, ctx=ctx)
+    rep.table_build_s = table.info.build_ms * 1e-3
+    rep.analytic_time_s = ra.wall_time_s
+    rep.interp_time_s = rep.wall_time_s + rep.table_build_s
+    rep.speedup = rep.analytic_time_s / rep.interp_time_s
+    return rep
 
 
 def fill_rows_pair(dmesh: DeviceMesh, mode: Mode, table: DeviceTable | None = None,
