@@ -231,6 +231,27 @@ gk_status gk_compare_fills(gk_ctx* ctx, const gk_c128* test, const gk_c128* ref,
                            size_t N, size_t row_begin, size_t ld, double* max_rel_re,
                            double* max_rel_im);
 
+/* bench_compare (matfill.hpp:262-294) on the device, host mesh in: direct
+   fill, then the table fill over a plan with r_max = 1.01 x
+   max_vertex_distance (cfg->r_min kept) and the given Lagrange degree, the
+   table build charged to the table side; with repeats > 1 the two fills
+   interleave and the fastest device time per side counts; compare_fills of
+   the two matrices.  Needs 2 N^2 x 16 B of device memory, like the
+   reference's two host matrices. */
+typedef struct gk_bench_report {
+  gk_fill_report fill; /* the table fill's report (wall_time_s: its fastest) */
+  double max_rel_re, max_rel_im;
+  double speedup;         /* analytic_time_s / interp_time_s */
+  double analytic_time_s; /* fastest direct fill (device time) */
+  double interp_time_s;   /* fastest table fill + table build */
+  double table_build_s;   /* device table build */
+} gk_bench_report;
+gk_status gk_bench_compare(gk_ctx* ctx, const double* vertices, size_t nv,
+                           const uint32_t* triangles, size_t nt, int outer_points,
+                           int inner_points_per_edge, const gk_medium* medium,
+                           const gk_sampling_config* cfg, int lagrange_degree, gk_kind kind,
+                           int repeats, gk_bench_report* out);
+
 /* max_vertex_distance (mesh.hpp:62-68) of a device mesh: exact O(V^2) scan,
    bit-identical to the reference (its r_max convention in bench_compare,
    matfill.hpp:270, is 1.01 x this). */

@@ -14,6 +14,8 @@
 // std::overflow_error, std::runtime_error).  Link with -lgk.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <complex>
 #include <cstdint>
 #include <span>
@@ -85,17 +87,47 @@ struct KernelMatrix {
   const Complex& at(std::size_t p, std::size_t q) const { return z[p * n + q]; }
 };
 
-// gktab::FillReport (matfill.hpp:33-47), the fields fill_matrix sets
+// gktab::FillReport (matfill.hpp:33-47); the last six fields are set by
+// bench_compare only
 struct FillReport {
   std::size_t N = 0;
   int m = 0, n = 0;
   std::uint64_t predicted_calls = 0, actual_calls = 0, fallback_calls = 0;
   double wall_time_s = 0.0;
+  double max_rel_re = 0.0, max_rel_im = 0.0;
+  double speedup = 0.0, analytic_time_s = 0.0, interp_time_s = 0.0, table_build_s = 0.0;
   static FillReport from(const gk_fill_report& r) {
-    return {static_cast<std::size_t>(r.N), r.m, r.n, r.predicted_calls, r.actual_calls,
-            r.fallback_calls, r.wall_time_s};
+    FillReport f;
+    f.N = static_cast<std::size_t>(r.N);
+    f.m = r.m;
+    f.n = r.n;
+    f.predicted_calls = r.predicted_calls;
+    f.actual_calls = r.actual_calls;
+    f.fallback_calls = r.fallback_calls;
+    f.wall_time_s = r.wall_time_s;
+    return f;
   }
 };
+
+// gktab::FillErrorStats / compare_fills (matfill.hpp:230-254), host matrices
+struct FillErrorStats {
+  double max_rel_re = 0.0;
+  double max_rel_im = 0.0;
+};
+inline FillErrorStats compare_fills(const KernelMatrix& test, const KernelMatrix& ref) {
+  if (test.n != ref.n) throw std::invalid_argument("compare_fills: size mismatch");
+  FillErrorStats st;
+  for (std::size_t p = 0; p < ref.n; ++p)
+    for (std::size_t q = 0; q < ref.n; ++q) {
+      if (p == q) continue;
+      const Complex a = ref.at(p, q), b = test.at(p, q);
+      if (a.real() != 0.0)
+        st.max_rel_re = std::max(st.max_rel_re, std::abs(b.real() - a.real()) / std::abs(a.real()));
+      if (a.imag() != 0.0)
+        st.max_rel_im = std::max(st.max_rel_im, std::abs(b.imag() - a.imag()) / std::abs(a.imag()));
+    }
+  return st;
+}
 
 inline double wavenumber(const Medium& m) {
   double re = 0, im = 0;
@@ -214,6 +246,29 @@ inline std::pair<KernelMatrix, FillReport> fill_matrix(
                             static_cast<gk_kind>(kind), reinterpret_cast<gk_c128*>(z.z.data()),
                             &rep));
   return {std::move(z), FillReport::from(rep)};
+}
+
+// bench_compare (matfill.hpp:262-294) on the GPU: direct vs table fill of the
+// same mesh, table built over [cfg.r_min, 1.01 max_vertex_distance]
+inline FillReport bench_compare(Context& ctx, const TriangleMesh& mesh, const QuadratureSpec& spec,
+                                const Medium& medium, SamplingConfig cfg,
+                                int lagrange_degree = 3,
+                                KernelKind kind = KernelKind::GreenOverR, int repeats = 1) {
+  gk_bench_report r{};
+  const gk_sampling_config c = cfg.c();
+  const gk_medium m = medium.c();
+  check(gk_bench_compare(ctx.get(), mesh.vertices.data(), mesh.vertices.size() / 3,
+                         mesh.triangles.data(), mesh.triangle_count(), spec.outer_points,
+                         spec.inner_points_per_edge, &m, &c, lagrange_degree,
+                         static_cast<gk_kind>(kind), repeats, &r));
+  FillReport f = FillReport::from(r.fill);
+  f.max_rel_re = r.max_rel_re;
+  f.max_rel_im = r.max_rel_im;
+  f.speedup = r.speedup;
+  f.analytic_time_s = r.analytic_time_s;
+  f.interp_time_s = r.interp_time_s;
+  f.table_build_s = r.table_build_s;
+  return f;
 }
 
 }  // namespace gk

@@ -75,6 +75,12 @@ class FillReportC(C.Structure):
                 ("fallback_calls", C.c_uint64), ("wall_time_s", C.c_double)]
 
 
+class BenchReportC(C.Structure):
+    _fields_ = [("fill", FillReportC), ("max_rel_re", C.c_double), ("max_rel_im", C.c_double),
+                ("speedup", C.c_double), ("analytic_time_s", C.c_double),
+                ("interp_time_s", C.c_double), ("table_build_s", C.c_double)]
+
+
 class TableInfoC(C.Structure):
     _fields_ = [("nodes", C.c_uint64), ("zeros", C.c_uint64), ("hash_buckets", C.c_uint64),
                 ("lookup_buckets", C.c_uint64), ("r_min", C.c_double), ("r_max", C.c_double),
@@ -127,6 +133,8 @@ PROTOTYPES = {
     "gk_predicted_calls": [C.c_uint64, C.c_uint64, C.c_uint64, _u64p],
     "gk_compare_fills": [_vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_max_vertex_distance": [_vp, _vp, _dp],
+    "gk_bench_compare": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, _vp, _vp,
+                         C.c_int, C.c_int, C.c_int, _vp],
     "gk_sphere_mesh": [C.c_double, C.c_int, _vp, _szp, _vp, _szp],
     "gk_plate_mesh": [C.c_double, C.c_int, _vp, _szp, _vp, _szp],
     "gk_jitter": [_vp, C.c_size_t, C.c_uint64, C.c_double],

@@ -842,6 +842,62 @@ gk_status gk_fill_matrix_host(gk_ctx* c, const double* verts, size_t nv, const u
   return st;
 }
 
+gk_status gk_bench_compare(gk_ctx* c, const double* verts, size_t nv, const uint32_t* tris,
+                           size_t nt, int m, int n, const gk_medium* med,
+                           const gk_sampling_config* cfg, int degree, gk_kind kind, int repeats,
+                           gk_bench_report* out) {
+  gk_mesh* mesh = nullptr;
+  gk_table* table = nullptr;
+  gk::DevBuf<gk_c128> za, zi;
+  gk_status st = guarded([&] {
+    check_ctx(c);
+    need(med && cfg && out, GK_ERR_INVALID_ARGUMENT, "null argument");
+    need(repeats >= 1, GK_ERR_INVALID_ARGUMENT, "bench_compare: repeats must be >= 1");
+    need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
+    double k_re, k_im;
+    wavenumber(*med, k_re, k_im);
+    auto ok = [](gk_status s) {
+      if (s != GK_OK) gk::fail(s, g_last_error);
+    };
+    ok(gk_mesh_create(c, verts, nv, tris, nt, m, n, &mesh));
+    double maxd = 0.0;
+    ok(gk_max_vertex_distance(c, mesh, &maxd));
+    gk_sampling_config cc = *cfg;
+    cc.r_max = maxd * 1.01;  // matfill.hpp:270
+    ok(gk_table_build(c, &cc, med, degree, &table));
+    use_device(c);
+    za.alloc(nt * nt, c->stream);
+    zi.alloc(nt * nt, c->stream);
+    gk_fill_report ra{}, ri{};
+    fill_rows_impl(c, mesh, GK_MODE_DIRECT, nullptr, kind, k_re, k_im, 0, nt, za.p, nullptr, nt,
+                   &ra);
+    fill_rows_impl(c, mesh, GK_MODE_TABLE, table, kind, k_re, k_im, 0, nt, zi.p, nullptr, nt,
+                   &ri);
+    for (int rep = 1; rep < repeats; ++rep) {  // interleaved (matfill.hpp:279-284)
+      gk_fill_report r2{}, r3{};
+      fill_rows_impl(c, mesh, GK_MODE_DIRECT, nullptr, kind, k_re, k_im, 0, nt, za.p, nullptr,
+                     nt, &r2);
+      ra.wall_time_s = std::min(ra.wall_time_s, r2.wall_time_s);
+      fill_rows_impl(c, mesh, GK_MODE_TABLE, table, kind, k_re, k_im, 0, nt, zi.p, nullptr, nt,
+                     &r3);
+      ri.wall_time_s = std::min(ri.wall_time_s, r3.wall_time_s);
+    }
+    gk_bench_report r{};
+    r.fill = ri;
+    ok(gk_compare_fills(c, zi.p, za.p, nt, nt, 0, nt, &r.max_rel_re, &r.max_rel_im));
+    r.table_build_s = table->info.build_ms * 1e-3;
+    r.analytic_time_s = ra.wall_time_s;
+    r.interp_time_s = ri.wall_time_s + r.table_build_s;
+    r.speedup = r.analytic_time_s / r.interp_time_s;
+    *out = r;
+  });
+  za.reset();
+  zi.reset();
+  gk_table_destroy(table);
+  gk_mesh_destroy(mesh);
+  return st;
+}
+
 gk_status gk_predicted_calls(uint64_t N, uint64_t m, uint64_t n, uint64_t* out) {
   return guarded([&] {
     need(out != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");

@@ -457,31 +457,23 @@ def bench_compare(mesh: TriangleMesh, spec: QuadratureSpec, medium: Medium = Med
                   cfg: SamplingConfig | None = None, lagrange_degree: int = 3,
                   kind: KernelKind = KernelKind.GreenOverR, repeats: int = 1,
                   ctx: Context | None = None) -> FillReport:
-    """bench_compare (matfill.hpp:262-294) on the device: direct fill, then the
-    table fill over a plan with r_max = 1.01 x max_vertex_distance (cfg.r_min
-    kept), the table build charged to the table side; with repeats > 1 the two
-    fills interleave and the fastest device time per side counts.  Times are
-    CUDA-event device times (fills) and the device build time (table)."""
-    if repeats < 1:
-        raise _lib.InvalidArgument("bench_compare: repeats must be >= 1")
-    cfg = dataclasses.replace(cfg or SamplingConfig())
+    """bench_compare (matfill.hpp:262-294) on the device (gk_bench_compare):
+    direct fill, then the table fill over a plan with r_max = 1.01 x
+    max_vertex_distance (cfg.r_min kept), the table build charged to the
+    table side; with repeats > 1 the fills interleave and the fastest device
+    time per side counts."""
     ctx = ctx or Context.get()
-    dm = DeviceMesh(mesh, spec, ctx)
-    k = wavenumber(medium)
-    cfg.r_max = dm.max_vertex_distance() * 1.01
-    table = DeviceTable(cfg, medium, lagrange_degree, ctx=ctx)
-    za, ra = fill_rows(dm, Mode.DIRECT, kind=kind, k=k)
-    zi, rep = fill_rows(dm, Mode.TABLE, kind=kind, table=table)
-    for _ in range(1, repeats):
-        _, r2 = fill_rows(dm, Mode.DIRECT, kind=kind, k=k, out=za)
-        ra.wall_time_s = min(ra.wall_time_s, r2.wall_time_s)
-        _, r3 = fill_rows(dm, Mode.TABLE, kind=kind, table=table, out=zi)
-        rep.wall_time_s = min(rep.wall_time_s, r3.wall_time_s)
-    rep.max_rel_re, rep.max_rel_im = compare_fills(zi, za, ctx=ctx)
-    rep.table_build_s = table.info.build_ms * 1e-3
-    rep.analytic_time_s = ra.wall_time_s
-    rep.interp_time_s = rep.wall_time_s + rep.table_build_s
-    rep.speedup = rep.analytic_time_s / rep.interp_time_s
+    cfg = cfg or SamplingConfig()
+    r = _lib.BenchReportC()
+    check(lib().gk_bench_compare(ctx.h, mesh.vertices.ctypes.data, mesh.vertices.shape[0],
+                                 mesh.triangles.ctypes.data, mesh.triangles.shape[0],
+                                 spec.outer_points, spec.inner_points_per_edge,
+                                 C.byref(medium.c()), C.byref(cfg.c()), lagrange_degree,
+                                 int(kind), repeats, C.byref(r)), "bench_compare")
+    rep = FillReport.from_c(r.fill)
+    rep.max_rel_re, rep.max_rel_im = r.max_rel_re, r.max_rel_im
+    rep.speedup, rep.analytic_time_s = r.speedup, r.analytic_time_s
+    rep.interp_time_s, rep.table_build_s = r.interp_time_s, r.table_build_s
     return rep
 
 

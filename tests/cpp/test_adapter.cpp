@@ -4,7 +4,8 @@
 //   * reference-config zeros {0.25, 0.5, 0.75, 1} (test_sampling.cpp:42-49),
 //   * node reproduction (test_evaluator.cpp:24-31),
 //   * exception types (test_evaluator.cpp:83-91, test_matfill.cpp:23-26, 183-191),
-//   * table fill vs direct fill agreement (acceptance criterion 5 gate, 1e-4).
+//   * table fill vs direct fill agreement (acceptance criterion 5 gate, 1e-4),
+//   * bench_compare report consistency (test_matfill.cpp:167-181).
 // Built by __graft_entry__.build(); run by tests/test_gpu_cpp.py.
 #include <cmath>
 #include <cstdio>
@@ -92,6 +93,24 @@ int main() {
     CHECK(worst <= 1e-4);
     CHECK(rt.actual_calls == 3ull * 4 * 3 * 320 * 319 && rd.actual_calls == rt.actual_calls);
     std::printf("N=320 table vs direct: max elementwise relative error %.3g\n", worst);
+  }
+  // BenchCompare.ReportConsistency (test_matfill.cpp:167-181)
+  {
+    const auto mesh80 = gk::generate_sphere_mesh(0.5, 1);
+    gk::SamplingConfig cfg;
+    cfg.samples_per_wavelength = 10000;
+    const auto r = gk::bench_compare(ctx, mesh80, {4, 3}, gk::Medium{}, cfg);
+    CHECK(r.N == 80u && r.actual_calls == 3ull * 4 * 3 * 80 * 79 && r.fallback_calls == 0u);
+    CHECK(r.speedup > 0.0 && r.analytic_time_s > 0.0);
+    CHECK(std::fabs(r.interp_time_s - (r.wall_time_s + r.table_build_s)) <= 1e-12);
+    CHECK(r.max_rel_re <= 1e-4 && r.max_rel_im <= 1e-4);
+    CHECK(throws<std::invalid_argument>(
+        [&] { gk::bench_compare(ctx, mesh80, {4, 3}, gk::Medium{}, cfg, 3, gk::KernelKind::GreenOverR, 0); }));
+    // host compare_fills of the two fills == the device report's statistic
+    auto [zd, rd] = gk::fill_matrix(ctx, mesh80, {4, 3}, gk::Mode::Direct, gk::Medium{});
+    const auto same = gk::compare_fills(zd, zd);
+    CHECK(same.max_rel_re == 0.0 && same.max_rel_im == 0.0);
+    (void)rd;
   }
   std::printf("%s (%d failure(s))\n", failures ? "FAILED" : "ALL OK", failures);
   return failures ? 1 : 0;

@@ -105,6 +105,7 @@ def test_bench_compare_report_consistency(gk):
     assert rep.N == 80 and rep.actual_calls == 3 * 4 * 3 * 80 * 79
     assert rep.fallback_calls == 0
     assert rep.speedup > 0 and rep.analytic_time_s > 0 and rep.table_build_s > 0
+    assert rep.predicted_calls == 3 * 4 * 3 * 80 * 80 and rep.wall_time_s > 0
     assert abs(rep.interp_time_s - (rep.wall_time_s + rep.table_build_s)) <= 1e-12
     assert rep.max_rel_re <= 1e-4 and rep.max_rel_im <= 1e-4
     with pytest.raises(gk.InvalidArgument):
