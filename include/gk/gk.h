@@ -146,6 +146,21 @@ gk_status gk_eval_batch_async(gk_ctx* ctx, const gk_table* table, gk_kind kind, 
 gk_status gk_eval_status_reset(gk_ctx* ctx, uint64_t* status);
 gk_status gk_eval_status_read(gk_ctx* ctx, const uint64_t* status, uint64_t* fallbacks);
 
+/* error_sweep (bounds.hpp:113-186) of a device table: probe_count uniformly
+   spaced radii over [r_min, r_max] (endpoints included), the device
+   interpolant against the device's analytic evaluation (libdevice sincos,
+   within ~1 ulp of glibc).  The device tabulates Exp with linear and Green
+   with Lagrange interpolation, so method must be GK_INTERP_LINEAR for Exp
+   and GK_INTERP_LAGRANGE for Green (else GK_ERR_INVALID_ARGUMENT). */
+typedef enum gk_interp { GK_INTERP_LINEAR = 0, GK_INTERP_LAGRANGE = 1 } gk_interp;
+typedef struct gk_sweep_report {
+  uint64_t probe_count;
+  double max_rel_re, max_rel_im, max_abs, worst_r, max_abs_at_exact_zero;
+  uint64_t decade_histogram[24]; /* slot d: relative modulus error in [1e(d-20), 1e(d-19)) */
+} gk_sweep_report;
+gk_status gk_error_sweep(gk_ctx* ctx, const gk_table* table, gk_kind kind, gk_interp method,
+                         uint64_t probe_count, gk_sweep_report* out);
+
 /* locate (table.hpp:87-102) on the device: for each radius the bracketing
    interval j with a_j <= r < a_{j+1} (r = r_max maps to nodes-2).  radii and
    out are device pointers; a radius outside [r_min, r_max] fails with

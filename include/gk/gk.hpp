@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdio>
+#include <ostream>
 #include <cstdint>
 #include <span>
 #include <stdexcept>
@@ -168,6 +170,15 @@ class Context {
 };
 
 // gktab::KernelEvaluator (evaluator.hpp:102-309) with its tables on the GPU
+// gktab::InterpMethod (bounds.hpp:15) and ErrorSweepReport (bounds.hpp:113-124)
+enum class InterpMethod { Linear = GK_INTERP_LINEAR, Lagrange = GK_INTERP_LAGRANGE };
+struct ErrorSweepReport {
+  std::size_t probe_count = 0;
+  double max_rel_re = 0.0, max_rel_im = 0.0, max_abs = 0.0, worst_r = 0.0;
+  double max_abs_at_exact_zero = 0.0;
+  std::uint64_t decade_histogram[24] = {};
+};
+
 class DeviceEvaluator {
  public:
   DeviceEvaluator(Context& ctx, const SamplingConfig& cfg, const Medium& medium = {},
@@ -203,6 +214,23 @@ class DeviceEvaluator {
   }
   Complex eval_exp(double r) const { return eval_kernel(KernelKind::PlainExp, r); }
   Complex eval_green(double r) const { return eval_kernel(KernelKind::GreenOverR, r); }
+
+  // error_sweep (bounds.hpp:128-186) of this device table: Exp with Linear,
+  // Green with Lagrange (the device's interpolants)
+  ErrorSweepReport error_sweep(KernelKind kind, InterpMethod method, std::size_t probes) const {
+    gk_sweep_report r{};
+    check(gk_error_sweep(ctx_->get(), h_, static_cast<gk_kind>(kind),
+                         static_cast<gk_interp>(method), probes, &r));
+    ErrorSweepReport e;
+    e.probe_count = static_cast<std::size_t>(r.probe_count);
+    e.max_rel_re = r.max_rel_re;
+    e.max_rel_im = r.max_rel_im;
+    e.max_abs = r.max_abs;
+    e.worst_r = r.worst_r;
+    e.max_abs_at_exact_zero = r.max_abs_at_exact_zero;
+    for (int d = 0; d < 24; ++d) e.decade_histogram[d] = r.decade_histogram[d];
+    return e;
+  }
 
   std::vector<double> abscissae() const {
     std::vector<double> a(info_.nodes);
@@ -246,6 +274,33 @@ inline std::pair<KernelMatrix, FillReport> fill_matrix(
                             static_cast<gk_kind>(kind), reinterpret_cast<gk_c128*>(z.z.data()),
                             &rep));
   return {std::move(z), FillReport::from(rep)};
+}
+
+// io.hpp:23-27, 134-156: the reference's report rows, %.17g numbers
+inline std::string format_g17(double v) {
+  char buf[40];
+  std::snprintf(buf, sizeof(buf), "%.17g", v);
+  return buf;
+}
+inline void write_bench_csv(std::ostream& out, const FillReport& r) {
+  out << "N,m,n,predicted_calls,actual_calls,fallback_calls,analytic_s,interp_s,speedup,"
+         "max_rel_re,max_rel_im\n";
+  out << r.N << ',' << r.m << ',' << r.n << ',' << r.predicted_calls << ',' << r.actual_calls
+      << ',' << r.fallback_calls << ',' << format_g17(r.analytic_time_s) << ','
+      << format_g17(r.interp_time_s) << ',' << format_g17(r.speedup) << ','
+      << format_g17(r.max_rel_re) << ',' << format_g17(r.max_rel_im) << '\n';
+}
+inline void write_sweep_csv_header(std::ostream& out) {
+  out << "kernel,method,probes,max_rel_re,max_rel_im,max_abs,worst_r\n";
+}
+inline void write_sweep_csv_row(std::ostream& out, KernelKind kind, InterpMethod method,
+                                int lagrange_degree, const ErrorSweepReport& r) {
+  out << (kind == KernelKind::PlainExp ? "exp" : "green") << ','
+      << (method == InterpMethod::Linear ? "linear" : "lagrange");
+  if (method == InterpMethod::Lagrange) out << lagrange_degree;
+  out << ',' << r.probe_count << ',' << format_g17(r.max_rel_re) << ','
+      << format_g17(r.max_rel_im) << ',' << format_g17(r.max_abs) << ','
+      << format_g17(r.worst_r) << '\n';
 }
 
 // bench_compare (matfill.hpp:262-294) on the GPU: direct vs table fill of the

@@ -551,6 +551,30 @@ class Ref:
         _chk(self.L.gr_dump_plan_csv(dptr(a), C.c_size_t(a.size), dptr(z) if z.size else None,
                                      C.c_size_t(z.size), path.encode()), "dump_plan_csv")
 
+    def error_sweep(self, ev, kind: int, method: int, probes: int):
+        """the reference's error_sweep (bounds.hpp:128-186) on a reference evaluator"""
+        d = np.zeros(5, np.float64)
+        hist = np.zeros(24, np.uint64)
+        _chk(self.L.gr_error_sweep(C.c_void_p(ev.h), C.c_int(kind), C.c_int(method),
+                                   C.c_uint64(probes), dptr(d), hist.ctypes.data_as(C.c_void_p)),
+             "error_sweep")
+        return dict(max_rel_re=d[0], max_rel_im=d[1], max_abs=d[2], worst_r=d[3],
+                    max_abs_at_exact_zero=d[4], decade_histogram=hist.tolist())
+
+    def write_bench_csv(self, ints, dbls, path: str) -> None:
+        """the reference's write_bench_csv (io.hpp:147-156) of a report"""
+        i = np.ascontiguousarray(ints, np.uint64)
+        d = np.ascontiguousarray(dbls, np.float64)
+        _chk(self.L.gr_write_bench_csv(i.ctypes.data_as(C.c_void_p), dptr(d), path.encode()),
+             "write_bench_csv")
+
+    def write_sweep_csv(self, kind, method, degree, probes, dbls, path: str) -> None:
+        """the reference's write_sweep_csv_header + _row (io.hpp:134-145)"""
+        d = np.ascontiguousarray(dbls, np.float64)
+        _chk(self.L.gr_write_sweep_csv(C.c_int(kind), C.c_int(method), C.c_int(degree),
+                                       C.c_uint64(probes), dptr(d), path.encode()),
+             "write_sweep_csv")
+
     def load_table_binary(self, path: str):
         kind, k, cnt = C.c_int(), C.c_double(), C.c_size_t()
         _chk(self.L.gr_load_table_binary(path.encode(), C.byref(kind), C.byref(k), C.byref(cnt),

@@ -428,6 +428,63 @@ int gr_dump_plan_csv(const double* absc, size_t n, const double* zeros, size_t n
   });
 }
 
+// write_bench_csv (io.hpp:147-156) of a report with the given fields -> path
+int gr_write_bench_csv(const uint64_t* ints /* N,m,n,pred,actual,fallback */,
+                       const double* dbls /* analytic,interp,speedup,re,im */, const char* path) {
+  return guarded([&] {
+    FillReport rep;
+    rep.N = static_cast<std::size_t>(ints[0]);
+    rep.m = static_cast<int>(ints[1]);
+    rep.n = static_cast<int>(ints[2]);
+    rep.predicted_calls = ints[3];
+    rep.actual_calls = ints[4];
+    rep.fallback_calls = ints[5];
+    rep.analytic_time_s = dbls[0];
+    rep.interp_time_s = dbls[1];
+    rep.speedup = dbls[2];
+    rep.max_rel_re = dbls[3];
+    rep.max_rel_im = dbls[4];
+    std::ofstream out(path);
+    write_bench_csv(out, rep);
+  });
+}
+
+// write_sweep_csv_header + _row (io.hpp:134-145) -> path
+int gr_write_sweep_csv(int kind, int method, int degree, uint64_t probes,
+                       const double* dbls /* re,im,abs,worst_r */, const char* path) {
+  return guarded([&] {
+    ErrorSweepReport rep;
+    rep.probe_count = static_cast<std::size_t>(probes);
+    rep.max_rel_re = dbls[0];
+    rep.max_rel_im = dbls[1];
+    rep.max_abs = dbls[2];
+    rep.worst_r = dbls[3];
+    std::ofstream out(path);
+    write_sweep_csv_header(out);
+    write_sweep_csv_row(out, kind == 0 ? KernelKind::PlainExp : KernelKind::GreenOverR,
+                        method == 0 ? InterpMethod::Linear : InterpMethod::Lagrange, degree, rep);
+  });
+}
+
+// error_sweep (bounds.hpp:128-186) of a reference evaluator: dbls[0..5] =
+// max_rel_re, max_rel_im, max_abs, worst_r, max_abs_at_exact_zero; hist[24]
+int gr_error_sweep(void* h, int kind, int method, uint64_t probes, double* dbls,
+                   uint64_t* hist) {
+  return guarded([&] {
+    const auto* ev = static_cast<const KernelEvaluator*>(h);
+    const ErrorSweepReport r =
+        error_sweep(*ev, kind == 0 ? KernelKind::PlainExp : KernelKind::GreenOverR,
+                    method == 0 ? InterpMethod::Linear : InterpMethod::Lagrange,
+                    static_cast<std::size_t>(probes));
+    dbls[0] = r.max_rel_re;
+    dbls[1] = r.max_rel_im;
+    dbls[2] = r.max_abs;
+    dbls[3] = r.worst_r;
+    dbls[4] = r.max_abs_at_exact_zero;
+    for (int d = 0; d < 24; ++d) hist[d] = r.decade_histogram[d];
+  });
+}
+
 int gr_dump_table_binary(void* h, int kind, const char* path) {
   return guarded([&] {
     const auto* ev = static_cast<const KernelEvaluator*>(h);

@@ -4,8 +4,8 @@ Drop-in for the reference ``gktab`` fill hot path: device table build,
 table lookup/evaluation, direct evaluation and the triangle-pair fill driver,
 all in hand-written CUDA (libgk.so, C ABI in include/gk/gk.h).
 """
-from .gktab import (Context, DeviceMesh, DeviceTable, EvalStatus, FillReport, KernelKind, Medium,
-                    Mode, QuadratureSpec, SamplingConfig, TriangleMesh, bench_compare,
+from .gktab import (Context, DeviceMesh, DeviceTable, ErrorSweepReport, EvalStatus, FillReport,
+                    InterpMethod, KernelKind, Medium, Mode, QuadratureSpec, SamplingConfig, TriangleMesh, bench_compare,
                     compare_fills, eval_batch,
                     eval_batch_async, fill_matrix, fill_rows, fill_rows_host, fill_rows_pair,
                     generate_plate_mesh, generate_sphere_mesh, jitter, predicted_calls,
@@ -14,7 +14,8 @@ from ._lib import (DomainError, GkError, InvalidArgument, OutOfRange, OverflowEr
                    RuntimeErrorGk, LIB_PATH)
 
 __all__ = [
-    "Context", "DeviceMesh", "DeviceTable", "EvalStatus", "FillReport", "KernelKind", "Medium",
+    "Context", "DeviceMesh", "DeviceTable", "ErrorSweepReport", "EvalStatus", "FillReport",
+    "InterpMethod", "KernelKind", "Medium",
     "Mode", "QuadratureSpec", "SamplingConfig", "TriangleMesh", "bench_compare", "compare_fills",
     "eval_batch", "eval_batch_async",
     "fill_matrix", "fill_rows", "fill_rows_host", "fill_rows_pair", "generate_plate_mesh",

@@ -75,6 +75,12 @@ class FillReportC(C.Structure):
                 ("fallback_calls", C.c_uint64), ("wall_time_s", C.c_double)]
 
 
+class SweepReportC(C.Structure):
+    _fields_ = [("probe_count", C.c_uint64), ("max_rel_re", C.c_double),
+                ("max_rel_im", C.c_double), ("max_abs", C.c_double), ("worst_r", C.c_double),
+                ("max_abs_at_exact_zero", C.c_double), ("decade_histogram", C.c_uint64 * 24)]
+
+
 class BenchReportC(C.Structure):
     _fields_ = [("fill", FillReportC), ("max_rel_re", C.c_double), ("max_rel_im", C.c_double),
                 ("speedup", C.c_double), ("analytic_time_s", C.c_double),
@@ -133,6 +139,7 @@ PROTOTYPES = {
     "gk_predicted_calls": [C.c_uint64, C.c_uint64, C.c_uint64, _u64p],
     "gk_compare_fills": [_vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_max_vertex_distance": [_vp, _vp, _dp],
+    "gk_error_sweep": [_vp, _vp, C.c_int, C.c_int, C.c_uint64, _vp],
     "gk_bench_compare": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, _vp, _vp,
                          C.c_int, C.c_int, C.c_int, _vp],
     "gk_sphere_mesh": [C.c_double, C.c_int, _vp, _szp, _vp, _szp],

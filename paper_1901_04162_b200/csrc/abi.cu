@@ -418,6 +418,53 @@ gk_status gk_compare_fills(gk_ctx* c, const gk_c128* test, const gk_c128* ref, s
   });
 }
 
+gk_status gk_error_sweep(gk_ctx* c, const gk_table* t, gk_kind kind, gk_interp method,
+                         uint64_t probes, gk_sweep_report* out) {
+  return guarded([&] {
+    check_ctx(c);
+    need(t != nullptr && out != nullptr, GK_ERR_INVALID_ARGUMENT, "null argument");
+    need(probes >= 1, GK_ERR_INVALID_ARGUMENT, "error_sweep: need at least one probe");
+    need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
+    need((kind == GK_KIND_EXP && method == GK_INTERP_LINEAR) ||
+             (kind == GK_KIND_GREEN && method == GK_INTERP_LAGRANGE),
+         GK_ERR_INVALID_ARGUMENT,
+         "error_sweep: the device tabulates Exp with linear and Green with Lagrange "
+         "interpolation");
+    use_device(c);
+    gk::DevBuf<unsigned long long> w;
+    gk::DevBuf<double> comb;
+    w.alloc(32, c->stream);
+    comb.alloc(probes, c->stream);
+    unsigned long long init[32] = {};
+    init[5] = ~0ull;
+    GK_CUDA(cudaMemcpyAsync(w.p, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    gk::launch_sweep(c, t, kind, probes, comb.p, w.p);
+    unsigned long long h[32];
+    GK_CUDA(cudaMemcpyAsync(h, w.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    auto dbl = [&](int i) {
+      double v;
+      std::memcpy(&v, &h[i], sizeof(double));
+      return v;
+    };
+    gk_sweep_report r{};
+    r.probe_count = probes;
+    r.max_rel_re = dbl(0);
+    r.max_rel_im = dbl(1);
+    r.max_abs = dbl(2);
+    r.max_abs_at_exact_zero = dbl(3);
+    // the probe radius exactly as the kernel formed it (bounds.hpp:141-145)
+    const uint64_t i = h[5] == ~0ull ? 0 : h[5];
+    const double a = t->dev.r_min, b = t->dev.r_max;
+    const double step = probes == 1 ? 0.0 : (b - a) / static_cast<double>(probes - 1);
+    double rr = i + 1 == probes ? b : a + static_cast<double>(i) * step;
+    rr = rr < a ? a : (rr > b ? b : rr);
+    r.worst_r = rr;
+    for (int d = 0; d < 24; ++d) r.decade_histogram[d] = h[8 + d];
+    *out = r;
+  });
+}
+
 gk_status gk_max_vertex_distance(gk_ctx* c, const gk_mesh* mesh, double* out) {
   return guarded([&] {
     check_ctx(c);

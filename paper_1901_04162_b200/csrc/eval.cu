@@ -108,6 +108,107 @@ void launch_locate(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, ui
   GK_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------ error_sweep
+
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* w, double v) {
+  if (v > 0.0) atomicMax(w, static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// probe i of error_sweep (bounds.hpp:141-145): r = a + i step, r_max at the
+// end -- rounded like the reference (no contraction), so the probes are its own
+__device__ __forceinline__ double sweep_probe(uint64_t i, uint64_t n, double a, double b) {
+  const double step = n == 1 ? 0.0 : __ddiv_rn(__dsub_rn(b, a), static_cast<double>(n - 1));
+  double r = i + 1 == n ? b : __dadd_rn(a, __dmul_rn(static_cast<double>(i), step));
+  r = r < a ? a : r;
+  return r > b ? b : r;
+}
+
+template <int KIND, int DEG>
+__global__ void sweep_kernel(TableDev T, uint64_t n, double* __restrict__ comb,
+                             unsigned long long* w) {
+  double mre = 0.0, mim = 0.0, mab = 0.0, mz = 0.0, mc = 0.0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const double r = sweep_probe(i, n, T.r_min, T.r_max);
+    const double2 ap = KIND == GK_KIND_EXP ? exp_table(r, T)
+                       : (DEG == 3 ? green_table<3>(r, T) : green_table_any(r, T));
+    const double2 ex = analytic_sincos(KIND, T.k_re, T.k_im, r);
+    const double dre = fabs(ap.x - ex.x), dim = fabs(ap.y - ex.y);
+    const double dmod = hypot(ap.x - ex.x, ap.y - ex.y);
+    mab = fmax(mab, dmod);
+    double c = 0.0;
+    if (ex.x != 0.0) {
+      const double rel = dre / fabs(ex.x);
+      mre = fmax(mre, rel);
+      c = fmax(c, rel);
+    } else if (dre > 0.0) {
+      mz = fmax(mz, dre);
+    }
+    if (ex.y != 0.0) {
+      const double rel = dim / fabs(ex.y);
+      mim = fmax(mim, rel);
+      c = fmax(c, rel);
+    } else if (dim > 0.0) {
+      mz = fmax(mz, dim);
+    }
+    comb[i] = c;
+    mc = fmax(mc, c);
+    const double mod = hypot(ex.x, ex.y);
+    if (mod > 0.0 && dmod > 0.0) {
+      int d = static_cast<int>(floor(log10(dmod / mod))) + 20;
+      d = d < 0 ? 0 : (d > 23 ? 23 : d);
+      atomicAdd(w + 8 + d, 1ull);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+    mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, o));
+    mab = fmax(mab, __shfl_xor_sync(0xffffffffu, mab, o));
+    mz = fmax(mz, __shfl_xor_sync(0xffffffffu, mz, o));
+    mc = fmax(mc, __shfl_xor_sync(0xffffffffu, mc, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomic_max_pos(w, mre);
+    atomic_max_pos(w + 1, mim);
+    atomic_max_pos(w + 2, mab);
+    atomic_max_pos(w + 3, mz);
+    atomic_max_pos(w + 4, mc);
+  }
+}
+
+// the first probe attaining the maximum combined error (strict > in the
+// reference's loop keeps the first one)
+__global__ void sweep_argmax_kernel(const double* __restrict__ comb, uint64_t n,
+                                    unsigned long long* w) {
+  const double mc = __longlong_as_double(static_cast<long long>(w[4]));
+  unsigned long long best = ~0ull;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    if (comb[i] == mc && i < best) best = i;
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(0xffffffffu, best, o);
+    best = v < best ? v : best;
+  }
+  if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(w + 5, best);
+}
+
+void launch_sweep(gk_ctx* ctx, const gk_table* t, int kind, uint64_t probes, double* comb,
+                  unsigned long long* w) {
+  size_t grid = (probes + 255) / 256;
+  const size_t cap = static_cast<size_t>(ctx->sm_count) * 16;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  const unsigned g = static_cast<unsigned>(grid);
+  const TableDev T = t->dev;
+  if (kind == GK_KIND_EXP) sweep_kernel<GK_KIND_EXP, 0><<<g, 256, 0, ctx->stream>>>(T, probes, comb, w);
+  else if (T.degree == 3) sweep_kernel<GK_KIND_GREEN, 3><<<g, 256, 0, ctx->stream>>>(T, probes, comb, w);
+  else sweep_kernel<GK_KIND_GREEN, 0><<<g, 256, 0, ctx->stream>>>(T, probes, comb, w);
+  GK_CUDA(cudaGetLastError());
+  sweep_argmax_kernel<<<g, 256, 0, ctx->stream>>>(comb, probes, w);
+  count_launches(2);
+  GK_CUDA(cudaGetLastError());
+}
+
 // ---------------------------------------------------------- compare_fills
 
 __global__ void compare_kernel(const double2* __restrict__ test, const double2* __restrict__ ref,

@@ -111,6 +111,11 @@ void launch_points(gk_mesh* mesh, const double* d_verts, const uint32_t* d_tris,
 // max over vertex pairs of |a - b|^2 (reference summation order) -> *d2_bits
 void launch_max_vertex_d2(const double* verts, size_t nv, unsigned long long* d2_bits,
                           cudaStream_t s);
+// error_sweep (bounds.hpp:128-186): w[0..4] = max_rel_re, max_rel_im, max_abs,
+// max_abs_at_exact_zero, max combined (double bits); w[5] = first probe index
+// at the max combined; w[8..31] decade histogram.  `comb` scratch [probes].
+void launch_sweep(gk_ctx* ctx, const gk_table* t, int kind, uint64_t probes, double* comb,
+                  unsigned long long* w);
 // compare_fills partial maxima (as non-negative double bits) -> w[0] (re), w[1] (im)
 void launch_compare(gk_ctx* ctx, const gk_c128* test, const gk_c128* ref, size_t rows, size_t N,
                     size_t row_begin, size_t ld, unsigned long long* w);

@@ -27,6 +27,13 @@ class KernelKind(enum.IntEnum):
     GreenOverR = 1
 
 
+class InterpMethod(enum.IntEnum):
+    """gktab::InterpMethod (bounds.hpp:15)"""
+
+    Linear = 0
+    Lagrange = 1
+
+
 class Mode(enum.IntEnum):
     """AnalyticKernel (DIRECT) vs TableKernel (TABLE), matfill.hpp:59-87"""
 
@@ -111,6 +118,19 @@ class FillReport:
     def from_c(cls, r: FillReportC) -> "FillReport":
         return cls(r.N, r.m, r.n, r.predicted_calls, r.actual_calls, r.fallback_calls,
                    r.wall_time_s)
+
+
+@dataclass
+class ErrorSweepReport:
+    """gktab::ErrorSweepReport (bounds.hpp:113-124)"""
+
+    probe_count: int = 0
+    max_rel_re: float = 0.0
+    max_rel_im: float = 0.0
+    max_abs: float = 0.0
+    worst_r: float = 0.0
+    max_abs_at_exact_zero: float = 0.0
+    decade_histogram: list = field(default_factory=lambda: [0] * 24)
 
 
 def wavenumber(medium: Medium) -> complex:
@@ -292,6 +312,18 @@ class DeviceTable:
         check(lib().gk_locate(self.ctx.h, self.h, r.data_ptr() if r.numel() else None, r.numel(),
                               out.data_ptr() if r.numel() else None), "locate")
         return out
+
+    def error_sweep(self, kind: KernelKind, method: InterpMethod | None = None,
+                    probe_count: int = 10000) -> ErrorSweepReport:
+        """error_sweep (bounds.hpp:128-186) on the device: the device's methods
+        (Exp linear, Green Lagrange) against the device analytic evaluation."""
+        if method is None:
+            method = InterpMethod.Linear if kind == KernelKind.PlainExp else InterpMethod.Lagrange
+        r = _lib.SweepReportC()
+        check(lib().gk_error_sweep(self.ctx.h, self.h, int(kind), int(method), probe_count,
+                                   C.byref(r)), "error_sweep")
+        return ErrorSweepReport(r.probe_count, r.max_rel_re, r.max_rel_im, r.max_abs, r.worst_r,
+                                r.max_abs_at_exact_zero, list(r.decade_histogram))
 
     def eval_exp(self, r: float) -> complex:
         return complex(self.eval_batch(KernelKind.PlainExp, [r]).cpu()[0])

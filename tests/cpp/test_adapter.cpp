@@ -9,6 +9,7 @@
 // Built by __graft_entry__.build(); run by tests/test_gpu_cpp.py.
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <stdexcept>
 #include <vector>
 
@@ -111,6 +112,31 @@ int main() {
     const auto same = gk::compare_fills(zd, zd);
     CHECK(same.max_rel_re == 0.0 && same.max_rel_im == 0.0);
     (void)rd;
+  }
+  // error_sweep on the device + the reference's CSV row format
+  {
+    gk::DeviceEvaluator e(ctx, gk::SamplingConfig{});
+    const auto rs = e.error_sweep(gk::KernelKind::GreenOverR, gk::InterpMethod::Lagrange, 10000);
+    CHECK(rs.probe_count == 10000 && rs.max_rel_re > 0.0 && std::isfinite(rs.max_rel_re));
+    CHECK(rs.max_abs > 0.0 && std::isfinite(rs.max_abs));
+    CHECK(throws<std::invalid_argument>(
+        [&] { e.error_sweep(gk::KernelKind::PlainExp, gk::InterpMethod::Lagrange, 10); }));
+    std::ostringstream os;
+    gk::write_sweep_csv_header(os);
+    gk::write_sweep_csv_row(os, gk::KernelKind::GreenOverR, gk::InterpMethod::Lagrange, 3, rs);
+    CHECK(os.str().rfind("kernel,method,probes,max_rel_re,max_rel_im,max_abs,worst_r\ngreen,lagrange3,10000,", 0) == 0);
+    gk::FillReport fr;
+    fr.N = 20;
+    fr.m = 4;
+    fr.n = 3;
+    fr.predicted_calls = 14400;
+    fr.actual_calls = 13680;
+    fr.speedup = 0.1;
+    std::ostringstream ob;
+    gk::write_bench_csv(ob, fr);
+    CHECK(ob.str() == "N,m,n,predicted_calls,actual_calls,fallback_calls,analytic_s,interp_s,"
+                      "speedup,max_rel_re,max_rel_im\n20,4,3,14400,13680,0,0,0,"
+                      "0.10000000000000001,0,0\n");
   }
   std::printf("%s (%d failure(s))\n", failures ? "FAILED" : "ALL OK", failures);
   return failures ? 1 : 0;

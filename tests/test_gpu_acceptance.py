@@ -150,3 +150,32 @@ def test_criterion8_determinism_and_nodes(gk):
     z2, _ = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
     import torch
     assert torch.equal(z1, z2)
+
+
+@pytest.mark.parametrize("S,refine", [(1000, True), (1000, False), (10000, True)])
+def test_device_error_sweep_matches_reference(gk, oracle, ref, S, refine):
+    """gk_error_sweep (device) vs the reference's own error_sweep
+    (bounds.hpp:128-186) on the same plan: same probes, maxima within the
+    few-ulp differences of table and analytic values, same histogram up to
+    probes on a decade boundary."""
+    t = gk.DeviceTable(ref_cfg(gk, S, refine))
+    d = t.download()
+    rev = ref.evaluator(oracle.make_plan(d["abscissae"], d["zeros"]), K)
+    n = 100000
+    grid = d["abscissae"][0] + np.arange(n) * ((d["abscissae"][-1] - d["abscissae"][0]) / (n - 1))
+    grid[-1] = d["abscissae"][-1]
+    for kind, method in ((EXP, 0), (GREEN, 1)):
+        dev = t.error_sweep(gk.KernelKind(kind), gk.InterpMethod(method), n)
+        want = ref.error_sweep(rev, kind, method, n)
+        assert dev.probe_count == n
+        for key in ("max_rel_re", "max_rel_im", "max_abs"):
+            assert abs(getattr(dev, key) - want[key]) <= 1e-5 * want[key] + 1e-300, key
+        assert dev.worst_r in grid
+        diff = sum(abs(a - b) for a, b in zip(dev.decade_histogram, want["decade_histogram"]))
+        assert diff <= n // 1000
+        # probes with zero error (on nodes) are not binned, as in the reference
+        assert abs(sum(dev.decade_histogram) - sum(want["decade_histogram"])) <= n // 1000
+    with pytest.raises(gk.InvalidArgument):
+        t.error_sweep(gk.KernelKind.PlainExp, gk.InterpMethod.Lagrange, 10)
+    with pytest.raises(gk.InvalidArgument):
+        t.error_sweep(gk.KernelKind.GreenOverR, gk.InterpMethod.Lagrange, 0)
