@@ -409,6 +409,7 @@ def main():
                    "l2": "output Z >> L2 (no flush needed); inputs resident"},
         "fill_time_s": main_res["ms_per_step"] * 1e-3,
         "roofline": {"bound": "fp64", "achieved": main_res["kernel_tflops"], "peak": p64,
+                     "peak_nominal": 148 * 64 * 2 * 1.965e9 / 1e12,
                      "unit": "TFLOP/s", "frac": main_res["kernel_tflops"] / p64,
                      "traffic": traffic,
                      "note": f"{FLOPS_PER_EVAL} algorithmic FP64 flops/eval (SURVEY 8d, FMA=2) x "
