@@ -27,11 +27,16 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
 SOURCES = {
     "build.cu": ["-fmad=false"],
     "fill.cu": [],
+    "fill_mo1.cu": [],
+    "fill_mo3.cu": [],
+    "fill_mo4.cu": [],
+    "fill_mo6.cu": [],
+    "fill_mo7.cu": [],
     "eval.cu": [],
     "abi.cu": [],
     "host.cpp": [],
 }
-HEADERS = ["gk_device.cuh", "gk_internal.h"]
+HEADERS = ["gk_device.cuh", "gk_internal.h", "fill_kernels.cuh"]
 
 
 def _newer(src_files, target) -> bool:

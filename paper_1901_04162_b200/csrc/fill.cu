@@ -1,781 +1,12 @@
-// fill.cu -- K1 distance range, K3 table fill, K4 direct fill.
-//
-// The fill replaces fill_matrix's fill_rows loop (matfill.hpp:169-203) with
-// AnalyticKernel::accumulate (DIRECT, kernel.hpp:48-61) or
-// TableKernel::accumulate -> accumulate_green (TABLE, evaluator.hpp:150-194).
-//
-// Work decomposition: a CTA of 8 warps owns a tile of 8 observation rows x
-// 128 source columns; warp w takes row p = tile_row*8 + w, lane l takes the
-// columns q = tile_col*128 + 32 b + l (b = 0..3), so every warp store is one
-// coalesced 512-byte complex128 row segment.  The m outer points of p live in
-// registers; the 3n inner points of q stream from a [3n][N] plane layout
-// (coalesced 32-byte loads, L1/L2 resident).  Each lane keeps one complex
-// accumulator per outer point (sum_i w_i K(r_oi)) and finishes the entry with
-// sum_o w_o acc_o -- the reference's double sum regrouped (same terms).
+// fill.cu -- fill dispatch (launch_fill), K1 distance range, phase and
+// attenuation tables.  The fill kernels live in fill_kernels.cuh.
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
-#include <cstring>
-#include <math_constants.h>
 
-#include "gk_internal.h"
+#include "fill_kernels.cuh"
 
 namespace gk {
-
-constexpr int kRowsPerTile = 8;  // one row per warp
-constexpr int kMaxColBlocks = 32;  // 32-column blocks per tile (adaptive, see launch_fill)
-constexpr int kThreads = 32 * kRowsPerTile;
-constexpr int kKindPair = 2;  // fused Exp + Green fill sharing r
-
-// per-entry accumulators: one complex per outer point, two for the fused pair
-template <int MO, bool PAIR>
-struct Acc {
-  double2 e[MO], g[PAIR ? MO : 1];
-  __device__ __forceinline__ void zero() {
-#pragma unroll
-    for (int o = 0; o < MO; ++o) {
-      e[o] = make_double2(0.0, 0.0);
-      if constexpr (PAIR) g[o] = make_double2(0.0, 0.0);
-    }
-  }
-  // acc += w * (c - j s) for kind KIND; y = 1/r for the Green weight
-  template <int KIND>
-  __device__ __forceinline__ void add(int o, double w, double y, double2 cs) {
-    if constexpr (KIND == kKindPair) {
-      e[o].x = __fma_rn(w, cs.x, e[o].x);
-      e[o].y = __fma_rn(-w, cs.y, e[o].y);
-      const double wg = __dmul_rn(w, y);
-      g[o].x = __fma_rn(wg, cs.x, g[o].x);
-      g[o].y = __fma_rn(-wg, cs.y, g[o].y);
-    } else {
-      const double wk = KIND == GK_KIND_GREEN ? __dmul_rn(w, y) : w;
-      e[o].x = __fma_rn(wk, cs.x, e[o].x);
-      e[o].y = __fma_rn(-wk, cs.y, e[o].y);
-    }
-  }
-  // acc += w * v (table values: v = K(r) for the kind, vg = Green for the pair)
-  __device__ __forceinline__ void add_values(int o, double w, double2 v, double2 vg) {
-    e[o].x = __fma_rn(w, v.x, e[o].x);
-    e[o].y = __fma_rn(w, v.y, e[o].y);
-    if constexpr (PAIR) {
-      g[o].x = __fma_rn(w, vg.x, g[o].x);
-      g[o].y = __fma_rn(w, vg.y, g[o].y);
-    }
-  }
-  // finish sum_o w_o acc_o and store (self pairs stay zero, matfill.hpp:178).
-  // A non-finite entry can only come from a zero-distance point pair, which
-  // the reference rejects (eval_analytic, kernel.hpp:51-53): counted in *bad.
-  template <class W>
-  __device__ __forceinline__ void finish(const W& wo, bool self, bool valid, double2* z,
-                                         double2* z2, size_t off, unsigned long long* bad) {
-    double2 re = make_double2(0.0, 0.0), rg = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int o = 0; o < MO; ++o) {
-      const double w = wo(o);
-      re.x = __fma_rn(w, e[o].x, re.x);
-      re.y = __fma_rn(w, e[o].y, re.y);
-      if constexpr (PAIR) {
-        rg.x = __fma_rn(w, g[o].x, rg.x);
-        rg.y = __fma_rn(w, g[o].y, rg.y);
-      }
-    }
-    if (self) re = rg = make_double2(0.0, 0.0);
-    if (valid && !(isfinite(re.x) && isfinite(re.y) && isfinite(rg.x) && isfinite(rg.y)))
-      atomicAdd(bad, 1ull);
-    if (valid) {
-      __stcs(z + off, re);
-      if constexpr (PAIR) __stcs(z2 + off, rg);
-    }
-  }
-};
-
-__global__ void atten_kernel(double* E, int n);
-
-struct FillArgs {
-  const double4* outer;
-  const double4* inner;
-  size_t N;
-  int ipt;
-  size_t row_begin, row_end;
-  size_t ncb, ntiles;
-  int cpt;  // column blocks per tile
-  double2* z;   // Exp or Green (or Exp for the fused pair fill)
-  double2* z2;  // fused pair fill: Green
-  size_t ldz;
-  TableDev T;
-  const double2* phase;
-  double K1, k_re, k_im;
-  const double4* bounds;  // per-triangle (centroid, rho_outer), for tile radius bounds
-  const double* binner;   // per-triangle rho_inner
-  double window_est;      // estimated radius spread of a 16 x 64 tile (staging heuristic)
-  const double* atten;  // lossy: exp(-n / 512), n < natten
-  int natten;
-  double KA;            // -k_im * 512
-  unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max, [2] non-finite entries
-};
-
-// Column-block walk shared by both kernels: the (column block, inner point)
-// iterations of a tile are flattened into one loop so the next inner point is
-// always in flight (register double buffer) while the current one is used.
-struct InnerWalk {
-  const double4* inner;
-  size_t N, q0base;
-  int ipt, ncb;
-  __device__ __forceinline__ void load(int cb, int i, int lane, double2& xy, double2& zw,
-                                       size_t& q, bool& valid) const {
-    const size_t qr = q0base + 32 * static_cast<size_t>(cb) + lane;
-    valid = qr < N;
-    q = valid ? qr : N - 1;
-    const double2* p = reinterpret_cast<const double2*>(inner + static_cast<size_t>(i) * N + q);
-    xy = __ldg(p);
-    zw = __ldg(p + 1);
-  }
-};
-
-// --------------------------------------------------- TMA bulk-copy helpers
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
-
-// one-shot copy of `bytes` (multiple of 16, 16 B aligned) global -> shared,
-// issued by thread 0 as a TMA bulk copy; every thread waits on the mbarrier
-__device__ __forceinline__ void stage_bulk(void* dst, const void* src, uint32_t bytes,
-                                          uint64_t* bar) {
-  if (threadIdx.x == 0) {
-    mbar_init(bar);
-    mbar_expect_tx(bar, bytes);
-    tma_load_1d(dst, src, bytes, bar);
-  }
-  __syncthreads();  // barrier initialised before anyone polls it
-  mbar_wait(bar, 0);
-}
-
-// K4: direct evaluation.  Per eval: 6 (r^2) + 6 (rsqrt, r) + 11 (phase,
-// table lookup, complex combine) + 3 (weight, accumulate) = 26 FP64 ops.
-// The warp's outer points sit in shared memory (broadcast loads, one
-// wavefront each) instead of registers, so ~80 registers per thread allow 3
-// CTAs (24 warps) per SM to hide the FP64 dependency latency.
-template <int MO, int KIND, bool LOSSY, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A) {
-  extern __shared__ double2 tab[];  // kPhaseM phase entries (128 KB) [+ attenuation table]
-  __shared__ double so[kRowsPerTile][MO][4];
-  __shared__ uint64_t bar;
-  stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
-  double* att = reinterpret_cast<double*>(tab + kPhaseM);
-  if constexpr (LOSSY)
-    for (int i = threadIdx.x; i < A.natten; i += blockDim.x) att[i] = A.atten[i];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t N = A.N;
-  double (*my)[4] = so[warp];
-
-  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-    const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
-    const size_t p = A.row_begin + tr * kRowsPerTile + warp;
-    if (p >= A.row_end) continue;  // warp-uniform
-    __syncwarp();
-    if (lane < MO) {
-      const double4 P = A.outer[p * MO + lane];
-      my[lane][0] = P.x;
-      my[lane][1] = P.y;
-      my[lane][2] = P.z;
-      my[lane][3] = P.w;
-    }
-    __syncwarp();
-    const size_t q0base = tc * (32 * static_cast<size_t>(A.cpt));
-    int ncb = static_cast<int>((N - q0base + 31) / 32);
-    if (ncb > A.cpt) ncb = A.cpt;
-    const InnerWalk W{A.inner, N, q0base, A.ipt, ncb};
-    const int iters = ncb * A.ipt;
-    double2 nxy, nzw;
-    size_t q;
-    bool valid;
-    W.load(0, 0, lane, nxy, nzw, q, valid);
-    Acc<MO, KIND == kKindPair> acc;
-    acc.zero();
-    int ncb_next = 0, ni = 0;  // (column block, inner point) of the prefetch
-    for (int it = 0; it < iters; ++it) {
-      const double2 pxy = nxy, pzw = nzw;
-      const size_t qc = q;
-      const bool vc = valid;
-      if (++ni == A.ipt) {
-        ni = 0;
-        ++ncb_next;
-      }
-      const bool block_done = ni == 0;
-      if (it + 1 < iters) W.load(ncb_next, ni, lane, nxy, nzw, q, valid);
-#pragma unroll
-      for (int o = 0; o < MO; ++o) {
-        const double2 oxy = *reinterpret_cast<const double2*>(&my[o][0]);
-        const double oz = my[o][2];
-        const double d2 = dist2(oxy.x, oxy.y, oz, pxy.x, pxy.y, pzw.x);
-        const double y = rsqrt_fast(d2);
-        const double r = __dmul_rn(d2, y);
-        const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
-        double w = pzw.y;
-        if constexpr (LOSSY) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
-        acc.template add<KIND>(o, w, y, cs);
-      }
-      if (block_done) {  // column block complete: finish the entry
-        acc.finish([&](int o) { return my[o][3]; }, qc == p, vc, A.z, A.z2,
-                   (p - A.row_begin) * A.ldz + qc, A.counters + 2);
-        acc.zero();
-      }
-    }
-  }
-}
-
-// K4 fast path (IPT = 3n known at compile time, n = 1..5): the inner-point
-// loop of a column block is fully unrolled with a one-point register
-// prefetch, the outer points live in registers and 12 warps x 1 CTA per SM
-// (~160 registers each) keep the FP64 pipe fed.  Non-FP64 instructions cost
-// an issue cycle each while an FP64 warp instruction holds the 16-lane pipe
-// for two, so this variant's ~9 non-FP64 instructions/eval (vs ~16 in the
-// runtime-IPT kernel) are worth ~12% (ablations: scripts/direct_variants.cu).
-// (The fused pair fill carries twice the accumulators: 8 warps, ~200 registers.)
-#ifndef GK_WARPS_V4
-#define GK_WARPS_V4 12  // scripts/build_variant.sh experiments override it
-#endif
-template <int KIND>
-__host__ __device__ constexpr int warps_v4() { return KIND == kKindPair ? 8 : GK_WARPS_V4; }
-
-template <int MO, int IPT, int KIND, bool LOSSY>
-__global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(const FillArgs A) {
-  constexpr int kWarpsV4 = warps_v4<KIND>();
-  extern __shared__ double2 tab[];  // kPhaseM phase entries (128 KB) [+ attenuation table]
-  __shared__ double sw[kWarpsV4][MO];
-  __shared__ uint64_t bar;
-  stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
-  double* att = reinterpret_cast<double*>(tab + kPhaseM);
-  if constexpr (LOSSY)
-    for (int i = threadIdx.x; i < A.natten; i += blockDim.x) att[i] = A.atten[i];
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t N = A.N;
-  const double4* last = A.inner + (N - 1);
-
-  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-    const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
-    const size_t p = A.row_begin + tr * kWarpsV4 + warp;
-    if (p >= A.row_end) continue;  // warp-uniform
-    double ox[MO], oy[MO], oz[MO];
-#pragma unroll
-    for (int o = 0; o < MO; ++o) {
-      const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
-      const double2 zw = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o) + 1);
-      ox[o] = xy.x;
-      oy[o] = xy.y;
-      oz[o] = zw.x;
-      if (lane == 0) sw[warp][o] = zw.y;
-    }
-    __syncwarp();
-    const size_t q0 = tc * (32 * static_cast<size_t>(A.cpt));
-    int nblk = static_cast<int>((N - q0 + 31) / 32);
-    if (nblk > A.cpt) nblk = A.cpt;
-    const double4* colp = A.inner + q0 + lane;  // column block 0, inner point 0
-    double2 cxy, czw;
-    {
-      const double2* ptr = reinterpret_cast<const double2*>(colp <= last ? colp : last);
-      cxy = __ldg(ptr);
-      czw = __ldg(ptr + 1);
-    }
-    for (int cb = 0; cb < nblk; ++cb) {
-      const double4* cp = colp <= last ? colp : last;
-      Acc<MO, KIND == kKindPair> acc;
-      acc.zero();
-#pragma unroll
-      for (int i = 0; i < IPT; ++i) {
-        const double2 pxy = cxy, pzw = czw;
-        const double4* np = (i + 1 < IPT) ? cp + (i + 1) * N : (colp + 32 <= last ? colp + 32 : last);
-        cxy = __ldg(reinterpret_cast<const double2*>(np));
-        czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
-#pragma unroll
-        for (int o = 0; o < MO; ++o) {
-          const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-          const double y = rsqrt_fast(d2);
-          const double r = __dmul_rn(d2, y);
-          const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
-          double w = pzw.y;
-          if constexpr (LOSSY) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
-          acc.template add<KIND>(o, w, y, cs);
-        }
-      }
-      const size_t q = q0 + 32 * static_cast<size_t>(cb) + lane;
-      acc.finish([&](int o) { return sw[warp][o]; }, q == p, q < N, A.z, A.z2,
-                 (p - A.row_begin) * A.ldz + q, A.counters + 2);
-      colp += 32;
-    }
-    __syncwarp();
-  }
-}
-
-// K3: table evaluation (the paper's method) with the reference's fallback.
-template <int MO, int KIND, int DEG>
-__global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t N = A.N;
-  unsigned long long n_low = 0, n_high = 0;
-
-  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-    const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
-    const size_t p = A.row_begin + tr * kRowsPerTile + warp;
-    if (p >= A.row_end) continue;  // warp-uniform
-    double ox[MO], oy[MO], oz[MO];
-#pragma unroll
-    for (int o = 0; o < MO; ++o) {
-      const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
-      const double zz = __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 2);
-      ox[o] = xy.x;
-      oy[o] = xy.y;
-      oz[o] = zz;
-    }
-    const size_t q0base = tc * (32 * static_cast<size_t>(A.cpt));
-    int ncb = static_cast<int>((N - q0base + 31) / 32);
-    if (ncb > A.cpt) ncb = A.cpt;
-    const InnerWalk W{A.inner, N, q0base, A.ipt, ncb};
-    const int iters = ncb * A.ipt;
-    double2 nxy, nzw;
-    size_t q;
-    bool valid;
-    W.load(0, 0, lane, nxy, nzw, q, valid);
-    Acc<MO, KIND == kKindPair> acc;
-    acc.zero();
-    int ncb_next = 0, ni = 0;  // (column block, inner point) of the prefetch
-    for (int it = 0; it < iters; ++it) {
-      const double2 pxy = nxy, pzw = nzw;
-      const size_t qc = q;
-      const bool vc = valid;
-      if (++ni == A.ipt) {
-        ni = 0;
-        ++ncb_next;
-      }
-      const bool block_done = ni == 0;
-      const bool self = qc == p;
-      if (it + 1 < iters) W.load(ncb_next, ni, lane, nxy, nzw, q, valid);
-#pragma unroll
-      for (int o = 0; o < MO; ++o) {
-        const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-        const double r = __dmul_rn(d2, rsqrt_fast(d2));
-        double2 v, vg = make_double2(0.0, 0.0);
-        if constexpr (KIND == kKindPair) pair_table<DEG>(r, A.T, v, vg);
-        else if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, A.T);
-        else if constexpr (DEG == 3) v = green_table<3>(r, A.T);
-        else v = green_table_any(r, A.T);
-        const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
-        if (__any_sync(0xffffffffu, oob)) {
-          if (oob) {
-            if (!self && vc) {
-              // the reference's eval_kernel fallback (evaluator.hpp:199-205)
-              const unsigned calls = KIND == kKindPair ? 2u : 1u;
-              if constexpr (KIND == kKindPair) {
-                v = analytic_sincos(GK_KIND_EXP, A.T.k_re, A.T.k_im, r);
-                vg = analytic_sincos(GK_KIND_GREEN, A.T.k_re, A.T.k_im, r);
-              } else {
-                v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
-              }
-              if (r > A.T.r_max) n_high += calls; else n_low += calls;
-            } else {
-              v = vg = make_double2(0.0, 0.0);
-            }
-          }
-        }
-        acc.add_values(o, pzw.y, v, vg);
-      }
-      if (block_done) {
-        acc.finish([&](int o) { return __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3); },
-                   self, vc, A.z, A.z2, (p - A.row_begin) * A.ldz + qc, A.counters + 2);
-        acc.zero();
-      }
-    }
-  }
-  for (int o = 16; o; o >>= 1) {
-    n_low += __shfl_xor_sync(0xffffffffu, n_low, o);
-    n_high += __shfl_xor_sync(0xffffffffu, n_high, o);
-  }
-  if (lane == 0 && n_low) atomicAdd(A.counters, n_low);
-  if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
-}
-
-// ------------------------------------------------ K3 with a shared-memory table
-//
-// North star part (2): the table a tile needs is held in shared memory.  Per
-// tile (16 rows x 32 cpt columns) the CTA bounds the tile's radii from the
-// per-triangle centroids and radii (as K1 does), maps [r_lo, r_hi] to the
-// lookup-bucket and record ranges it can touch, and stages exactly those
-// slices with TMA bulk copies (cp.async.bulk + mbarrier).  A table that fits
-// whole is staged once per CTA; a tile whose window exceeds the budget reads
-// the global table through L1 instead (correct either way: same code path,
-// different TableWin).
-
-constexpr int kStagedWarps = 16;
-
-struct StageArgs {
-  uint32_t lk_cap, j_cap;  // shared-memory capacity in buckets / records
-  int whole;               // the whole table fits: stage once
-};
-
-
-// the fill of one tile through a table window (shared or global)
-template <bool SMEM, int MO, int KIND, int DEG>
-__device__ __forceinline__ void table_tile(const FillArgs& A, const TableWin& win, size_t p0,
-                                           size_t tc, unsigned long long& n_low,
-                                           unsigned long long& n_high) {
-  constexpr bool WANT_E = KIND == GK_KIND_EXP || KIND == kKindPair;
-  constexpr bool WANT_G = KIND == GK_KIND_GREEN || KIND == kKindPair;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t N = A.N;
-  const size_t p = p0 + warp;
-  if (p >= A.row_end) return;  // warp-uniform
-  double ox[MO], oy[MO], oz[MO];
-#pragma unroll
-  for (int o = 0; o < MO; ++o) {
-    const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
-    const double zz = __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 2);
-    ox[o] = xy.x;
-    oy[o] = xy.y;
-    oz[o] = zz;
-  }
-  const size_t q0base = tc * (32 * static_cast<size_t>(A.cpt));
-  int ncb = static_cast<int>((N - q0base + 31) / 32);
-  if (ncb > A.cpt) ncb = A.cpt;
-  const InnerWalk W{A.inner, N, q0base, A.ipt, ncb};
-  const int iters = ncb * A.ipt;
-  double2 nxy, nzw;
-  size_t q;
-  bool valid;
-  W.load(0, 0, lane, nxy, nzw, q, valid);
-  Acc<MO, KIND == kKindPair> acc;
-  acc.zero();
-  int ncb_next = 0, ni = 0;
-  for (int it = 0; it < iters; ++it) {
-    const double2 pxy = nxy, pzw = nzw;
-    const size_t qc = q;
-    const bool vc = valid;
-    if (++ni == A.ipt) {
-      ni = 0;
-      ++ncb_next;
-    }
-    const bool block_done = ni == 0;
-    const bool self = qc == p;
-    if (it + 1 < iters) W.load(ncb_next, ni, lane, nxy, nzw, q, valid);
-#pragma unroll
-    for (int o = 0; o < MO; ++o) {
-      const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-      const double r = __dmul_rn(d2, rsqrt_fast(d2));
-      double2 ve = make_double2(0.0, 0.0), vg = make_double2(0.0, 0.0);
-      win_eval<SMEM, DEG, WANT_E, WANT_G>(r, A.T, win, ve, vg);
-      const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
-      if (__any_sync(0xffffffffu, oob)) {
-        if (oob) {
-          if (!self && vc) {
-            // the reference's eval_kernel fallback (evaluator.hpp:199-205)
-            if constexpr (WANT_E) ve = analytic_sincos(GK_KIND_EXP, A.T.k_re, A.T.k_im, r);
-            if constexpr (WANT_G) vg = analytic_sincos(GK_KIND_GREEN, A.T.k_re, A.T.k_im, r);
-            const unsigned calls = KIND == kKindPair ? 2u : 1u;
-            if (r > A.T.r_max) n_high += calls; else n_low += calls;
-          } else {
-            ve = vg = make_double2(0.0, 0.0);
-          }
-        }
-      }
-      if constexpr (KIND == kKindPair) acc.add_values(o, pzw.y, ve, vg);
-      else acc.add_values(o, pzw.y, KIND == GK_KIND_EXP ? ve : vg, vg);
-    }
-    if (block_done) {
-      acc.finish([&](int o) { return __ldg(reinterpret_cast<const double*>(A.outer + p * MO + o) + 3); },
-                 self, vc, A.z, A.z2, (p - A.row_begin) * A.ldz + qc, A.counters + 2);
-      acc.zero();
-    }
-  }
-}
-
-template <int MO, int KIND, int DEG>
-__global__ void __launch_bounds__(32 * kStagedWarps, 1)
-    table_staged_kernel(const FillArgs A, const StageArgs S) {
-  constexpr bool WANT_E = KIND == GK_KIND_EXP || KIND == kKindPair;
-  const int grs = DEG > 0 ? 2 + 2 * (DEG + 1) : A.T.grs;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* s_lk = reinterpret_cast<uint32_t*>(smem);
-  double* s_grec = reinterpret_cast<double*>(smem + static_cast<size_t>(S.lk_cap) * 4);
-  double* s_erec = s_grec + static_cast<size_t>(S.j_cap) * grs;
-  __shared__ uint64_t bar;
-  __shared__ double red_lo[kStagedWarps], red_hi[kStagedWarps];
-  __shared__ uint32_t cur[4];   // staged window: b0, nb, j0, nj (nb = 0: none)
-  __shared__ uint32_t want[4];  // window this tile needs
-  __shared__ int mode;          // 0: shared window, 1: global table
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t n = static_cast<uint32_t>(A.T.nrec);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar);
-    cur[1] = 0;
-  }
-  __syncthreads();
-  uint32_t phase = 0;
-  unsigned long long n_low = 0, n_high = 0;
-  const TableWin gwin{A.T.grec, A.T.erec, A.T.lk, 0u, A.T.nlk, 0u, n};
-  const size_t N = A.N;
-
-  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-    const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
-    const size_t p0 = A.row_begin + tr * kStagedWarps;
-    if (!S.whole) {
-      // conservative radius range of the tile's pairs (centroid +- radii)
-      const size_t q0 = tc * (32 * static_cast<size_t>(A.cpt));
-      const size_t ncols = (N - q0) < 32 * static_cast<size_t>(A.cpt) ? N - q0 : 32 * static_cast<size_t>(A.cpt);
-      double lo = CUDART_INF, hi = 0.0;
-      for (size_t k = threadIdx.x; k < kStagedWarps * ncols; k += blockDim.x) {
-        const size_t pp = p0 + k / ncols, qq = q0 + k % ncols;
-        if (pp >= A.row_end || qq == pp) continue;
-        const double4 bp = A.bounds[pp];
-        const double4 bq = A.bounds[qq];
-        const double dx = bp.x - bq.x, dy = bp.y - bq.y, dz = bp.z - bq.z;
-        const double dc = sqrt(dx * dx + dy * dy + dz * dz);
-        const double rho = bp.w + __ldg(A.binner + qq);
-        lo = fmin(lo, (dc - rho) * (1.0 - 1e-12));
-        hi = fmax(hi, (dc + rho) * (1.0 + 1e-12));
-      }
-      for (int o = 16; o; o >>= 1) {
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
-      if (lane == 0) {
-        red_lo[warp] = lo;
-        red_hi[warp] = hi;
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        for (int w = 1; w < kStagedWarps; ++w) {
-          lo = fmin(lo, red_lo[w]);
-          hi = fmax(hi, red_hi[w]);
-        }
-        lo = fmax(lo, A.T.r_min);
-        hi = fmin(hi, A.T.r_max);
-        if (!(lo <= hi)) lo = hi = A.T.r_min;  // no in-range pair: any valid window
-        const uint32_t b_lo = lookup_bucket(lo, A.T), b_hi = lookup_bucket(hi, A.T);
-        const uint32_t b0 = b_lo & ~3u;
-        const uint32_t nb = (b_hi + 1 - b0 + 3) & ~3u;
-        const uint32_t j_lo = __ldg(A.T.lk + b_lo);
-        uint32_t j_hi = __ldg(A.T.lk + b_hi) + 1;
-        if (j_hi > n - 1) j_hi = n - 1;
-        want[0] = b0;
-        want[1] = nb;
-        want[2] = j_lo;
-        want[3] = j_hi - j_lo + 1;
-        const bool covered = cur[1] != 0 && b0 >= cur[0] && b0 + nb <= cur[0] + cur[1] &&
-                             j_lo >= cur[2] && j_hi < cur[2] + cur[3];
-        mode = covered ? 0 : (nb <= S.lk_cap && want[3] <= S.j_cap ? 2 : 1);
-      }
-    } else if (threadIdx.x == 0) {
-      want[0] = 0;
-      want[1] = (A.T.nlk + 3) & ~3u;
-      want[2] = 0;
-      want[3] = n;
-      mode = cur[1] != 0 ? 0 : 2;
-    }
-    __syncthreads();
-    if (mode == 2) {  // stage the window with TMA bulk copies
-      if (threadIdx.x == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        cur[0] = want[0];
-        cur[1] = want[1];
-        cur[2] = want[2];
-        cur[3] = want[3];
-        const uint32_t lk_bytes = want[1] * 4;
-        const uint32_t g_bytes = want[3] * grs * 8;
-        const uint32_t e_bytes = WANT_E ? want[3] * 6 * 8 : 0;
-        mbar_expect_tx(&bar, lk_bytes + g_bytes + e_bytes);
-        tma_load_1d(s_lk, A.T.lk + want[0], lk_bytes, &bar);
-        tma_load_1d(s_grec, A.T.grec + static_cast<size_t>(want[2]) * grs, g_bytes, &bar);
-        if (WANT_E) tma_load_1d(s_erec, A.T.erec + static_cast<size_t>(want[2]) * 6, e_bytes, &bar);
-      }
-      mbar_wait(&bar, phase);
-      phase ^= 1u;
-      __syncthreads();
-    }
-    if (mode != 1) {
-      const TableWin swin{s_grec, s_erec, s_lk, cur[0], cur[1], cur[2], cur[3]};
-      table_tile<true, MO, KIND, DEG>(A, swin, p0, tc, n_low, n_high);
-    } else {
-      table_tile<false, MO, KIND, DEG>(A, gwin, p0, tc, n_low, n_high);
-    }
-    __syncthreads();  // the window may be restaged for the next tile
-  }
-  for (int o = 16; o; o >>= 1) {
-    n_low += __shfl_xor_sync(0xffffffffu, n_low, o);
-    n_high += __shfl_xor_sync(0xffffffffu, n_high, o);
-  }
-  if (lane == 0 && n_low) atomicAdd(A.counters, n_low);
-  if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
-}
-
-template <class K>
-void launch_kernel(gk_ctx* ctx, K kernel, const FillArgs& a, size_t smem, int threads = kThreads) {
-  if (smem > 48 * 1024)
-    GK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-  int per_sm = 0;
-  GK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
-  if (per_sm < 1) per_sm = 1;
-  size_t grid = static_cast<size_t>(ctx->sm_count) * per_sm;
-  if (grid > a.ntiles) grid = a.ntiles;
-  if (grid < 1) grid = 1;
-  kernel<<<static_cast<unsigned>(grid), threads, smem, ctx->stream>>>(a);
-  count_launches(1);
-  GK_CUDA(cudaGetLastError());
-}
-
-// widest tiles (fewest cold starts) that still leave >= 16 tiles per
-// resident CTA for load balance
-void set_tiling(const gk_ctx* ctx, FillArgs& a, int rows_per_tile, int ctas_per_sm) {
-  const size_t row_blocks = (a.row_end - a.row_begin + rows_per_tile - 1) / rows_per_tile;
-  const size_t col_blocks = (a.N + 31) / 32;
-  const size_t want = static_cast<size_t>(ctx->sm_count) * ctas_per_sm * 16;
-  int cpt = kMaxColBlocks;
-  while (cpt > 1 && row_blocks * ((col_blocks + cpt - 1) / cpt) < want) cpt /= 2;
-  a.cpt = cpt;
-  a.ncb = (col_blocks + cpt - 1) / cpt;
-  a.ntiles = row_blocks * a.ncb;
-}
-
-template <int MO, int IPT, int KIND, bool LOSSY>
-void launch_v4(gk_ctx* ctx, FillArgs a, size_t smem) {
-  set_tiling(ctx, a, warps_v4<KIND>(), 1);
-  launch_kernel(ctx, direct_kernel_v4<MO, IPT, KIND, LOSSY>, a, smem, 32 * warps_v4<KIND>());
-}
-
-template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
-void launch_one(gk_ctx* ctx, FillArgs a) {
-  if constexpr (MODE == GK_MODE_DIRECT) {
-    const size_t smem = kPhaseM * sizeof(double2) + (LOSSY ? a.natten * sizeof(double) : 0);
-    static const bool use_v4 = [] {
-      const char* e = std::getenv("GK_DIRECT_V4");
-      return !(e && e[0] == '0');
-    }();
-    if (use_v4) {
-      switch (a.ipt) {  // n = 1..5 Gauss points per edge: fully unrolled fast path
-        case 3: return launch_v4<MO, 3, KIND, LOSSY>(ctx, a, smem);
-        case 6: return launch_v4<MO, 6, KIND, LOSSY>(ctx, a, smem);
-        case 9: return launch_v4<MO, 9, KIND, LOSSY>(ctx, a, smem);
-        case 12: return launch_v4<MO, 12, KIND, LOSSY>(ctx, a, smem);
-        case 15: return launch_v4<MO, 15, KIND, LOSSY>(ctx, a, smem);
-        default: break;
-      }
-    }
-    set_tiling(ctx, a, kRowsPerTile, 2);
-    launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 2>, a, smem);
-  } else {
-    // GK_TABLE_SMEM: 0 = L1 kernel, 2 = always stage (tests), unset/1 = auto.
-    // GK_TABLE_SMEM_BUDGET (bytes) shrinks the window budget (tests).  Read per
-    // launch so a test can exercise every path in one process.
-    const char* env = std::getenv("GK_TABLE_SMEM");
-    const int staging = env ? std::atoi(env) : 1;
-    if (staging == 0) {
-      set_tiling(ctx, a, kRowsPerTile, 2);
-      launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
-      return;
-    }
-    // shared-memory window sizing: whole table if it fits, else proportional caps
-    constexpr bool want_e = KIND == GK_KIND_EXP || KIND == kKindPair;
-    const size_t rec_bytes = static_cast<size_t>(a.T.grs) * 8 + (want_e ? 48 : 0);
-    size_t budget = 200 * 1024;
-    if (const char* b = std::getenv("GK_TABLE_SMEM_BUDGET")) {
-      const long v = std::atol(b);
-      if (v >= 4096 && static_cast<size_t>(v) < budget) budget = static_cast<size_t>(v);
-    }
-    StageArgs S{};
-    const size_t nlk4 = (static_cast<size_t>(a.T.nlk) + 3) & ~size_t(3);
-    if (nlk4 * 4 + a.T.nrec * rec_bytes <= budget) {
-      S.whole = 1;
-      S.lk_cap = static_cast<uint32_t>(nlk4);
-      S.j_cap = a.T.nrec;
-      set_tiling(ctx, a, kStagedWarps, 1);
-    } else {
-      const double per_rec = static_cast<double>(a.T.nlk) / a.T.nrec;  // buckets per record
-      const size_t j_cap = static_cast<size_t>(budget / (rec_bytes + 4.0 * per_rec * 1.5));
-      // records a typical tile window spans; when it clearly exceeds the
-      // capacity (dense tables, e.g. S = 1e4 on large meshes) every tile would
-      // fall back to global reads: use the L1 kernel with its wider tiles
-      const double est = a.T.nrec * a.window_est / (a.T.r_max - a.T.r_min);
-      if (staging != 2 && est > 2.0 * static_cast<double>(j_cap)) {
-        set_tiling(ctx, a, kRowsPerTile, 2);
-        launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
-        return;
-      }
-      S.j_cap = static_cast<uint32_t>(j_cap);
-      S.lk_cap = static_cast<uint32_t>(((budget - j_cap * rec_bytes) / 4) & ~size_t(3));
-      set_tiling(ctx, a, kStagedWarps, 1);
-      // narrow tiles keep each tile's radius window small
-      a.cpt = 2;
-      a.ncb = (a.N + 63) / 64;
-      a.ntiles = ((a.row_end - a.row_begin + kStagedWarps - 1) / kStagedWarps) * a.ncb;
-    }
-    const size_t smem = static_cast<size_t>(S.lk_cap) * 4 + static_cast<size_t>(S.j_cap) * rec_bytes;
-    auto k = table_staged_kernel<MO, KIND, DEG>;
-    GK_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-    size_t grid = static_cast<size_t>(ctx->sm_count);
-    if (grid > a.ntiles) grid = a.ntiles;
-    if (grid < 1) grid = 1;
-    k<<<static_cast<unsigned>(grid), 32 * kStagedWarps, smem, ctx->stream>>>(a, S);
-    count_launches(1);
-    GK_CUDA(cudaGetLastError());
-  }
-}
-
-template <int MO>
-void dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, bool lossy) {
-  if (mode == GK_MODE_DIRECT) {
-    if (kind == GK_KIND_GREEN) {
-      if (lossy) launch_one<MO, GK_MODE_DIRECT, GK_KIND_GREEN, 0, true>(ctx, a);
-      else launch_one<MO, GK_MODE_DIRECT, GK_KIND_GREEN, 0, false>(ctx, a);
-    } else if (kind == GK_KIND_EXP) {
-      if (lossy) launch_one<MO, GK_MODE_DIRECT, GK_KIND_EXP, 0, true>(ctx, a);
-      else launch_one<MO, GK_MODE_DIRECT, GK_KIND_EXP, 0, false>(ctx, a);
-    } else {
-      if (lossy) launch_one<MO, GK_MODE_DIRECT, kKindPair, 0, true>(ctx, a);
-      else launch_one<MO, GK_MODE_DIRECT, kKindPair, 0, false>(ctx, a);
-    }
-  } else {
-    if (kind == GK_KIND_EXP) launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, false>(ctx, a);
-    else if (kind == GK_KIND_GREEN && degree == 3)
-      launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, false>(ctx, a);
-    else if (kind == GK_KIND_GREEN) launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, false>(ctx, a);
-    else if (degree == 3) launch_one<MO, GK_MODE_TABLE, kKindPair, 3, false>(ctx, a);
-    else launch_one<MO, GK_MODE_TABLE, kKindPair, 0, false>(ctx, a);
-  }
-}
 
 void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                  int kind, double k_re, double k_im, size_t row_begin, size_t row_end,

@@ -1,0 +1,7 @@
+// fill_mo7.cu -- the fill kernels for 7 outer point(s) per triangle
+// (one translation unit per outer-point count: parallel compilation).
+#include "fill_kernels.cuh"
+
+namespace gk {
+template void dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, bool);
+}  // namespace gk
