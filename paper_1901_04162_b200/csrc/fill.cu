@@ -8,6 +8,8 @@
 
 namespace gk {
 
+__global__ void lossy_phase_kernel(double2* tab, double* ahi, int nhi, double c);
+
 void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                  int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
                  gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* counters) {
@@ -33,7 +35,34 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.counters = counters;
   if (row_end <= row_begin || mesh->N == 0) return;
   DevBuf<double> atten;
-  if (mode == GK_MODE_DIRECT && k_im != 0.0) {
+  DevBuf<double2> lossy_tab;
+  int att = 0;
+  static const bool phase_att = [] {
+    const char* e = std::getenv("GK_LOSSY_PHASE");
+    return !(e && e[0] == '0');
+  }();
+  if (mode == GK_MODE_DIRECT && k_im != 0.0 && k_im < 0.0 && k_re > 0.0 && phase_att &&
+      kPi * -k_im / (k_re * kPhaseM) <= 1e-3) {
+    // attenuation coupled to the phase reduction (cis_phase_att): per-fill
+    // scaled phase table + exp(c M hi) for the hi = n >> 13 that occur
+    att = 1;
+    const double c = k_im / a.K1;
+    a.nhi = static_cast<int>(a.K1 * mesh->diameter / kPhaseM) + 2;
+    const size_t nhi2 = (static_cast<size_t>(a.nhi) + 1) / 2;  // double2 slots
+    lossy_tab.alloc(kPhaseM + nhi2, ctx->stream);
+    const int nthreads = kPhaseM > a.nhi ? kPhaseM : a.nhi;
+    lossy_phase_kernel<<<(nthreads + 255) / 256, 256, 0, ctx->stream>>>(
+        lossy_tab.p, reinterpret_cast<double*>(lossy_tab.p + kPhaseM), a.nhi, c);
+    count_launches(1);
+    GK_CUDA(cudaGetLastError());
+    a.phase = lossy_tab.p;
+    a.ahi = reinterpret_cast<const double*>(lossy_tab.p + kPhaseM);
+    a.q1 = c;
+    a.q2 = c * c / 2.0;
+    a.q3 = c * c * c / 6.0;
+    a.q4 = c * c * c * c / 24.0;
+  } else if (mode == GK_MODE_DIRECT && k_im != 0.0) {
+    att = 2;
     if (!(k_im < 0.0)) fail(GK_ERR_INVALID_ARGUMENT, "lossy medium needs Im k < 0 (attenuation)");
     // radii are bounded by the mesh's bounding-box diagonal
     const double xmax = -k_im * mesh->diameter * kAttenScale;
@@ -48,15 +77,27 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
     a.atten = atten.p;
   }
   const int degree = table ? table->dev.degree : 3;
-  const bool lossy = k_im != 0.0;
   switch (mesh->m) {
-    case 1: dispatch_mo<1>(ctx, a, mode, kind, degree, lossy); break;
-    case 3: dispatch_mo<3>(ctx, a, mode, kind, degree, lossy); break;
-    case 4: dispatch_mo<4>(ctx, a, mode, kind, degree, lossy); break;
-    case 6: dispatch_mo<6>(ctx, a, mode, kind, degree, lossy); break;
-    case 7: dispatch_mo<7>(ctx, a, mode, kind, degree, lossy); break;
+    case 1: dispatch_mo<1>(ctx, a, mode, kind, degree, att); break;
+    case 3: dispatch_mo<3>(ctx, a, mode, kind, degree, att); break;
+    case 4: dispatch_mo<4>(ctx, a, mode, kind, degree, att); break;
+    case 6: dispatch_mo<6>(ctx, a, mode, kind, degree, att); break;
+    case 7: dispatch_mo<7>(ctx, a, mode, kind, degree, att); break;
     default: fail(GK_ERR_INVALID_ARGUMENT, "QuadratureSpec: outer_points must be one of 1, 3, 4, 6, 7");
   }
+}
+
+// lossy_phase_kernel: tab[lo] = (cos, sin)(2 pi lo / M) exp(c lo) and
+// ahi[h] = exp(c M h), c = k_im / K1 (cis_phase_att)
+__global__ void lossy_phase_kernel(double2* tab, double* ahi, int nhi, double c) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < kPhaseM) {
+    double s, co;
+    sincospi(2.0 * i / kPhaseM, &s, &co);
+    const double e = exp(c * i);
+    tab[i] = make_double2(co * e, s * e);
+  }
+  if (i < nhi) ahi[i] = exp(c * (static_cast<double>(kPhaseM) * i));
 }
 
 __global__ void atten_kernel(double* E, int n) {

@@ -111,7 +111,13 @@ struct FillArgs {
   const double4* bounds;  // per-triangle (centroid, rho_outer), for tile radius bounds
   const double* binner;   // per-triangle rho_inner
   double window_est;      // estimated radius spread of a 16 x 64 tile (staging heuristic)
-  const double* atten;  // lossy: exp(-n / 512), n < natten
+  // lossy media: ATT 1 = attenuation coupled to the phase reduction
+  // (cis_phase_att: phase = the per-fill scaled table, ahi[nhi], q = c^j/j!),
+  // ATT 2 = the legacy table exp(-n / 512), n < natten (|k_im| > 2.6 k_re)
+  const double* ahi;
+  int nhi;
+  double q1, q2, q3, q4;
+  const double* atten;
   int natten;
   double KA;            // -k_im * 512
   unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max, [2] non-finite entries
@@ -191,15 +197,18 @@ __device__ __forceinline__ void stage_bulk(void* dst, const void* src, uint32_t 
 // The warp's outer points sit in shared memory (broadcast loads, one
 // wavefront each) instead of registers, so ~80 registers per thread allow 3
 // CTAs (24 warps) per SM to hide the FP64 dependency latency.
-template <int MO, int KIND, bool LOSSY, int MINB>
+template <int MO, int KIND, int ATT, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A) {
   extern __shared__ double2 tab[];  // kPhaseM phase entries (128 KB) [+ attenuation table]
   __shared__ double so[kRowsPerTile][MO][4];
   __shared__ uint64_t bar;
   stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
   double* att = reinterpret_cast<double*>(tab + kPhaseM);
-  if constexpr (LOSSY)
+  if constexpr (ATT == 1)
+    for (int i = threadIdx.x; i < A.nhi; i += blockDim.x) att[i] = A.ahi[i];
+  if constexpr (ATT == 2)
     for (int i = threadIdx.x; i < A.natten; i += blockDim.x) att[i] = A.atten[i];
+  const PhaseAtt pa{att, A.nhi, A.q1, A.q2, A.q3, A.q4};
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t N = A.N;
@@ -247,9 +256,16 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
         const double d2 = dist2(oxy.x, oxy.y, oz, pxy.x, pxy.y, pzw.x);
         const double y = rsqrt_fast(d2);
         const double r = __dmul_rn(d2, y);
-        const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
         double w = pzw.y;
-        if constexpr (LOSSY) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
+        double2 cs;  // (cos kr, sin kr)
+        if constexpr (ATT == 1) {
+          double a;
+          cs = cis_phase_att(r, A.K1, tab, pa, a);
+          w = __dmul_rn(w, a);
+        } else {
+          cs = cis_phase(r, A.K1, tab);
+          if constexpr (ATT == 2) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
+        }
         acc.template add<KIND>(o, w, y, cs);
       }
       if (block_done) {  // column block complete: finish the entry
@@ -275,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
 template <int KIND>
 __host__ __device__ constexpr int warps_v4() { return KIND == kKindPair ? 8 : GK_WARPS_V4; }
 
-template <int MO, int IPT, int KIND, bool LOSSY>
+template <int MO, int IPT, int KIND, int ATT>
 __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(const FillArgs A) {
   constexpr int kWarpsV4 = warps_v4<KIND>();
   extern __shared__ double2 tab[];  // kPhaseM phase entries (128 KB) [+ attenuation table]
@@ -283,8 +299,11 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
   __shared__ uint64_t bar;
   stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
   double* att = reinterpret_cast<double*>(tab + kPhaseM);
-  if constexpr (LOSSY)
+  if constexpr (ATT == 1)
+    for (int i = threadIdx.x; i < A.nhi; i += blockDim.x) att[i] = A.ahi[i];
+  if constexpr (ATT == 2)
     for (int i = threadIdx.x; i < A.natten; i += blockDim.x) att[i] = A.atten[i];
+  const PhaseAtt pa{att, A.nhi, A.q1, A.q2, A.q3, A.q4};
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t N = A.N;
@@ -330,9 +349,16 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
           const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
           const double y = rsqrt_fast(d2);
           const double r = __dmul_rn(d2, y);
-          const double2 cs = cis_phase(r, A.K1, tab);  // (cos kr, sin kr)
           double w = pzw.y;
-          if constexpr (LOSSY) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
+          double2 cs;  // (cos kr, sin kr)
+          if constexpr (ATT == 1) {
+            double a;
+            cs = cis_phase_att(r, A.K1, tab, pa, a);
+            w = __dmul_rn(w, a);
+          } else {
+            cs = cis_phase(r, A.K1, tab);
+            if constexpr (ATT == 2) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
+          }
           acc.template add<KIND>(o, w, y, cs);
         }
       }
@@ -673,32 +699,34 @@ inline void set_tiling(const gk_ctx* ctx, FillArgs& a, int rows_per_tile, int ct
   a.ntiles = row_blocks * a.ncb;
 }
 
-template <int MO, int IPT, int KIND, bool LOSSY>
+template <int MO, int IPT, int KIND, int ATT>
 void launch_v4(gk_ctx* ctx, FillArgs a, size_t smem) {
   set_tiling(ctx, a, warps_v4<KIND>(), 1);
-  launch_kernel(ctx, direct_kernel_v4<MO, IPT, KIND, LOSSY>, a, smem, 32 * warps_v4<KIND>());
+  launch_kernel(ctx, direct_kernel_v4<MO, IPT, KIND, ATT>, a, smem, 32 * warps_v4<KIND>());
 }
 
-template <int MO, int MODE, int KIND, int DEG, bool LOSSY>
+template <int MO, int MODE, int KIND, int DEG, int ATT>
 void launch_one(gk_ctx* ctx, FillArgs a) {
   if constexpr (MODE == GK_MODE_DIRECT) {
-    const size_t smem = kPhaseM * sizeof(double2) + (LOSSY ? a.natten * sizeof(double) : 0);
+    const size_t smem = kPhaseM * sizeof(double2) +
+                        (ATT == 1 ? a.nhi * sizeof(double) : 0) +
+                        (ATT == 2 ? a.natten * sizeof(double) : 0);
     static const bool use_v4 = [] {
       const char* e = std::getenv("GK_DIRECT_V4");
       return !(e && e[0] == '0');
     }();
     if (use_v4) {
       switch (a.ipt) {  // n = 1..5 Gauss points per edge: fully unrolled fast path
-        case 3: return launch_v4<MO, 3, KIND, LOSSY>(ctx, a, smem);
-        case 6: return launch_v4<MO, 6, KIND, LOSSY>(ctx, a, smem);
-        case 9: return launch_v4<MO, 9, KIND, LOSSY>(ctx, a, smem);
-        case 12: return launch_v4<MO, 12, KIND, LOSSY>(ctx, a, smem);
-        case 15: return launch_v4<MO, 15, KIND, LOSSY>(ctx, a, smem);
+        case 3: return launch_v4<MO, 3, KIND, ATT>(ctx, a, smem);
+        case 6: return launch_v4<MO, 6, KIND, ATT>(ctx, a, smem);
+        case 9: return launch_v4<MO, 9, KIND, ATT>(ctx, a, smem);
+        case 12: return launch_v4<MO, 12, KIND, ATT>(ctx, a, smem);
+        case 15: return launch_v4<MO, 15, KIND, ATT>(ctx, a, smem);
         default: break;
       }
     }
     set_tiling(ctx, a, kRowsPerTile, 2);
-    launch_kernel(ctx, direct_kernel<MO, KIND, LOSSY, 2>, a, smem);
+    launch_kernel(ctx, direct_kernel<MO, KIND, ATT, 2>, a, smem);
   } else {
     // GK_TABLE_SMEM: 0 = L1 kernel, 2 = always stage (tests), unset/1 = auto.
     // GK_TABLE_SMEM_BUDGET (bytes) shrinks the window budget (tests).  Read per
@@ -758,34 +786,34 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
   }
 }
 
+template <int MO, int KIND>
+void dispatch_att(gk_ctx* ctx, const FillArgs& a, int att) {
+  if (att == 1) launch_one<MO, GK_MODE_DIRECT, KIND, 0, 1>(ctx, a);
+  else if (att == 2) launch_one<MO, GK_MODE_DIRECT, KIND, 0, 2>(ctx, a);
+  else launch_one<MO, GK_MODE_DIRECT, KIND, 0, 0>(ctx, a);
+}
+
 template <int MO>
-void dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, bool lossy) {
+void dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, int att) {
   if (mode == GK_MODE_DIRECT) {
-    if (kind == GK_KIND_GREEN) {
-      if (lossy) launch_one<MO, GK_MODE_DIRECT, GK_KIND_GREEN, 0, true>(ctx, a);
-      else launch_one<MO, GK_MODE_DIRECT, GK_KIND_GREEN, 0, false>(ctx, a);
-    } else if (kind == GK_KIND_EXP) {
-      if (lossy) launch_one<MO, GK_MODE_DIRECT, GK_KIND_EXP, 0, true>(ctx, a);
-      else launch_one<MO, GK_MODE_DIRECT, GK_KIND_EXP, 0, false>(ctx, a);
-    } else {
-      if (lossy) launch_one<MO, GK_MODE_DIRECT, kKindPair, 0, true>(ctx, a);
-      else launch_one<MO, GK_MODE_DIRECT, kKindPair, 0, false>(ctx, a);
-    }
+    if (kind == GK_KIND_GREEN) dispatch_att<MO, GK_KIND_GREEN>(ctx, a, att);
+    else if (kind == GK_KIND_EXP) dispatch_att<MO, GK_KIND_EXP>(ctx, a, att);
+    else dispatch_att<MO, kKindPair>(ctx, a, att);
   } else {
-    if (kind == GK_KIND_EXP) launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, false>(ctx, a);
+    if (kind == GK_KIND_EXP) launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, 0>(ctx, a);
     else if (kind == GK_KIND_GREEN && degree == 3)
-      launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, false>(ctx, a);
-    else if (kind == GK_KIND_GREEN) launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, false>(ctx, a);
-    else if (degree == 3) launch_one<MO, GK_MODE_TABLE, kKindPair, 3, false>(ctx, a);
-    else launch_one<MO, GK_MODE_TABLE, kKindPair, 0, false>(ctx, a);
+      launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, 0>(ctx, a);
+    else if (kind == GK_KIND_GREEN) launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, 0>(ctx, a);
+    else if (degree == 3) launch_one<MO, GK_MODE_TABLE, kKindPair, 3, 0>(ctx, a);
+    else launch_one<MO, GK_MODE_TABLE, kKindPair, 0, 0>(ctx, a);
   }
 }
 
 // one explicit instantiation per translation unit (fill_mo<m>.cu)
-extern template void dispatch_mo<1>(gk_ctx*, const FillArgs&, gk_mode, int, int, bool);
-extern template void dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, bool);
-extern template void dispatch_mo<4>(gk_ctx*, const FillArgs&, gk_mode, int, int, bool);
-extern template void dispatch_mo<6>(gk_ctx*, const FillArgs&, gk_mode, int, int, bool);
-extern template void dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, bool);
+extern template void dispatch_mo<1>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template void dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template void dispatch_mo<4>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template void dispatch_mo<6>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template void dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
 
 }  // namespace gk

@@ -32,6 +32,7 @@ constexpr double kMagicRint = 6755399441055744.0; // 1.5 * 2^52
 // with c the minimax constant on [0, D^2] (kCosMinimax): max error
 // 0.00715 D^4 = 1.5e-16 (0.7 ulp of 1) for one DMUL instead of FMA + DMUL.
 constexpr int kPhaseM = 8192;
+constexpr int kPhaseLog2 = 13;
 // c = -1/2 + b D^2, b = (sqrt 2 - 1)/12: the error x(-1/2 - c) + x^2/24,
 // x = delta^2, equioscillates at x = D^2 and x = -12(-1/2 - c)
 constexpr double kPhaseD = kPi / kPhaseM;
@@ -248,6 +249,44 @@ __device__ __forceinline__ double2 cis_phase(double r, double K1, const double2*
   const double2 T = tab[idx];
   const double c = __fma_rn(-T.y, s, __fma_rn(T.x, v, T.x));
   const double sn = __fma_rn(T.x, s, __fma_rn(T.y, v, T.y));
+  return make_double2(c, sn);
+}
+
+// Lossy media (complex k, k_im < 0), attenuation coupled to the phase
+// reduction: with n + f = r K1 as in cis_phase, exp(k_im r) =
+// exp(c lo) exp(c M hi) exp(c f), c = k_im / K1, n = hi M + lo.  The first
+// factor is folded into the (per-fill) scaled phase table
+// tab[lo] = (cos, sin)(2 pi lo / M) exp(c lo), the second is ahi[hi] (a few
+// entries), the third a degree-4 polynomial in f (|c f| <= 1e-3 by
+// construction: dropped term < 1e-17).  Returns the rotation like cis_phase
+// and the attenuation factor in *att: 6 FP64 ops more than lossless
+// (4 polynomial + 1 product, + 1 for the weight at the call site).
+struct PhaseAtt {
+  const double* ahi;
+  int nhi;
+  double q1, q2, q3, q4;  // c, c^2/2, c^3/6, c^4/24
+};
+__device__ __forceinline__ double2 cis_phase_att(double r, double K1, const double2* tab,
+                                                 const PhaseAtt& pa, double& att) {
+  constexpr double C = 2.0 * kPi / kPhaseM;
+  constexpr double a1 = kCosMinimax * C * C;
+  constexpr double s1 = C;
+  constexpr double s3 = -C * C * C / 6.0;
+  const double t = __fma_rn(r, K1, kMagicRint);
+  const double nf = t - kMagicRint;
+  const double f = __fma_rn(r, K1, -nf);
+  const unsigned n = static_cast<unsigned>(__double2loint(t));
+  const unsigned idx = n & (kPhaseM - 1);
+  unsigned hi = n >> kPhaseLog2;
+  hi = hi < static_cast<unsigned>(pa.nhi) ? hi : static_cast<unsigned>(pa.nhi - 1);
+  const double g = __dmul_rn(f, f);
+  const double v = __dmul_rn(a1, g);
+  const double s = __dmul_rn(f, __fma_rn(s3, g, s1));
+  const double2 T = tab[idx];
+  const double c = __fma_rn(-T.y, s, __fma_rn(T.x, v, T.x));
+  const double sn = __fma_rn(T.x, s, __fma_rn(T.y, v, T.y));
+  const double p = __fma_rn(__fma_rn(__fma_rn(__fma_rn(pa.q4, f, pa.q3), f, pa.q2), f, pa.q1), f, 1.0);
+  att = __dmul_rn(pa.ahi[hi], p);
   return make_double2(c, sn);
 }
 

@@ -153,6 +153,27 @@ def test_lossy_plate_parity(gk, oracle):
     assert np.all(np.abs(zt.cpu().numpy() - ref) <= B_t)
 
 
+@pytest.mark.parametrize("kval", ["c4", "eps1-20j", "1-6j"])
+@pytest.mark.parametrize("m,n", [(6, 4), (3, 7)])
+def test_lossy_attenuation_paths(gk, oracle, kval, m, n):
+    """Both lossy direct paths vs the complex-k oracle: attenuation coupled to
+    the phase reduction (|Im k| <= 2.6 Re k: C4's medium and eps_r = 1 - 20j)
+    and the attenuation table (an explicit k = 1 - 6j; no physical medium with
+    eps_r > 0 gets there); the fused kernel (n <= 5) and the generic one (n = 7)."""
+    mesh = gk.generate_plate_mesh(1.0, 6)
+    k = {"c4": lambda: complex(gk.wavenumber(gk.Medium(1.0, 4.0, 1.0, -0.4))),
+         "eps1-20j": lambda: complex(gk.wavenumber(gk.Medium(1.0, 1.0, 1.0, -20.0))),
+         "1-6j": lambda: complex(1.0, -6.0)}[kval]()
+    assert k.imag < 0
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+    zd, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k)
+    ref, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, DIRECT, k.real, k_im=k.imag,
+                              threads=8)
+    B = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, None, abs(k), ULPS)
+    err = np.abs(zd.cpu().numpy() - ref)
+    assert np.all(err <= B), float(np.max(err / np.maximum(B, 1e-300)))
+
+
 def test_fill_matrix_host_end_to_end(gk, oracle):
     mesh = sphere(gk, 1)
     k = 2 * np.pi
