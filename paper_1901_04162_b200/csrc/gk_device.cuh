@@ -20,6 +20,24 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// GK_DASSERT: device-side index/contract checks, compiled in only for the
+// assert build (scripts/build_variant.sh asserts -DGK_DEVICE_ASSERTS), which
+// stands in for compute-sanitizer (closed on the GPU pool): a failure traps
+// the kernel and the ABI call returns GK_ERR_RUNTIME.
+#ifdef GK_DEVICE_ASSERTS
+#include <cstdio>
+#define GK_DASSERT(c)                                                                 \
+  do {                                                                                \
+    if (!(c)) {                                                                       \
+      printf("GK_DASSERT failed: %s (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__, \
+             blockIdx.x, threadIdx.x);                                                \
+      __trap();                                                                       \
+    }                                                                                 \
+  } while (0)
+#else
+#define GK_DASSERT(c) ((void)0)
+#endif
+
 namespace gk {
 
 constexpr double kPi = 3.14159265358979323846;
@@ -90,9 +108,12 @@ __device__ __forceinline__ uint32_t lookup_bucket(double r, const TableDev& t) {
 __device__ __forceinline__ uint32_t locate_interval(double r, const TableDev& t,
                                                     const double* grec, int grs, double& aj) {
   const uint32_t base = __ldg(t.lk + lookup_bucket(r, t));
+  GK_DASSERT(base < t.nrec);
   const double2 ab = __ldg(reinterpret_cast<const double2*>(grec + static_cast<size_t>(base) * grs));
   const bool hi = r >= ab.y;
   aj = hi ? ab.y : ab.x;
+  // the located interval brackets r (table.hpp:87-102 contract) for r in range
+  GK_DASSERT(!(r >= t.r_min && r <= t.r_max) || (aj <= r && base + (hi ? 1u : 0u) < t.nrec));
   return base + (hi ? 1u : 0u);
 }
 
@@ -189,8 +210,10 @@ template <bool SMEM>
 __device__ __forceinline__ uint32_t win_locate(double r, const TableDev& t, const TableWin& w,
                                                int grs, double& aj) {
   uint32_t b = lookup_bucket(r, t) - w.b0;
+  GK_DASSERT(!SMEM || b < w.nb || !(r >= t.r_min && r <= t.r_max));  // window covers the tile
   b = b < w.nb ? b : w.nb - 1;
   uint32_t base = win_ld<SMEM>(w.lk + b) - w.j0;
+  GK_DASSERT(!SMEM || base < w.nj || !(r >= t.r_min && r <= t.r_max));
   base = base < w.nj ? base : w.nj - 1;
   const double2 ab = win_ld<SMEM>(reinterpret_cast<const double2*>(w.grec + static_cast<size_t>(base) * grs));
   const bool hi = r >= ab.y;
