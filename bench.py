@@ -534,7 +534,7 @@ def hbm_peak_gbs():
         return 7700.0, "B200_PROFILING.md fallback"
 
 
-def run_c1(gk, ctx, iters=1000, sets=8):
+def run_c1(gk, ctx, iters=1024, sets=8):
     """C1 (BASELINE configs[0]): standalone eval_batch of 2^20 seeded radii in
     [1e-3, 2] m, k = 4 pi, through gk_eval_batch_async, `iters` back-to-back
     launches rotating over `sets` radius/output buffers (192 MB > L2, so every
@@ -552,27 +552,48 @@ def run_c1(gk, ctx, iters=1000, sets=8):
     peak, peak_src = hbm_peak_gbs()
     res = {"n": n, "iters": iters, "bytes_per_eval": 24, "peak_gbs": peak, "peak": peak_src}
     variants = [("direct", None)] + [(f"table_S{S}", S) for S in (1000, 10000)]
+    res["graph"] = "the same launches captured once in a CUDA graph and replayed"
     for name, S in variants:
         t = None
         if S:
             t = gk.DeviceTable(gk.SamplingConfig(r_min=1e-3, r_max=2.0, samples_per_wavelength=S),
                                med, ctx=ctx)
         for kind in (gk.KernelKind.PlainExp, gk.KernelKind.GreenOverR):
+            def run():
+                for i in range(iters):
+                    gk.eval_batch_async(kind, rs[i % sets], outs[i % sets], st, table=t, k=k)
             for i in range(2 * sets):  # warm-up
                 gk.eval_batch_async(kind, rs[i % sets], outs[i % sets], st, table=t, k=k)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for i in range(iters):
-                gk.eval_batch_async(kind, rs[i % sets], outs[i % sets], st, table=t, k=k)
+            run()
             e1.record()
             torch.cuda.synchronize()
-            st.read()
             us = e0.elapsed_time(e1) * 1e3 / iters
-            gbs = n * 24 / (us * 1e-6) / 1e9
+            # CUDA graph of the same launches (no per-launch host overhead)
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    ctx.bind_stream()
+                    run()
+            ctx.bind_stream()
+            g.replay()
+            torch.cuda.synchronize()
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ug = e0.elapsed_time(e1) * 1e3 / iters
+            st.read()
+            del g
+            gbs, gbs_g = n * 24 / (us * 1e-6) / 1e9, n * 24 / (ug * 1e-6) / 1e9
             res[f"{name}:{'exp' if kind == gk.KernelKind.PlainExp else 'green'}"] = {
                 "us_per_batch": us, "evals_per_s": n / (us * 1e-6), "gbs": gbs,
-                "hbm_frac": gbs / peak}
+                "hbm_frac": gbs / peak, "graph_us_per_batch": ug,
+                "graph_evals_per_s": n / (ug * 1e-6), "graph_hbm_frac": gbs_g / peak}
         st.reset()
     return res
 
