@@ -29,6 +29,12 @@ constexpr int kRowsPerTile = 8;  // one row per warp
 constexpr int kMaxColBlocks = 32;  // 32-column blocks per tile (adaptive, see launch_fill)
 constexpr int kThreads = 32 * kRowsPerTile;
 constexpr int kKindPair = 2;  // fused Exp + Green fill sharing r
+#ifndef GK_TABLE_WARPS
+#define GK_TABLE_WARPS 8  // table_kernel (L1 path): rows per CTA
+#endif
+#ifndef GK_TABLE_CTAS
+#define GK_TABLE_CTAS 2   // table_kernel: resident CTAs per SM
+#endif
 
 // per-entry accumulators: one complex per outer point, two for the fused pair
 template <int MO, bool PAIR>
@@ -373,14 +379,14 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
 
 // K3: table evaluation (the paper's method) with the reference's fallback.
 template <int MO, int KIND, int DEG>
-__global__ void __launch_bounds__(kThreads, 2) table_kernel(const FillArgs A) {
+__global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kernel(const FillArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t N = A.N;
   unsigned long long n_low = 0, n_high = 0;
 
   for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
     const size_t tr = tile / A.ncb, tc = tile - tr * A.ncb;
-    const size_t p = A.row_begin + tr * kRowsPerTile + warp;
+    const size_t p = A.row_begin + tr * GK_TABLE_WARPS + warp;
     if (p >= A.row_end) continue;  // warp-uniform
     double ox[MO], oy[MO], oz[MO];
 #pragma unroll
@@ -734,8 +740,8 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
     const char* env = std::getenv("GK_TABLE_SMEM");
     const int staging = env ? std::atoi(env) : 1;
     if (staging == 0) {
-      set_tiling(ctx, a, kRowsPerTile, 2);
-      launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
+      set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
+      launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
       return;
     }
     // shared-memory window sizing: whole table if it fits, else proportional caps
@@ -761,8 +767,8 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
       // fall back to global reads: use the L1 kernel with its wider tiles
       const double est = a.T.nrec * a.window_est / (a.T.r_max - a.T.r_min);
       if (staging != 2 && est > 2.0 * static_cast<double>(j_cap)) {
-        set_tiling(ctx, a, kRowsPerTile, 2);
-        launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0);
+        set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
+        launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
         return;
       }
       S.j_cap = static_cast<uint32_t>(j_cap);
