@@ -272,6 +272,21 @@ gk_status gk_bench_compare(gk_ctx* ctx, const double* vertices, size_t nv,
    matfill.hpp:270, is 1.01 x this). */
 gk_status gk_max_vertex_distance(gk_ctx* ctx, const gk_mesh* mesh, double* out);
 
+/* ------------------------------------------- peer memory (fused fill+gather)
+   The optional gather of Z fused into the fill: the destination
+   rank allocates the full matrix with gk_shared_alloc and sends the 64-byte
+   IPC handle to the other ranks (any transport), they map it with
+   gk_ipc_open, and every rank's gk_fill_rows stores its row block straight
+   into that matrix (NVLink peer stores on one node; no separate gather).
+   gk_ipc_open'ed pointers are released with gk_ipc_close, the allocation
+   with gk_shared_free after every rank has closed it. */
+#define GK_IPC_HANDLE_BYTES 64
+gk_status gk_shared_alloc(gk_ctx* ctx, size_t bytes, void** dptr,
+                          unsigned char handle[GK_IPC_HANDLE_BYTES]);
+gk_status gk_shared_free(gk_ctx* ctx, void* dptr);
+gk_status gk_ipc_open(gk_ctx* ctx, const unsigned char handle[GK_IPC_HANDLE_BYTES], void** dptr);
+gk_status gk_ipc_close(gk_ctx* ctx, void* dptr);
+
 /* predicted_calls (matfill.hpp:50-56): 3 m n N^2 with the overflow guard */
 gk_status gk_predicted_calls(uint64_t N, uint64_t m, uint64_t n, uint64_t* out);
 

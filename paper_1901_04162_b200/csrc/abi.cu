@@ -945,6 +945,58 @@ gk_status gk_bench_compare(gk_ctx* c, const double* verts, size_t nv, const uint
   return st;
 }
 
+gk_status gk_shared_alloc(gk_ctx* c, size_t bytes, void** dptr, unsigned char* handle) {
+  return guarded([&] {
+    check_ctx(c);
+    need(dptr && handle && bytes > 0, GK_ERR_INVALID_ARGUMENT, "gk_shared_alloc: bad argument");
+    use_device(c);
+    void* p = nullptr;
+    GK_CUDA(cudaMalloc(&p, bytes));  // IPC needs a plain cudaMalloc allocation
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      gk::fail(GK_ERR_RUNTIME, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+    }
+    static_assert(sizeof(h) == GK_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof(h));
+    *dptr = p;
+  });
+}
+
+gk_status gk_shared_free(gk_ctx* c, void* dptr) {
+  return guarded([&] {
+    check_ctx(c);
+    if (!dptr) return;
+    use_device(c);
+    GK_CUDA(cudaDeviceSynchronize());
+    GK_CUDA(cudaFree(dptr));
+  });
+}
+
+gk_status gk_ipc_open(gk_ctx* c, const unsigned char* handle, void** dptr) {
+  return guarded([&] {
+    check_ctx(c);
+    need(handle && dptr, GK_ERR_INVALID_ARGUMENT, "gk_ipc_open: bad argument");
+    use_device(c);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    GK_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    *dptr = p;
+  });
+}
+
+gk_status gk_ipc_close(gk_ctx* c, void* dptr) {
+  return guarded([&] {
+    check_ctx(c);
+    if (!dptr) return;
+    use_device(c);
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    GK_CUDA(cudaIpcCloseMemHandle(dptr));
+  });
+}
+
 gk_status gk_predicted_calls(uint64_t N, uint64_t m, uint64_t n, uint64_t* out) {
   return guarded([&] {
     need(out != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");

@@ -9,9 +9,10 @@ the thread count.  Here the same chunking runs one rank per GPU:
 2. ONE 16-byte all-reduce (MIN of {r_min, -r_max}) makes it global,
 3. every rank builds the identical table from the global range (the device
    build is deterministic) and fills its rows -- no data-path collective,
-4. optionally the row blocks are gathered to one rank (point-to-point sends
-   into the destination's row slices; NVLink under NCCL), reported apart
-   from the fill.
+4. optionally the row blocks are gathered to one rank: point-to-point sends
+   into the destination's row slices after the fill (gather_rows), or fused
+   with it -- every rank's fill kernel storing straight into the destination
+   rank's matrix through CUDA IPC peer memory (fill_rows_gathered).
 
 Works with any torch.distributed backend: NCCL on GPUs (tensors on the
 rank's device), gloo on CPU (the tests).
@@ -73,6 +74,75 @@ def gather_rows(z_local, N: int, dst: int = 0, out=None, group=None):
     return out
 
 
+class _DeviceMatrix:
+    """__cuda_array_interface__ view of raw device memory (torch.as_tensor
+    keeps this object alive while the tensor lives; `release` runs after)."""
+
+    def __init__(self, ptr: int, shape, release=None):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<c16",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+        self._release = release
+
+    def __del__(self):
+        if self._release is not None:
+            try:
+                self._release()
+            except Exception:  # interpreter shutdown
+                pass
+
+
+def fill_rows_gathered(dmesh, mode, kind=None, table=None, k: complex = 0.0, dst: int = 0,
+                       group=None):
+    """Fill and gather fused (SURVEY 8e step 5 without a separate collective):
+    rank `dst` allocates the full N x N matrix as shareable device memory
+    (gk_shared_alloc), its 64-byte IPC handle is broadcast over the process
+    group, every other rank maps it (gk_ipc_open), and each rank's fill kernel
+    stores its row block rows_of(rank, world, N) straight into it -- NVLink
+    peer stores between the GPUs of one node, overlapped with the compute by
+    construction.  Returns (Z, report) on `dst` (Z a complex128 CUDA tensor
+    owning the allocation) and (None, report) elsewhere."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from . import gktab
+    from ._lib import check, lib
+
+    kind = gktab.KernelKind.GreenOverR if kind is None else kind
+    ctx = dmesh.ctx
+    N = dmesh.N
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    rb, re = rows_of(rank, world, N)
+    handle = (C.c_ubyte * 64)()
+    ptr = C.c_void_p()
+    if rank == dst:
+        check(lib().gk_shared_alloc(ctx.h, N * N * 16, C.byref(ptr), handle), "gk_shared_alloc")
+    on_dev = dist.get_backend(group) == "nccl"
+    ht = torch.tensor(list(bytes(handle)), dtype=torch.uint8,
+                      device=f"cuda:{ctx.device}" if on_dev else "cpu")
+    dist.broadcast(ht, src=dst, group=group)
+    if rank != dst:
+        handle = (C.c_ubyte * 64).from_buffer_copy(bytes(ht.cpu().tolist()))
+        check(lib().gk_ipc_open(ctx.h, handle, C.byref(ptr)), "gk_ipc_open")
+    h, p = ctx.h, ptr.value
+    release = (lambda: lib().gk_shared_free(h, C.c_void_p(p))) if rank == dst else None
+    full = torch.as_tensor(_DeviceMatrix(p, (N, N), release), device=f"cuda:{ctx.device}")
+    rep = None
+    try:
+        if re > rb:
+            _, rep = gktab.fill_rows(dmesh, mode, kind=kind, table=table, k=k, row_begin=rb,
+                                     row_end=re, out=full[rb:re])
+        ctx.synchronize()
+        dist.barrier(group)   # every block has landed in dst's matrix
+    finally:
+        if rank != dst:
+            del full
+            check(lib().gk_ipc_close(h, C.c_void_p(p)), "gk_ipc_close")
+    return (full if rank == dst else None), rep
+
+
 def shard_summary(world: int, N: int) -> list[tuple[int, int]]:
     """All row blocks, rank order (for reports)."""
     return [rows_of(r, world, N) for r in range(world)]
@@ -83,4 +153,5 @@ def evals_of_rows(rows: int, N: int, m: int, n: int) -> int:
     return 3 * m * n * rows * (N - 1) if N > 0 else 0
 
 
-__all__ = ["rows_of", "global_distance_range", "gather_rows", "shard_summary", "evals_of_rows"]
+__all__ = ["rows_of", "global_distance_range", "gather_rows", "fill_rows_gathered",
+           "shard_summary", "evals_of_rows"]
