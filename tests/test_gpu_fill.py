@@ -282,3 +282,36 @@ def test_table_staging_paths_bit_identical(gk, monkeypatch, level, S, r_min):
         assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
         assert torch.equal(o[2], outs[0][2]) and o[3:] == outs[0][3:]
     assert (outs[0][3] > 0) == (r_min is not None)
+
+
+def test_degenerate_sizes_and_strided_output(gk, oracle):
+    """N = 1 (only the self pair: Z = 0, no calls), N = 2, empty row ranges,
+    and an output block with ldz > N (a window of a larger matrix)."""
+    import torch
+    one = gk.TriangleMesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float), np.array([[0, 1, 2]]))
+    for mode, kw in ((gk.Mode.DIRECT, dict(k=2 * np.pi)), (gk.Mode.TABLE, None)):
+        dm = gk.DeviceMesh(one, gk.QuadratureSpec(6, 4))
+        if kw is None:   # the only pair is the self pair: the range is empty
+            kw = dict(table=gk.DeviceTable(gk.SamplingConfig(r_min=0.1, r_max=2.0)))
+        z, rep = gk.fill_rows(dm, mode, **kw)
+        assert z.shape == (1, 1) and complex(z[0, 0].item()) == 0
+        assert rep.actual_calls == 0 and rep.predicted_calls == 3 * 6 * 4
+    two = gk.TriangleMesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 0.7], [1, 0, 0.7],
+                                    [0, 1, 0.7]], float), np.array([[0, 1, 2], [3, 4, 5]]))
+    dm = gk.DeviceMesh(two, gk.QuadratureSpec(4, 3))
+    z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    ref, orep = oracle.fill_rows(two.vertices, two.triangles, 4, 3, DIRECT, 2 * np.pi)
+    B = oracle.entry_bounds(two.vertices, two.triangles, 4, 3, None, 2 * np.pi, ULPS)
+    assert np.all(np.abs(z.cpu().numpy() - ref) <= B) and rep.actual_calls == orep.actual_calls
+    # empty row range
+    mesh = sphere(gk, 1)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi, row_begin=7, row_end=7)
+    assert z.shape[0] == 0 and rep.actual_calls == 0
+    # strided output: rows 10..30 into columns [5, 5 + N) of a wider buffer
+    big = torch.full((20, dm.N + 13), complex(7, 7), dtype=torch.complex128, device="cuda:0")
+    win = big[:, 5:5 + dm.N]
+    gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi, row_begin=10, row_end=30, out=win)
+    full, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    assert torch.equal(win, full[10:30])
+    assert torch.all(big[:, :5] == complex(7, 7)) and torch.all(big[:, 5 + dm.N:] == complex(7, 7))
