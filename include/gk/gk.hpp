@@ -276,6 +276,37 @@ inline std::pair<KernelMatrix, FillReport> fill_matrix(
   return {std::move(z), FillReport::from(rep)};
 }
 
+// The reference's plugin seam itself: a type satisfying gktab's duck-typed
+// Kernel concept (matfill.hpp:59-87: accumulate(kind, radii, weights) and
+// fallback_count()), backed by a device table.  It drops into the reference's
+// own fill_matrix unchanged -- correct, but one device round trip per matrix
+// entry, so it is for validation; the fast path replaces fill_matrix itself
+// (gk::fill_matrix, one launch for the whole matrix).
+class DeviceTableKernel {
+ public:
+  explicit DeviceTableKernel(const DeviceEvaluator* ev) : ev_(ev) {}
+  // Kind: gk::KernelKind or the reference's own gktab::KernelKind (same values)
+  template <class Kind>
+  Complex accumulate(Kind kind, std::span<const double> radii,
+                     std::span<const double> weights) const {
+    if (radii.size() != weights.size())
+      throw std::invalid_argument("accumulate: radii and weights differ in length");
+    const std::vector<Complex> v =
+        ev_->eval_batch(static_cast<KernelKind>(static_cast<int>(kind)), radii);
+    Complex acc{0.0, 0.0};
+    for (std::size_t i = 0; i < v.size(); ++i) acc += weights[i] * v[i];
+    return acc;
+  }
+  template <class Kind>
+  Complex operator()(Kind kind, double r) const {
+    return ev_->eval_kernel(static_cast<KernelKind>(static_cast<int>(kind)), r);
+  }
+  std::uint64_t fallback_count() const { return ev_->fallback_count(); }
+
+ private:
+  const DeviceEvaluator* ev_;
+};
+
 // io.hpp:23-27, 134-156: the reference's report rows, %.17g numbers
 inline std::string format_g17(double v) {
   char buf[40];

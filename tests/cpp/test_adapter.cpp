@@ -113,6 +113,22 @@ int main() {
     CHECK(same.max_rel_re == 0.0 && same.max_rel_im == 0.0);
     (void)rd;
   }
+  // the Kernel-concept adapter: accumulate == sum of w * eval_batch, fallbacks counted
+  {
+    gk::DeviceEvaluator e(ctx, gk::SamplingConfig{});
+    const gk::DeviceTableKernel kern(&e);
+    const std::vector<double> r = {5e-5, 0.25, 0.5, 0.75};  // the first is below r_min
+    const std::vector<double> w = {0.5, 1.0, -2.0, 0.25};
+    const gk::Complex a = kern.accumulate(gk::KernelKind::GreenOverR, r, w);
+    const auto v = e.eval_batch(gk::KernelKind::GreenOverR, r);
+    gk::Complex want{0.0, 0.0};
+    for (int i = 0; i < 4; ++i) want += w[i] * v[i];
+    CHECK(a == want);
+    CHECK(kern.fallback_count() == 2);  // one per batch that met r < r_min
+    CHECK(throws<std::invalid_argument>(
+        [&] { kern.accumulate(gk::KernelKind::GreenOverR, r, std::span<const double>(w.data(), 3)); }));
+  }
+
   // error_sweep on the device + the reference's CSV row format
   {
     gk::DeviceEvaluator e(ctx, gk::SamplingConfig{});
