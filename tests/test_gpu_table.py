@@ -224,3 +224,40 @@ def test_eval_batch_async_matches_sync_and_reports(gk, oracle):
     st.reset()
     gk.eval_batch_async(gk.KernelKind.PlainExp, rd, out, st, k=2.0)  # direct: no fallbacks
     assert st.read() == 0
+
+
+@pytest.mark.parametrize("degree", [1, 2, 4, 5, 7])
+def test_lagrange_degrees_vs_oracle(gk, oracle, degree):
+    """Green interpolation of degree != 3 (the reference's generic
+    interp_lagrange, evaluator.hpp:40-95, with its stencil rule): device
+    records vs the oracle's evaluator of the same degree on the same plan --
+    rounding-level, eval_batch and a table-mode fill; test_evaluator.cpp:167-186
+    checks degrees 2 and 4 against the pointwise bound, done here too."""
+    c = gk.SamplingConfig(r_min=1e-3, r_max=2.0, samples_per_wavelength=1000)
+    med = gk.Medium(lambda0=0.5)
+    t = gk.DeviceTable(c, med, lagrange_degree=degree)
+    assert t.info.degree == degree
+    p = _oracle_plan(oracle, c, med)
+    ev = oracle.evaluator(p, oracle.wavenumber(0.5), degree=degree)
+    r = splitmix64_uniform(3, 1 << 16, 1e-3, 2.0)
+    got = t.eval_batch(gk.KernelKind.GreenOverR, r).cpu().numpy()
+    ref = ev.eval_batch(GREEN, r)
+    assert np.max(np.abs(got - ref) / (np.abs(ref) + 1.0 / r)) <= 1e-11
+    k = oracle.wavenumber(0.5)
+    exact = oracle.eval_analytic_batch(GREEN, k, r[::16])
+    bound = oracle.pointwise_bounds(ev, GREEN, 1, r[::16])
+    assert np.all(np.abs(got[::16] - exact) <= bound + 64 * 2.0 ** -53 * (1 + k * r[::16]) / r[::16])
+    # table-mode fill with this degree
+    mesh = gk.jitter(gk.generate_sphere_mesh(0.5, 1), 5, 1e-3)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(4, 3))
+    lo, hi = dm.distance_range()
+    tf = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=2000),
+                        gk.Medium(), lagrange_degree=degree)
+    d = tf.download()
+    evf = oracle.evaluator(oracle.make_plan(d["abscissae"], d["zeros"]), 2 * math.pi,
+                           degree=degree)
+    zt, _ = gk.fill_rows(dm, gk.Mode.TABLE, table=tf)
+    ref_t, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, 4, 3, 1, 2 * math.pi, ev=evf,
+                                threads=8)
+    B = oracle.entry_bounds(mesh.vertices, mesh.triangles, 4, 3, None, 2 * math.pi, 64.0)
+    assert np.all(np.abs(zt.cpu().numpy() - ref_t) <= B)
