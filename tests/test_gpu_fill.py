@@ -219,19 +219,20 @@ def test_fill_rows_host_matches_device(gk):
     assert rep_h.actual_calls == rep_d.actual_calls
 
 
-@pytest.mark.parametrize("mode", ["direct", "table"])
+@pytest.mark.parametrize("mode", ["direct", "table", "lossy", "lossy_table"])
 @pytest.mark.parametrize("m,n", [(6, 4), (7, 5), (3, 7)])
 def test_fused_pair_fill_equals_separate_fills(gk, mode, m, n):
-    """gk_fill_rows_pair: Exp and Green from one pass, bitwise equal to two fills."""
+    """gk_fill_rows_pair: Exp and Green from one pass, bitwise equal to two
+    fills (real k, and the C4 complex k in both modes)."""
     import torch
     mesh = sphere(gk, 2)
     dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
-    k = 2 * np.pi
-    kw = dict(k=k)
-    if mode == "table":
+    med = gk.Medium(1.0, 4.0, 1.0, -0.4) if mode.startswith("lossy") else gk.Medium()
+    kw = dict(k=gk.wavenumber(med))
+    if mode.endswith("table"):
         lo, hi = dm.distance_range()
-        kw = dict(table=gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi)))
-    md = gk.Mode.DIRECT if mode == "direct" else gk.Mode.TABLE
+        kw = dict(table=gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi), med))
+    md = gk.Mode.TABLE if mode.endswith("table") else gk.Mode.DIRECT
     ze, zg, rep = gk.fill_rows_pair(dm, md, **kw)
     e, _ = gk.fill_rows(dm, md, kind=gk.KernelKind.PlainExp, **kw)
     g, rg = gk.fill_rows(dm, md, kind=gk.KernelKind.GreenOverR, **kw)
