@@ -90,6 +90,7 @@ typedef struct gk_table_info {
 int gk_abi_version(void);
 const char* gk_last_error(void);
 gk_status gk_ctx_create(int device, gk_ctx** out);
+/* Destroy a context after the tables and meshes created on it. */
 gk_status gk_ctx_destroy(gk_ctx* ctx);
 /* Run on the caller's cudaStream_t (e.g. torch.cuda.current_stream()), used
    as-is: 0 is the legacy default stream.  gk_ctx_use_own_stream restores the

@@ -165,8 +165,10 @@ gk_status gk_ctx_destroy(gk_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    // every context-owned buffer is released on the stream before it goes away
     c->scratch.reset();
     c->phase.reset();
+    c->phase_small.reset();
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->own) cudaStreamDestroy(c->own);

@@ -2,6 +2,7 @@
 // evaluator.hpp:209-221, and eval_analytic, kernel.hpp:48-61) and the FP64
 // peak microbenchmark used as the fill's roofline denominator.
 #include <cstdint>
+#include <cstdlib>
 
 #include "gk_internal.h"
 
@@ -11,10 +12,13 @@ namespace gk {
 // (eval_kernel -> eval_exp/eval_green or eval_analytic, evaluator.hpp:199-205)
 enum : unsigned { V_OK = 0, V_INVALID = 1, V_DOMAIN = 2, V_RANGE = 3 };
 
-template <int KIND, bool TABLE, int DEG>
+// FAST (table == NULL, real k): cis_phase_small + a correctly rounded
+// reciprocal instead of libdevice sincos and a division
+template <int KIND, bool TABLE, int DEG, bool FAST = false>
 __global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
                                   double2* __restrict__ out, TableDev T, double k_re,
-                                  double k_im, unsigned long long* w) {
+                                  double k_im, unsigned long long* w,
+                                  const double2* __restrict__ ptab = nullptr, double K1s = 0.0) {
   unsigned long long fb = 0;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -37,7 +41,16 @@ __global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
         bad = V_INVALID;
       }
       if (bad == V_OK) {
-        v = analytic_sincos(KIND, k_re, k_im, r);
+        if constexpr (FAST) {
+          const double2 cs = cis_phase_small(r, K1s, ptab);  // (cos kr, sin kr)
+          v = make_double2(cs.x, -cs.y);
+          if (KIND == GK_KIND_GREEN) {
+            const double y = __drcp_rn(r);
+            v = make_double2(__dmul_rn(v.x, y), __dmul_rn(v.y, y));
+          }
+        } else {
+          v = analytic_sincos(KIND, k_re, k_im, r);
+        }
         if (TABLE) ++fb;
       }
     }
@@ -50,6 +63,12 @@ __global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
   }
 }
 
+// GK_EVAL_LIBDEVICE=1: eval_batch through libdevice sincos (A/B, tests)
+static bool fast_eval() {
+  const char* e = std::getenv("GK_EVAL_LIBDEVICE");
+  return !(e && e[0] == '1');
+}
+
 template <int KIND>
 void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, double2* out,
                       double k_re, double k_im, unsigned long long* w) {
@@ -60,7 +79,10 @@ void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n,
   const unsigned g = static_cast<unsigned>(grid);
   TableDev T{};
   if (t) T = t->dev;
-  if (!t)
+  if (!t && k_im == 0.0 && fast_eval())
+    eval_batch_kernel<KIND, false, 0, true><<<g, 256, 0, ctx->stream>>>(
+        r, n, out, T, k_re, k_im, w, ctx->phase_small.p, k_re * kPhaseSmall / (2.0 * kPi));
+  else if (!t)
     eval_batch_kernel<KIND, false, 0><<<g, 256, 0, ctx->stream>>>(r, n, out, T, k_re, k_im, w);
   else if (KIND == GK_KIND_GREEN && T.degree == 3)
     eval_batch_kernel<KIND, true, 3><<<g, 256, 0, ctx->stream>>>(r, n, out, T, k_re, k_im, w);

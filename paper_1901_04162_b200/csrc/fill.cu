@@ -212,18 +212,21 @@ void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row
 
 // ------------------------------------------------------- phase table
 
-__global__ void phase_kernel(double2* tab) {
+__global__ void phase_kernel(double2* tab, int M) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= kPhaseM) return;
+  if (i >= M) return;
   double s, c;
-  sincospi(2.0 * i / kPhaseM, &s, &c);
+  sincospi(2.0 * i / M, &s, &c);
   tab[i] = make_double2(c, s);
 }
 
 void init_phase_table(gk_ctx* ctx) {
   ctx->phase.alloc(kPhaseM, ctx->stream);
-  phase_kernel<<<(kPhaseM + 255) / 256, 256, 0, ctx->stream>>>(ctx->phase.p);
-  count_launches(1);
+  phase_kernel<<<(kPhaseM + 255) / 256, 256, 0, ctx->stream>>>(ctx->phase.p, kPhaseM);
+  ctx->phase_small.alloc(kPhaseSmall, ctx->stream);
+  phase_kernel<<<(kPhaseSmall + 255) / 256, 256, 0, ctx->stream>>>(ctx->phase_small.p,
+                                                                  kPhaseSmall);
+  count_launches(2);
   GK_CUDA(cudaGetLastError());
 }
 

@@ -63,6 +63,7 @@ struct gk_ctx {
   int sm_count = 0;
   gk::DevBuf<unsigned long long> scratch;  // counters / reductions (64 words)
   gk::DevBuf<double2> phase;               // direct-mode phase table (kPhaseM)
+  gk::DevBuf<double2> phase_small;         // eval_batch phase table (kPhaseSmall, L1-resident)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
