@@ -409,7 +409,9 @@ def main():
         "config": {"workload": cfg["name"], "mode": chosen,
                    "samples_per_wavelength": args.S if chosen == "table" else None,
                    "parallelism": f"row-block x{world}",
-                   "l2": "output Z >> L2 (no flush needed); inputs resident"},
+                   "l2": "no flush: every step streams Z (rows x N x 16 B, 107 GB at C5) "
+                         "through L2; the quadrature points (<= 47 MB) are re-read ~N times "
+                         "within each step, so their L2 residency is the steady state"},
         "fill_time_s": main_res["ms_per_step"] * 1e-3,
         "roofline": {"bound": "fp64", "achieved": main_res["kernel_tflops"], "peak": p64,
                      "peak_nominal": 148 * 64 * 2 * 1.965e9 / 1e12,
