@@ -316,3 +316,40 @@ def test_degenerate_sizes_and_strided_output(gk, oracle):
     full, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
     assert torch.equal(win, full[10:30])
     assert torch.all(big[:, :5] == complex(7, 7)) and torch.all(big[:, 5 + dm.N:] == complex(7, 7))
+
+
+def test_separate_contexts_on_separate_host_threads(gk):
+    """SURVEY 8b threading contract: a context is not re-entrant, but separate
+    contexts (each with its own stream) may be driven from separate host
+    threads concurrently; every thread gets the single-threaded result."""
+    import threading
+
+    import torch
+    mesh = sphere(gk, 2)
+    ref, _ = gk.fill_rows(gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4)), gk.Mode.DIRECT,
+                          k=2 * np.pi)
+    ref = ref.cpu()
+    results, errors = {}, []
+
+    def work(i):
+        try:
+            ctx = gk.Context(0)   # its own gk_ctx and stream
+            dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), ctx)
+            lo, hi = dm.distance_range()
+            t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi), gk.Medium(), ctx=ctx)
+            for _ in range(3):
+                z, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+                zt, _ = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+            results[i] = (z.cpu(), zt.cpu())
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for i in range(4):
+        assert torch.equal(results[i][0], ref)
+        assert torch.equal(results[i][1], results[0][1])
