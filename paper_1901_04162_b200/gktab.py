@@ -192,6 +192,17 @@ class Context:
         check(lib().gk_ctx_create(device, C.byref(h)), "gk_ctx_create")
         self.h = h
 
+    def __del__(self):
+        # tables and meshes hold a reference to their context, so this runs
+        # only after they are gone (gk_ctx_destroy's ordering rule)
+        h = getattr(self, "h", None)
+        if h and _lib._lib is not None:
+            try:
+                _lib._lib.gk_ctx_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
     @classmethod
     def get(cls, device: int = 0) -> "Context":
         if device not in cls._cache:

@@ -127,7 +127,8 @@ def fill_rows_gathered(dmesh, mode, kind=None, table=None, k: complex = 0.0, dst
         handle = (C.c_ubyte * 64).from_buffer_copy(bytes(ht.cpu().tolist()))
         check(lib().gk_ipc_open(ctx.h, handle, C.byref(ptr)), "gk_ipc_open")
     h, p = ctx.h, ptr.value
-    release = (lambda: lib().gk_shared_free(h, C.c_void_p(p))) if rank == dst else None
+    # the closure holds the Context itself: it must outlive the allocation
+    release = (lambda c=ctx: lib().gk_shared_free(c.h, C.c_void_p(p))) if rank == dst else None
     full = torch.as_tensor(_DeviceMatrix(p, (N, N), release), device=f"cuda:{ctx.device}")
     rep = None
     try:
