@@ -333,6 +333,10 @@ def main():
         results[mode] = {"ms_per_step": ms, "fill_kernel_ms": fill_ms,
                          "evals_per_s": total_evals / (ms * 1e-3),
                          "kernel_tflops": evals_per_launch * FLOPS_PER_EVAL / (fill_ms * 1e-3) / 1e12}
+    # the timed fills ran asynchronously: surface any fallback / range / r = 0
+    # error now (outside the timed region), like a synchronous fill would
+    ctx.fill_check()
+
     # the headline mode: the faster of direct and the table at the configured S
     chosen = args.mode if args.mode != "auto" else min(("direct", "table"),
                                                        key=lambda x: results[x]["ms_per_step"])

@@ -208,6 +208,13 @@ gk_status gk_fill_rows(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_
                        gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
                        gk_c128* z, size_t ldz, gk_fill_report* report);
 
+/* Asynchronous fills (report == NULL) accumulate their fallback, out-of-range
+   and zero-distance counts in the context; gk_fill_check synchronises, returns
+   the accumulated fallbacks, resets the counts and fails like the synchronous
+   call would have (GK_ERR_OUT_OF_RANGE / GK_ERR_DOMAIN) if any fill since the
+   last check met such a pair. */
+gk_status gk_fill_check(gk_ctx* ctx, uint64_t* fallbacks);
+
 /* Fused Exp + Green fill sharing every radius (and, in TABLE mode, every
    lookup): z_exp gets the PlainExp matrix, z_green the GreenOverR matrix, each
    bit-identical to the separate gk_fill_rows result.  The EFIE-type use the

@@ -107,6 +107,19 @@ uint64_t predicted(uint64_t N, uint64_t m, uint64_t n) {
 
 void check_ctx(const gk_ctx* c) { need(c != nullptr, GK_ERR_INVALID_ARGUMENT, "null gk_ctx"); }
 
+// scratch words 32..34: counters accumulated by asynchronous fills
+constexpr int kAsyncFillCounters = 32;
+
+// the reference's exceptions for fill counters {fallbacks, > r_max, non-finite}
+void raise_fill_errors(const unsigned long long* h) {
+  if (h[1])
+    gk::fail(GK_ERR_OUT_OF_RANGE,
+             "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
+  if (h[2])
+    gk::fail(GK_ERR_DOMAIN, "eval_analytic: exp(-jkr)/r is singular at r = 0 (" +
+                                std::to_string(h[2]) + " entries meet a zero-distance point pair)");
+}
+
 void use_device(const gk_ctx* c) { GK_CUDA(cudaSetDevice(c->device)); }
 
 }  // namespace
@@ -702,7 +715,9 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
   const uint64_t kinds = kind == 2 ? 2 : 1;
   const uint64_t pred = predicted(mesh->N, mesh->m, mesh->n);
   use_device(c);
-  unsigned long long* cnt = c->scratch.p + 16;
+  // synchronous fills count into their own words; asynchronous ones (report
+  // == NULL) accumulate in the context until gk_fill_check reads them
+  unsigned long long* cnt = c->scratch.p + (report ? 16 : kAsyncFillCounters);
   if (report) {
     GK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
@@ -723,15 +738,24 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
   report->actual_calls = kinds * 3ull * mesh->m * mesh->n * rows * (mesh->N - 1);
   report->fallback_calls = h[0] + h[1];
   report->wall_time_s = ms * 1e-3;
-  if (h[1])
-    gk::fail(GK_ERR_OUT_OF_RANGE,
-             "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
-  if (h[2])
-    gk::fail(GK_ERR_DOMAIN, "eval_analytic: exp(-jkr)/r is singular at r = 0 (" +
-                                std::to_string(h[2]) + " entries meet a zero-distance point pair)");
+  raise_fill_errors(h);
 }
 
 }  // namespace
+
+gk_status gk_fill_check(gk_ctx* c, uint64_t* fallbacks) {
+  return guarded([&] {
+    check_ctx(c);
+    use_device(c);
+    unsigned long long* cnt = c->scratch.p + kAsyncFillCounters;
+    unsigned long long h[3];
+    GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(h), c->stream));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    if (fallbacks) *fallbacks = h[0] + h[1];
+    raise_fill_errors(h);
+  });
+}
 
 gk_status gk_fill_rows(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t,
                        gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
@@ -830,12 +854,7 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       report->fallback_calls = h[0] + h[1];
       report->wall_time_s = ms * 1e-3;
     }
-    if (h[1])
-      gk::fail(GK_ERR_OUT_OF_RANGE,
-               "accumulate_green: " + std::to_string(h[1]) + " radii above the tabulated r_max");
-    if (h[2])
-      gk::fail(GK_ERR_DOMAIN, "eval_analytic: exp(-jkr)/r is singular at r = 0 (" +
-                                  std::to_string(h[2]) + " entries meet a zero-distance point pair)");
+    raise_fill_errors(h);
   } catch (...) {
     cleanup();
     throw;

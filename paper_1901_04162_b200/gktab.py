@@ -219,6 +219,14 @@ class Context:
     def synchronize(self) -> None:
         check(lib().gk_ctx_synchronize(self.h), "synchronize")
 
+    def fill_check(self) -> int:
+        """Synchronise; raise like a synchronous fill if any asynchronous fill
+        (report=False) since the last check met r > r_max or r = 0; return and
+        reset their accumulated fallback count."""
+        fb = C.c_uint64()
+        check(lib().gk_fill_check(self.h, C.byref(fb)), "fill_matrix")
+        return fb.value
+
     def fp64_peak_tflops(self) -> float:
         out = C.c_double()
         check(lib().gk_bench_fp64_peak(self.h, C.byref(out)), "fp64_peak")

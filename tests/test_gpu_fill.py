@@ -353,3 +353,32 @@ def test_separate_contexts_on_separate_host_threads(gk):
     for i in range(4):
         assert torch.equal(results[i][0], ref)
         assert torch.equal(results[i][1], results[0][1])
+
+
+def test_async_fill_errors_surface_at_fill_check(gk):
+    """Asynchronous fills (report=False) accumulate their counts in the
+    context; fill_check returns the fallbacks and raises the reference's
+    exceptions like the synchronous call."""
+    ctx = gk.Context.get(0)
+    ctx.fill_check()   # start clean
+    mesh = gk.generate_sphere_mesh(0.5, 1)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(1, 1))
+    from oracle.pyoracle import Oracle
+    hi = Oracle().max_vertex_distance(mesh.vertices) * 1.01
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=0.3, r_max=hi))
+    _, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)           # synchronous reference
+    for _ in range(3):
+        gk.fill_rows(dm, gk.Mode.TABLE, table=t, report=False)
+    assert ctx.fill_check() == 3 * rep.fallback_calls > 0
+    assert ctx.fill_check() == 0                                 # reset
+    low = gk.DeviceTable(gk.SamplingConfig(r_min=1e-3, r_max=0.5))
+    gk.fill_rows(dm, gk.Mode.TABLE, table=low, report=False)     # radii above r_max
+    with pytest.raises(gk.OutOfRange):
+        ctx.fill_check()
+    v = np.array([[0, 0, 0], [3, 0, 0], [0, 3, 0], [0.5, 1, 0], [1.5, 1, 0], [1, 1, 1]], float)
+    zero = gk.DeviceMesh(gk.TriangleMesh(v, np.array([[0, 1, 2], [3, 4, 5]])),
+                         gk.QuadratureSpec(1, 1))
+    gk.fill_rows(zero, gk.Mode.DIRECT, k=2 * np.pi, report=False)
+    with pytest.raises(gk.DomainError):
+        ctx.fill_check()
+    assert ctx.fill_check() == 0
