@@ -20,7 +20,7 @@ import math
 import numpy as np
 import pytest
 
-from oracle.pyoracle import DIRECT, EXP, GREEN, SamplingConfig as OCfg, splitmix64_uniform
+from oracle.pyoracle import DIRECT, EXP, GREEN, splitmix64_uniform
 
 pytestmark = pytest.mark.gpu
 ULP = 2.0 ** -53

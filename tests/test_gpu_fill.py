@@ -9,7 +9,7 @@ of the phase k r, which the reference itself carries.
 import numpy as np
 import pytest
 
-from oracle.pyoracle import DIRECT, EXP, GREEN, TABLE, SamplingConfig as OCfg
+from oracle.pyoracle import DIRECT, EXP, TABLE
 
 pytestmark = pytest.mark.gpu
 
