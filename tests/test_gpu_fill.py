@@ -22,7 +22,8 @@ def sphere(gk, level, radius=1.0, seed=1901, amp=1e-3):
 
 def test_points_bit_exact(gk, oracle):
     for mesh, m, n in [(sphere(gk, 2), 6, 4), (sphere(gk, 1, 0.5), 7, 5),
-                       (gk.generate_plate_mesh(1.0, 10), 4, 3), (sphere(gk, 0), 1, 1)]:
+                       (gk.generate_plate_mesh(1.0, 10), 4, 3), (sphere(gk, 0), 1, 1),
+                       (sphere(gk, 1), 3, 2), (sphere(gk, 1), 3, 6), (sphere(gk, 1), 6, 32)]:
         dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
         go, gi = dm.points()
         oo, oi = oracle.points(mesh.vertices, mesh.triangles, m, n)
@@ -204,6 +205,10 @@ def test_mesh_validation(gk):
     mesh = gk.generate_sphere_mesh(0.5, 0)
     with pytest.raises(gk.InvalidArgument):
         gk.DeviceMesh(mesh, gk.QuadratureSpec(5, 1))
+    with pytest.raises(gk.InvalidArgument, match="<= 32"):   # device limit (documented)
+        gk.DeviceMesh(mesh, gk.QuadratureSpec(4, 33))
+    with pytest.raises(gk.InvalidArgument):
+        gk.DeviceMesh(mesh, gk.QuadratureSpec(4, 0))
     bad = gk.TriangleMesh(mesh.vertices, np.array([[0, 1, 99]]))
     with pytest.raises(gk.InvalidArgument):
         gk.DeviceMesh(bad, gk.QuadratureSpec(4, 3))
