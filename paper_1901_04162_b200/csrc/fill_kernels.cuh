@@ -475,7 +475,10 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 // the global table through L1 instead (correct either way: same code path,
 // different TableWin).
 
-constexpr int kStagedWarps = 16;
+#ifndef GK_STAGED_WARPS
+#define GK_STAGED_WARPS 16
+#endif
+constexpr int kStagedWarps = GK_STAGED_WARPS;
 
 struct StageArgs {
   uint32_t lk_cap, j_cap;  // shared-memory capacity in buckets / records
