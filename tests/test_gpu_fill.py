@@ -387,3 +387,34 @@ def test_async_fill_errors_surface_at_fill_check(gk):
     with pytest.raises(gk.DomainError):
         ctx.fill_check()
     assert ctx.fill_check() == 0
+
+
+@pytest.mark.parametrize("lam", [0.01, 1000.0])
+def test_extreme_wavelengths(gk, oracle, lam):
+    """kr up to ~1250 (lambda = 1 cm on the unit sphere: phase rounding grows
+    like the reference's, the (1 + |k| r) factor of the bound) and kr ~ 0.01
+    (lambda = 1 km: G ~ 1/r), both modes."""
+    mesh = sphere(gk, 2)
+    k = 2 * np.pi / lam
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(4, 3))
+    zd, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, row_begin=0, row_end=64)
+    ref, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, 4, 3, DIRECT, k, threads=8,
+                              row_begin=0, row_end=64)
+    B = oracle.entry_bounds(mesh.vertices, mesh.triangles, 4, 3, None, k, ULPS,
+                            row_begin=0, row_end=64)
+    assert np.all(np.abs(zd.cpu().numpy() - ref) <= B)
+    lo, hi = dm.distance_range()
+    # S such that the base interval is <= 1 mm (lambda = 1 km at S = 1000 would
+    # leave fewer than two intervals: build_plan rejects it, like the reference)
+    S = max(1000, int(lam / 1e-3))
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S),
+                       gk.Medium(lambda0=lam))
+    d = t.download()
+    ev = oracle.evaluator(oracle.make_plan(d["abscissae"], d["zeros"]), k)
+    zt, _ = gk.fill_rows(dm, gk.Mode.TABLE, table=t, row_begin=0, row_end=64)
+    ref_t, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, 4, 3, TABLE, k, ev=ev, threads=8,
+                                row_begin=0, row_end=64)
+    Bt = oracle.entry_bounds(mesh.vertices, mesh.triangles, 4, 3, ev, k, ULPS, row_begin=0,
+                             row_end=64)
+    assert np.all(np.abs(zt.cpu().numpy() - ref) <= Bt)
+    assert np.all(np.abs(zt.cpu().numpy() - ref_t) <= B)
