@@ -418,3 +418,34 @@ def test_extreme_wavelengths(gk, oracle, lam):
                              row_end=64)
     assert np.all(np.abs(zt.cpu().numpy() - ref) <= Bt)
     assert np.all(np.abs(zt.cpu().numpy() - ref_t) <= B)
+
+
+def test_no_device_memory_growth_over_repeated_lifecycles(gk):
+    """Create / fill / destroy meshes, tables, bench_compare and streamed host
+    fills repeatedly: after a warm-up cycle the device's free memory stays
+    flat (every stream-ordered allocation is freed and reused by the pool)."""
+    import gc
+
+    import torch
+
+    def cycle():
+        mesh = sphere(gk, 2)
+        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+        lo, hi = dm.distance_range()
+        t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=4000))
+        gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+        gk.fill_rows_pair(dm, gk.Mode.DIRECT, k=2 * np.pi)
+        z = np.zeros((50, dm.N), np.complex128)
+        gk.fill_rows_host(dm, gk.Mode.DIRECT, z, k=2 * np.pi, row_begin=0, row_end=50)
+        t.error_sweep(gk.KernelKind.GreenOverR, probe_count=10000)
+        gk.bench_compare(gk.generate_sphere_mesh(0.5, 1), gk.QuadratureSpec(4, 3))
+        del t, dm
+        gc.collect()
+        torch.cuda.synchronize()
+
+    cycle()
+    free0 = torch.cuda.mem_get_info(0)[0]
+    for _ in range(5):
+        cycle()
+    free1 = torch.cuda.mem_get_info(0)[0]
+    assert free0 - free1 <= 64 << 20, (free0 - free1) / 2 ** 20
