@@ -129,7 +129,11 @@ def fill_rows_gathered(dmesh, mode, kind=None, table=None, k: complex = 0.0, dst
     h, p = ctx.h, ptr.value
     # the closure holds the Context itself: it must outlive the allocation
     release = (lambda c=ctx: lib().gk_shared_free(c.h, C.c_void_p(p))) if rank == dst else None
-    full = torch.as_tensor(_DeviceMatrix(p, (N, N), release), device=f"cuda:{ctx.device}")
+    # no device= here: the mapped memory lives on dst's GPU and torch must take
+    # the device from the pointer -- asking for this rank's device would make
+    # it copy the matrix instead of viewing the peer memory
+    full = torch.as_tensor(_DeviceMatrix(p, (N, N), release))
+    assert full.data_ptr() == p, "fill_rows_gathered: the matrix must be a view, not a copy"
     rep = None
     try:
         if re > rb:
