@@ -475,7 +475,12 @@ def fill_rows(dmesh: DeviceMesh, mode: Mode, kind: KernelKind = KernelKind.Green
     rows = row_end - row_begin
     if out is None:
         out = torch.empty((rows, N), dtype=torch.complex128, device=f"cuda:{ctx.device}")
-    assert out.dtype == torch.complex128 and out.is_cuda and out.stride(1) == 1
+    if not (out.dtype == torch.complex128 and out.is_cuda and out.dim() == 2
+            and out.stride(1) == 1 and out.shape[0] >= rows and out.shape[1] >= N
+            and (rows <= 1 or out.stride(0) >= N)):
+        raise _lib.InvalidArgument(
+            f"fill_rows: out must be a CUDA complex128 ({rows}, >= {N}) view with unit "
+            f"column stride (got {tuple(out.shape)}, {out.dtype})")
     kc = complex(k)
     rep = FillReportC()
     check(lib().gk_fill_rows(ctx.h, dmesh.h, int(mode), table.h if table else None, int(kind),

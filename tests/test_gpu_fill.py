@@ -449,3 +449,16 @@ def test_no_device_memory_growth_over_repeated_lifecycles(gk):
         cycle()
     free1 = torch.cuda.mem_get_info(0)[0]
     assert free0 - free1 <= 64 << 20, (free0 - free1) / 2 ** 20
+
+
+def test_fill_rows_rejects_bad_output(gk):
+    """A too-small, strided or wrong-dtype output is rejected before launch."""
+    import torch
+    dm = gk.DeviceMesh(sphere(gk, 1), gk.QuadratureSpec(4, 3))
+    for bad in (torch.empty((10, dm.N), dtype=torch.complex128, device="cuda:0"),       # rows
+                torch.empty((dm.N, dm.N - 1), dtype=torch.complex128, device="cuda:0"),  # cols
+                torch.empty((dm.N, dm.N), dtype=torch.complex64, device="cuda:0"),
+                torch.empty((dm.N, 2 * dm.N), dtype=torch.complex128, device="cuda:0")[:, ::2],
+                torch.empty((dm.N, dm.N), dtype=torch.complex128)):
+        with pytest.raises(gk.InvalidArgument):
+            gk.fill_rows(dm, gk.Mode.DIRECT, k=1.0, out=bad)
