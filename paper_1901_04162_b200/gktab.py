@@ -405,8 +405,11 @@ def eval_batch_async(kind: KernelKind, radii, out, status: EvalStatus,
     ctx = status.ctx
     kc = complex(k)
     n = radii.numel()
-    if out.numel() < n or out.dtype != _torch().complex128 or radii.dtype != _torch().float64:
-        raise _lib.InvalidArgument("eval_batch_async: float64 radii and complex128 out[n]")
+    if (out.numel() < n or out.dtype != _torch().complex128 or radii.dtype != _torch().float64
+            or not (radii.is_cuda and out.is_cuda) or not (radii.is_contiguous()
+                                                           and out.is_contiguous())):
+        raise _lib.InvalidArgument("eval_batch_async: contiguous CUDA float64 radii and "
+                                   "complex128 out[n]")
     check(lib().gk_eval_batch_async(ctx.h, table.h if table else None, int(kind), kc.real, kc.imag,
                                     radii.data_ptr() if n else None, n,
                                     out.data_ptr() if n else None, status.words.data_ptr()),

@@ -229,6 +229,10 @@ def test_eval_batch_async_matches_sync_and_reports(gk, oracle):
     st.reset()
     gk.eval_batch_async(gk.KernelKind.PlainExp, rd, out, st, k=2.0)  # direct: no fallbacks
     assert st.read() == 0
+    with pytest.raises(gk.InvalidArgument):   # host tensors are rejected, not dereferenced
+        gk.eval_batch_async(gk.KernelKind.PlainExp, rd.cpu(), out, st, k=2.0)
+    with pytest.raises(gk.InvalidArgument):
+        gk.eval_batch_async(gk.KernelKind.PlainExp, rd, out[:10], st, k=2.0)
 
 
 @pytest.mark.parametrize("degree", [1, 2, 4, 5, 7])
