@@ -204,7 +204,12 @@ class Context:
             self.h = None
 
     @classmethod
-    def get(cls, device: int = 0) -> "Context":
+    def get(cls, device: int | None = None) -> "Context":
+        """The cached context of `device` (default: torch's current CUDA
+        device, i.e. the one torch.cuda.set_device(local_rank) selected),
+        bound to torch's current stream."""
+        if device is None:
+            device = _torch().cuda.current_device()
         if device not in cls._cache:
             cls._cache[device] = cls(device)
         ctx = cls._cache[device]
