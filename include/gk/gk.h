@@ -134,6 +134,18 @@ gk_status gk_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double
                         double k_im, const double* radii, size_t n, gk_c128* out,
                         uint64_t* fallbacks);
 
+/* The reference's plugin seam in batch: Kernel::accumulate (matfill.hpp:59-87;
+   TableKernel -> KernelEvaluator::accumulate_green, evaluator.hpp:150-194, when
+   table != NULL, AnalyticKernel{k} when NULL) for nblocks independent blocks:
+   out[b] = sum_i K(radii[b*block_len + i]) * weights[b*block_len + i].
+   Device buffers; one warp per block (lanes stride the block, warp-shuffle
+   reduction).  For callers with their own quadrature.  Errors like
+   eval_batch (the first failing flat index), fallbacks counted. */
+gk_status gk_accumulate_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,
+                              double k_im, const double* radii, const double* weights,
+                              size_t block_len, size_t nblocks, gk_c128* out,
+                              uint64_t* fallbacks);
+
 /* Stream-ordered form of gk_eval_batch for pipelines that launch many batches
    back to back (no host synchronisation per call).  `status` is a DEVICE
    array of 2 words that accumulates over calls: status[0] += fallbacks,

@@ -497,6 +497,34 @@ gk_status gk_max_vertex_distance(gk_ctx* c, const gk_mesh* mesh, double* out) {
   });
 }
 
+gk_status gk_accumulate_batch(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
+                              double k_im, const double* radii, const double* weights,
+                              size_t len, size_t nblocks, gk_c128* out, uint64_t* fallbacks) {
+  return guarded([&] {
+    check_ctx(c);
+    need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
+    if (t) {
+      k_re = t->dev.k_re;
+      k_im = t->dev.k_im;
+    }
+    need(k_re >= 0.0, GK_ERR_INVALID_ARGUMENT, "eval_analytic: k must be >= 0");
+    if (fallbacks) *fallbacks = 0;
+    if (nblocks == 0) return;
+    need(out != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");
+    need(len == 0 || (radii && weights), GK_ERR_INVALID_ARGUMENT, "null buffer");
+    use_device(c);
+    unsigned long long* w = c->scratch.p;
+    const unsigned long long init[2] = {0ull, ~0ull};
+    GK_CUDA(cudaMemcpyAsync(w, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    gk::launch_accumulate(c, t, kind, k_re, k_im, radii, weights, len, nblocks, out, w);
+    unsigned long long res[2];
+    GK_CUDA(cudaMemcpyAsync(res, w, sizeof(res), cudaMemcpyDeviceToHost, c->stream));
+    GK_CUDA(cudaStreamSynchronize(c->stream));
+    if (fallbacks) *fallbacks = res[0];
+    raise_bad_radius(res[1], radii);
+  });
+}
+
 gk_status gk_eval_batch_async(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
                               double k_im, const double* radii, size_t n, gk_c128* out,
                               uint64_t* status) {

@@ -130,6 +130,106 @@ void launch_locate(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, ui
   GK_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------- accumulate (K5b)
+
+template <int KIND, bool TABLE, int DEG, bool FAST>
+__global__ void accumulate_kernel(const double* __restrict__ radii,
+                                  const double* __restrict__ wts, size_t len, size_t nblocks,
+                                  double2* __restrict__ out, TableDev T, double k_re,
+                                  double k_im, unsigned long long* w,
+                                  const double2* __restrict__ ptab, double K1s) {
+  const int lane = threadIdx.x & 31;
+  const size_t warps = static_cast<size_t>(gridDim.x) * (blockDim.x >> 5);
+  unsigned long long fb = 0;
+  for (size_t b = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) >> 5; b < nblocks;
+       b += warps) {
+    double re = 0.0, im = 0.0;
+    for (size_t i = lane; i < len; i += 32) {
+      const size_t e = b * len + i;
+      const double r = radii[e];
+      unsigned bad = V_OK;
+      double2 v = make_double2(0.0, 0.0);
+      if (TABLE && r >= T.r_min) {
+        if (!(r <= T.r_max)) bad = V_RANGE;
+        else if (KIND == GK_KIND_EXP) v = exp_table(r, T);
+        else v = DEG == 3 ? green_table<3>(r, T) : green_table_any(r, T);
+      } else {
+        if (KIND == GK_KIND_GREEN) {
+          if (r == 0.0) bad = V_DOMAIN;
+          else if (!(r > 0.0)) bad = V_INVALID;
+        } else if (!(r >= 0.0)) {
+          bad = V_INVALID;
+        }
+        if (bad == V_OK) {
+          if constexpr (FAST) {
+            const double2 cs = cis_phase_small(r, K1s, ptab);
+            v = make_double2(cs.x, -cs.y);
+            if (KIND == GK_KIND_GREEN) {
+              const double y = __drcp_rn(r);
+              v = make_double2(__dmul_rn(v.x, y), __dmul_rn(v.y, y));
+            }
+          } else {
+            v = analytic_sincos(KIND, k_re, k_im, r);
+          }
+          if (TABLE) ++fb;
+        }
+      }
+      if (bad) atomicMin(w + 1, (static_cast<unsigned long long>(e) << 3) | bad);
+      const double wi = wts[e];
+      re = __fma_rn(v.x, wi, re);
+      im = __fma_rn(v.y, wi, im);
+    }
+    for (int o = 16; o; o >>= 1) {
+      re += __shfl_xor_sync(0xffffffffu, re, o);
+      im += __shfl_xor_sync(0xffffffffu, im, o);
+    }
+    if (lane == 0) out[b] = make_double2(re, im);
+  }
+  if (TABLE) {
+    for (int o = 16; o; o >>= 1) fb += __shfl_xor_sync(0xffffffffu, fb, o);
+    if (lane == 0 && fb) atomicAdd(w, fb);
+  }
+}
+
+template <int KIND>
+void launch_accumulate_kind(gk_ctx* ctx, const gk_table* t, const double* r, const double* wts,
+                            size_t len, size_t nblocks, double2* out, double k_re, double k_im,
+                            unsigned long long* w) {
+  size_t grid = (nblocks + 7) / 8;  // 8 warps (blocks of the sum) per CTA
+  const size_t cap = static_cast<size_t>(ctx->sm_count) * 16;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  const unsigned g = static_cast<unsigned>(grid);
+  TableDev T{};
+  if (t) T = t->dev;
+  const double K1s = k_re * kPhaseSmall / (2.0 * kPi);
+  const double2* ptab = ctx->phase_small.p;
+  if (!t && k_im == 0.0 && fast_eval())
+    accumulate_kernel<KIND, false, 0, true><<<g, 256, 0, ctx->stream>>>(
+        r, wts, len, nblocks, out, T, k_re, k_im, w, ptab, K1s);
+  else if (!t)
+    accumulate_kernel<KIND, false, 0, false><<<g, 256, 0, ctx->stream>>>(
+        r, wts, len, nblocks, out, T, k_re, k_im, w, ptab, K1s);
+  else if (KIND == GK_KIND_GREEN && T.degree == 3)
+    accumulate_kernel<KIND, true, 3, false><<<g, 256, 0, ctx->stream>>>(
+        r, wts, len, nblocks, out, T, k_re, k_im, w, ptab, K1s);
+  else
+    accumulate_kernel<KIND, true, 0, false><<<g, 256, 0, ctx->stream>>>(
+        r, wts, len, nblocks, out, T, k_re, k_im, w, ptab, K1s);
+  count_launches(1);
+  GK_CUDA(cudaGetLastError());
+}
+
+void launch_accumulate(gk_ctx* ctx, const gk_table* t, gk_kind kind, double k_re, double k_im,
+                       const double* r, const double* wts, size_t len, size_t nblocks,
+                       gk_c128* out, unsigned long long* w) {
+  double2* o = reinterpret_cast<double2*>(out);
+  if (kind == GK_KIND_GREEN)
+    launch_accumulate_kind<GK_KIND_GREEN>(ctx, t, r, wts, len, nblocks, o, k_re, k_im, w);
+  else
+    launch_accumulate_kind<GK_KIND_EXP>(ctx, t, r, wts, len, nblocks, o, k_re, k_im, w);
+}
+
 // ------------------------------------------------------------ error_sweep
 
 __device__ __forceinline__ void atomic_max_pos(unsigned long long* w, double v) {

@@ -117,6 +117,11 @@ void launch_max_vertex_d2(const double* verts, size_t nv, unsigned long long* d2
 // at the max combined; w[8..31] decade histogram.  `comb` scratch [probes].
 void launch_sweep(gk_ctx* ctx, const gk_table* t, int kind, uint64_t probes, double* comb,
                   unsigned long long* w);
+// Kernel::accumulate for nblocks blocks of block_len radii -> out[nblocks];
+// w[0] fallbacks, w[1] first bad (flat index << 3 | code)
+void launch_accumulate(gk_ctx* ctx, const gk_table* t, gk_kind kind, double k_re, double k_im,
+                       const double* r, const double* wts, size_t block_len, size_t nblocks,
+                       gk_c128* out, unsigned long long* w);
 // compare_fills partial maxima (as non-negative double bits) -> w[0] (re), w[1] (im)
 void launch_compare(gk_ctx* ctx, const gk_c128* test, const gk_c128* ref, size_t rows, size_t N,
                     size_t row_begin, size_t ld, unsigned long long* w);

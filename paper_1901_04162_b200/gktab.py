@@ -382,6 +382,34 @@ def eval_batch(kind: KernelKind, radii, table: DeviceTable | None = None, k: com
     return out
 
 
+def accumulate_batch(kind: KernelKind, radii, weights, table: "DeviceTable | None" = None,
+                     k: complex = 0.0, ctx: "Context | None" = None):
+    """Kernel::accumulate (matfill.hpp:59-87) for a batch of blocks:
+    out[b] = sum_i K(radii[b, i]) weights[b, i], with TableKernel semantics
+    (KernelEvaluator::accumulate_green, evaluator.hpp:150-194) when a table is
+    given and AnalyticKernel{k} otherwise.  radii/weights: (nblocks, block_len)
+    arrays or tensors.  Returns (complex128 CUDA tensor [nblocks], fallbacks)."""
+    torch = _torch()
+    ctx = ctx or (table.ctx if table else Context.get())
+    r = _as_device_f64(radii, ctx.device)
+    w = _as_device_f64(weights, ctx.device)
+    if r.dim() == 1:
+        r, w = r.reshape(1, -1), w.reshape(1, -1)
+    if r.shape != w.shape or r.dim() != 2:
+        raise _lib.InvalidArgument("accumulate_batch: radii and weights must be (nblocks, len)")
+    nb, ln = r.shape
+    out = torch.empty(nb, dtype=torch.complex128, device=r.device)
+    fb = C.c_uint64()
+    kc = complex(k)
+    check(lib().gk_accumulate_batch(ctx.h, table.h if table else None, int(kind), kc.real,
+                                    kc.imag, r.data_ptr() if r.numel() else None,
+                                    w.data_ptr() if w.numel() else None, ln, nb,
+                                    out.data_ptr() if nb else None, C.byref(fb)), "accumulate")
+    if table is not None:
+        table.fallbacks += fb.value
+    return out, fb.value
+
+
 class EvalStatus:
     """Device-resident status of stream-ordered eval_batch calls
     (gk_eval_batch_async): fallback count and the first failing radius."""

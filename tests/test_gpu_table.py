@@ -270,3 +270,46 @@ def test_lagrange_degrees_vs_oracle(gk, oracle, degree):
                                 threads=8)
     B = oracle.entry_bounds(mesh.vertices, mesh.triangles, 4, 3, None, 2 * math.pi, 64.0)
     assert np.all(np.abs(zt.cpu().numpy() - ref_t) <= B)
+
+
+def test_accumulate_batch_vs_reference(gk, oracle, ref):
+    """gk_accumulate_batch: the reference's Kernel::accumulate for many blocks at
+    once -- TableKernel (accumulate_green, evaluator.hpp:150-194) and
+    AnalyticKernel (matfill.hpp:58-68) -- vs the reference itself per block."""
+    c = gk.SamplingConfig(r_min=1e-3, r_max=2.0, samples_per_wavelength=1000)
+    med = gk.Medium(lambda0=0.5)
+    t = gk.DeviceTable(c, med)
+    d = t.download()
+    plan = oracle.make_plan(d["abscissae"], d["zeros"])
+    k = oracle.wavenumber(0.5)
+    rev = ref.evaluator(plan, k)
+    nb, ln = 400, 72
+    r = splitmix64_uniform(11, nb * ln, 2e-4, 2.0).reshape(nb, ln)   # some below r_min
+    w = np.random.default_rng(5).uniform(-1.0, 1.0, (nb, ln))
+    f0 = t.fallbacks
+    got, fb = gk.accumulate_batch(gk.KernelKind.GreenOverR, r, w, table=t)
+    got = got.cpu().numpy()
+    assert fb == t.fallbacks - f0 == int(np.sum(r < d["abscissae"][0])) > 0
+    for b in range(0, nb, 7):
+        want = rev.accumulate_green(r[b], w[b])
+        scale = np.sum(np.abs(w[b]) / r[b])
+        assert abs(got[b] - want) <= 1e-11 * scale, b
+    # Exp through the table and both kinds direct (AnalyticKernel{k})
+    ge, _ = gk.accumulate_batch(gk.KernelKind.PlainExp, r, w, table=t)
+    ev_vals = rev.eval_batch(EXP, r.reshape(-1)).reshape(nb, ln)
+    assert np.max(np.abs(ge.cpu().numpy() - np.sum(ev_vals * w, axis=1))) <= 1e-12 * ln
+    for kind in (EXP, GREEN):
+        gd, fbd = gk.accumulate_batch(gk.KernelKind(kind), r, w, k=k)
+        vals = oracle.eval_analytic_batch(kind, k, r.reshape(-1)).reshape(nb, ln)
+        tol = np.sum(np.abs(w) * 8 * ULP * (1 + k * r) * np.abs(vals), axis=1) * 4
+        assert np.all(np.abs(gd.cpu().numpy() - np.sum(vals * w, axis=1)) <= tol) and fbd == 0
+    # errors carry the flat index of the first bad radius
+    bad = r.copy()
+    bad[3, 5] = 3.0
+    with pytest.raises(gk.InvalidArgument, match=r"\[221\]"):
+        gk.accumulate_batch(gk.KernelKind.GreenOverR, bad, w, table=t)
+    bad[3, 5] = 0.0
+    with pytest.raises(gk.InvalidArgument, match=r"\[221\]"):
+        gk.accumulate_batch(gk.KernelKind.GreenOverR, bad, w, k=k)
+    empty, fbe = gk.accumulate_batch(gk.KernelKind.GreenOverR, np.zeros((0, 4)), np.zeros((0, 4)), k=k)
+    assert empty.numel() == 0 and fbe == 0
