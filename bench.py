@@ -571,7 +571,7 @@ def hbm_peak_gbs():
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), \
             "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
     except (OSError, ValueError, KeyError):
-        return 7700.0, "B200_PROFILING.md fallback"
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
 
 
 def run_c1(gk, ctx, iters=1024, sets=8):
