@@ -1,5 +1,16 @@
 // fill.cu -- fill dispatch (launch_fill), K1 distance range, phase and
 // attenuation tables.  The fill kernels live in fill_kernels.cuh.
+//
+// launch_fill is fill_matrix's fill_rows loop (matfill.hpp:169-203) for a row
+// block [row_begin, row_end) -- the reference's per-thread chunk
+// (matfill.hpp:206-221) -- with AnalyticKernel (DIRECT, kernel.hpp:48-61) or
+// TableKernel (TABLE, evaluator.hpp:150-194); self pairs stay zero
+// (matfill.hpp:178).  K1 (launch_range) replaces max_vertex_distance
+// (mesh.hpp:62-68) x 1.01 (matfill.hpp:270) and the fixed r_min
+// (gktab_main.cpp:62) by the exact min/max quadrature-pair distance, so a
+// device table spans exactly the radii the fill meets.  Complex k (lossy
+// media) follows eval_analytic's form exp(-jkr) with k -> k_re + j k_im
+// (kernel.hpp:48-61 extended; no reference path, kernel.hpp:23-24).
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
