@@ -146,6 +146,13 @@ gk_status gk_accumulate_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, 
                               size_t block_len, size_t nblocks, gk_c128* out,
                               uint64_t* fallbacks);
 
+/* gk_accumulate_batch from HOST buffers (radii/weights[block_len * nblocks]
+   in, out[nblocks] back): the FFI-friendly form of the Kernel seam. */
+gk_status gk_accumulate_batch_host(gk_ctx* ctx, const gk_table* table, gk_kind kind,
+                                   double k_re, double k_im, const double* radii,
+                                   const double* weights, size_t block_len, size_t nblocks,
+                                   gk_c128* out, uint64_t* fallbacks);
+
 /* Stream-ordered form of gk_eval_batch for pipelines that launch many batches
    back to back (no host synchronisation per call).  `status` is a DEVICE
    array of 2 words that accumulates over calls: status[0] += fallbacks,

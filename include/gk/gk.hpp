@@ -209,6 +209,17 @@ class DeviceEvaluator {
     fallbacks_ += fb;
     return out;
   }
+  // Kernel::accumulate of one block (sum_i K(r_i) w_i) on the device
+  Complex accumulate(KernelKind kind, std::span<const double> radii,
+                     std::span<const double> weights) const {
+    Complex out{0.0, 0.0};
+    std::uint64_t fb = 0;
+    check(gk_accumulate_batch_host(ctx_->get(), h_, static_cast<gk_kind>(kind), 0.0, 0.0,
+                                   radii.data(), weights.data(), radii.size(), 1,
+                                   reinterpret_cast<gk_c128*>(&out), &fb));
+    fallbacks_ += fb;
+    return out;
+  }
   Complex eval_kernel(KernelKind kind, double r) const {
     return eval_batch(kind, std::span<const double>(&r, 1))[0];
   }
@@ -285,17 +296,14 @@ inline std::pair<KernelMatrix, FillReport> fill_matrix(
 class DeviceTableKernel {
  public:
   explicit DeviceTableKernel(const DeviceEvaluator* ev) : ev_(ev) {}
-  // Kind: gk::KernelKind or the reference's own gktab::KernelKind (same values)
+  // Kind: gk::KernelKind or the reference's own gktab::KernelKind (same values);
+  // the sum runs on the device (gk_accumulate_batch_host, one block)
   template <class Kind>
   Complex accumulate(Kind kind, std::span<const double> radii,
                      std::span<const double> weights) const {
     if (radii.size() != weights.size())
       throw std::invalid_argument("accumulate: radii and weights differ in length");
-    const std::vector<Complex> v =
-        ev_->eval_batch(static_cast<KernelKind>(static_cast<int>(kind)), radii);
-    Complex acc{0.0, 0.0};
-    for (std::size_t i = 0; i < v.size(); ++i) acc += weights[i] * v[i];
-    return acc;
+    return ev_->accumulate(static_cast<KernelKind>(static_cast<int>(kind)), radii, weights);
   }
   template <class Kind>
   Complex operator()(Kind kind, double r) const {

@@ -143,6 +143,8 @@ PROTOTYPES = {
     "gk_fill_check": [_vp, _u64p],
     "gk_accumulate_batch": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, _vp, C.c_size_t,
                             C.c_size_t, _vp, _u64p],
+    "gk_accumulate_batch_host": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, _vp,
+                                 C.c_size_t, C.c_size_t, _vp, _u64p],
     "gk_shared_alloc": [_vp, C.c_size_t, C.POINTER(C.c_void_p), _vp],
     "gk_shared_free": [_vp, _vp],
     "gk_ipc_open": [_vp, _vp, C.POINTER(C.c_void_p)],

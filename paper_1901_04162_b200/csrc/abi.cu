@@ -607,6 +607,40 @@ gk_status gk_eval_batch_host(gk_ctx* c, const gk_table* t, gk_kind kind, double 
   return st;
 }
 
+gk_status gk_accumulate_batch_host(gk_ctx* c, const gk_table* t, gk_kind kind, double k_re,
+                                   double k_im, const double* radii, const double* weights,
+                                   size_t len, size_t nblocks, gk_c128* out,
+                                   uint64_t* fallbacks) {
+  gk::DevBuf<double> dr, dw;
+  gk::DevBuf<gk_c128> dout;
+  gk_status st = guarded([&] {
+    check_ctx(c);
+    if (fallbacks) *fallbacks = 0;
+    if (nblocks == 0) return;
+    need(out != nullptr && (len == 0 || (radii && weights)), GK_ERR_INVALID_ARGUMENT,
+         "null buffer");
+    use_device(c);
+    const size_t n = len * nblocks;
+    dr.alloc(n, c->stream);
+    dw.alloc(n, c->stream);
+    dout.alloc(nblocks, c->stream);
+    if (n) {
+      GK_CUDA(cudaMemcpyAsync(dr.p, radii, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      GK_CUDA(cudaMemcpyAsync(dw.p, weights, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    }
+  });
+  if (st == GK_OK && nblocks) {
+    st = gk_accumulate_batch(c, t, kind, k_re, k_im, dr.p, dw.p, len, nblocks, dout.p, fallbacks);
+    if (st == GK_OK)
+      st = guarded([&] {
+        GK_CUDA(cudaMemcpyAsync(out, dout.p, nblocks * sizeof(gk_c128), cudaMemcpyDeviceToHost,
+                                c->stream));
+        GK_CUDA(cudaStreamSynchronize(c->stream));
+      });
+  }
+  return st;
+}
+
 gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32_t* tris,
                          size_t nt, int m, int n, gk_mesh** out) {
   return guarded([&] {

@@ -122,8 +122,12 @@ int main() {
     const gk::Complex a = kern.accumulate(gk::KernelKind::GreenOverR, r, w);
     const auto v = e.eval_batch(gk::KernelKind::GreenOverR, r);
     gk::Complex want{0.0, 0.0};
-    for (int i = 0; i < 4; ++i) want += w[i] * v[i];
-    CHECK(a == want);
+    double scale = 0.0;
+    for (int i = 0; i < 4; ++i) {
+      want += w[i] * v[i];
+      scale += std::abs(w[i] * v[i]);
+    }
+    CHECK(std::abs(a - want) <= 1e-14 * scale);  // device shuffle-reduction order
     CHECK(kern.fallback_count() == 2);  // one per batch that met r < r_min
     CHECK(throws<std::invalid_argument>(
         [&] { kern.accumulate(gk::KernelKind::GreenOverR, r, std::span<const double>(w.data(), 3)); }));
