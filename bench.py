@@ -467,6 +467,11 @@ def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals, rank, wor
     z = zh.numpy()
     m = gk.Mode.TABLE if mode == "table" else gk.Mode.DIRECT
     k = gk.wavenumber(medium)
+    # the step's inputs (the mesh) live in pinned host memory, copied in every step
+    pv = torch.from_numpy(mesh.vertices).pin_memory()
+    pt = torch.from_numpy(mesh.triangles.view(np.int32)).pin_memory()
+    mesh = gk.TriangleMesh(pv.numpy(), pt.numpy().view(np.uint32))
+    assert mesh.vertices.ctypes.data == pv.data_ptr()   # no copy: the pinned buffers
 
     def step():
         if full:
