@@ -896,8 +896,12 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt, cnt);
       GK_CUDA(cudaEventRecord(filled[b], c->stream));
       GK_CUDA(cudaStreamWaitEvent(copy, filled[b], 0));
-      GK_CUDA(cudaMemcpy2DAsync(z_host + (rb - row_begin) * ldz, ldz * sizeof(gk_c128), dz[b],
-                                row_bytes, row_bytes, re - rb, cudaMemcpyDeviceToHost, copy));
+      if (ldz == nt)  // contiguous rows on both sides: one linear copy
+        GK_CUDA(cudaMemcpyAsync(z_host + (rb - row_begin) * ldz, dz[b], (re - rb) * row_bytes,
+                                cudaMemcpyDeviceToHost, copy));
+      else
+        GK_CUDA(cudaMemcpy2DAsync(z_host + (rb - row_begin) * ldz, ldz * sizeof(gk_c128), dz[b],
+                                  row_bytes, row_bytes, re - rb, cudaMemcpyDeviceToHost, copy));
       GK_CUDA(cudaEventRecord(copied[b], copy));
     }
     GK_CUDA(cudaEventRecord(c->ev1, c->stream));

@@ -133,6 +133,29 @@ int main() {
         [&] { kern.accumulate(gk::KernelKind::GreenOverR, r, std::span<const double>(w.data(), 3)); }));
   }
 
+  // gk_fill_rows_host into a strided host window (ldz_host > N: the 2D-copy path)
+  {
+    const auto mesh = gk::generate_sphere_mesh(0.5, 1);  // N = 80
+    const std::size_t N = mesh.triangle_count(), ld = N + 7, rows = 50;
+    gk_mesh* m = nullptr;
+    CHECK(gk_mesh_create(ctx.get(), mesh.vertices.data(), mesh.vertices.size() / 3,
+                         mesh.triangles.data(), N, 4, 3, &m) == GK_OK);
+    std::vector<gk::Complex> strided(rows * ld, gk::Complex(7.0, 7.0)), dense(rows * N);
+    CHECK(gk_fill_rows_host(ctx.get(), m, GK_MODE_DIRECT, nullptr, GK_KIND_GREEN, 6.283185307179586,
+                            0.0, 10, 10 + rows, reinterpret_cast<gk_c128*>(strided.data()), ld,
+                            nullptr) == GK_OK);
+    CHECK(gk_fill_rows_host(ctx.get(), m, GK_MODE_DIRECT, nullptr, GK_KIND_GREEN, 6.283185307179586,
+                            0.0, 10, 10 + rows, reinterpret_cast<gk_c128*>(dense.data()), N,
+                            nullptr) == GK_OK);
+    bool same = true, pad_kept = true;
+    for (std::size_t r = 0; r < rows; ++r) {
+      for (std::size_t q = 0; q < N; ++q) same = same && strided[r * ld + q] == dense[r * N + q];
+      for (std::size_t q = N; q < ld; ++q) pad_kept = pad_kept && strided[r * ld + q] == gk::Complex(7.0, 7.0);
+    }
+    CHECK(same && pad_kept);
+    gk_mesh_destroy(m);
+  }
+
   // error_sweep on the device + the reference's CSV row format
   {
     gk::DeviceEvaluator e(ctx, gk::SamplingConfig{});
