@@ -179,9 +179,16 @@ gk_status gk_ctx_destroy(gk_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     // every context-owned buffer is released on the stream before it goes away
+    if (c->pipe.copy) cudaStreamSynchronize(c->pipe.copy);
     c->scratch.reset();
     c->phase.reset();
     c->phase_small.reset();
+    for (int b = 0; b < 2; ++b) {
+      c->pipe.buf[b].reset();
+      if (c->pipe.filled[b]) cudaEventDestroy(c->pipe.filled[b]);
+      if (c->pipe.copied[b]) cudaEventDestroy(c->pipe.copied[b]);
+    }
+    if (c->pipe.copy) cudaStreamDestroy(c->pipe.copy);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->own) cudaStreamDestroy(c->own);
@@ -865,26 +872,25 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
   size_t first = (size_t(32) << 20) / row_bytes;
   if (first < 8) first = 8;
   if (first > chunk) first = chunk;
-  cudaStream_t copy = nullptr;
-  gk_c128* dz[2] = {nullptr, nullptr};
-  cudaEvent_t filled[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
-  auto cleanup = [&] {
-    if (copy) cudaStreamSynchronize(copy);
+  HostFillPipe& P = c->pipe;
+  auto cleanup = [&] {  // leave both streams idle; the pipe itself is kept
+    if (P.copy) cudaStreamSynchronize(P.copy);
     cudaStreamSynchronize(c->stream);
-    for (int b = 0; b < 2; ++b) {
-      if (dz[b]) cudaFreeAsync(dz[b], c->stream);
-      if (filled[b]) cudaEventDestroy(filled[b]);
-      if (copied[b]) cudaEventDestroy(copied[b]);
-    }
-    if (copy) cudaStreamDestroy(copy);
   };
   try {
-    GK_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
-      GK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dz[b]), chunk * row_bytes, c->stream));
-      GK_CUDA(cudaEventCreateWithFlags(&filled[b], cudaEventDisableTiming));
-      GK_CUDA(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+    if (!P.copy) {
+      GK_CUDA(cudaStreamCreateWithFlags(&P.copy, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        GK_CUDA(cudaEventCreateWithFlags(&P.filled[b], cudaEventDisableTiming));
+        GK_CUDA(cudaEventCreateWithFlags(&P.copied[b], cudaEventDisableTiming));
+      }
     }
+    for (int b = 0; b < 2; ++b)
+      if (P.buf[b].n < chunk * nt) P.buf[b].alloc(chunk * nt, c->stream);
+    cudaStream_t copy = P.copy;
+    gk_c128* dz[2] = {P.buf[0].p, P.buf[1].p};
+    cudaEvent_t* filled = P.filled;
+    cudaEvent_t* copied = P.copied;
     unsigned long long* cnt = c->scratch.p + 16;
     GK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));

@@ -56,6 +56,14 @@ struct DevBuf {
 
 }  // namespace gk
 
+// gk_fill_rows_host's double-buffered fill -> D2H pipeline, kept by the
+// context across calls (no per-call stream / event / buffer churn)
+struct HostFillPipe {
+  cudaStream_t copy = nullptr;
+  cudaEvent_t filled[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+  gk::DevBuf<gk_c128> buf[2];
+};
+
 struct gk_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -65,6 +73,7 @@ struct gk_ctx {
   gk::DevBuf<double2> phase;               // direct-mode phase table (kPhaseM)
   gk::DevBuf<double2> phase_small;         // eval_batch phase table (kPhaseSmall, L1-resident)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  HostFillPipe pipe;
 };
 
 struct gk_table {

@@ -38,3 +38,16 @@ for b in range(0, N, rows_win):
     gk.fill_rows_host(dm, gk.Mode.DIRECT, z, k=2*np.pi/0.15, row_begin=b, row_end=min(N, b + rows_win))
 dt = time.perf_counter() - t
 print(f"fill_rows_host x26: {dt:.3f} s = {N*N*16/dt/1e9:.1f} GB/s")
+
+# the pure copy again, with a C5 direct fill running concurrently on another stream
+zdev = torch.empty((8192, N), dtype=torch.complex128, device="cuda")
+fs = torch.cuda.Stream()
+with torch.cuda.stream(fs):
+    ctx.bind_stream(fs)
+    for b in range(0, 6):
+        gk.fill_rows(dm, gk.Mode.DIRECT, k=2*np.pi/0.15, row_begin=0, row_end=8192, out=zdev,
+                     report=False)
+t = time.perf_counter(); tot = pure(); dt = time.perf_counter() - t
+torch.cuda.synchronize()
+ctx.bind_stream()
+print(f"pure D2H beside a running fill: {tot/1e9:.1f} GB in {dt:.3f} s = {tot/dt/1e9:.1f} GB/s")
