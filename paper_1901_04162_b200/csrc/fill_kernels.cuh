@@ -534,7 +534,7 @@ __device__ __forceinline__ void table_tile(const FillArgs& A, const TableWin& wi
       const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
       const double r = __dmul_rn(d2, rsqrt_fast(d2));
       double2 ve = make_double2(0.0, 0.0), vg = make_double2(0.0, 0.0);
-      win_eval<SMEM, DEG, WANT_E, WANT_G>(r, A.T, win, ve, vg);
+      win_eval<SMEM, DEG, WANT_E, WANT_G>(r, A.T, win, ve, vg, vc && !self);
       const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
       if (__any_sync(0xffffffffu, oob)) {
         if (oob) {

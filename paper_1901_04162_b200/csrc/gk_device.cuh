@@ -206,14 +206,17 @@ __device__ __forceinline__ T win_ld(const T* p) {
   else return __ldg(p);
 }
 
+// used: the lane's value is kept (a valid, non-self pair) -- padding and self
+// lanes also evaluate, their radii may lie outside the tile's window and
+// their (clamped, meaningless) values are discarded
 template <bool SMEM>
 __device__ __forceinline__ uint32_t win_locate(double r, const TableDev& t, const TableWin& w,
-                                               int grs, double& aj) {
+                                               int grs, double& aj, bool used = true) {
   uint32_t b = lookup_bucket(r, t) - w.b0;
-  GK_DASSERT(!SMEM || b < w.nb || !(r >= t.r_min && r <= t.r_max));  // window covers the tile
+  GK_DASSERT(!SMEM || !used || b < w.nb || !(r >= t.r_min && r <= t.r_max));  // window covers
   b = b < w.nb ? b : w.nb - 1;
   uint32_t base = win_ld<SMEM>(w.lk + b) - w.j0;
-  GK_DASSERT(!SMEM || base < w.nj || !(r >= t.r_min && r <= t.r_max));
+  GK_DASSERT(!SMEM || !used || base < w.nj || !(r >= t.r_min && r <= t.r_max));
   base = base < w.nj ? base : w.nj - 1;
   const double2 ab = win_ld<SMEM>(reinterpret_cast<const double2*>(w.grec + static_cast<size_t>(base) * grs));
   const bool hi = r >= ab.y;
@@ -225,11 +228,11 @@ __device__ __forceinline__ uint32_t win_locate(double r, const TableDev& t, cons
 // Green (degree DEG, or runtime degree for DEG = 0), Exp, or both for one r
 template <bool SMEM, int DEG, bool WANT_E, bool WANT_G>
 __device__ __forceinline__ void win_eval(double r, const TableDev& t, const TableWin& w,
-                                         double2& e, double2& g) {
+                                         double2& e, double2& g, bool used = true) {
   const int grs = DEG > 0 ? 2 + 2 * (DEG + 1) : t.grs;
   const int deg = DEG > 0 ? DEG : t.degree;
   double aj;
-  const uint32_t j = win_locate<SMEM>(r, t, w, grs, aj);
+  const uint32_t j = win_locate<SMEM>(r, t, w, grs, aj, used);
   const double u = r - aj;
   if constexpr (WANT_E) {
     const double2* ce = reinterpret_cast<const double2*>(w.erec + static_cast<size_t>(j) * 6 + 2);
