@@ -313,3 +313,13 @@ def test_accumulate_batch_vs_reference(gk, oracle, ref):
         gk.accumulate_batch(gk.KernelKind.GreenOverR, bad, w, k=k)
     empty, fbe = gk.accumulate_batch(gk.KernelKind.GreenOverR, np.zeros((0, 4)), np.zeros((0, 4)), k=k)
     assert empty.numel() == 0 and fbe == 0
+
+
+def test_wire_format_write_errors(gk, tmp_path):
+    """io.hpp's writers throw runtime_error on an unwritable path; so do ours."""
+    t = gk.DeviceTable(gk.SamplingConfig())
+    bad = str(tmp_path / "missing_dir" / "x.gktb")
+    with pytest.raises(gk.RuntimeErrorGk):
+        t.dump_table_binary(gk.KernelKind.GreenOverR, bad)
+    with pytest.raises(gk.RuntimeErrorGk):
+        t.dump_plan_csv(str(tmp_path / "missing_dir" / "plan.csv"))
