@@ -146,6 +146,36 @@ void launch_max_vertex_d2(const double* verts, size_t nv, unsigned long long* d2
   GK_CUDA(cudaGetLastError());
 }
 
+// arithmetic locate (TableDev::coarse): for run c, base points 64 c .. 64 c + 64
+// (r_min + i t_eff, this unit has no FMA contraction, so the values are the
+// plan's bits) must be consecutive plan nodes; verified by exact search
+__global__ void coarse_runs_kernel(const double* __restrict__ absc, size_t n, double r_min,
+                                   double t_eff, uint32_t ncoarse, int32_t* __restrict__ coarse) {
+  const size_t c = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (c >= ncoarse) return;
+  long long first = -1;
+  for (int k = 0; k <= 64; ++k) {
+    const long long i = static_cast<long long>(c) * 64 + k;
+    const double a = r_min + static_cast<double>(i) * t_eff;
+    size_t lo = 0, hi = n;  // lower bound of a
+    while (lo < hi) {
+      const size_t mid = (lo + hi) / 2;
+      if (absc[mid] < a) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo >= n || absc[lo] != a) {
+      coarse[c] = -1;
+      return;
+    }
+    if (k == 0) first = static_cast<long long>(lo);
+    else if (static_cast<long long>(lo) != first + k) {
+      coarse[c] = -1;
+      return;
+    }
+  }
+  coarse[c] = static_cast<int32_t>(first - static_cast<long long>(c) * 64);
+}
+
 // ---------------------------------------------------------- plan (K2)
 
 struct PlanScalars {
@@ -729,6 +759,23 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
   absc.p = nullptr;
   absc.n = 0;
 
+  // arithmetic-locate runs: whole runs strictly inside the base grid (the last
+  // base interval ends at r_max itself and is left to the lookup path)
+  {
+    const long long runs = (S.steps - 1) / 64;
+    d.ncoarse = runs > 0 && runs < (1LL << 26) ? static_cast<uint32_t>(runs) : 0u;
+    d.t_eff = S.t_eff;
+    d.inv_t = 1.0 / S.t_eff;
+    if (d.ncoarse) {
+      t->coarse.alloc(d.ncoarse, st);
+      coarse_runs_kernel<<<grid_for(d.ncoarse, 128), 128, 0, st>>>(absc.p ? absc.p : t->absc.p, n,
+                                                                   S.r_min, S.t_eff, d.ncoarse,
+                                                                   t->coarse.p);
+      count_launches(1);
+      GK_CUDA(cudaGetLastError());
+    }
+    d.coarse = t->coarse.p;
+  }
   d.grec = t->grec.p;
   d.erec = t->erec.p;
   d.lk = t->lk.p;

@@ -79,6 +79,7 @@ void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n,
   const unsigned g = static_cast<unsigned>(grid);
   TableDev T{};
   if (t) T = t->dev;
+  if (!table_arith_enabled()) T.ncoarse = 0;
   if (!t && k_im == 0.0 && fast_eval())
     eval_batch_kernel<KIND, false, 0, true><<<g, 256, 0, ctx->stream>>>(
         r, n, out, T, k_re, k_im, w, ctx->phase_small.p, k_re * kPhaseSmall / (2.0 * kPi));
@@ -202,6 +203,7 @@ void launch_accumulate_kind(gk_ctx* ctx, const gk_table* t, const double* r, con
   const unsigned g = static_cast<unsigned>(grid);
   TableDev T{};
   if (t) T = t->dev;
+  if (!table_arith_enabled()) T.ncoarse = 0;
   const double K1s = k_re * kPhaseSmall / (2.0 * kPi);
   const double2* ptab = ctx->phase_small.p;
   if (!t && k_im == 0.0 && fast_eval())

@@ -39,6 +39,7 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.z2 = reinterpret_cast<double2*>(z2);
   a.ldz = ldz;
   if (table) a.T = table->dev;
+  if (!table_arith_enabled()) a.T.ncoarse = 0;
   a.phase = ctx->phase.p;
   a.K1 = k_re * kPhaseM / (2.0 * kPi);
   a.k_re = k_re;

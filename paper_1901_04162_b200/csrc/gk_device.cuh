@@ -74,6 +74,12 @@ struct TableDev {
   int degree;
   int grs;  // Green record stride in doubles = 2 + 2 (degree + 1)
   double k_re, k_im;
+  // arithmetic locate on the uniform base grid (arith_locate): base point i is
+  // r_min + i t_eff; coarse[c] = plan index - i for the 65 base points
+  // 64 c .. 64 c + 64 when they are consecutive plan nodes, else -1
+  const int32_t* coarse;
+  uint32_t ncoarse;  // 0: off
+  double t_eff, inv_t;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -105,8 +111,49 @@ __device__ __forceinline__ uint32_t lookup_bucket(double r, const TableDev& t) {
 }
 
 // interval index of r (table.hpp:87-102 semantics, sentinel at r_max)
+// base point i of the plan's uniform grid, rounded like build_plan
+// (sampling.hpp:167, no contraction)
+__device__ __forceinline__ double base_point(const TableDev& t, long long i) {
+  return __dadd_rn(t.r_min, __dmul_rn(static_cast<double>(i), t.t_eff));
+}
+
+// Interval of r by arithmetic where r lies in a verified run of consecutive
+// base-grid nodes (away from the refinement windows around zeros): no lookup
+// bucket and no record header are read.  Returns false where the run
+// structure does not hold (the caller takes the lookup path); when it
+// returns true, j and a_j equal the lookup path's exactly.
+__device__ __forceinline__ bool arith_locate(double r, const TableDev& t, uint32_t& j,
+                                             double& aj) {
+  if (t.ncoarse == 0 || !(r >= t.r_min)) return false;
+  long long i = static_cast<long long>((r - t.r_min) * t.inv_t);  // guess, exact after the fix
+  const long long imax = static_cast<long long>(t.ncoarse) * 64;
+  if (i >= imax) return false;
+  double a0 = base_point(t, i), a1 = base_point(t, i + 1);
+  if (r < a0) {
+    if (i == 0) return false;
+    --i;
+    a1 = a0;
+    a0 = base_point(t, i);
+  } else if (r >= a1) {
+    ++i;
+    if (i >= imax) return false;
+    a0 = a1;
+    a1 = base_point(t, i + 1);
+  }
+  if (!(a0 <= r && r < a1)) return false;
+  const int32_t off = __ldg(t.coarse + (i >> 6));
+  if (off < 0) return false;
+  j = static_cast<uint32_t>(i + off);
+  aj = a0;
+  return true;
+}
+
 __device__ __forceinline__ uint32_t locate_interval(double r, const TableDev& t,
                                                     const double* grec, int grs, double& aj) {
+  {
+    uint32_t j;
+    if (arith_locate(r, t, j, aj)) return j;
+  }
   const uint32_t base = __ldg(t.lk + lookup_bucket(r, t));
   GK_DASSERT(base < t.nrec);
   const double2 ab = __ldg(reinterpret_cast<const double2*>(grec + static_cast<size_t>(base) * grs));
@@ -212,6 +259,10 @@ __device__ __forceinline__ T win_ld(const T* p) {
 template <bool SMEM>
 __device__ __forceinline__ uint32_t win_locate(double r, const TableDev& t, const TableWin& w,
                                                int grs, double& aj, bool used = true) {
+  if constexpr (!SMEM) {  // in shared memory the lookup is cheaper than the arithmetic
+    uint32_t j;
+    if (arith_locate(r, t, j, aj) && j - w.j0 < w.nj) return j - w.j0;
+  }
   uint32_t b = lookup_bucket(r, t) - w.b0;
   GK_DASSERT(!SMEM || !used || b < w.nb || !(r >= t.r_min && r <= t.r_max));  // window covers
   b = b < w.nb ? b : w.nb - 1;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -85,6 +86,7 @@ struct gk_table {
   gk::DevBuf<uint32_t> hash;  // reference-format buckets (table.hpp:40-82)
   gk::DevBuf<double> grec, erec;
   gk::DevBuf<uint32_t> lk;
+  gk::DevBuf<int32_t> coarse;  // arithmetic-locate runs (TableDev::coarse)
   std::vector<double> zeros;  // zero_locations (host copy)
 };
 
@@ -102,6 +104,13 @@ struct gk_mesh {
 };
 
 namespace gk {
+
+// GK_TABLE_ARITH=0: table lookups without the arithmetic-locate fast path
+// (A/B and tests; read per launch)
+inline bool table_arith_enabled() {
+  const char* e = std::getenv("GK_TABLE_ARITH");
+  return !(e && e[0] == '0');
+}
 
 // launch accounting (gk_launch_count)
 void count_launches(unsigned long long n);

@@ -462,3 +462,35 @@ def test_fill_rows_rejects_bad_output(gk):
                 torch.empty((dm.N, dm.N), dtype=torch.complex128)):
         with pytest.raises(gk.InvalidArgument):
             gk.fill_rows(dm, gk.Mode.DIRECT, k=1.0, out=bad)
+
+
+@pytest.mark.parametrize("S,refine", [(1000, True), (10000, True), (300, True), (1000, False)])
+def test_table_arithmetic_locate_bit_identical(gk, monkeypatch, S, refine):
+    """The arithmetic interval index on verified runs of the uniform base grid
+    (TableDev::coarse) gives exactly the lookup path's bits: fills through the
+    staged, L1 and global-fallback paths and eval_batch, with GK_TABLE_ARITH on
+    and off."""
+    import torch
+    mesh = sphere(gk, 3)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S,
+                                         refine=refine), gk.Medium(lambda0=0.3))
+    r = torch.linspace(lo, hi, 200001, dtype=torch.float64, device="cuda:0")
+    out = {}
+    for arith in ("1", "0"):
+        monkeypatch.setenv("GK_TABLE_ARITH", arith)
+        res = []
+        for smem in ("0", "2", None):
+            if smem is None:
+                monkeypatch.delenv("GK_TABLE_SMEM", raising=False)
+            else:
+                monkeypatch.setenv("GK_TABLE_SMEM", smem)
+            ze, zg, rep = gk.fill_rows_pair(dm, gk.Mode.TABLE, table=t, row_begin=100, row_end=300)
+            res += [ze, zg]
+        monkeypatch.delenv("GK_TABLE_SMEM", raising=False)
+        res.append(t.eval_batch(gk.KernelKind.GreenOverR, r))
+        res.append(t.eval_batch(gk.KernelKind.PlainExp, r))
+        out[arith] = res
+    for a, b in zip(out["1"], out["0"]):
+        assert torch.equal(a, b)
