@@ -145,6 +145,7 @@ __device__ __forceinline__ bool arith_locate(double r, const TableDev& t, uint32
   if (off < 0) return false;
   j = static_cast<uint32_t>(i + off);
   aj = a0;
+  GK_DASSERT(j + 1 < t.nrec);  // a run never reaches the r_max sentinel
   return true;
 }
 
