@@ -56,12 +56,6 @@ constexpr int kPhaseLog2 = 13;
 constexpr double kPhaseD = kPi / kPhaseM;
 constexpr double kCosMinimax = -0.5 + (1.4142135623730951 - 1.0) / 12.0 * kPhaseD * kPhaseD;
 
-// read-only double4 load (two 16 B loads; __ldg has no double4 overload)
-__device__ __forceinline__ double4 ldg4(const double4* p) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-  return make_double4(a.x, a.y, b.x, b.y);
-}
 
 struct TableDev {
   const double* grec;  // Green interval records
@@ -406,11 +400,6 @@ __device__ __forceinline__ double atten_table(double r, double KA, const double*
   return __dmul_rn(E[idx], p);
 }
 
-// exp(-j k r) as (re, im)
-__device__ __forceinline__ double2 expmjkr_phase(double r, double K1, const double2* tab) {
-  const double2 cs = cis_phase(r, K1, tab);
-  return make_double2(cs.x, -cs.y);
-}
 
 // reference-accuracy direct kernel via libdevice sincos (the accuracy oracle
 // on the device side and the fallback of the table path, evaluator.hpp:199-205)
