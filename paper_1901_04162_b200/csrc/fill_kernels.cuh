@@ -475,6 +475,9 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 // the global table through L1 instead (correct either way: same code path,
 // different TableWin).
 
+#ifndef GK_STAGED_CPT
+#define GK_STAGED_CPT 2  // 32-column blocks per staged tile (windowed mode)
+#endif
 #ifndef GK_STAGED_WARPS
 #define GK_STAGED_WARPS 16
 #endif
@@ -778,8 +781,8 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
       S.lk_cap = static_cast<uint32_t>(((budget - j_cap * rec_bytes) / 4) & ~size_t(3));
       set_tiling(ctx, a, kStagedWarps, 1);
       // narrow tiles keep each tile's radius window small
-      a.cpt = 2;
-      a.ncb = (a.N + 63) / 64;
+      a.cpt = GK_STAGED_CPT;
+      a.ncb = (a.N + 32 * GK_STAGED_CPT - 1) / (32 * GK_STAGED_CPT);
       a.ntiles = ((a.row_end - a.row_begin + kStagedWarps - 1) / kStagedWarps) * a.ncb;
     }
     const size_t smem = static_cast<size_t>(S.lk_cap) * 4 + static_cast<size_t>(S.j_cap) * rec_bytes;
