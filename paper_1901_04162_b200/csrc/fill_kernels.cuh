@@ -475,6 +475,9 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 // the global table through L1 instead (correct either way: same code path,
 // different TableWin).
 
+#ifndef GK_TILES_PER_CTA
+#define GK_TILES_PER_CTA 16  // set_tiling: widest tiles leaving this many per resident CTA
+#endif
 #ifndef GK_STAGED_CPT
 #define GK_STAGED_CPT 2  // 32-column blocks per staged tile (windowed mode)
 #endif
@@ -703,7 +706,7 @@ void launch_kernel(gk_ctx* ctx, K kernel, const FillArgs& a, size_t smem, int th
 inline void set_tiling(const gk_ctx* ctx, FillArgs& a, int rows_per_tile, int ctas_per_sm) {
   const size_t row_blocks = (a.row_end - a.row_begin + rows_per_tile - 1) / rows_per_tile;
   const size_t col_blocks = (a.N + 31) / 32;
-  const size_t want = static_cast<size_t>(ctx->sm_count) * ctas_per_sm * 16;
+  const size_t want = static_cast<size_t>(ctx->sm_count) * ctas_per_sm * GK_TILES_PER_CTA;
   int cpt = kMaxColBlocks;
   while (cpt > 1 && row_blocks * ((col_blocks + cpt - 1) / cpt) < want) cpt /= 2;
   a.cpt = cpt;
