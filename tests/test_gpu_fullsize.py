@@ -4,10 +4,11 @@ A full C5 matrix is 107 GB and ~4.8e11 evaluations: too large for a CPU
 check, but every row is independent (matfill.hpp:169-203).  So each config
 is filled on the device for three 2-row blocks (first, middle and last rows)
 against the FULL mesh.  The same rows are computed on the CPU by
- * the reference itself (oracle/_ref, AnalyticKernel through the reference's
-   own staging loop: gr_fill_sampled_rows) for direct mode, real k;
+ * the reference itself (oracle/_ref: AnalyticKernel / TableKernel through
+   the reference's own staging loop, gr_fill_sampled_rows; the table built by
+   the reference's KernelEvaluator on the device table's own plan), real k;
  * the oracle (pinned bitwise to the reference, test_oracle_vs_ref.py) for
-   complex k (C4) and for table mode on the device table's own plan.
+   complex k (C4), where the reference has no path.
 Tolerance: the per-entry bound B_pq of tests/test_gpu_fill.py.
 """
 import math
@@ -114,3 +115,28 @@ def test_row_blocks_tile_the_full_matrix_checksum(gk, case):
         assert torch.equal(part, full[b:e])
     assert torch.all(torch.diagonal(full) == 0)
     assert math.isfinite(float(full.abs().sum()))
+
+
+@pytest.mark.parametrize("S", [1000, 10000])
+def test_table_fullsize_vs_reference_itself(gk, oracle, ref, case, S):
+    """Real-k configs: the device table fill against the reference's own
+    TableKernel fill (fill_sampled_rows through KernelEvaluator, built on the
+    device table's plan) -- not only the pinned oracle."""
+    name, c, mesh, med, dm = case
+    kc = complex(gk.wavenumber(med))
+    if kc.imag != 0.0:
+        pytest.skip("the reference is real-k only (kernel.hpp:23-24)")
+    m, n, N = c["m"], c["n"], mesh.triangle_count()
+    lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S), med)
+    d = t.download()
+    plan = oracle.make_plan(d["abscissae"], d["zeros"])
+    rev = ref.evaluator(plan, kc.real)
+    for rb, re in _row_blocks(N):
+        z, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t, row_begin=rb, row_end=re)
+        want, calls, _ = ref.fill_sampled_rows(mesh.vertices, mesh.triangles, m, n, TABLE,
+                                               kc.real, np.arange(rb, re), ev=rev, threads=8)
+        B_d = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, None, abs(kc), ULPS,
+                                  row_begin=rb, row_end=re)
+        assert np.all(np.abs(z.cpu().numpy() - want) <= B_d), (name, S, rb)
+        assert calls == rep.actual_calls
