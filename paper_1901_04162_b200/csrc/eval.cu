@@ -63,6 +63,10 @@ __global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
   }
 }
 
+#ifndef GK_EVAL_BLOCKS_PER_SM
+#define GK_EVAL_BLOCKS_PER_SM 32  // eval_batch grid cap (blocks of 256 per SM)
+#endif
+
 // GK_EVAL_LIBDEVICE=1: eval_batch through libdevice sincos (A/B, tests)
 static bool fast_eval() {
   const char* e = std::getenv("GK_EVAL_LIBDEVICE");
@@ -73,7 +77,7 @@ template <int KIND>
 void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, double2* out,
                       double k_re, double k_im, unsigned long long* w) {
   size_t grid = (n + 255) / 256;
-  const size_t cap = static_cast<size_t>(ctx->sm_count) * 32;
+  const size_t cap = static_cast<size_t>(ctx->sm_count) * GK_EVAL_BLOCKS_PER_SM;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   const unsigned g = static_cast<unsigned>(grid);
