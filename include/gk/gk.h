@@ -76,6 +76,10 @@ typedef struct gk_fill_report {
   int m, n;
   uint64_t predicted_calls, actual_calls, fallback_calls;
   double wall_time_s; /* device time of the fill kernels (CUDA events) */
+  /* kernel evaluations the device performed for these entries: actual_calls,
+     or fewer where the direct fill evaluates each shared edge of a closed
+     mesh once for both of its triangles (K4e) */
+  uint64_t evaluations;
 } gk_fill_report;
 
 typedef struct gk_table_info {
@@ -207,6 +211,20 @@ gk_status gk_mesh_create(gk_ctx* ctx, const double* vertices, size_t nv,
 /* host copies: outer[4][nt*m] (x,y,z,w planes), inner[4][nt*3n] */
 gk_status gk_mesh_points_download(const gk_mesh* mesh, double* outer, double* inner);
 gk_status gk_mesh_destroy(gk_mesh* mesh);
+
+/* Shared-edge blocks of a mesh (no reference counterpart: the direct fill's
+   evaluation-sharing structure, DESIGN.md §5 K4e).  blocks = 0 when the mesh
+   was created with GK_EDGE=0. */
+typedef struct gk_mesh_edge_info {
+  uint64_t blocks, edge_slots; /* evaluated edge slots incl. warp padding */
+  double work_ratio;           /* edge_slots / (3 nt): far-tile work vs the reference */
+  double delta;                /* max |point - reversed-edge point| over shared sides */
+  double r_far;                /* the shared points serve tiles at least this far apart */
+  uint64_t edges;              /* distinct edges summed over blocks (no padding) */
+  double rho_mean;             /* mean bounding radius of a block */
+  int ordered;                 /* 1: blocks follow a spatial (bisection) order of the triangles */
+} gk_mesh_edge_info;
+gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out);
 
 /* K1: min and max quadrature-point pair distance over observation rows
    [row_begin,row_end) and every source q != p (replaces max_vertex_distance

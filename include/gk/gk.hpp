@@ -98,6 +98,7 @@ struct FillReport {
   double wall_time_s = 0.0;
   double max_rel_re = 0.0, max_rel_im = 0.0;
   double speedup = 0.0, analytic_time_s = 0.0, interp_time_s = 0.0, table_build_s = 0.0;
+  std::uint64_t evaluations = 0;  // device evaluations (<= actual_calls: shared edges)
   static FillReport from(const gk_fill_report& r) {
     FillReport f;
     f.N = static_cast<std::size_t>(r.N);
@@ -107,6 +108,7 @@ struct FillReport {
     f.actual_calls = r.actual_calls;
     f.fallback_calls = r.fallback_calls;
     f.wall_time_s = r.wall_time_s;
+    f.evaluations = r.evaluations;
     return f;
   }
 };

@@ -72,7 +72,8 @@ class SamplingConfigC(C.Structure):
 class FillReportC(C.Structure):
     _fields_ = [("N", C.c_uint64), ("m", C.c_int), ("n", C.c_int),
                 ("predicted_calls", C.c_uint64), ("actual_calls", C.c_uint64),
-                ("fallback_calls", C.c_uint64), ("wall_time_s", C.c_double)]
+                ("fallback_calls", C.c_uint64), ("wall_time_s", C.c_double),
+                ("evaluations", C.c_uint64)]
 
 
 class SweepReportC(C.Structure):
@@ -126,6 +127,7 @@ PROTOTYPES = {
     "gk_mesh_create": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.POINTER(_vp)],
     "gk_mesh_points_download": [_vp, _vp, _vp],
     "gk_mesh_destroy": [_vp],
+    "gk_mesh_edge_info_get": [_vp, _vp],
     "gk_distance_range": [_vp, _vp, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_fill_rows": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_double, C.c_size_t,
                      C.c_size_t, _vp, C.c_size_t, C.POINTER(FillReportC)],

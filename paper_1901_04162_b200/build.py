@@ -35,6 +35,7 @@ SOURCES = {
     "eval.cu": [],
     "abi.cu": [],
     "host.cpp": [],
+    "edges.cu": [],
 }
 HEADERS = ["gk_device.cuh", "gk_internal.h", "fill_kernels.cuh"]
 

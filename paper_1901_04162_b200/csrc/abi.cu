@@ -695,12 +695,27 @@ gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32
       GK_CUDA(cudaMemcpyAsync(mesh->verts.p, verts, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, c->stream));
       GK_CUDA(cudaMemcpyAsync(dt.p, tris, 3 * nt * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
       gk::launch_points(mesh, mesh->verts.p, dt.p, c->stream);
+      gk::build_edge_blocks(mesh, verts, tris);
       GK_CUDA(cudaStreamSynchronize(c->stream));
     } catch (...) {
       delete mesh;
       throw;
     }
     *out = mesh;
+  });
+}
+
+gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out) {
+  return guarded([&] {
+    need(mesh != nullptr && out != nullptr, GK_ERR_INVALID_ARGUMENT, "null argument");
+    out->blocks = mesh->nblk;
+    out->edge_slots = mesh->nblk ? mesh->ep.n / static_cast<size_t>(mesh->n) : 0;
+    out->work_ratio = mesh->edge_ratio;
+    out->delta = mesh->edge_delta;
+    out->r_far = mesh->r_far;
+    out->edges = mesh->edges;
+    out->rho_mean = mesh->rho_mean;
+    out->ordered = mesh->ordered ? 1 : 0;
   });
 }
 
@@ -788,13 +803,14 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
   // == NULL) accumulate in the context until gk_fill_check reads them
   unsigned long long* cnt = c->scratch.p + (report ? 16 : kAsyncFillCounters);
   if (report) {
-    GK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), c->stream));
+    GK_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
   }
-  gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, z2, ldz, cnt);
+  const bool counted =
+      gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, z2, ldz, cnt);
   if (!report) return;
   GK_CUDA(cudaEventRecord(c->ev1, c->stream));
-  unsigned long long h[3];
+  unsigned long long h[4];
   GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   GK_CUDA(cudaStreamSynchronize(c->stream));
   float ms = 0.f;
@@ -807,6 +823,7 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
   report->actual_calls = kinds * 3ull * mesh->m * mesh->n * rows * (mesh->N - 1);
   report->fallback_calls = h[0] + h[1];
   report->wall_time_s = ms * 1e-3;
+  report->evaluations = counted ? h[3] : report->actual_calls;
   raise_fill_errors(h);
 }
 
@@ -817,7 +834,7 @@ gk_status gk_fill_check(gk_ctx* c, uint64_t* fallbacks) {
     check_ctx(c);
     use_device(c);
     unsigned long long* cnt = c->scratch.p + kAsyncFillCounters;
-    unsigned long long h[3];
+    unsigned long long h[4];
     GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     GK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(h), c->stream));
     GK_CUDA(cudaStreamSynchronize(c->stream));
@@ -892,14 +909,15 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
     cudaEvent_t* filled = P.filled;
     cudaEvent_t* copied = P.copied;
     unsigned long long* cnt = c->scratch.p + 16;
-    GK_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(unsigned long long), c->stream));
+    GK_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
     size_t idx = 0, step = first;
+    bool counted = false;
     for (size_t rb = row_begin; rb < row_end; rb += step, step = std::min(chunk, 2 * step), ++idx) {
       const size_t re = rb + step < row_end ? rb + step : row_end;
       const int b = static_cast<int>(idx & 1);
       if (idx >= 2) GK_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
-      gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt, cnt);
+      counted = gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt, cnt);
       GK_CUDA(cudaEventRecord(filled[b], c->stream));
       GK_CUDA(cudaStreamWaitEvent(copy, filled[b], 0));
       if (ldz == nt)  // contiguous rows on both sides: one linear copy
@@ -911,7 +929,7 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       GK_CUDA(cudaEventRecord(copied[b], copy));
     }
     GK_CUDA(cudaEventRecord(c->ev1, c->stream));
-    unsigned long long h[3];
+    unsigned long long h[4];
     GK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     GK_CUDA(cudaStreamSynchronize(copy));
     GK_CUDA(cudaStreamSynchronize(c->stream));
@@ -925,6 +943,7 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       report->actual_calls = 3ull * mesh->m * mesh->n * (row_end - row_begin) * (nt - 1);
       report->fallback_calls = h[0] + h[1];
       report->wall_time_s = ms * 1e-3;
+      report->evaluations = counted ? h[3] : report->actual_calls;
     }
     raise_fill_errors(h);
   } catch (...) {

@@ -1,0 +1,348 @@
+// edges.cu -- shared-edge blocks for the direct fill (direct_edge_kernel).
+//
+// The reference evaluates, for every source triangle q, the n Gauss points of
+// each of its 3 edges (inner_points, matfill.hpp:132-144) against every outer
+// point of p (fill_rows, matfill.hpp:185-198).  On a closed mesh every edge
+// belongs to two triangles, traversed in opposite directions, so the same n
+// points (up to the rounding of a + (b - a) x vs b + (a - b) x', with the
+// Gauss-Legendre weights symmetric, quadrature.hpp:85-110) are evaluated
+// twice per outer point.  A block groups a contiguous range of source
+// triangles; each distinct edge of the block is evaluated once per outer
+// point, in the orientation of the first block triangle that uses it (those
+// points are copied from the reference-exact inner points, so they are
+// bit-identical for that triangle), and Z[p][q] is the sum of q's three edge
+// sums.
+//
+// Parity: the other triangle's points differ from the evaluated ones by at
+// most `edge_delta` (measured here on the device points).  For a term with
+// weight w and distance r the value moves by at most |w| delta (1 + |k| r) /
+// r^2, i.e. delta / (64 u r) of the stated per-term tolerance
+// |w| 64 u (1 + |k| r) / r (u = 2^-53).  The kernel uses the
+// shared points only where every pair of the (row, block) tile is at least
+// r_far = delta / (32 u) apart -- at most half the tolerance -- and the
+// reference's own per-triangle points everywhere else.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "gk_internal.h"
+
+namespace gk {
+
+namespace {
+
+// owner slot code: (t << 3) | (side << 1) | pad
+__global__ void edge_gather_kernel(const double4* __restrict__ inner, size_t N, int n,
+                                   const unsigned long long* __restrict__ owner, size_t nslots,
+                                   double4* __restrict__ ep) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i >= nslots * n) return;
+  const size_t slot = i / n;
+  const int g = static_cast<int>(i - slot * n);
+  const unsigned long long o = owner[slot];
+  const size_t t = static_cast<size_t>(o >> 3);
+  const int s = static_cast<int>((o >> 1) & 3);
+  double4 P = inner[static_cast<size_t>(s * n + g) * N + t];
+  if (o & 1) P.w = 0.0;  // padding lane: a real point of the block, zero weight
+  ep[((slot >> 5) * n + g) * 32 + (slot & 31)] = P;
+}
+
+// max over the sides (t, s) that do not own their edge slot of
+// |inner point g of (t, s) - evaluated point n-1-g of the slot| (the reversed
+// parameterisation pairs g with n-1-g; the weights are equal)
+__global__ void edge_delta_kernel(const double4* __restrict__ inner, size_t N, int n,
+                                  const uint32_t* __restrict__ gslot,
+                                  const unsigned long long* __restrict__ owner,
+                                  const double4* __restrict__ ep, unsigned long long* dmax) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  double d = 0.0;
+  if (i < 3 * N * static_cast<size_t>(n)) {
+    const size_t ts = i / n;
+    const int g = static_cast<int>(i - ts * n);
+    const size_t t = ts / 3;
+    const int s = static_cast<int>(ts - 3 * t);
+    const uint32_t slot = gslot[ts];
+    const unsigned long long mine = (static_cast<unsigned long long>(t) << 3) | (s << 1);
+    if (owner[slot] != mine) {
+      const double4 P = inner[static_cast<size_t>(s * n + g) * N + t];
+      const double4 Q = ep[((slot >> 5) * static_cast<size_t>(n) + (n - 1 - g)) * 32 + (slot & 31)];
+      const double dx = P.x - Q.x, dy = P.y - Q.y, dz = P.z - Q.z;
+      d = sqrt(dx * dx + dy * dy + dz * dz);
+      if (P.w != Q.w) d = INFINITY;  // weights must match exactly (symmetric rule)
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
+  if ((threadIdx.x & 31) == 0 && d > 0.0) atomicMax(dmax, __double_as_longlong(d));
+}
+
+}  // namespace
+
+void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris) {
+  const size_t N = mesh->N, nv = mesh->nv;
+  const int n = mesh->n;
+  mesh->nblk = 0;
+  mesh->edge_ratio = 1.0;
+  mesh->r_far = INFINITY;
+  if (const char* e = std::getenv("GK_EDGE"))
+    if (e[0] == '0') return;
+  size_t cap = 32 * kEdgeChunksDefault;
+  if (const char* e = std::getenv("GK_EDGE_CHUNKS")) {  // block size (tests, A/B)
+    const long c = std::atol(e);
+    if (c >= 1 && c * 32 <= kEdgeCap) cap = static_cast<size_t>(c) * 32;
+  }
+  mesh->ecap = static_cast<int>(cap);
+  if (N > (size_t(1) << 30)) return;
+
+  // global edge ids: edges bucketed by their lower vertex (CSR), distinct
+  // upper vertices numbered within each bucket
+  std::vector<uint32_t> start(nv + 1, 0);
+  for (size_t t = 0; t < N; ++t)
+    for (int s = 0; s < 3; ++s) {
+      const uint32_t a = tris[3 * t + s], b = tris[3 * t + (s + 1) % 3];
+      ++start[std::min(a, b) + 1];
+    }
+  for (size_t v = 0; v < nv; ++v) start[v + 1] += start[v];
+  std::vector<uint32_t> fillp(start.begin(), start.end() - 1), hi(3 * N), side_of(3 * N);
+  for (size_t t = 0; t < N; ++t)
+    for (int s = 0; s < 3; ++s) {
+      const uint32_t a = tris[3 * t + s], b = tris[3 * t + (s + 1) % 3];
+      const uint32_t slot = fillp[std::min(a, b)]++;
+      hi[slot] = std::max(a, b);
+      side_of[slot] = static_cast<uint32_t>(3 * t + s);
+    }
+  std::vector<uint32_t> gid(3 * N);
+  uint32_t nedges = 0;
+  for (size_t v = 0; v < nv; ++v)
+    for (uint32_t i = start[v]; i < start[v + 1]; ++i) {
+      uint32_t id = nedges;
+      for (uint32_t j = start[v]; j < i; ++j)
+        if (hi[j] == hi[i]) {
+          id = gid[side_of[j]];
+          break;
+        }
+      if (id == nedges) ++nedges;
+      gid[side_of[i]] = id;
+    }
+
+  double X = 0.0;
+  for (size_t i = 0; i < 3 * nv; ++i) X = std::max(X, std::fabs(verts[i]));
+
+  // Blocks: greedy over the triangles in traversal order `ord` (position j
+  // holds triangle ord[j]), <= cap distinct edges each.  Identity order keeps
+  // every warp store one 512-byte run; a bisection order of the centroids is
+  // used instead when it gives much more compact blocks (the row-major plate,
+  // and the icosphere, whose own order still spans ~0.4 m per block at C5):
+  // the far test needs compact blocks.
+  struct Blocks {
+    std::vector<EdgeBlock> blocks;
+    std::vector<unsigned long long> owner;
+    std::vector<ushort4> eidx;   // by position
+    std::vector<uint32_t> gslot; // by (triangle, side)
+    uint64_t edges = 0;
+    double rho_mean = 0.0;
+  };
+  std::vector<uint32_t> stamp(nedges), local(nedges);
+  // cuts (optional): positions where a block must start (subtree leaves)
+  auto make_blocks = [&](const std::vector<uint32_t>* ord, const std::vector<size_t>* cuts) {
+    Blocks R;
+    R.eidx.resize(N);
+    R.gslot.resize(3 * N);
+    std::fill(stamp.begin(), stamp.end(), UINT32_MAX);
+    uint32_t tb = 0, ne = 0, bid = 0;
+    size_t first_slot = 0;
+    auto finish_block = [&](uint32_t te) {
+      EdgeBlock B{};
+      B.tb = tb;
+      B.te = te;
+      B.c0 = static_cast<uint32_t>(first_slot / 32);
+      B.ne = ne;
+      R.blocks.push_back(B);
+      R.edges += ne;
+      const unsigned long long first = R.owner[first_slot];
+      while (R.owner.size() % 32) R.owner.push_back(first | 1ull);
+      first_slot = R.owner.size();
+    };
+    size_t next_cut = 0;
+    for (size_t j = 0; j < N; ++j) {
+      const size_t t = ord ? (*ord)[j] : j;
+      int fresh = 0;
+      for (int s = 0; s < 3; ++s) fresh += stamp[gid[3 * t + s]] != bid;
+      bool cut = false;
+      if (cuts) {
+        while (next_cut < cuts->size() && (*cuts)[next_cut] < j) ++next_cut;
+        cut = next_cut < cuts->size() && (*cuts)[next_cut] == j;
+      }
+      if ((cut || ne + fresh > cap) && j > tb) {
+        finish_block(static_cast<uint32_t>(j));
+        ++bid;
+        tb = static_cast<uint32_t>(j);
+        ne = 0;
+      }
+      uint16_t li[3];
+      for (int s = 0; s < 3; ++s) {
+        const uint32_t e = gid[3 * t + s];
+        if (stamp[e] != bid) {
+          stamp[e] = bid;
+          local[e] = ne++;
+          R.owner.push_back((static_cast<unsigned long long>(t) << 3) | (static_cast<unsigned>(s) << 1));
+        }
+        li[s] = static_cast<uint16_t>(local[e]);
+        R.gslot[3 * t + s] = static_cast<uint32_t>(first_slot + local[e]);
+      }
+      R.eidx[j] = make_ushort4(li[0], li[1], li[2], 0);
+    }
+    finish_block(static_cast<uint32_t>(N));
+    // bounding sphere of each block's vertices (every inner point lies on a
+    // segment between two of them); the margin covers the points' rounding
+    for (EdgeBlock& B : R.blocks) {
+      double c[3] = {0.0, 0.0, 0.0};
+      for (uint32_t j = B.tb; j < B.te; ++j) {
+        const size_t t = ord ? (*ord)[j] : j;
+        for (int s = 0; s < 3; ++s)
+          for (int d = 0; d < 3; ++d) c[d] += verts[3 * static_cast<size_t>(tris[3 * t + s]) + d];
+      }
+      const double cnt = 3.0 * (B.te - B.tb);
+      for (double& x : c) x /= cnt;
+      double rho = 0.0;
+      for (uint32_t j = B.tb; j < B.te; ++j) {
+        const size_t t = ord ? (*ord)[j] : j;
+        for (int s = 0; s < 3; ++s) {
+          const double* v = verts + 3 * static_cast<size_t>(tris[3 * t + s]);
+          const double dx = v[0] - c[0], dy = v[1] - c[1], dz = v[2] - c[2];
+          rho = std::max(rho, std::sqrt(dx * dx + dy * dy + dz * dz));
+        }
+      }
+      B.cx = c[0];
+      B.cy = c[1];
+      B.cz = c[2];
+      B.rho = rho * (1.0 + 1e-12) + 1e-12 * X;
+      R.rho_mean += B.rho / static_cast<double>(R.blocks.size());
+    }
+    return R;
+  };
+
+  Blocks R = make_blocks(nullptr, nullptr);
+  // spatial order: recursive coordinate bisection of the centroids (split on
+  // the longest axis) whose leaves are the blocks: a leaf is a range of at
+  // most T triangles with <= cap distinct edges, and splits fall on multiples
+  // of T so that nearly all leaves are full
+  std::vector<uint32_t> sorder(N);
+  std::vector<size_t> cuts;
+  {
+    std::vector<double> cen(3 * N);
+    for (size_t t = 0; t < N; ++t)
+      for (int d = 0; d < 3; ++d) {
+        double c = 0.0;
+        for (int s = 0; s < 3; ++s) c += verts[3 * static_cast<size_t>(tris[3 * t + s]) + d];
+        cen[3 * t + d] = c / 3.0;
+      }
+    for (size_t j = 0; j < N; ++j) sorder[j] = static_cast<uint32_t>(j);
+    std::vector<uint32_t> seen(nedges, UINT32_MAX);
+    uint32_t probe = 0;
+    auto edges_of = [&](size_t lo, size_t hi) {
+      size_t cnt = 0;
+      ++probe;
+      for (size_t j = lo; j < hi; ++j)
+        for (int s = 0; s < 3; ++s) {
+          const uint32_t e = gid[3 * static_cast<size_t>(sorder[j]) + s];
+          if (seen[e] != probe) {
+            seen[e] = probe;
+            ++cnt;
+          }
+        }
+      return cnt;
+    };
+    const size_t T = std::max<size_t>(1, (cap * 61) / 100);  // ~1.6 edges per triangle
+    std::vector<std::pair<size_t, size_t>> stack{{0, N}};
+    while (!stack.empty()) {
+      const auto [lo, hi] = stack.back();
+      stack.pop_back();
+      const size_t c = hi - lo;
+      size_t mid;
+      if (c <= T) {
+        if (edges_of(lo, hi) <= cap || c == 1) {
+          cuts.push_back(lo);
+          continue;
+        }
+        mid = lo + c / 2;
+      } else {
+        const size_t L = (c + T - 1) / T;
+        mid = lo + (L / 2) * T;
+      }
+      double bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (size_t j = lo; j < hi; ++j)
+        for (int d = 0; d < 3; ++d) {
+          bl[d] = std::min(bl[d], cen[3 * sorder[j] + d]);
+          bh[d] = std::max(bh[d], cen[3 * sorder[j] + d]);
+        }
+      int ax = 0;
+      for (int d = 1; d < 3; ++d)
+        if (bh[d] - bl[d] > bh[ax] - bl[ax]) ax = d;
+      std::nth_element(sorder.begin() + lo, sorder.begin() + mid, sorder.begin() + hi,
+                       [&](uint32_t u, uint32_t v) {
+                         const double cu = cen[3 * u + ax], cv = cen[3 * v + ax];
+                         return cu < cv || (cu == cv && u < v);
+                       });
+      stack.push_back({mid, hi});
+      stack.push_back({lo, mid});
+    }
+    std::sort(cuts.begin(), cuts.end());
+  }
+  Blocks Rm = make_blocks(&sorder, &cuts);
+  bool ordered = Rm.rho_mean < 0.75 * R.rho_mean;
+  if (const char* e = std::getenv("GK_EDGE_ORDER"))  // 0: mesh order, 1: bisection order (A/B)
+    ordered = e[0] == '1';
+  if (ordered) R = std::move(Rm);
+  const std::vector<EdgeBlock>& blocks = R.blocks;
+  const std::vector<unsigned long long>& owner = R.owner;
+
+  cudaStream_t st = mesh->ctx->stream;
+  const size_t nslots = owner.size();
+  DevBuf<unsigned long long> d_owner;
+  DevBuf<uint32_t> d_gslot;
+  d_owner.alloc(nslots, st);
+  d_gslot.alloc(3 * N, st);
+  mesh->eblk.alloc(blocks.size(), st);
+  mesh->eidx.alloc(N, st);
+  mesh->ep.alloc(nslots * n, st);
+  GK_CUDA(cudaMemcpyAsync(d_owner.p, owner.data(), nslots * sizeof(unsigned long long),
+                          cudaMemcpyHostToDevice, st));
+  GK_CUDA(cudaMemcpyAsync(d_gslot.p, R.gslot.data(), 3 * N * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  GK_CUDA(cudaMemcpyAsync(mesh->eblk.p, blocks.data(), blocks.size() * sizeof(EdgeBlock),
+                          cudaMemcpyHostToDevice, st));
+  GK_CUDA(cudaMemcpyAsync(mesh->eidx.p, R.eidx.data(), N * sizeof(ushort4), cudaMemcpyHostToDevice, st));
+  if (ordered) {
+    mesh->btri.alloc(N, st);
+    GK_CUDA(cudaMemcpyAsync(mesh->btri.p, sorder.data(), N * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  }
+  const size_t work = nslots * n;
+  edge_gather_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, st>>>(
+      mesh->inner.p, N, n, d_owner.p, nslots, mesh->ep.p);
+  count_launches(1);
+  GK_CUDA(cudaGetLastError());
+  unsigned long long* dmax = mesh->ctx->scratch.p + 30;
+  GK_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+  const size_t work2 = 3 * N * static_cast<size_t>(n);
+  edge_delta_kernel<<<static_cast<unsigned>((work2 + 255) / 256), 256, 0, st>>>(
+      mesh->inner.p, N, n, d_gslot.p, d_owner.p, mesh->ep.p, dmax);
+  count_launches(1);
+  GK_CUDA(cudaGetLastError());
+  unsigned long long hbits = 0;
+  GK_CUDA(cudaMemcpyAsync(&hbits, dmax, sizeof(hbits), cudaMemcpyDeviceToHost, st));
+  GK_CUDA(cudaStreamSynchronize(st));
+  double delta;
+  std::memcpy(&delta, &hbits, sizeof(delta));
+  mesh->nblk = blocks.size();
+  mesh->edges = R.edges;
+  mesh->rho_mean = R.rho_mean;
+  mesh->ordered = ordered;
+  mesh->edge_delta = delta;
+  mesh->edge_ratio = static_cast<double>(nslots) / (3.0 * static_cast<double>(N));
+  // delta / r_far = 32 u: the reversed-edge rounding stays under half the
+  // per-term tolerance (u = 2^-53); a tiny floor keeps r_far > 0
+  mesh->r_far = std::isfinite(delta) ? std::max(delta * 0x1p48, 1e-300) : INFINITY;
+}
+
+}  // namespace gk

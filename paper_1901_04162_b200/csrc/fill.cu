@@ -21,7 +21,7 @@ namespace gk {
 
 __global__ void lossy_phase_kernel(double2* tab, double* ahi, int nhi, double c);
 
-void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
+bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                  int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
                  gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* counters) {
   FillArgs a{};
@@ -45,7 +45,8 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.k_re = k_re;
   a.k_im = k_im;
   a.counters = counters;
-  if (row_end <= row_begin || mesh->N == 0) return;
+  if (row_end <= row_begin || mesh->N == 0) return false;
+
   DevBuf<double> atten;
   DevBuf<double2> lossy_tab;
   int att = 0;
@@ -88,6 +89,22 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
     GK_CUDA(cudaGetLastError());
     a.atten = atten.p;
   }
+  // shared edges (edges.cu) pay where the blocks share most edges (closed
+  // meshes) and are small against the mesh (N >= 4096: on C2, 1280 triangles
+  // in 6 blocks, most tiles are near and the fill is 1.4x slower); the edge
+  // kernel runs one kind at a time, n = 1..5, lossless or with the
+  // phase-coupled attenuation (its few ahi entries fit beside the edge sums)
+  if (mode == GK_MODE_DIRECT && kind != 2 && edge_fill_enabled() && mesh->nblk > 0 &&
+      mesh->edge_ratio < 0.85 && mesh->n <= 5 && (att == 0 || (att == 1 && a.nhi <= 2048)) &&
+      (mesh->N >= 4096 || edge_fill_forced())) {
+    a.eblk = mesh->eblk.p;
+    a.ep = mesh->ep.p;
+    a.eidx = mesh->eidx.p;
+    a.btri = mesh->ordered ? mesh->btri.p : nullptr;
+    a.nblk = mesh->nblk;
+    a.ecap = mesh->ecap;
+    a.r_far = mesh->r_far;
+  }
   const int degree = table ? table->dev.degree : 3;
   switch (mesh->m) {
     case 1: dispatch_mo<1>(ctx, a, mode, kind, degree, att); break;
@@ -97,6 +114,7 @@ void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
     case 7: dispatch_mo<7>(ctx, a, mode, kind, degree, att); break;
     default: fail(GK_ERR_INVALID_ARGUMENT, "QuadratureSpec: outer_points must be one of 1, 3, 4, 6, 7");
   }
+  return a.nblk > 0;
 }
 
 // lossy_phase_kernel: tab[lo] = (cos, sin)(2 pi lo / M) exp(c lo) and

@@ -126,7 +126,16 @@ struct FillArgs {
   const double* atten;
   int natten;
   double KA;            // -k_im * 512
-  unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max, [2] non-finite entries
+  unsigned long long* counters;  // [0] fallbacks (r < r_min), [1] r > r_max, [2] non-finite entries,
+                                 // [3] kernel evaluations performed
+  // shared-edge fill (direct_edge_kernel, edges.cu)
+  const EdgeBlock* eblk;
+  const double4* ep;
+  const ushort4* eidx;
+  const uint32_t* btri;  // triangle at each block position (null: identity)
+  size_t nblk;
+  int ecap;  // edge-sum slots per warp (>= every block's edge count)
+  double r_far;
 };
 
 // Column-block walk shared by both kernels: the (column block, inner point)
@@ -375,6 +384,148 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
     }
     __syncwarp();
   }
+}
+
+// One direct term w K(|o - P|) into acc[o] (the v4 loop body).
+template <int MO, int KIND, int ATT>
+__device__ __forceinline__ void direct_term(Acc<MO, false>& acc, int o, double ox, double oy,
+                                            double oz, double2 pxy, double2 pzw,
+                                            const FillArgs& A, const double2* tab,
+                                            const PhaseAtt& pa, const double* att) {
+  const double d2 = dist2(ox, oy, oz, pxy.x, pxy.y, pzw.x);
+  const double y = rsqrt_fast(d2);
+  const double r = __dmul_rn(d2, y);
+  double w = pzw.y;
+  double2 cs;
+  if constexpr (ATT == 1) {
+    double a;
+    cs = cis_phase_att(r, A.K1, tab, pa, a);
+    w = __dmul_rn(w, a);
+  } else {
+    cs = cis_phase(r, A.K1, tab);
+    if constexpr (ATT == 2) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
+  }
+  acc.template add<KIND>(o, w, y, cs);
+}
+
+// K4e: the direct fill with shared edges (edges.cu).  A tile is 12 rows x one
+// edge block.  Where every pair of (row p, block) is at least r_far apart, the
+// warp evaluates each distinct edge of the block once (lane = edge, the n
+// points fully unrolled: m x n terms per lane), keeps the edge sums
+// E[e] = sum_o w_o sum_i w_i K(r_oi) in shared memory and writes
+// Z[p][q] = E[e0(q)] + E[e1(q)] + E[e2(q)] for the block's triangles
+// (coalesced streaming stores).  Nearer tiles take the per-triangle loop on
+// the reference's own points.  On a closed mesh the far path performs ~0.55
+// of the reference's evaluations.
+template <int MO, int NPE, int KIND, int ATT>
+__global__ void __launch_bounds__(32 * GK_WARPS_V4, 1) direct_edge_kernel(const FillArgs A) {
+  constexpr int W = GK_WARPS_V4;
+  constexpr int IPT = 3 * NPE;
+  extern __shared__ double2 tab[];  // phase [kPhaseM] | edge sums [W][ecap] | attenuation
+  __shared__ double sw[W][MO];
+  __shared__ uint64_t bar;
+  stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
+  double2* const sE = tab + kPhaseM;
+  double* att = reinterpret_cast<double*>(sE + W * A.ecap);
+  if constexpr (ATT == 1)
+    for (int i = threadIdx.x; i < A.nhi; i += blockDim.x) att[i] = A.ahi[i];
+  const PhaseAtt pa{att, A.nhi, A.q1, A.q2, A.q3, A.q4};
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t N = A.N;
+  double2* const myE = sE + warp * A.ecap;
+  unsigned long long nev = 0;
+
+  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    const size_t tr = tile / A.nblk, b = tile - tr * A.nblk;
+    const size_t p = A.row_begin + tr * W + warp;
+    if (p >= A.row_end) continue;  // warp-uniform
+    double ox[MO], oy[MO], oz[MO];
+#pragma unroll
+    for (int o = 0; o < MO; ++o) {
+      const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
+      const double2 zw = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o) + 1);
+      ox[o] = xy.x;
+      oy[o] = xy.y;
+      oz[o] = zw.x;
+      if (lane == 0) sw[warp][o] = zw.y;
+    }
+    const EdgeBlock B = A.eblk[b];
+    const double4 bp = A.bounds[p];
+    const double dx = bp.x - B.cx, dy = bp.y - B.cy, dz = bp.z - B.cz;
+    const double gap = sqrt(dx * dx + dy * dy + dz * dz) - bp.w - B.rho;
+    __syncwarp();
+    if (gap >= A.r_far) {
+      const int nch = static_cast<int>((B.ne + 31) >> 5);
+      const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
+      double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
+      double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
+      for (int c = 0; c < nch; ++c) {
+        Acc<MO, false> acc;
+        acc.zero();
+#pragma unroll
+        for (int g = 0; g < NPE; ++g) {
+          const double2 pxy = cxy, pzw = czw;
+          const double4* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 32
+                                                : (c + 1 < nch ? (c + 1) * NPE * 32 : 0));
+          cxy = __ldg(reinterpret_cast<const double2*>(np));
+          czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
+#pragma unroll
+          for (int o = 0; o < MO; ++o)
+            direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att);
+        }
+        double2 e = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int o = 0; o < MO; ++o) {
+          const double w = sw[warp][o];
+          e.x = __fma_rn(w, acc.e[o].x, e.x);
+          e.y = __fma_rn(w, acc.e[o].y, e.y);
+        }
+        myE[c * 32 + lane] = e;
+      }
+      nev += static_cast<unsigned long long>(B.ne) * NPE * MO;
+      __syncwarp();
+      for (uint32_t jb = B.tb; jb < B.te; jb += 32) {
+        const uint32_t j = jb + lane;
+        if (j < B.te) {
+          const uint32_t q = A.btri ? __ldg(A.btri + j) : j;
+          const uint2 ei = __ldg(reinterpret_cast<const uint2*>(A.eidx + j));  // ushort4
+          const double2 e0 = myE[ei.x & 0xffffu], e1 = myE[ei.x >> 16], e2 = myE[ei.y & 0xffffu];
+          double2 zv = make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y);
+          if (q == p) zv = make_double2(0.0, 0.0);
+          if (!(isfinite(zv.x) && isfinite(zv.y))) atomicAdd(A.counters + 2, 1ull);
+          __stcs(A.z + (p - A.row_begin) * A.ldz + q, zv);
+        }
+      }
+      __syncwarp();  // myE is rewritten by the next tile
+    } else {
+      // near tile: the reference's own points of each source triangle
+      unsigned nq = 0;
+      for (uint32_t jb = B.tb; jb < B.te; jb += 32) {
+        const uint32_t j = jb + lane;
+        const bool valid = j < B.te;
+        const uint32_t jj = valid ? j : B.te - 1;
+        const size_t qq = A.btri ? __ldg(A.btri + jj) : jj;
+        const size_t q = qq;
+        nq += __popc(__ballot_sync(0xffffffffu, valid && q != p));
+        Acc<MO, false> acc;
+        acc.zero();
+#pragma unroll 1
+        for (int i = 0; i < IPT; ++i) {
+          const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + qq);
+          const double2 pxy = __ldg(ptr), pzw = __ldg(ptr + 1);
+#pragma unroll
+          for (int o = 0; o < MO; ++o)
+            direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att);
+        }
+        acc.finish([&](int o) { return sw[warp][o]; }, q == p, valid, A.z, A.z2,
+                   (p - A.row_begin) * A.ldz + qq, A.counters + 2);
+      }
+      nev += static_cast<unsigned long long>(nq) * IPT * MO;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && nev) atomicAdd(A.counters + 3, nev);
 }
 
 // K3: table evaluation (the paper's method) with the reference's fallback.
@@ -730,6 +881,26 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
       const char* e = std::getenv("GK_DIRECT_V4");
       return !(e && e[0] == '0');
     }();
+    // shared-edge path (edges.cu): single kind, lossless or phase-coupled
+    // attenuation, n = 1..5; launch_fill leaves nblk = 0 where it does not pay
+    if constexpr (KIND != kKindPair && ATT != 2) {
+      const size_t esmem = kPhaseM * sizeof(double2) + GK_WARPS_V4 * a.ecap * sizeof(double2) +
+                           (ATT == 1 ? a.nhi * sizeof(double) : 0);
+      if (a.nblk > 0) {
+        auto go = [&](auto kern) {
+          a.ntiles = ((a.row_end - a.row_begin + GK_WARPS_V4 - 1) / GK_WARPS_V4) * a.nblk;
+          launch_kernel(ctx, kern, a, esmem, 32 * GK_WARPS_V4);
+        };
+        switch (a.ipt) {
+          case 3: return go(direct_edge_kernel<MO, 1, KIND, ATT>);
+          case 6: return go(direct_edge_kernel<MO, 2, KIND, ATT>);
+          case 9: return go(direct_edge_kernel<MO, 3, KIND, ATT>);
+          case 12: return go(direct_edge_kernel<MO, 4, KIND, ATT>);
+          case 15: return go(direct_edge_kernel<MO, 5, KIND, ATT>);
+          default: fail(GK_ERR_RUNTIME, "shared-edge fill: n must be 1..5");
+        }
+      }
+    }
     if (use_v4) {
       switch (a.ipt) {  // n = 1..5 Gauss points per edge: fully unrolled fast path
         case 3: return launch_v4<MO, 3, KIND, ATT>(ctx, a, smem);

@@ -101,6 +101,21 @@ struct gk_mesh {
   gk::DevBuf<double4> bounds; // [N]        (cx, cy, cz, rho_outer), rho_inner in binner
   gk::DevBuf<double> binner;  // [N]
   gk::DevBuf<double> verts;   // [3 nv] vertices (max_vertex_distance)
+  // shared-edge blocks (build_edge_blocks): every distinct edge of a block of
+  // source triangles is evaluated once and serves the (usually two)
+  // triangles that share it; used for (row, block) pairs at least r_far apart
+  gk::DevBuf<gk::EdgeBlock> eblk;  // [nblk]
+  gk::DevBuf<double4> ep;          // [chunks][n][32] edge points (owner orientation)
+  gk::DevBuf<ushort4> eidx;        // [N] block-local edge index of each side, by position
+  gk::DevBuf<uint32_t> btri;       // [N] triangle at each position (spatial order), or empty
+  uint64_t edges = 0;
+  int ecap = 0;  // edges per block (shared-memory slots per warp)
+  double rho_mean = 0.0;
+  bool ordered = false;
+  size_t nblk = 0;
+  double r_far = INFINITY;   // pairs this far apart absorb the reversed-edge rounding
+  double edge_delta = 0.0;   // max |point - reversed-edge point| over shared sides
+  double edge_ratio = 1.0;   // evaluated edges / (3 N): the far-path work fraction
 };
 
 namespace gk {
@@ -110,6 +125,19 @@ namespace gk {
 inline bool table_arith_enabled() {
   const char* e = std::getenv("GK_TABLE_ARITH");
   return !(e && e[0] == '0');
+}
+
+// GK_EDGE=0: direct fills without the shared-edge path (A/B and tests; read
+// per launch; GK_EDGE=0 at mesh creation also skips building the blocks)
+inline bool edge_fill_enabled() {
+  const char* e = std::getenv("GK_EDGE");
+  return !(e && e[0] == '0');
+}
+
+// GK_EDGE=2: the shared-edge path also for small meshes (tests)
+inline bool edge_fill_forced() {
+  const char* e = std::getenv("GK_EDGE");
+  return e && e[0] == '2';
 }
 
 // launch accounting (gk_launch_count)
@@ -127,6 +155,9 @@ void validate_mesh(const double* v, size_t nv, const uint32_t* t, size_t nt);
 // kernels launched by abi.cu (defined in build.cu / fill.cu / eval.cu)
 void launch_points(gk_mesh* mesh, const double* d_verts, const uint32_t* d_tris,
                    cudaStream_t s);
+// shared-edge blocks of a mesh whose points launch_points has produced
+// (edges.cu); synchronises the context stream
+void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris);
 // max over vertex pairs of |a - b|^2 (reference summation order) -> *d2_bits
 void launch_max_vertex_d2(const double* verts, size_t nv, unsigned long long* d2_bits,
                           cudaStream_t s);
@@ -145,8 +176,10 @@ void launch_compare(gk_ctx* ctx, const gk_c128* test, const gk_c128* ref, size_t
                     size_t row_begin, size_t ld, unsigned long long* w);
 void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg, double k_zero,
                         double t_nominal, double k_re, double k_im, int degree);
-// kind: GK_KIND_EXP, GK_KIND_GREEN, or 2 = fused pair (z = Exp, z2 = Green)
-void launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
+// kind: GK_KIND_EXP, GK_KIND_GREEN, or 2 = fused pair (z = Exp, z2 = Green).
+// Returns true when the shared-edge kernel ran: it counts the evaluations it
+// performed into counters[3]; otherwise they equal the reference's calls.
+bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                  int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
                  gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* d_fallbacks);
 void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,

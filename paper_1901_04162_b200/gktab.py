@@ -113,11 +113,13 @@ class FillReport:
     analytic_time_s: float = 0.0
     interp_time_s: float = 0.0
     table_build_s: float = 0.0
+    # kernel evaluations the device performed (<= actual_calls: shared edges)
+    evaluations: int = 0
 
     @classmethod
     def from_c(cls, r: FillReportC) -> "FillReport":
         return cls(r.N, r.m, r.n, r.predicted_calls, r.actual_calls, r.fallback_calls,
-                   r.wall_time_s)
+                   r.wall_time_s, evaluations=r.evaluations)
 
 
 @dataclass
@@ -479,6 +481,20 @@ class DeviceMesh:
         i = np.zeros((4, self.N * 3 * n), np.float64)
         check(lib().gk_mesh_points_download(self.h, o.ctypes.data, i.ctypes.data), "points")
         return o, i
+
+    def edge_info(self) -> dict:
+        """Shared-edge blocks of the direct fill (gk_mesh_edge_info_get)."""
+        out = (C.c_double * 8)()
+        check(lib().gk_mesh_edge_info_get(self.h, C.cast(out, C.c_void_p)), "edge_info")
+        raw = bytes(out)
+        blocks, slots = np.frombuffer(raw[:16], np.uint64)
+        ratio, delta, r_far = np.frombuffer(raw[16:40], np.float64)
+        edges = np.frombuffer(raw[40:48], np.uint64)[0]
+        rho = np.frombuffer(raw[48:56], np.float64)[0]
+        ordered = np.frombuffer(raw[56:60], np.int32)[0]
+        return dict(blocks=int(blocks), edge_slots=int(slots), work_ratio=float(ratio),
+                    delta=float(delta), r_far=float(r_far), edges=int(edges),
+                    rho_mean=float(rho), ordered=bool(ordered))
 
     def max_vertex_distance(self) -> float:
         """max_vertex_distance (mesh.hpp:62-68), exact, on the device."""

@@ -1,0 +1,149 @@
+"""Shared-edge direct fill (K4e, csrc/edges.cu) vs the oracle.
+
+The reference evaluates every source triangle's own edge points
+(inner_points, matfill.hpp:132-144).  The shared-edge kernel evaluates each
+distinct edge of a block of source triangles once, in the orientation of its
+first triangle, for (row, block) tiles at least r_far = delta / (32 u) apart,
+delta being the measured largest distance between a point and its
+reversed-edge twin.  The bar is the same as every direct fill's
+(tests/test_gpu_fill.py):
+  |Z_gpu - Z_cpu_direct| <= B_pq = sum_{o,i} |w_o w_i| 64 2^-53 (1 + |k| r) / r
+which the reversed-edge rounding uses at most half of per term.
+"""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import DIRECT, EXP, GREEN
+
+pytestmark = pytest.mark.gpu
+
+ULPS = 64.0
+
+
+def sphere(gk, level, radius=1.0, seed=1901, amp=1e-3):
+    return gk.jitter(gk.generate_sphere_mesh(radius, level), seed, amp)
+
+
+@pytest.fixture
+def forced(monkeypatch):
+    """shared edges on small meshes, with small blocks so that far tiles exist"""
+    monkeypatch.setenv("GK_EDGE", "2")
+    monkeypatch.setenv("GK_EDGE_CHUNKS", "4")
+    return monkeypatch
+
+
+def _check(gk, oracle, mesh, m, n, k, kind=None):
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+    info = dm.edge_info()
+    kw = dict(k=k) if kind is None else dict(k=k, kind=kind)
+    z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, **kw)
+    kc = complex(k)
+    ref, orep = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, DIRECT, kc.real,
+                                 kind=EXP if kind == gk.KernelKind.PlainExp else GREEN,
+                                 k_im=kc.imag, threads=8)
+    err = np.abs(z.cpu().numpy() - ref)
+    if kind == gk.KernelKind.PlainExp:  # the Exp bar of test_gpu_fill.test_fill_exp_kind
+        assert np.max(err) <= 1e-13 * np.abs(ref).max() * 80
+    else:
+        B = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, None, abs(kc), ULPS)
+        assert np.all(err <= B), float(np.max(err / np.maximum(B, 1e-300)))
+    N = mesh.triangle_count()
+    assert rep.actual_calls == orep.actual_calls == 3 * m * n * N * (N - 1)
+    assert np.all(np.diag(z.cpu().numpy()) == 0)
+    return dm, info, rep
+
+
+@pytest.mark.parametrize("m,n", [(6, 4), (7, 5), (3, 1), (1, 2)])
+def test_edge_fill_parity_sphere(gk, oracle, forced, m, n):
+    dm, info, rep = _check(gk, oracle, sphere(gk, 3), m, n, 2 * np.pi)
+    assert info["blocks"] > 1 and info["work_ratio"] < 0.85, info
+    # the far threshold is the measured reversed-edge rounding / (32 u)
+    assert 0 < info["delta"] < 1e-15
+    assert info["r_far"] == info["delta"] * 2.0 ** 48
+    # the shared edges did run: fewer evaluations than the reference's calls
+    assert rep.evaluations < 0.8 * rep.actual_calls
+
+
+def test_edge_fill_parity_lossy_plate(gk, oracle, forced):
+    """C4's medium (attenuation coupled to the phase reduction) on an open,
+    row-major plate: blocks follow the bisection order."""
+    mesh = gk.generate_plate_mesh(1.0, 20)
+    k = complex(gk.wavenumber(gk.Medium(1.0, 4.0, 1.0, -0.4)))
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, k)
+    assert info["ordered"]
+    assert rep.evaluations < 0.85 * rep.actual_calls
+
+
+def test_edge_fill_exp_kind(gk, oracle, forced):
+    mesh = sphere(gk, 3)
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi, kind=gk.KernelKind.PlainExp)
+    assert rep.evaluations < 0.8 * rep.actual_calls
+
+
+def test_edge_fill_close_to_per_triangle_fill(gk, forced):
+    """same matrix as the reference-order kernel up to rounding"""
+    mesh = sphere(gk, 3)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    ze, re_ = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    forced.setenv("GK_EDGE", "0")
+    zt, rt = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    assert rt.evaluations == rt.actual_calls and re_.evaluations < rt.evaluations
+    rel = ((ze - zt).abs() / zt.abs().clamp_min(1e-300)).max().item()
+    assert rel < 1e-12
+
+
+def test_edge_near_tiles_bit_identical_to_per_triangle_fill(gk, monkeypatch):
+    """blocks as large as the mesh: every tile is near and takes the
+    reference's own points in the reference's order (bitwise the v4 kernel)"""
+    import torch
+    monkeypatch.setenv("GK_EDGE", "2")
+    monkeypatch.delenv("GK_EDGE_CHUNKS", raising=False)
+    mesh = sphere(gk, 2)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    z1, r1 = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    monkeypatch.setenv("GK_EDGE", "0")
+    z0, r0 = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    assert torch.equal(z1, z0)
+    assert r1.evaluations == r0.evaluations == r0.actual_calls
+
+
+def test_edge_row_blocks_union_bit_exact(gk, forced):
+    import torch
+    mesh = sphere(gk, 3)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    full, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    N = dm.N
+    parts, evals = [], 0
+    for b, e in [(0, 417), (417, 418), (418, 1000), (1000, N)]:
+        z, r = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi, row_begin=b, row_end=e)
+        parts.append(z)
+        evals += r.evaluations
+    assert torch.equal(torch.cat(parts), full)
+    assert evals == rep.evaluations
+
+
+def test_edge_fill_host_pipeline_and_async(gk, forced):
+    """the streamed host fill and the asynchronous fill take the same path"""
+    import torch
+    mesh = sphere(gk, 3)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    zh = np.empty((dm.N, dm.N), np.complex128)
+    reph = gk.fill_rows_host(dm, gk.Mode.DIRECT, zh, k=2 * np.pi)
+    assert np.array_equal(zh, z.cpu().numpy()) and reph.evaluations == rep.evaluations
+    za, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi, report=False)
+    assert dm.ctx.fill_check() == 0
+    assert torch.equal(za, z)
+
+
+def test_edge_blocks_skip_meshes_without_shared_edges(gk, oracle, monkeypatch):
+    """disconnected triangles share no edge: the per-triangle kernel runs"""
+    monkeypatch.setenv("GK_EDGE", "2")
+    rng = np.random.default_rng(7)
+    N = 300
+    base = rng.uniform(-1, 1, (N, 1, 3))
+    verts = (base + rng.uniform(-0.05, 0.05, (N, 3, 3))).reshape(-1, 3)
+    tris = np.arange(3 * N, dtype=np.uint32).reshape(N, 3)
+    mesh = gk.TriangleMesh(verts, tris)
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi)
+    assert info["work_ratio"] >= 0.85 and rep.evaluations == rep.actual_calls
