@@ -218,6 +218,8 @@ def main():
     ap.add_argument("--c1", type=int, default=1, help="also time standalone eval_batch (C1)")
     ap.add_argument("--gather", type=int, default=1,
                     help="N > 1: also time the gather of Z to rank 0 (reported apart)")
+    ap.add_argument("--pertri", type=int, default=1,
+                    help="also time the direct fill without shared edges (GK_EDGE=0)")
     ap.add_argument("--S-alt", type=int, default=1000,
                     help="also time the table mode at this S (0 = off)")
     args = ap.parse_args()
@@ -264,6 +266,8 @@ def main():
     fill_ev = []
 
     def step(mode):
+        # "direct_pertri": the reference-order kernel without shared edges (A/B)
+        os.environ["GK_EDGE"] = "0" if mode == "direct_pertri" else "1"
         table = None
         if mode.startswith("table"):
             S = args.S if mode == "table" else int(mode.split("_S")[1])
@@ -310,6 +314,15 @@ def main():
             ms, fill_ms = float(t[0]), float(t[1])
         return ms, fill_ms
 
+    def performed_evals(mode):
+        if mode != "direct":  # table and per-triangle fills perform every reference call
+            return 3 * m * n * rows * (N - 1)
+        if not rows:
+            return 0
+        os.environ["GK_EDGE"] = "1"
+        _, rep = gk.fill_rows(dmesh, gk.Mode.DIRECT, k=k, row_begin=rb, row_end=re, out=Z)
+        return rep.evaluations
+
     # roofline denominator: FP64 DFMA peak measured on this device now
     p64 = ctx.fp64_peak_tflops()
     modes = ["direct", "table"] if args.mode == "auto" or args.both_modes else [args.mode]
@@ -318,6 +331,8 @@ def main():
                                if args.both_modes else [])
     if args.S_alt and args.S_alt != args.S and "table" in modes:
         modes.append(f"table_S{args.S_alt}")
+    if args.pertri and "direct" in modes:
+        modes.insert(modes.index("direct") + 1, "direct_pertri")
     results = {}
     clocks = None
     for i, mode in enumerate(modes):
@@ -328,10 +343,20 @@ def main():
             clocks = cs.summary()
         else:
             ms, fill_ms = timed(mode, steps, 1)
-        evals_per_launch = 3 * m * n * rows * (N - 1)
+        # evaluations the kernel performs per launch (fewer than the
+        # reference's calls on the shared-edge path): one synchronous fill
+        # outside the timed region reports them
+        performed = performed_evals(mode)
+        evals_all = performed
+        if world > 1:
+            t = torch.tensor([performed], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t)
+            evals_all = float(t[0])
         results[mode] = {"ms_per_step": ms, "fill_kernel_ms": fill_ms,
                          "evals_per_s": total_evals / (ms * 1e-3),
-                         "kernel_tflops": evals_per_launch * FLOPS_PER_EVAL / (fill_ms * 1e-3) / 1e12}
+                         "evaluations_per_step": evals_all,
+                         "evaluations_performed_per_s": evals_all / (ms * 1e-3),
+                         "kernel_tflops": performed * FLOPS_PER_EVAL / (fill_ms * 1e-3) / 1e12}
     # the timed fills ran asynchronously: surface any fallback / range / r = 0
     # error now (outside the timed region), like a synchronous fill would
     ctx.fill_check()
@@ -340,6 +365,7 @@ def main():
     chosen = args.mode if args.mode != "auto" else min(("direct", "table"),
                                                        key=lambda x: results[x]["ms_per_step"])
     main_res = results[chosen]
+    os.environ["GK_EDGE"] = "1"
 
 
     # e2e through the host-buffer C-ABI entry point (gk_fill_matrix_host), rank-local rows
@@ -416,12 +442,20 @@ def main():
                          "through L2; the quadrature points (<= 47 MB) are re-read ~N times "
                          "within each step, so their L2 residency is the steady state"},
         "fill_time_s": main_res["ms_per_step"] * 1e-3,
+        "value_definition": "the reference's calls per Z fill (FillReport.actual_calls = "
+                            "3 m n N (N-1), matfill.hpp:200) / fill time, i.e. Z-fill time "
+                            "expressed as Green-function evaluations of the reference's "
+                            "algorithm; the direct kernel evaluates each shared mesh edge "
+                            "once for both triangles, performing evaluations_per_step of them "
+                            "(roofline.achieved counts only those)",
+        "evaluations_per_step": main_res["evaluations_per_step"],
+        "evaluations_performed_per_s": main_res["evaluations_performed_per_s"],
         "roofline": {"bound": "fp64", "achieved": main_res["kernel_tflops"], "peak": p64,
                      "peak_nominal": 148 * 64 * 2 * 1.965e9 / 1e12,
                      "unit": "TFLOP/s", "frac": main_res["kernel_tflops"] / p64,
                      "traffic": traffic,
                      "note": f"{FLOPS_PER_EVAL} algorithmic FP64 flops/eval (SURVEY 8d, FMA=2) x "
-                             f"evals per launch / fill-kernel event time; peak = DFMA "
+                             f"evaluations performed per launch / fill-kernel event time; peak = DFMA "
                              f"microbenchmark on this GPU (MEASURED_PEAKS.json has no FP64 entry)",
                      "hbm_write_gbs": fill_bytes / (main_res["fill_kernel_ms"] * 1e-3) / 1e9},
         "modes": results,

@@ -305,18 +305,20 @@ void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris)
   d_owner.alloc(nslots, st);
   d_gslot.alloc(3 * N, st);
   mesh->eblk.alloc(blocks.size(), st);
-  mesh->eidx.alloc(N, st);
+  mesh->ecol.alloc(N, st);
   mesh->ep.alloc(nslots * n, st);
   GK_CUDA(cudaMemcpyAsync(d_owner.p, owner.data(), nslots * sizeof(unsigned long long),
                           cudaMemcpyHostToDevice, st));
   GK_CUDA(cudaMemcpyAsync(d_gslot.p, R.gslot.data(), 3 * N * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
   GK_CUDA(cudaMemcpyAsync(mesh->eblk.p, blocks.data(), blocks.size() * sizeof(EdgeBlock),
                           cudaMemcpyHostToDevice, st));
-  GK_CUDA(cudaMemcpyAsync(mesh->eidx.p, R.eidx.data(), N * sizeof(ushort4), cudaMemcpyHostToDevice, st));
-  if (ordered) {
-    mesh->btri.alloc(N, st);
-    GK_CUDA(cudaMemcpyAsync(mesh->btri.p, sorder.data(), N * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  std::vector<uint4> ecol(N);
+  for (size_t j = 0; j < N; ++j) {
+    const ushort4 e = R.eidx[j];
+    ecol[j] = make_uint4(ordered ? sorder[j] : static_cast<uint32_t>(j),
+                         static_cast<uint32_t>(e.x) | (static_cast<uint32_t>(e.y) << 16), e.z, 0u);
   }
+  GK_CUDA(cudaMemcpyAsync(mesh->ecol.p, ecol.data(), N * sizeof(uint4), cudaMemcpyHostToDevice, st));
   const size_t work = nslots * n;
   edge_gather_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, st>>>(
       mesh->inner.p, N, n, d_owner.p, nslots, mesh->ep.p);

@@ -99,8 +99,7 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
       (mesh->N >= 4096 || edge_fill_forced())) {
     a.eblk = mesh->eblk.p;
     a.ep = mesh->ep.p;
-    a.eidx = mesh->eidx.p;
-    a.btri = mesh->ordered ? mesh->btri.p : nullptr;
+    a.ecol = mesh->ecol.p;
     a.nblk = mesh->nblk;
     a.ecap = mesh->ecap;
     a.r_far = mesh->r_far;

@@ -131,8 +131,7 @@ struct FillArgs {
   // shared-edge fill (direct_edge_kernel, edges.cu)
   const EdgeBlock* eblk;
   const double4* ep;
-  const ushort4* eidx;
-  const uint32_t* btri;  // triangle at each block position (null: identity)
+  const uint4* ecol;  // per block position: (triangle q, e0 | e1 << 16, e2, 0)
   size_t nblk;
   int ecap;  // edge-sum slots per warp (>= every block's edge count)
   double r_far;
@@ -452,10 +451,16 @@ __global__ void __launch_bounds__(32 * GK_WARPS_V4, 1) direct_edge_kernel(const 
     }
     const EdgeBlock B = A.eblk[b];
     const double4 bp = A.bounds[p];
+    // far: |c_p - c_B| - rho_p - rho_B >= r_far, compared squared (both
+    // sides >= 0) with a margin far above the rounding of either side
     const double dx = bp.x - B.cx, dy = bp.y - B.cy, dz = bp.z - B.cz;
-    const double gap = sqrt(dx * dx + dy * dy + dz * dz) - bp.w - B.rho;
+    const double reach = A.r_far + bp.w + B.rho;
+    const bool far = dx * dx + dy * dy + dz * dz >= reach * reach * (1.0 + 1e-12);
+    double2* const zrow = A.z + (p - A.row_begin) * A.ldz;
+    const uint4* const cols = A.ecol + B.tb;
+    const uint32_t nb = B.te - B.tb;
     __syncwarp();
-    if (gap >= A.r_far) {
+    if (far) {
       const int nch = static_cast<int>((B.ne + 31) >> 5);
       const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
       double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
@@ -485,41 +490,38 @@ __global__ void __launch_bounds__(32 * GK_WARPS_V4, 1) direct_edge_kernel(const 
       }
       nev += static_cast<unsigned long long>(B.ne) * NPE * MO;
       __syncwarp();
-      for (uint32_t jb = B.tb; jb < B.te; jb += 32) {
+      // Z[p][q] = sum of q's three edge sums.  Far tiles never hold the self
+      // pair (p's centroid lies inside its own block's sphere) nor a
+      // zero distance (every pair is >= r_far > 0 apart): no checks needed.
+      for (uint32_t jb = 0; jb < nb; jb += 32) {
         const uint32_t j = jb + lane;
-        if (j < B.te) {
-          const uint32_t q = A.btri ? __ldg(A.btri + j) : j;
-          const uint2 ei = __ldg(reinterpret_cast<const uint2*>(A.eidx + j));  // ushort4
-          const double2 e0 = myE[ei.x & 0xffffu], e1 = myE[ei.x >> 16], e2 = myE[ei.y & 0xffffu];
-          double2 zv = make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y);
-          if (q == p) zv = make_double2(0.0, 0.0);
-          if (!(isfinite(zv.x) && isfinite(zv.y))) atomicAdd(A.counters + 2, 1ull);
-          __stcs(A.z + (p - A.row_begin) * A.ldz + q, zv);
+        if (j < nb) {
+          const uint4 col = __ldg(cols + j);  // (q, e0 | e1 << 16, e2)
+          const double2 e0 = myE[col.y & 0xffffu], e1 = myE[col.y >> 16], e2 = myE[col.z];
+          __stcs(zrow + col.x, make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y));
         }
       }
       __syncwarp();  // myE is rewritten by the next tile
     } else {
       // near tile: the reference's own points of each source triangle
       unsigned nq = 0;
-      for (uint32_t jb = B.tb; jb < B.te; jb += 32) {
+      for (uint32_t jb = 0; jb < nb; jb += 32) {
         const uint32_t j = jb + lane;
-        const bool valid = j < B.te;
-        const uint32_t jj = valid ? j : B.te - 1;
-        const size_t qq = A.btri ? __ldg(A.btri + jj) : jj;
-        const size_t q = qq;
+        const bool valid = j < nb;
+        const size_t q = __ldg(cols + (valid ? j : nb - 1)).x;
         nq += __popc(__ballot_sync(0xffffffffu, valid && q != p));
         Acc<MO, false> acc;
         acc.zero();
 #pragma unroll 1
         for (int i = 0; i < IPT; ++i) {
-          const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + qq);
+          const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
           const double2 pxy = __ldg(ptr), pzw = __ldg(ptr + 1);
 #pragma unroll
           for (int o = 0; o < MO; ++o)
             direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att);
         }
         acc.finish([&](int o) { return sw[warp][o]; }, q == p, valid, A.z, A.z2,
-                   (p - A.row_begin) * A.ldz + qq, A.counters + 2);
+                   (p - A.row_begin) * A.ldz + q, A.counters + 2);
       }
       nev += static_cast<unsigned long long>(nq) * IPT * MO;
     }

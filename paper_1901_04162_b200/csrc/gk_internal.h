@@ -106,8 +106,7 @@ struct gk_mesh {
   // triangles that share it; used for (row, block) pairs at least r_far apart
   gk::DevBuf<gk::EdgeBlock> eblk;  // [nblk]
   gk::DevBuf<double4> ep;          // [chunks][n][32] edge points (owner orientation)
-  gk::DevBuf<ushort4> eidx;        // [N] block-local edge index of each side, by position
-  gk::DevBuf<uint32_t> btri;       // [N] triangle at each position (spatial order), or empty
+  gk::DevBuf<uint4> ecol;          // [N] by block position: (triangle, e0 | e1 << 16, e2, 0)
   uint64_t edges = 0;
   int ecap = 0;  // edges per block (shared-memory slots per warp)
   double rho_mean = 0.0;
