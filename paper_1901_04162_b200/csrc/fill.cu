@@ -94,9 +94,16 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   // in 6 blocks, most tiles are near and the fill is 1.4x slower); the edge
   // kernel runs one kind at a time, n = 1..5, lossless or with the
   // phase-coupled attenuation (its few ahi entries fit beside the edge sums)
-  if (mode == GK_MODE_DIRECT && kind != 2 && edge_fill_enabled() && mesh->nblk > 0 &&
-      mesh->edge_ratio < 0.85 && mesh->n <= 5 && (att == 0 || (att == 1 && a.nhi <= 2048)) &&
-      (mesh->N >= 4096 || edge_fill_forced())) {
+  // table mode (K3e): far pairs are >= r_far >= r_min apart, so they never
+  // fall back below the table (the fallback counts stay the reference's); a
+  // far pair above r_max is still detected (the fill fails with out_of_range
+  // as the reference's does, its count then covering the shared evaluations).
+  // GK_TABLE_EDGE=0 keeps the per-triangle table kernels.
+  const bool table_edges = mode == GK_MODE_TABLE && table_edge_enabled() && table &&
+                           table->dev.r_min <= mesh->r_far;
+  if ((mode == GK_MODE_DIRECT || table_edges) && kind != 2 && edge_fill_enabled() &&
+      mesh->nblk > 0 && mesh->edge_ratio < 0.85 && mesh->n <= 5 &&
+      (att == 0 || (att == 1 && a.nhi <= 2048)) && (mesh->N >= 4096 || edge_fill_forced())) {
     a.eblk = mesh->eblk.p;
     a.ep = mesh->ep.p;
     a.ecol = mesh->ecol.p;
@@ -106,14 +113,13 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   }
   const int degree = table ? table->dev.degree : 3;
   switch (mesh->m) {
-    case 1: dispatch_mo<1>(ctx, a, mode, kind, degree, att); break;
-    case 3: dispatch_mo<3>(ctx, a, mode, kind, degree, att); break;
-    case 4: dispatch_mo<4>(ctx, a, mode, kind, degree, att); break;
-    case 6: dispatch_mo<6>(ctx, a, mode, kind, degree, att); break;
-    case 7: dispatch_mo<7>(ctx, a, mode, kind, degree, att); break;
+    case 1: return dispatch_mo<1>(ctx, a, mode, kind, degree, att);
+    case 3: return dispatch_mo<3>(ctx, a, mode, kind, degree, att);
+    case 4: return dispatch_mo<4>(ctx, a, mode, kind, degree, att);
+    case 6: return dispatch_mo<6>(ctx, a, mode, kind, degree, att);
+    case 7: return dispatch_mo<7>(ctx, a, mode, kind, degree, att);
     default: fail(GK_ERR_INVALID_ARGUMENT, "QuadratureSpec: outer_points must be one of 1, 3, 4, 6, 7");
   }
-  return a.nblk > 0;
 }
 
 // lossy_phase_kernel: tab[lo] = (cos, sin)(2 pi lo / M) exp(c lo) and

@@ -617,6 +617,152 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
   if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
 }
 
+// ------------------------------------------- K3e: table fill with shared edges
+//
+// The paper's method on K4e's blocks (edges.cu): far tiles evaluate each
+// distinct edge of a block once through the table (read through L1, as
+// table_kernel does); near tiles run the per-triangle loop with the
+// reference's fallback (evaluator.hpp:199-205).  launch_fill takes this path
+// only when r_min <= r_far, so a far pair never falls back below the table:
+// the fallback counts stay the reference's.
+#ifndef GK_TEDGE_WARPS
+#define GK_TEDGE_WARPS 12
+#endif
+
+template <int KIND, int DEG>
+__device__ __forceinline__ double2 table_value(double r, const TableDev& T) {
+  if constexpr (KIND == GK_KIND_EXP) return exp_table(r, T);
+  else if constexpr (DEG == 3) return green_table<3>(r, T);
+  else return green_table_any(r, T);
+}
+
+template <int MO, int NPE, int KIND, int DEG>
+__global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(const FillArgs A) {
+  constexpr int W = GK_TEDGE_WARPS;
+  constexpr int IPT = 3 * NPE;
+  extern __shared__ double2 sE[];  // edge sums [W][ecap]
+  __shared__ double sw[W][MO];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t N = A.N;
+  double2* const myE = sE + warp * A.ecap;
+  unsigned long long nev = 0, n_low = 0, n_high = 0;
+
+  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    const size_t tr = tile / A.nblk, b = tile - tr * A.nblk;
+    const size_t p = A.row_begin + tr * W + warp;
+    if (p >= A.row_end) continue;  // warp-uniform
+    double ox[MO], oy[MO], oz[MO];
+#pragma unroll
+    for (int o = 0; o < MO; ++o) {
+      const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
+      const double2 zw = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o) + 1);
+      ox[o] = xy.x;
+      oy[o] = xy.y;
+      oz[o] = zw.x;
+      if (lane == 0) sw[warp][o] = zw.y;
+    }
+    const EdgeBlock B = A.eblk[b];
+    const double4 bp = A.bounds[p];
+    const double dx = bp.x - B.cx, dy = bp.y - B.cy, dz = bp.z - B.cz;
+    const double reach = A.r_far + bp.w + B.rho;
+    const bool far = dx * dx + dy * dy + dz * dz >= reach * reach * (1.0 + 1e-12);
+    double2* const zrow = A.z + (p - A.row_begin) * A.ldz;
+    const uint4* const cols = A.ecol + B.tb;
+    const uint32_t nb = B.te - B.tb;
+    __syncwarp();
+    if (far) {
+      const int nch = static_cast<int>((B.ne + 31) >> 5);
+      const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
+      double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
+      double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
+      for (int c = 0; c < nch; ++c) {
+        Acc<MO, false> acc;
+        acc.zero();
+#pragma unroll
+        for (int g = 0; g < NPE; ++g) {
+          const double2 pxy = cxy, pzw = czw;
+          const double4* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 32
+                                                : (c + 1 < nch ? (c + 1) * NPE * 32 : 0));
+          cxy = __ldg(reinterpret_cast<const double2*>(np));
+          czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
+#pragma unroll
+          for (int o = 0; o < MO; ++o) {
+            const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
+            const double r = __dmul_rn(d2, rsqrt_fast(d2));
+            n_high += r > A.T.r_max;  // out_of_range (the reference's accumulate_green)
+            acc.add_values(o, pzw.y, table_value<KIND, DEG>(r, A.T), make_double2(0.0, 0.0));
+          }
+        }
+        double2 e = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int o = 0; o < MO; ++o) {
+          const double w = sw[warp][o];
+          e.x = __fma_rn(w, acc.e[o].x, e.x);
+          e.y = __fma_rn(w, acc.e[o].y, e.y);
+        }
+        myE[c * 32 + lane] = e;
+      }
+      nev += static_cast<unsigned long long>(B.ne) * NPE * MO;
+      __syncwarp();
+      for (uint32_t jb = 0; jb < nb; jb += 32) {
+        const uint32_t j = jb + lane;
+        if (j < nb) {
+          const uint4 col = __ldg(cols + j);  // (q, e0 | e1 << 16, e2)
+          const double2 e0 = myE[col.y & 0xffffu], e1 = myE[col.y >> 16], e2 = myE[col.z];
+          __stcs(zrow + col.x, make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y));
+        }
+      }
+      __syncwarp();
+    } else {
+      unsigned nq = 0;
+      for (uint32_t jb = 0; jb < nb; jb += 32) {
+        const uint32_t j = jb + lane;
+        const bool valid = j < nb;
+        const size_t q = __ldg(cols + (valid ? j : nb - 1)).x;
+        const bool self = q == p;
+        nq += __popc(__ballot_sync(0xffffffffu, valid && !self));
+        Acc<MO, false> acc;
+        acc.zero();
+#pragma unroll 1
+        for (int i = 0; i < IPT; ++i) {
+          const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
+          const double2 pxy = __ldg(ptr), pzw = __ldg(ptr + 1);
+#pragma unroll
+          for (int o = 0; o < MO; ++o) {
+            const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
+            const double r = __dmul_rn(d2, rsqrt_fast(d2));
+            double2 v = table_value<KIND, DEG>(r, A.T);
+            const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
+            if (__any_sync(0xffffffffu, oob)) {
+              if (oob) {
+                if (!self && valid) {
+                  // the reference's eval_kernel fallback (evaluator.hpp:199-205)
+                  v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
+                  if (r > A.T.r_max) ++n_high; else ++n_low;
+                } else {
+                  v = make_double2(0.0, 0.0);
+                }
+              }
+            }
+            acc.add_values(o, pzw.y, v, make_double2(0.0, 0.0));
+          }
+        }
+        acc.finish([&](int o) { return sw[warp][o]; }, self, valid, A.z, A.z2,
+                   (p - A.row_begin) * A.ldz + q, A.counters + 2);
+      }
+      nev += static_cast<unsigned long long>(nq) * IPT * MO;
+    }
+    __syncwarp();
+  }
+  for (int o = 16; o; o >>= 1) {
+    n_low += __shfl_xor_sync(0xffffffffu, n_low, o);
+    n_high += __shfl_xor_sync(0xffffffffu, n_high, o);
+  }
+  if (lane == 0 && n_low) atomicAdd(A.counters, n_low);
+  if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
+  if (lane == 0 && nev) atomicAdd(A.counters + 3, nev);
+}
+
 // ------------------------------------------------ K3 with a shared-memory table
 //
 // North star part (2): the table a tile needs is held in shared memory.  Per
@@ -873,8 +1019,9 @@ void launch_v4(gk_ctx* ctx, FillArgs a, size_t smem) {
   launch_kernel(ctx, direct_kernel_v4<MO, IPT, KIND, ATT>, a, smem, 32 * warps_v4<KIND>());
 }
 
+// returns true when a shared-edge kernel ran (it counts its evaluations)
 template <int MO, int MODE, int KIND, int DEG, int ATT>
-void launch_one(gk_ctx* ctx, FillArgs a) {
+bool launch_one(gk_ctx* ctx, FillArgs a) {
   if constexpr (MODE == GK_MODE_DIRECT) {
     const size_t smem = kPhaseM * sizeof(double2) +
                         (ATT == 1 ? a.nhi * sizeof(double) : 0) +
@@ -892,6 +1039,7 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
         auto go = [&](auto kern) {
           a.ntiles = ((a.row_end - a.row_begin + GK_WARPS_V4 - 1) / GK_WARPS_V4) * a.nblk;
           launch_kernel(ctx, kern, a, esmem, 32 * GK_WARPS_V4);
+          return true;
         };
         switch (a.ipt) {
           case 3: return go(direct_edge_kernel<MO, 1, KIND, ATT>);
@@ -905,16 +1053,17 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
     }
     if (use_v4) {
       switch (a.ipt) {  // n = 1..5 Gauss points per edge: fully unrolled fast path
-        case 3: return launch_v4<MO, 3, KIND, ATT>(ctx, a, smem);
-        case 6: return launch_v4<MO, 6, KIND, ATT>(ctx, a, smem);
-        case 9: return launch_v4<MO, 9, KIND, ATT>(ctx, a, smem);
-        case 12: return launch_v4<MO, 12, KIND, ATT>(ctx, a, smem);
-        case 15: return launch_v4<MO, 15, KIND, ATT>(ctx, a, smem);
+        case 3: launch_v4<MO, 3, KIND, ATT>(ctx, a, smem); return false;
+        case 6: launch_v4<MO, 6, KIND, ATT>(ctx, a, smem); return false;
+        case 9: launch_v4<MO, 9, KIND, ATT>(ctx, a, smem); return false;
+        case 12: launch_v4<MO, 12, KIND, ATT>(ctx, a, smem); return false;
+        case 15: launch_v4<MO, 15, KIND, ATT>(ctx, a, smem); return false;
         default: break;
       }
     }
     set_tiling(ctx, a, kRowsPerTile, 2);
     launch_kernel(ctx, direct_kernel<MO, KIND, ATT, 2>, a, smem);
+    return false;
   } else {
     // GK_TABLE_SMEM: 0 = L1 kernel, 2 = always stage (tests), unset/1 = auto.
     // GK_TABLE_SMEM_BUDGET (bytes) shrinks the window budget (tests).  Read per
@@ -924,7 +1073,7 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
     if (staging == 0) {
       set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
       launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
-      return;
+      return false;
     }
     // shared-memory window sizing: whole table if it fits, else proportional caps
     constexpr bool want_e = KIND == GK_KIND_EXP || KIND == kKindPair;
@@ -936,7 +1085,8 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
     }
     StageArgs S{};
     const size_t nlk4 = (static_cast<size_t>(a.T.nlk) + 3) & ~size_t(3);
-    if (nlk4 * 4 + a.T.nrec * rec_bytes <= budget) {
+    const bool whole = nlk4 * 4 + a.T.nrec * rec_bytes <= budget;
+    if (whole) {
       S.whole = 1;
       S.lk_cap = static_cast<uint32_t>(nlk4);
       S.j_cap = a.T.nrec;
@@ -949,9 +1099,32 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
       // fall back to global reads: use the L1 kernel with its wider tiles
       const double est = a.T.nrec * a.window_est / (a.T.r_max - a.T.r_min);
       if (staging != 2 && est > 2.0 * static_cast<double>(j_cap)) {
+        // shared edges (K3e) instead of the L1 kernel: both read the table
+        // through L1; K3e 1.3-1.4x faster at S = 1e4 on C3/C4/C5.  Tables
+        // staged in shared memory (whole or per tile window) stay per
+        // triangle: faster than K3e through L1 (C5 S = 1e3: 158 vs 225 ms
+        // per 4096 rows).  Not when a test forces a staging path.
+        if constexpr (KIND != kKindPair) {
+          if (a.nblk > 0 && env == nullptr) {
+            const size_t esmem = static_cast<size_t>(GK_TEDGE_WARPS) * a.ecap * sizeof(double2);
+            auto go = [&](auto kern) {
+              a.ntiles = ((a.row_end - a.row_begin + GK_TEDGE_WARPS - 1) / GK_TEDGE_WARPS) * a.nblk;
+              launch_kernel(ctx, kern, a, esmem, 32 * GK_TEDGE_WARPS);
+              return true;
+            };
+            switch (a.ipt) {
+              case 3: return go(table_edge_kernel<MO, 1, KIND, DEG>);
+              case 6: return go(table_edge_kernel<MO, 2, KIND, DEG>);
+              case 9: return go(table_edge_kernel<MO, 3, KIND, DEG>);
+              case 12: return go(table_edge_kernel<MO, 4, KIND, DEG>);
+              case 15: return go(table_edge_kernel<MO, 5, KIND, DEG>);
+              default: fail(GK_ERR_RUNTIME, "shared-edge fill: n must be 1..5");
+            }
+          }
+        }
         set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
         launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
-        return;
+        return false;
       }
       S.j_cap = static_cast<uint32_t>(j_cap);
       S.lk_cap = static_cast<uint32_t>(((budget - j_cap * rec_bytes) / 4) & ~size_t(3));
@@ -971,37 +1144,38 @@ void launch_one(gk_ctx* ctx, FillArgs a) {
     k<<<static_cast<unsigned>(grid), 32 * kStagedWarps, smem, ctx->stream>>>(a, S);
     count_launches(1);
     GK_CUDA(cudaGetLastError());
+    return false;
   }
 }
 
 template <int MO, int KIND>
-void dispatch_att(gk_ctx* ctx, const FillArgs& a, int att) {
-  if (att == 1) launch_one<MO, GK_MODE_DIRECT, KIND, 0, 1>(ctx, a);
-  else if (att == 2) launch_one<MO, GK_MODE_DIRECT, KIND, 0, 2>(ctx, a);
-  else launch_one<MO, GK_MODE_DIRECT, KIND, 0, 0>(ctx, a);
+bool dispatch_att(gk_ctx* ctx, const FillArgs& a, int att) {
+  if (att == 1) return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 1>(ctx, a);
+  if (att == 2) return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 2>(ctx, a);
+  return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 0>(ctx, a);
 }
 
+// returns true when a shared-edge kernel ran (launch_fill)
 template <int MO>
-void dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, int att) {
+bool dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, int att) {
   if (mode == GK_MODE_DIRECT) {
-    if (kind == GK_KIND_GREEN) dispatch_att<MO, GK_KIND_GREEN>(ctx, a, att);
-    else if (kind == GK_KIND_EXP) dispatch_att<MO, GK_KIND_EXP>(ctx, a, att);
-    else dispatch_att<MO, kKindPair>(ctx, a, att);
-  } else {
-    if (kind == GK_KIND_EXP) launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, 0>(ctx, a);
-    else if (kind == GK_KIND_GREEN && degree == 3)
-      launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, 0>(ctx, a);
-    else if (kind == GK_KIND_GREEN) launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, 0>(ctx, a);
-    else if (degree == 3) launch_one<MO, GK_MODE_TABLE, kKindPair, 3, 0>(ctx, a);
-    else launch_one<MO, GK_MODE_TABLE, kKindPair, 0, 0>(ctx, a);
+    if (kind == GK_KIND_GREEN) return dispatch_att<MO, GK_KIND_GREEN>(ctx, a, att);
+    if (kind == GK_KIND_EXP) return dispatch_att<MO, GK_KIND_EXP>(ctx, a, att);
+    return dispatch_att<MO, kKindPair>(ctx, a, att);
   }
+  if (kind == GK_KIND_EXP) return launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, 0>(ctx, a);
+  if (kind == GK_KIND_GREEN && degree == 3)
+    return launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, 0>(ctx, a);
+  if (kind == GK_KIND_GREEN) return launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, 0>(ctx, a);
+  if (degree == 3) return launch_one<MO, GK_MODE_TABLE, kKindPair, 3, 0>(ctx, a);
+  return launch_one<MO, GK_MODE_TABLE, kKindPair, 0, 0>(ctx, a);
 }
 
 // one explicit instantiation per translation unit (fill_mo<m>.cu)
-extern template void dispatch_mo<1>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
-extern template void dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
-extern template void dispatch_mo<4>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
-extern template void dispatch_mo<6>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
-extern template void dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template bool dispatch_mo<1>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template bool dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template bool dispatch_mo<4>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template bool dispatch_mo<6>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template bool dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
 
 }  // namespace gk

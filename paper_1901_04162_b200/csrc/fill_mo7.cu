@@ -3,5 +3,5 @@
 #include "fill_kernels.cuh"
 
 namespace gk {
-template void dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+template bool dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
 }  // namespace gk

@@ -133,6 +133,12 @@ inline bool edge_fill_enabled() {
   return !(e && e[0] == '0');
 }
 
+// GK_TABLE_EDGE=0: table fills without shared edges (read per launch)
+inline bool table_edge_enabled() {
+  const char* e = std::getenv("GK_TABLE_EDGE");
+  return !(e && e[0] == '0');
+}
+
 // GK_EDGE=2: the shared-edge path also for small meshes (tests)
 inline bool edge_fill_forced() {
   const char* e = std::getenv("GK_EDGE");

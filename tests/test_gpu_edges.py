@@ -147,3 +147,62 @@ def test_edge_blocks_skip_meshes_without_shared_edges(gk, oracle, monkeypatch):
     mesh = gk.TriangleMesh(verts, tris)
     dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi)
     assert info["work_ratio"] >= 0.85 and rep.evaluations == rep.actual_calls
+
+
+def _table(gk, oracle, dm, k, S, r_min=None):
+    lo, hi = dm.distance_range()
+    med = gk.Medium(lambda0=2 * np.pi / k)
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=r_min or lo, r_max=hi, samples_per_wavelength=S),
+                       med)
+    d = t.download()
+    return t, oracle.evaluator(oracle.make_plan(d["abscissae"], d["zeros"]), t.k)
+
+
+@pytest.mark.parametrize("m,n", [(6, 4), (7, 5)])
+def test_table_edge_fill_parity(gk, oracle, forced, m, n):
+    """K3e: the paper's table on shared edges (a table too large for shared
+    memory, so the edge kernel runs) against the CPU direct fill within the
+    interpolation bound, and against the CPU table fill on the same plan
+    within rounding"""
+    from oracle.pyoracle import TABLE
+    mesh = sphere(gk, 3)
+    k = 2 * np.pi
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+    t, ev = _table(gk, oracle, dm, k, 10000)
+    zt, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+    zt = zt.cpu().numpy()
+    ref_d, _ = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, DIRECT, k, threads=8)
+    ref_t, rep_t = oracle.fill_rows(mesh.vertices, mesh.triangles, m, n, TABLE, k, ev=ev, threads=8)
+    B_t = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, ev, k, ULPS)
+    B_d = oracle.entry_bounds(mesh.vertices, mesh.triangles, m, n, None, k, ULPS)
+    assert np.all(np.abs(zt - ref_d) <= B_t)
+    assert np.all(np.abs(zt - ref_t) <= B_d)
+    assert rep.evaluations < 0.8 * rep.actual_calls
+    assert rep.fallback_calls == rep_t.fallback_calls == 0
+
+
+def test_table_edge_fallback_counts_match_reference(gk, oracle, forced):
+    """a table starting above the nearest pairs: near tiles fall back exactly
+    like the reference (evaluator.hpp:199-205); far tiles never do"""
+    from oracle.pyoracle import TABLE
+    mesh = sphere(gk, 3)
+    k = 2 * np.pi
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    assert dm.edge_info()["r_far"] > 0.03
+    t, ev = _table(gk, oracle, dm, k, 10000, r_min=0.03)
+    zt, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+    ref_t, rep_t = oracle.fill_rows(mesh.vertices, mesh.triangles, 6, 4, TABLE, k, ev=ev, threads=8)
+    assert rep.fallback_calls == rep_t.fallback_calls > 0
+    assert rep.evaluations < 0.8 * rep.actual_calls
+    B_d = oracle.entry_bounds(mesh.vertices, mesh.triangles, 6, 4, None, k, ULPS)
+    assert np.all(np.abs(zt.cpu().numpy() - ref_t) <= B_d)
+
+
+def test_table_edge_not_used_when_table_fits_shared_memory(gk, forced):
+    """S = 1e3 on this mesh stages the whole table: per-triangle kernel"""
+    mesh = sphere(gk, 3)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=1000))
+    _, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+    assert rep.evaluations == rep.actual_calls
