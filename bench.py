@@ -315,12 +315,19 @@ def main():
         return ms, fill_ms
 
     def performed_evals(mode):
-        if mode != "direct":  # table and per-triangle fills perform every reference call
+        if mode == "direct_pertri":  # the per-triangle kernel performs every reference call
             return 3 * m * n * rows * (N - 1)
         if not rows:
             return 0
         os.environ["GK_EDGE"] = "1"
-        _, rep = gk.fill_rows(dmesh, gk.Mode.DIRECT, k=k, row_begin=rb, row_end=re, out=Z)
+        table = None
+        if mode.startswith("table"):
+            S = args.S if mode == "table" else int(mode.split("_S")[1])
+            lo, hi = global_range()
+            table = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
+                                                     samples_per_wavelength=S), medium, ctx=ctx)
+        _, rep = gk.fill_rows(dmesh, gk.Mode.TABLE if table else gk.Mode.DIRECT, table=table,
+                              k=k, row_begin=rb, row_end=re, out=Z)
         return rep.evaluations
 
     # roofline denominator: FP64 DFMA peak measured on this device now
@@ -344,7 +351,7 @@ def main():
         else:
             ms, fill_ms = timed(mode, steps, 1)
         # evaluations the kernel performs per launch (fewer than the
-        # reference's calls on the shared-edge path): one synchronous fill
+        # reference's calls on the shared-edge paths): one synchronous fill
         # outside the timed region reports them
         performed = performed_evals(mode)
         evals_all = performed
