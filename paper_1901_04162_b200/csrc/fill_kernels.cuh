@@ -386,14 +386,17 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
 }
 
 // One direct term w K(|o - P|) into acc[o] (the v4 loop body).
+// r_floor: the shared-edge far path asserts its precondition r >= r_far
 template <int MO, int KIND, int ATT>
 __device__ __forceinline__ void direct_term(Acc<MO, false>& acc, int o, double ox, double oy,
                                             double oz, double2 pxy, double2 pzw,
                                             const FillArgs& A, const double2* tab,
-                                            const PhaseAtt& pa, const double* att) {
+                                            const PhaseAtt& pa, const double* att,
+                                            double r_floor = 0.0) {
   const double d2 = dist2(ox, oy, oz, pxy.x, pxy.y, pzw.x);
   const double y = rsqrt_fast(d2);
   const double r = __dmul_rn(d2, y);
+  GK_DASSERT(r >= r_floor * (1.0 - 1e-12));
   double w = pzw.y;
   double2 cs;
   if constexpr (ATT == 1) {
@@ -462,6 +465,7 @@ __global__ void __launch_bounds__(32 * GK_WARPS_V4, 1) direct_edge_kernel(const 
     __syncwarp();
     if (far) {
       const int nch = static_cast<int>((B.ne + 31) >> 5);
+      GK_DASSERT(B.ne <= static_cast<uint32_t>(A.ecap) && B.tb < B.te && B.te <= N);
       const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
       double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
       double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
@@ -477,7 +481,8 @@ __global__ void __launch_bounds__(32 * GK_WARPS_V4, 1) direct_edge_kernel(const 
           czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
 #pragma unroll
           for (int o = 0; o < MO; ++o)
-            direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att);
+            direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att,
+                                       A.r_far);
         }
         double2 e = make_double2(0.0, 0.0);
 #pragma unroll
@@ -497,6 +502,7 @@ __global__ void __launch_bounds__(32 * GK_WARPS_V4, 1) direct_edge_kernel(const 
         const uint32_t j = jb + lane;
         if (j < nb) {
           const uint4 col = __ldg(cols + j);  // (q, e0 | e1 << 16, e2)
+          GK_DASSERT(col.x < N && (col.y & 0xffffu) < B.ne && (col.y >> 16) < B.ne && col.z < B.ne);
           const double2 e0 = myE[col.y & 0xffffu], e1 = myE[col.y >> 16], e2 = myE[col.z];
           __stcs(zrow + col.x, make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y));
         }
@@ -672,6 +678,7 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
     __syncwarp();
     if (far) {
       const int nch = static_cast<int>((B.ne + 31) >> 5);
+      GK_DASSERT(B.ne <= static_cast<uint32_t>(A.ecap) && B.tb < B.te && B.te <= N);
       const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
       double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
       double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
@@ -689,6 +696,7 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
           for (int o = 0; o < MO; ++o) {
             const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
             const double r = __dmul_rn(d2, rsqrt_fast(d2));
+            GK_DASSERT(r >= A.r_far * (1.0 - 1e-12));
             n_high += r > A.T.r_max;  // out_of_range (the reference's accumulate_green)
             acc.add_values(o, pzw.y, table_value<KIND, DEG>(r, A.T), make_double2(0.0, 0.0));
           }
@@ -708,6 +716,7 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
         const uint32_t j = jb + lane;
         if (j < nb) {
           const uint4 col = __ldg(cols + j);  // (q, e0 | e1 << 16, e2)
+          GK_DASSERT(col.x < N && (col.y & 0xffffu) < B.ne && (col.y >> 16) < B.ne && col.z < B.ne);
           const double2 e0 = myE[col.y & 0xffffu], e1 = myE[col.y >> 16], e2 = myE[col.z];
           __stcs(zrow + col.x, make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y));
         }
