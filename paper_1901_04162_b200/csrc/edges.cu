@@ -93,7 +93,8 @@ void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris)
     if (c >= 1 && c * 32 <= kEdgeCap) cap = static_cast<size_t>(c) * 32;
   }
   mesh->ecap = static_cast<int>(cap);
-  if (N > (size_t(1) << 30)) return;
+  // the edge kernels unroll the n points of an edge (n = 1..5)
+  if (N > (size_t(1) << 30) || n > 5) return;
 
   // global edge ids: edges bucketed by their lower vertex (CSR), distinct
   // upper vertices numbered within each bucket
