@@ -631,9 +631,19 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 // reference's fallback (evaluator.hpp:199-205).  launch_fill takes this path
 // only when r_min <= r_far, so a far pair never falls back below the table:
 // the fallback counts stay the reference's.
+// 16 warps with the edge-point loop unrolled by 2 (128 registers, a few
+// spilled): the L1/L2 gathers are latency-bound, so warps beat unrolling --
+// C5 S = 1e4, 4096 rows: 12 warps fully unrolled 219 ms, 12 x 1 200 ms,
+// 16 x 5 192 ms, 16 x 1 176 ms, 16 x 2 175 ms, 20 x 1 180 ms, 24 x 1 181 ms,
+// 32 x 1 193 ms (scripts/build_variant.sh)
 #ifndef GK_TEDGE_WARPS
-#define GK_TEDGE_WARPS 12
+#define GK_TEDGE_WARPS 16
 #endif
+#ifndef GK_TEDGE_GUNROLL
+#define GK_TEDGE_GUNROLL 2  // unroll of the edge-point loop
+#endif
+#define GK_PRAGMA(x) _Pragma(#x)
+#define GK_UNROLL(n) GK_PRAGMA(unroll n)
 
 template <int KIND, int DEG>
 __device__ __forceinline__ double2 table_value(double r, const TableDev& T) {
@@ -685,7 +695,7 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
       for (int c = 0; c < nch; ++c) {
         Acc<MO, false> acc;
         acc.zero();
-#pragma unroll
+        GK_UNROLL(GK_TEDGE_GUNROLL)
         for (int g = 0; g < NPE; ++g) {
           const double2 pxy = cxy, pzw = czw;
           const double4* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 32
@@ -1028,6 +1038,25 @@ void launch_v4(gk_ctx* ctx, FillArgs a, size_t smem) {
   launch_kernel(ctx, direct_kernel_v4<MO, IPT, KIND, ATT>, a, smem, 32 * warps_v4<KIND>());
 }
 
+// K3e launch (edge sums in shared memory, the table through L1)
+template <int MO, int KIND, int DEG>
+bool launch_table_edge(gk_ctx* ctx, FillArgs a) {
+  const size_t esmem = static_cast<size_t>(GK_TEDGE_WARPS) * a.ecap * sizeof(double2);
+  auto go = [&](auto kern) {
+    a.ntiles = ((a.row_end - a.row_begin + GK_TEDGE_WARPS - 1) / GK_TEDGE_WARPS) * a.nblk;
+    launch_kernel(ctx, kern, a, esmem, 32 * GK_TEDGE_WARPS);
+    return true;
+  };
+  switch (a.ipt) {
+    case 3: return go(table_edge_kernel<MO, 1, KIND, DEG>);
+    case 6: return go(table_edge_kernel<MO, 2, KIND, DEG>);
+    case 9: return go(table_edge_kernel<MO, 3, KIND, DEG>);
+    case 12: return go(table_edge_kernel<MO, 4, KIND, DEG>);
+    case 15: return go(table_edge_kernel<MO, 5, KIND, DEG>);
+    default: fail(GK_ERR_RUNTIME, "shared-edge fill: n must be 1..5");
+  }
+}
+
 // returns true when a shared-edge kernel ran (it counts its evaluations)
 template <int MO, int MODE, int KIND, int DEG, int ATT>
 bool launch_one(gk_ctx* ctx, FillArgs a) {
@@ -1079,6 +1108,8 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
     // launch so a test can exercise every path in one process.
     const char* env = std::getenv("GK_TABLE_SMEM");
     const int staging = env ? std::atoi(env) : 1;
+    if constexpr (KIND != kKindPair)  // GK_TABLE_EDGE=2: K3e whenever the blocks allow (A/B)
+      if (a.nblk > 0 && table_edge_forced()) return launch_table_edge<MO, KIND, DEG>(ctx, a);
     if (staging == 0) {
       set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
       launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
@@ -1113,24 +1144,8 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
         // staged in shared memory (whole or per tile window) stay per
         // triangle: faster than K3e through L1 (C5 S = 1e3: 158 vs 225 ms
         // per 4096 rows).  Not when a test forces a staging path.
-        if constexpr (KIND != kKindPair) {
-          if (a.nblk > 0 && env == nullptr) {
-            const size_t esmem = static_cast<size_t>(GK_TEDGE_WARPS) * a.ecap * sizeof(double2);
-            auto go = [&](auto kern) {
-              a.ntiles = ((a.row_end - a.row_begin + GK_TEDGE_WARPS - 1) / GK_TEDGE_WARPS) * a.nblk;
-              launch_kernel(ctx, kern, a, esmem, 32 * GK_TEDGE_WARPS);
-              return true;
-            };
-            switch (a.ipt) {
-              case 3: return go(table_edge_kernel<MO, 1, KIND, DEG>);
-              case 6: return go(table_edge_kernel<MO, 2, KIND, DEG>);
-              case 9: return go(table_edge_kernel<MO, 3, KIND, DEG>);
-              case 12: return go(table_edge_kernel<MO, 4, KIND, DEG>);
-              case 15: return go(table_edge_kernel<MO, 5, KIND, DEG>);
-              default: fail(GK_ERR_RUNTIME, "shared-edge fill: n must be 1..5");
-            }
-          }
-        }
+        if constexpr (KIND != kKindPair)
+          if (a.nblk > 0 && env == nullptr) return launch_table_edge<MO, KIND, DEG>(ctx, a);
         set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
         launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
         return false;

@@ -139,6 +139,11 @@ inline bool table_edge_enabled() {
   return !(e && e[0] == '0');
 }
 
+inline bool table_edge_forced() {
+  const char* e = std::getenv("GK_TABLE_EDGE");
+  return e && e[0] == '2';
+}
+
 // GK_EDGE=2: the shared-edge path also for small meshes (tests)
 inline bool edge_fill_forced() {
   const char* e = std::getenv("GK_EDGE");

@@ -7,7 +7,7 @@
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 NAME=$1; shift
-OUT=$ROOT/scripts/_variants/$NAME; mkdir -p "$OUT"
+OUT=${TMPDIR:-/tmp}/gk_variants/$NAME; mkdir -p "$OUT" "$ROOT/scripts/_variants"
 B=$ROOT/paper_1901_04162_b200/_build
 C=$ROOT/paper_1901_04162_b200/csrc
 python -m paper_1901_04162_b200.build >/dev/null
