@@ -419,9 +419,18 @@ __device__ __forceinline__ void direct_term(Acc<MO, false>& acc, int o, double o
 // (coalesced streaming stores).  Nearer tiles take the per-triangle loop on
 // the reference's own points.  On a closed mesh the far path performs ~0.55
 // of the reference's evaluations.
+#ifndef GK_EDGE_WARPS
+#define GK_EDGE_WARPS 12
+#endif
+#ifndef GK_EDGE_GUNROLL
+#define GK_EDGE_GUNROLL 5  // unroll of the edge-point loop (n <= 5: full)
+#endif
+#define GK_PRAGMA(x) _Pragma(#x)
+#define GK_UNROLL(n) GK_PRAGMA(unroll n)
+
 template <int MO, int NPE, int KIND, int ATT>
-__global__ void __launch_bounds__(32 * GK_WARPS_V4, 1) direct_edge_kernel(const FillArgs A) {
-  constexpr int W = GK_WARPS_V4;
+__global__ void __launch_bounds__(32 * GK_EDGE_WARPS, 1) direct_edge_kernel(const FillArgs A) {
+  constexpr int W = GK_EDGE_WARPS;
   constexpr int IPT = 3 * NPE;
   extern __shared__ double2 tab[];  // phase [kPhaseM] | edge sums [W][ecap] | attenuation
   __shared__ double sw[W][MO];
@@ -472,7 +481,7 @@ __global__ void __launch_bounds__(32 * GK_WARPS_V4, 1) direct_edge_kernel(const 
       for (int c = 0; c < nch; ++c) {
         Acc<MO, false> acc;
         acc.zero();
-#pragma unroll
+        GK_UNROLL(GK_EDGE_GUNROLL)
         for (int g = 0; g < NPE; ++g) {
           const double2 pxy = cxy, pzw = czw;
           const double4* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 32
@@ -642,8 +651,6 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 #ifndef GK_TEDGE_GUNROLL
 #define GK_TEDGE_GUNROLL 2  // unroll of the edge-point loop
 #endif
-#define GK_PRAGMA(x) _Pragma(#x)
-#define GK_UNROLL(n) GK_PRAGMA(unroll n)
 
 template <int KIND, int DEG>
 __device__ __forceinline__ double2 table_value(double r, const TableDev& T) {
@@ -1071,12 +1078,12 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
     // shared-edge path (edges.cu): single kind, lossless or phase-coupled
     // attenuation, n = 1..5; launch_fill leaves nblk = 0 where it does not pay
     if constexpr (KIND != kKindPair && ATT != 2) {
-      const size_t esmem = kPhaseM * sizeof(double2) + GK_WARPS_V4 * a.ecap * sizeof(double2) +
+      const size_t esmem = kPhaseM * sizeof(double2) + GK_EDGE_WARPS * a.ecap * sizeof(double2) +
                            (ATT == 1 ? a.nhi * sizeof(double) : 0);
       if (a.nblk > 0) {
         auto go = [&](auto kern) {
-          a.ntiles = ((a.row_end - a.row_begin + GK_WARPS_V4 - 1) / GK_WARPS_V4) * a.nblk;
-          launch_kernel(ctx, kern, a, esmem, 32 * GK_WARPS_V4);
+          a.ntiles = ((a.row_end - a.row_begin + GK_EDGE_WARPS - 1) / GK_EDGE_WARPS) * a.nblk;
+          launch_kernel(ctx, kern, a, esmem, 32 * GK_EDGE_WARPS);
           return true;
         };
         switch (a.ipt) {
