@@ -91,9 +91,10 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   }
   // shared edges (edges.cu) pay where the blocks share most edges (closed
   // meshes) and are small against the mesh (N >= 4096: on C2, 1280 triangles
-  // in 6 blocks, most tiles are near and the fill is 1.4x slower); the edge
-  // kernel runs one kind at a time, n = 1..5, lossless or with the
-  // phase-coupled attenuation (its few ahi entries fit beside the edge sums)
+  // in 6 blocks, most tiles are near and the fill is 1.4x slower); n = 1..5,
+  // lossless or with the phase-coupled attenuation (its ahi entries, <= 512
+  // for every kind so that the fused pair stays bitwise equal to the
+  // separate fills, fit beside the edge sums)
   // table mode (K3e): far pairs are >= r_far >= r_min apart, so they never
   // fall back below the table (the fallback counts stay the reference's); a
   // far pair above r_max is still detected (the fill fails with out_of_range
@@ -101,9 +102,9 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   // GK_TABLE_EDGE=0 keeps the per-triangle table kernels.
   const bool table_edges = mode == GK_MODE_TABLE && table_edge_enabled() && table &&
                            table->dev.r_min <= mesh->r_far;
-  if ((mode == GK_MODE_DIRECT || table_edges) && kind != 2 && edge_fill_enabled() &&
+  if ((mode == GK_MODE_DIRECT || table_edges) && edge_fill_enabled() &&
       mesh->nblk > 0 && mesh->edge_ratio < 0.85 && mesh->n <= 5 &&
-      (att == 0 || (att == 1 && a.nhi <= 2048)) && (mesh->N >= 4096 || edge_fill_forced())) {
+      (att == 0 || (att == 1 && a.nhi <= 512)) && (mesh->N >= 4096 || edge_fill_forced())) {
     a.eblk = mesh->eblk.p;
     a.ep = mesh->ep.p;
     a.ecol = mesh->ecol.p;

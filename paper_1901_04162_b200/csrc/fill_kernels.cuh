@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
 // One direct term w K(|o - P|) into acc[o] (the v4 loop body).
 // r_floor: the shared-edge far path asserts its precondition r >= r_far
 template <int MO, int KIND, int ATT>
-__device__ __forceinline__ void direct_term(Acc<MO, false>& acc, int o, double ox, double oy,
+__device__ __forceinline__ void direct_term(Acc<MO, KIND == kKindPair>& acc, int o, double ox, double oy,
                                             double oz, double2 pxy, double2 pzw,
                                             const FillArgs& A, const double2* tab,
                                             const PhaseAtt& pa, const double* att,
@@ -428,23 +428,29 @@ __device__ __forceinline__ void direct_term(Acc<MO, false>& acc, int o, double o
 #define GK_PRAGMA(x) _Pragma(#x)
 #define GK_UNROLL(n) GK_PRAGMA(unroll n)
 
+// the fused Exp + Green pair carries two sums per edge: 8 warps (as v4's pair)
+template <int KIND>
+__host__ __device__ constexpr int edge_warps() { return KIND == kKindPair ? 8 : GK_EDGE_WARPS; }
+
 template <int MO, int NPE, int KIND, int ATT>
-__global__ void __launch_bounds__(32 * GK_EDGE_WARPS, 1) direct_edge_kernel(const FillArgs A) {
-  constexpr int W = GK_EDGE_WARPS;
+__global__ void __launch_bounds__(32 * edge_warps<KIND>(), 1) direct_edge_kernel(const FillArgs A) {
+  constexpr int W = edge_warps<KIND>();
+  constexpr bool PAIR = KIND == kKindPair;
+  constexpr int NS = PAIR ? 2 : 1;  // edge sums per edge
   constexpr int IPT = 3 * NPE;
-  extern __shared__ double2 tab[];  // phase [kPhaseM] | edge sums [W][ecap] | attenuation
+  extern __shared__ double2 tab[];  // phase [kPhaseM] | edge sums [W][NS][ecap] | attenuation
   __shared__ double sw[W][MO];
   __shared__ uint64_t bar;
   stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
   double2* const sE = tab + kPhaseM;
-  double* att = reinterpret_cast<double*>(sE + W * A.ecap);
+  double* att = reinterpret_cast<double*>(sE + W * NS * A.ecap);
   if constexpr (ATT == 1)
     for (int i = threadIdx.x; i < A.nhi; i += blockDim.x) att[i] = A.ahi[i];
   const PhaseAtt pa{att, A.nhi, A.q1, A.q2, A.q3, A.q4};
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t N = A.N;
-  double2* const myE = sE + warp * A.ecap;
+  double2* const myE = sE + warp * NS * A.ecap;  // [NS][ecap]: Exp (or the kind), Green
   unsigned long long nev = 0;
 
   for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
@@ -479,7 +485,7 @@ __global__ void __launch_bounds__(32 * GK_EDGE_WARPS, 1) direct_edge_kernel(cons
       double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
       double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
       for (int c = 0; c < nch; ++c) {
-        Acc<MO, false> acc;
+        Acc<MO, PAIR> acc;
         acc.zero();
         GK_UNROLL(GK_EDGE_GUNROLL)
         for (int g = 0; g < NPE; ++g) {
@@ -493,16 +499,21 @@ __global__ void __launch_bounds__(32 * GK_EDGE_WARPS, 1) direct_edge_kernel(cons
             direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att,
                                        A.r_far);
         }
-        double2 e = make_double2(0.0, 0.0);
+        double2 e = make_double2(0.0, 0.0), eg = make_double2(0.0, 0.0);
 #pragma unroll
         for (int o = 0; o < MO; ++o) {
           const double w = sw[warp][o];
           e.x = __fma_rn(w, acc.e[o].x, e.x);
           e.y = __fma_rn(w, acc.e[o].y, e.y);
+          if constexpr (PAIR) {
+            eg.x = __fma_rn(w, acc.g[o].x, eg.x);
+            eg.y = __fma_rn(w, acc.g[o].y, eg.y);
+          }
         }
         myE[c * 32 + lane] = e;
+        if constexpr (PAIR) myE[A.ecap + c * 32 + lane] = eg;
       }
-      nev += static_cast<unsigned long long>(B.ne) * NPE * MO;
+      nev += static_cast<unsigned long long>(B.ne) * NPE * MO * NS;
       __syncwarp();
       // Z[p][q] = sum of q's three edge sums.  Far tiles never hold the self
       // pair (p's centroid lies inside its own block's sphere) nor a
@@ -514,6 +525,12 @@ __global__ void __launch_bounds__(32 * GK_EDGE_WARPS, 1) direct_edge_kernel(cons
           GK_DASSERT(col.x < N && (col.y & 0xffffu) < B.ne && (col.y >> 16) < B.ne && col.z < B.ne);
           const double2 e0 = myE[col.y & 0xffffu], e1 = myE[col.y >> 16], e2 = myE[col.z];
           __stcs(zrow + col.x, make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y));
+          if constexpr (PAIR) {
+            const double2* G = myE + A.ecap;
+            const double2 g0 = G[col.y & 0xffffu], g1 = G[col.y >> 16], g2 = G[col.z];
+            __stcs(A.z2 + (p - A.row_begin) * A.ldz + col.x,
+                   make_double2(g0.x + g1.x + g2.x, g0.y + g1.y + g2.y));
+          }
         }
       }
       __syncwarp();  // myE is rewritten by the next tile
@@ -525,7 +542,7 @@ __global__ void __launch_bounds__(32 * GK_EDGE_WARPS, 1) direct_edge_kernel(cons
         const bool valid = j < nb;
         const size_t q = __ldg(cols + (valid ? j : nb - 1)).x;
         nq += __popc(__ballot_sync(0xffffffffu, valid && q != p));
-        Acc<MO, false> acc;
+        Acc<MO, PAIR> acc;
         acc.zero();
 #pragma unroll 1
         for (int i = 0; i < IPT; ++i) {
@@ -538,7 +555,7 @@ __global__ void __launch_bounds__(32 * GK_EDGE_WARPS, 1) direct_edge_kernel(cons
         acc.finish([&](int o) { return sw[warp][o]; }, q == p, valid, A.z, A.z2,
                    (p - A.row_begin) * A.ldz + q, A.counters + 2);
       }
-      nev += static_cast<unsigned long long>(nq) * IPT * MO;
+      nev += static_cast<unsigned long long>(nq) * IPT * MO * NS;
     }
     __syncwarp();
   }
@@ -652,22 +669,30 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 #define GK_TEDGE_GUNROLL 2  // unroll of the edge-point loop
 #endif
 
+// the kind's table value v (the fused pair: Exp in v, Green in vg)
 template <int KIND, int DEG>
-__device__ __forceinline__ double2 table_value(double r, const TableDev& T) {
-  if constexpr (KIND == GK_KIND_EXP) return exp_table(r, T);
-  else if constexpr (DEG == 3) return green_table<3>(r, T);
-  else return green_table_any(r, T);
+__device__ __forceinline__ void table_values(double r, const TableDev& T, double2& v, double2& vg) {
+  if constexpr (KIND == kKindPair) pair_table<DEG>(r, T, v, vg);
+  else if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, T);
+  else if constexpr (DEG == 3) v = green_table<3>(r, T);
+  else v = green_table_any(r, T);
 }
 
+// the fused pair carries two sums per edge: 8 warps
+template <int KIND>
+__host__ __device__ constexpr int tedge_warps() { return KIND == kKindPair ? 8 : GK_TEDGE_WARPS; }
+
 template <int MO, int NPE, int KIND, int DEG>
-__global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(const FillArgs A) {
-  constexpr int W = GK_TEDGE_WARPS;
+__global__ void __launch_bounds__(32 * tedge_warps<KIND>(), 1) table_edge_kernel(const FillArgs A) {
+  constexpr int W = tedge_warps<KIND>();
+  constexpr bool PAIR = KIND == kKindPair;
+  constexpr int NS = PAIR ? 2 : 1;
   constexpr int IPT = 3 * NPE;
-  extern __shared__ double2 sE[];  // edge sums [W][ecap]
+  extern __shared__ double2 sE[];  // edge sums [W][NS][ecap]
   __shared__ double sw[W][MO];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t N = A.N;
-  double2* const myE = sE + warp * A.ecap;
+  double2* const myE = sE + warp * NS * A.ecap;
   unsigned long long nev = 0, n_low = 0, n_high = 0;
 
   for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
@@ -700,7 +725,7 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
       double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
       double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
       for (int c = 0; c < nch; ++c) {
-        Acc<MO, false> acc;
+        Acc<MO, PAIR> acc;
         acc.zero();
         GK_UNROLL(GK_TEDGE_GUNROLL)
         for (int g = 0; g < NPE; ++g) {
@@ -714,20 +739,27 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
             const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
             const double r = __dmul_rn(d2, rsqrt_fast(d2));
             GK_DASSERT(r >= A.r_far * (1.0 - 1e-12));
-            n_high += r > A.T.r_max;  // out_of_range (the reference's accumulate_green)
-            acc.add_values(o, pzw.y, table_value<KIND, DEG>(r, A.T), make_double2(0.0, 0.0));
+            n_high += (r > A.T.r_max) ? NS : 0;  // out_of_range (the reference's accumulate_green)
+            double2 v, vg = make_double2(0.0, 0.0);
+            table_values<KIND, DEG>(r, A.T, v, vg);
+            acc.add_values(o, pzw.y, v, vg);
           }
         }
-        double2 e = make_double2(0.0, 0.0);
+        double2 e = make_double2(0.0, 0.0), eg = make_double2(0.0, 0.0);
 #pragma unroll
         for (int o = 0; o < MO; ++o) {
           const double w = sw[warp][o];
           e.x = __fma_rn(w, acc.e[o].x, e.x);
           e.y = __fma_rn(w, acc.e[o].y, e.y);
+          if constexpr (PAIR) {
+            eg.x = __fma_rn(w, acc.g[o].x, eg.x);
+            eg.y = __fma_rn(w, acc.g[o].y, eg.y);
+          }
         }
         myE[c * 32 + lane] = e;
+        if constexpr (PAIR) myE[A.ecap + c * 32 + lane] = eg;
       }
-      nev += static_cast<unsigned long long>(B.ne) * NPE * MO;
+      nev += static_cast<unsigned long long>(B.ne) * NPE * MO * NS;
       __syncwarp();
       for (uint32_t jb = 0; jb < nb; jb += 32) {
         const uint32_t j = jb + lane;
@@ -736,6 +768,12 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
           GK_DASSERT(col.x < N && (col.y & 0xffffu) < B.ne && (col.y >> 16) < B.ne && col.z < B.ne);
           const double2 e0 = myE[col.y & 0xffffu], e1 = myE[col.y >> 16], e2 = myE[col.z];
           __stcs(zrow + col.x, make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y));
+          if constexpr (PAIR) {
+            const double2* G = myE + A.ecap;
+            const double2 g0 = G[col.y & 0xffffu], g1 = G[col.y >> 16], g2 = G[col.z];
+            __stcs(A.z2 + (p - A.row_begin) * A.ldz + col.x,
+                   make_double2(g0.x + g1.x + g2.x, g0.y + g1.y + g2.y));
+          }
         }
       }
       __syncwarp();
@@ -747,7 +785,7 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
         const size_t q = __ldg(cols + (valid ? j : nb - 1)).x;
         const bool self = q == p;
         nq += __popc(__ballot_sync(0xffffffffu, valid && !self));
-        Acc<MO, false> acc;
+        Acc<MO, PAIR> acc;
         acc.zero();
 #pragma unroll 1
         for (int i = 0; i < IPT; ++i) {
@@ -757,26 +795,32 @@ __global__ void __launch_bounds__(32 * GK_TEDGE_WARPS, 1) table_edge_kernel(cons
           for (int o = 0; o < MO; ++o) {
             const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
             const double r = __dmul_rn(d2, rsqrt_fast(d2));
-            double2 v = table_value<KIND, DEG>(r, A.T);
+            double2 v, vg = make_double2(0.0, 0.0);
+            table_values<KIND, DEG>(r, A.T, v, vg);
             const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
             if (__any_sync(0xffffffffu, oob)) {
               if (oob) {
                 if (!self && valid) {
                   // the reference's eval_kernel fallback (evaluator.hpp:199-205)
-                  v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
-                  if (r > A.T.r_max) ++n_high; else ++n_low;
+                  if constexpr (PAIR) {
+                    v = analytic_sincos(GK_KIND_EXP, A.T.k_re, A.T.k_im, r);
+                    vg = analytic_sincos(GK_KIND_GREEN, A.T.k_re, A.T.k_im, r);
+                  } else {
+                    v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
+                  }
+                  if (r > A.T.r_max) n_high += NS; else n_low += NS;
                 } else {
-                  v = make_double2(0.0, 0.0);
+                  v = vg = make_double2(0.0, 0.0);
                 }
               }
             }
-            acc.add_values(o, pzw.y, v, make_double2(0.0, 0.0));
+            acc.add_values(o, pzw.y, v, vg);
           }
         }
         acc.finish([&](int o) { return sw[warp][o]; }, self, valid, A.z, A.z2,
                    (p - A.row_begin) * A.ldz + q, A.counters + 2);
       }
-      nev += static_cast<unsigned long long>(nq) * IPT * MO;
+      nev += static_cast<unsigned long long>(nq) * IPT * MO * NS;
     }
     __syncwarp();
   }
@@ -1048,10 +1092,11 @@ void launch_v4(gk_ctx* ctx, FillArgs a, size_t smem) {
 // K3e launch (edge sums in shared memory, the table through L1)
 template <int MO, int KIND, int DEG>
 bool launch_table_edge(gk_ctx* ctx, FillArgs a) {
-  const size_t esmem = static_cast<size_t>(GK_TEDGE_WARPS) * a.ecap * sizeof(double2);
+  constexpr int W = tedge_warps<KIND>();
+  const size_t esmem = static_cast<size_t>(W) * (KIND == kKindPair ? 2 : 1) * a.ecap * sizeof(double2);
   auto go = [&](auto kern) {
-    a.ntiles = ((a.row_end - a.row_begin + GK_TEDGE_WARPS - 1) / GK_TEDGE_WARPS) * a.nblk;
-    launch_kernel(ctx, kern, a, esmem, 32 * GK_TEDGE_WARPS);
+    a.ntiles = ((a.row_end - a.row_begin + W - 1) / W) * a.nblk;
+    launch_kernel(ctx, kern, a, esmem, 32 * W);
     return true;
   };
   switch (a.ipt) {
@@ -1077,13 +1122,15 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
     }();
     // shared-edge path (edges.cu): single kind, lossless or phase-coupled
     // attenuation, n = 1..5; launch_fill leaves nblk = 0 where it does not pay
-    if constexpr (KIND != kKindPair && ATT != 2) {
-      const size_t esmem = kPhaseM * sizeof(double2) + GK_EDGE_WARPS * a.ecap * sizeof(double2) +
+    if constexpr (ATT != 2) {
+      constexpr int W = edge_warps<KIND>();
+      const size_t esmem = kPhaseM * sizeof(double2) +
+                           W * (KIND == kKindPair ? 2 : 1) * a.ecap * sizeof(double2) +
                            (ATT == 1 ? a.nhi * sizeof(double) : 0);
       if (a.nblk > 0) {
         auto go = [&](auto kern) {
-          a.ntiles = ((a.row_end - a.row_begin + GK_EDGE_WARPS - 1) / GK_EDGE_WARPS) * a.nblk;
-          launch_kernel(ctx, kern, a, esmem, 32 * GK_EDGE_WARPS);
+          a.ntiles = ((a.row_end - a.row_begin + W - 1) / W) * a.nblk;
+          launch_kernel(ctx, kern, a, esmem, 32 * W);
           return true;
         };
         switch (a.ipt) {
@@ -1115,8 +1162,8 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
     // launch so a test can exercise every path in one process.
     const char* env = std::getenv("GK_TABLE_SMEM");
     const int staging = env ? std::atoi(env) : 1;
-    if constexpr (KIND != kKindPair)  // GK_TABLE_EDGE=2: K3e whenever the blocks allow (A/B)
-      if (a.nblk > 0 && table_edge_forced()) return launch_table_edge<MO, KIND, DEG>(ctx, a);
+    // GK_TABLE_EDGE=2: K3e whenever the blocks allow (A/B)
+    if (a.nblk > 0 && table_edge_forced()) return launch_table_edge<MO, KIND, DEG>(ctx, a);
     if (staging == 0) {
       set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
       launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
@@ -1151,8 +1198,7 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
         // staged in shared memory (whole or per tile window) stay per
         // triangle: faster than K3e through L1 (C5 S = 1e3: 158 vs 225 ms
         // per 4096 rows).  Not when a test forces a staging path.
-        if constexpr (KIND != kKindPair)
-          if (a.nblk > 0 && env == nullptr) return launch_table_edge<MO, KIND, DEG>(ctx, a);
+        if (a.nblk > 0 && env == nullptr) return launch_table_edge<MO, KIND, DEG>(ctx, a);
         set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
         launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
         return false;

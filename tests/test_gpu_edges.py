@@ -206,3 +206,26 @@ def test_table_edge_not_used_when_table_fits_shared_memory(gk, forced):
     t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=1000))
     _, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
     assert rep.evaluations == rep.actual_calls
+
+
+@pytest.mark.parametrize("mode", ["direct", "lossy", "table"])
+def test_edge_fused_pair_equals_separate_fills(gk, forced, mode):
+    """gk_fill_rows_pair on shared edges: Exp and Green from one pass, bitwise
+    equal to the two separate shared-edge fills (direct, C4's lossy medium,
+    and the table read through L1)"""
+    import torch
+    mesh = sphere(gk, 3)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    med = gk.Medium(1.0, 4.0, 1.0, -0.4) if mode == "lossy" else gk.Medium()
+    kw = dict(k=gk.wavenumber(med))
+    if mode == "table":
+        lo, hi = dm.distance_range()
+        kw = dict(table=gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
+                                                         samples_per_wavelength=10000), med))
+    md = gk.Mode.TABLE if mode == "table" else gk.Mode.DIRECT
+    ze, zg, rep = gk.fill_rows_pair(dm, md, **kw)
+    e, re_ = gk.fill_rows(dm, md, kind=gk.KernelKind.PlainExp, **kw)
+    g, rg = gk.fill_rows(dm, md, kind=gk.KernelKind.GreenOverR, **kw)
+    assert torch.equal(ze, e) and torch.equal(zg, g)
+    assert rep.actual_calls == 2 * rg.actual_calls and rep.fallback_calls == 0
+    assert rep.evaluations == re_.evaluations + rg.evaluations < 0.8 * rep.actual_calls
