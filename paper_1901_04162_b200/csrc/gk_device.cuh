@@ -76,14 +76,17 @@ struct TableDev {
   double t_eff, inv_t;
 };
 
-// Shared-edge fill (direct_edge_kernel): a block is a contiguous range of
-// source triangles [tb, te) and the distinct edges its triangles use
-// (ne <= kEdgeCap), whose points sit at ep[c0 * n * 32 ...] as [chunk][point]
-// [32 lanes].  (cx, cy, cz, rho) bounds every inner point of the block.
-// edges per block: 11 warp-wide chunks by default (GK_EDGE_CHUNKS at mesh
-// creation: 1..12).  12 x 352 edge sums + the 128 KB phase table stay under
-// the 196 KB shared-memory carveout, leaving 60 KB of L1 for the block's points
-// (12 chunks: 228 KB carveout, 28 KB of L1, L1 hit 52 %)
+// Shared-edge fills (direct_edge_kernel, table_edge_kernel; edges.cu): a
+// block is the range [tb, te) of block positions (a bisection order of the
+// source triangles, or the mesh order) and the distinct edges its triangles
+// use (ne <= the mesh's edge cap), whose points sit at ep[c0 * n * 32 ...] as
+// [chunk][point][32 lanes].  (cx, cy, cz, rho) bounds every inner point of
+// the block.
+//
+// Edge cap: 11 warp-wide chunks (352 edges) by default, 1..12 with
+// GK_EDGE_CHUNKS at mesh creation.  12 warps x 352 edge sums + the 128 KB
+// phase table stay under the 196 KB shared-memory carveout, leaving 60 KB of
+// L1 for the block's points (12 chunks: 228 KB carveout, 28 KB of L1).
 constexpr int kEdgeCap = 384;
 constexpr int kEdgeChunksDefault = 11;
 struct EdgeBlock {

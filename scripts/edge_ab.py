@@ -46,8 +46,6 @@ def main():
         ra = fill(dm, k, rows, Za)
         os.environ["GK_EDGE"] = "2"  # forced: small meshes too
         rb = fill(dm, k, rows, Zb)
-        if "--rfar-q" in sys.argv:
-            print(f"r_far_q={info.get('r_far_q')}", end=" ")
         d = (Zb - Za).abs()
         rel = (d / Za.abs().clamp_min(1e-300)).max().item()
         R = info["edges"] / (3.0 * N)
