@@ -104,6 +104,7 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
                            table->dev.r_min <= mesh->r_far;
   if ((mode == GK_MODE_DIRECT || table_edges) && edge_fill_enabled() &&
       mesh->nblk > 0 && mesh->edge_ratio < 0.85 && mesh->n <= 5 &&
+      mesh->r_far < 0.25 * mesh->diameter &&  // else few far tiles (e.g. coordinates far from the origin)
       (att == 0 || (att == 1 && a.nhi <= 512)) && (mesh->N >= 4096 || edge_fill_forced())) {
     a.eblk = mesh->eblk.p;
     a.ep = mesh->ep.p;
