@@ -225,6 +225,18 @@ typedef struct gk_mesh_edge_info {
   int ordered;                 /* 1: blocks follow a spatial (bisection) order of the triangles */
 } gk_mesh_edge_info;
 gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out);
+/* The host part of the shared-edge blocks, without a device (tests): cut the
+   nt triangles into blocks of at most 32 * chunks distinct edges, in mesh
+   order (order_mode 0), in a bisection order of the centroids (1), or the
+   more compact of the two (-1).  Outputs (caller-allocated):
+   order[nt] = the triangle at each block position; edge_index[3 nt] = the
+   block-local edge index of each side of the triangle at each position;
+   block_start[nt + 1] = first position of each block followed by nt;
+   block_edges[nt] = distinct edges of each block; *nblocks; *ordered. */
+gk_status gk_edge_blocks_plan(const double* vertices, size_t nv, const uint32_t* triangles,
+                              size_t nt, int chunks, int order_mode, uint32_t* order,
+                              uint32_t* edge_index, uint32_t* block_start,
+                              uint32_t* block_edges, uint64_t* nblocks, int* ordered);
 
 /* K1: min and max quadrature-point pair distance over observation rows
    [row_begin,row_end) and every source q != p (replaces max_vertex_distance

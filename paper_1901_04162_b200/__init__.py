@@ -6,7 +6,8 @@ all in hand-written CUDA (libgk.so, C ABI in include/gk/gk.h).
 """
 from .gktab import (Context, DeviceMesh, DeviceTable, ErrorSweepReport, EvalStatus, FillReport,
                     InterpMethod, KernelKind, Medium, Mode, QuadratureSpec, SamplingConfig,
-                    TriangleMesh, accumulate_batch, bench_compare, compare_fills, eval_batch,
+                    TriangleMesh, accumulate_batch, bench_compare, compare_fills, edge_blocks_plan,
+                    eval_batch,
                     eval_batch_async, fill_matrix, fill_rows, fill_rows_host, fill_rows_pair,
                     generate_plate_mesh, generate_sphere_mesh, jitter, predicted_calls,
                     wavenumber)
@@ -16,7 +17,8 @@ from ._lib import (DomainError, GkError, InvalidArgument, OutOfRange, OverflowEr
 __all__ = [
     "Context", "DeviceMesh", "DeviceTable", "ErrorSweepReport", "EvalStatus", "FillReport",
     "InterpMethod", "KernelKind", "Medium", "Mode", "QuadratureSpec", "SamplingConfig",
-    "TriangleMesh", "accumulate_batch", "bench_compare", "compare_fills", "eval_batch",
+    "TriangleMesh", "accumulate_batch", "bench_compare", "compare_fills", "edge_blocks_plan",
+    "eval_batch",
     "eval_batch_async", "fill_matrix", "fill_rows", "fill_rows_host", "fill_rows_pair",
     "generate_plate_mesh", "generate_sphere_mesh", "jitter", "predicted_calls", "wavenumber",
     "DomainError", "GkError", "InvalidArgument", "OutOfRange", "OverflowErrorGk",

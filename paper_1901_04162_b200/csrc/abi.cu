@@ -719,6 +719,36 @@ gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out) {
   });
 }
 
+gk_status gk_edge_blocks_plan(const double* verts, size_t nv, const uint32_t* tris, size_t nt,
+                              int chunks, int order_mode, uint32_t* order, uint32_t* edge_index,
+                              uint32_t* block_start, uint32_t* block_edges, uint64_t* nblocks,
+                              int* ordered) {
+  return guarded([&] {
+    need(verts && tris && order && edge_index && block_start && block_edges && nblocks && ordered,
+         GK_ERR_INVALID_ARGUMENT, "null argument");
+    need(chunks >= 1 && chunks * 32 <= gk::kEdgeCap, GK_ERR_INVALID_ARGUMENT,
+         "gk_edge_blocks_plan: chunks must be 1..12");
+    need(order_mode >= -1 && order_mode <= 1, GK_ERR_INVALID_ARGUMENT, "bad order_mode");
+    gk::validate_mesh(verts, nv, tris, nt);
+    need(nt >= 1, GK_ERR_INVALID_ARGUMENT, "empty mesh");
+    const gk::EdgePlan P = gk::plan_edge_blocks(verts, nv, tris, nt, 32 * static_cast<size_t>(chunks),
+                                                order_mode);
+    for (size_t j = 0; j < nt; ++j) {
+      order[j] = P.order[j];
+      edge_index[3 * j] = P.eidx[j].x;
+      edge_index[3 * j + 1] = P.eidx[j].y;
+      edge_index[3 * j + 2] = P.eidx[j].z;
+    }
+    for (size_t b = 0; b < P.blocks.size(); ++b) {
+      block_start[b] = P.blocks[b].tb;
+      block_edges[b] = P.blocks[b].ne;
+    }
+    block_start[P.blocks.size()] = static_cast<uint32_t>(nt);
+    *nblocks = P.blocks.size();
+    *ordered = P.ordered ? 1 : 0;
+  });
+}
+
 gk_status gk_mesh_points_download(const gk_mesh* mesh, double* outer, double* inner) {
   return guarded([&] {
     need(mesh != nullptr, GK_ERR_INVALID_ARGUMENT, "null mesh");

@@ -79,23 +79,8 @@ __global__ void edge_delta_kernel(const double4* __restrict__ inner, size_t N, i
 
 }  // namespace
 
-void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris) {
-  const size_t N = mesh->N, nv = mesh->nv;
-  const int n = mesh->n;
-  mesh->nblk = 0;
-  mesh->edge_ratio = 1.0;
-  mesh->r_far = INFINITY;
-  if (const char* e = std::getenv("GK_EDGE"))
-    if (e[0] == '0') return;
-  size_t cap = 32 * kEdgeChunksDefault;
-  if (const char* e = std::getenv("GK_EDGE_CHUNKS")) {  // block size (tests, A/B)
-    const long c = std::atol(e);
-    if (c >= 1 && c * 32 <= kEdgeCap) cap = static_cast<size_t>(c) * 32;
-  }
-  mesh->ecap = static_cast<int>(cap);
-  // the edge kernels unroll the n points of an edge (n = 1..5)
-  if (N > (size_t(1) << 30) || n > 5) return;
-
+EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, size_t N,
+                          size_t cap, int order_mode) {
   // global edge ids: edges bucketed by their lower vertex (CSR), distinct
   // upper vertices numbered within each bucket
   std::vector<uint32_t> start(nv + 1, 0);
@@ -292,10 +277,45 @@ void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris)
     std::sort(cuts.begin(), cuts.end());
   }
   Blocks Rm = make_blocks(&sorder, &cuts);
-  bool ordered = Rm.rho_mean < 0.75 * R.rho_mean;
-  if (const char* e = std::getenv("GK_EDGE_ORDER"))  // 0: mesh order, 1: bisection order (A/B)
-    ordered = e[0] == '1';
+  bool ordered = order_mode < 0 ? Rm.rho_mean < 0.75 * R.rho_mean : order_mode == 1;
   if (ordered) R = std::move(Rm);
+  EdgePlan P;
+  P.blocks = std::move(R.blocks);
+  P.owner = std::move(R.owner);
+  P.eidx = std::move(R.eidx);
+  P.gslot = std::move(R.gslot);
+  P.edges = R.edges;
+  P.rho_mean = R.rho_mean;
+  P.ordered = ordered;
+  P.order.resize(N);
+  for (size_t j = 0; j < N; ++j) P.order[j] = ordered ? sorder[j] : static_cast<uint32_t>(j);
+  return P;
+}
+
+void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris) {
+  const size_t N = mesh->N, nv = mesh->nv;
+  const int n = mesh->n;
+  mesh->nblk = 0;
+  mesh->edge_ratio = 1.0;
+  mesh->r_far = INFINITY;
+  if (const char* e = std::getenv("GK_EDGE"))
+    if (e[0] == '0') return;
+  size_t cap = 32 * kEdgeChunksDefault;
+  if (const char* e = std::getenv("GK_EDGE_CHUNKS")) {  // block size (tests, A/B)
+    const long c = std::atol(e);
+    if (c >= 1 && c * 32 <= kEdgeCap) cap = static_cast<size_t>(c) * 32;
+  }
+  mesh->ecap = static_cast<int>(cap);
+  // the edge kernels unroll the n points of an edge (n = 1..5)
+  if (N > (size_t(1) << 30) || n > 5) return;
+  int order_mode = -1;
+  if (const char* e = std::getenv("GK_EDGE_ORDER"))  // 0: mesh order, 1: bisection order (A/B)
+    order_mode = e[0] == '1' ? 1 : 0;
+  EdgePlan R = plan_edge_blocks(verts, nv, tris, N, cap, order_mode);
+  const bool ordered = R.ordered;
+  double X = 0.0;
+  for (size_t i = 0; i < 3 * nv; ++i) X = std::max(X, std::fabs(verts[i]));
+  (void)X;
   const std::vector<EdgeBlock>& blocks = R.blocks;
   const std::vector<unsigned long long>& owner = R.owner;
 
@@ -316,7 +336,7 @@ void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris)
   std::vector<uint4> ecol(N);
   for (size_t j = 0; j < N; ++j) {
     const ushort4 e = R.eidx[j];
-    ecol[j] = make_uint4(ordered ? sorder[j] : static_cast<uint32_t>(j),
+    ecol[j] = make_uint4(R.order[j],
                          static_cast<uint32_t>(e.x) | (static_cast<uint32_t>(e.y) << 16), e.z, 0u);
   }
   GK_CUDA(cudaMemcpyAsync(mesh->ecol.p, ecol.data(), N * sizeof(uint4), cudaMemcpyHostToDevice, st));

@@ -165,8 +165,25 @@ void validate_mesh(const double* v, size_t nv, const uint32_t* t, size_t nt);
 // kernels launched by abi.cu (defined in build.cu / fill.cu / eval.cu)
 void launch_points(gk_mesh* mesh, const double* d_verts, const uint32_t* d_tris,
                    cudaStream_t s);
-// shared-edge blocks of a mesh whose points launch_points has produced
-// (edges.cu); synchronises the context stream
+// shared-edge blocks (edges.cu).  plan_edge_blocks is the host part: blocks
+// of at most `cap` distinct edges over the triangles in mesh order or in a
+// bisection order of the centroids (order_mode -1: the more compact, 0: mesh
+// order, 1: bisection); order[j] is the triangle at block position j, eidx[j]
+// its three block-local edge indices, owner[slot] = (t << 3) | (side << 1) |
+// padding of every edge slot, gslot[3 t + s] the slot of side s of t.
+struct EdgePlan {
+  std::vector<EdgeBlock> blocks;
+  std::vector<unsigned long long> owner;
+  std::vector<ushort4> eidx;
+  std::vector<uint32_t> gslot, order;
+  uint64_t edges = 0;
+  double rho_mean = 0.0;
+  bool ordered = false;
+};
+EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, size_t N,
+                          size_t cap, int order_mode);
+// the device part for a mesh whose points launch_points has produced;
+// synchronises the context stream
 void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris);
 // max over vertex pairs of |a - b|^2 (reference summation order) -> *d2_bits
 void launch_max_vertex_d2(const double* verts, size_t nv, unsigned long long* d2_bits,

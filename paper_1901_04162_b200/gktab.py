@@ -451,6 +451,27 @@ def eval_batch_async(kind: KernelKind, radii, out, status: EvalStatus,
           "eval_batch")
 
 
+def edge_blocks_plan(mesh: TriangleMesh, chunks: int = 11, order_mode: int = -1) -> dict:
+    """The host part of the shared-edge blocks (gk_edge_blocks_plan; no
+    device needed): block positions, triangle order and block-local edge
+    indices."""
+    nt = mesh.triangle_count()
+    order = np.zeros(nt, np.uint32)
+    eidx = np.zeros((nt, 3), np.uint32)
+    start = np.zeros(nt + 1, np.uint32)
+    nedge = np.zeros(nt, np.uint32)
+    nb = C.c_uint64()
+    ordered = C.c_int()
+    check(lib().gk_edge_blocks_plan(mesh.vertices.ctypes.data, mesh.vertices.shape[0],
+                                    mesh.triangles.ctypes.data, nt, chunks, order_mode,
+                                    order.ctypes.data, eidx.ctypes.data, start.ctypes.data,
+                                    nedge.ctypes.data, C.byref(nb), C.byref(ordered)),
+          "edge_blocks_plan")
+    n = nb.value
+    return dict(order=order, edge_index=eidx, block_start=np.append(start[:n], nt),
+                block_edges=nedge[:n], ordered=bool(ordered.value))
+
+
 class DeviceMesh:
     """A mesh resident on the device with its quadrature points (K0)."""
 
