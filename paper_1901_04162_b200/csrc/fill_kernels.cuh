@@ -422,6 +422,12 @@ __device__ __forceinline__ void direct_term(Acc<MO, KIND == kKindPair>& acc, int
 #ifndef GK_EDGE_WARPS
 #define GK_EDGE_WARPS 12
 #endif
+#ifndef GK_EDGE_ALLNEAR
+#define GK_EDGE_ALLNEAR 0  // A/B: every tile through the near path
+#endif
+#ifndef GK_EDGE_NEAR_UNROLL
+#define GK_EDGE_NEAR_UNROLL 1  // unroll of the near path's point loop
+#endif
 #ifndef GK_EDGE_GUNROLL
 #define GK_EDGE_GUNROLL 5  // unroll of the edge-point loop (n <= 5: full)
 #endif
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(32 * edge_warps<KIND>(), 1) direct_edge_kernel
     // sides >= 0) with a margin far above the rounding of either side
     const double dx = bp.x - B.cx, dy = bp.y - B.cy, dz = bp.z - B.cz;
     const double reach = A.r_far + bp.w + B.rho;
-    const bool far = dx * dx + dy * dy + dz * dz >= reach * reach * (1.0 + 1e-12);
+    const bool far = !GK_EDGE_ALLNEAR && dx * dx + dy * dy + dz * dz >= reach * reach * (1.0 + 1e-12);
     double2* const zrow = A.z + (p - A.row_begin) * A.ldz;
     const uint4* const cols = A.ecol + B.tb;
     const uint32_t nb = B.te - B.tb;
@@ -544,10 +550,17 @@ __global__ void __launch_bounds__(32 * edge_warps<KIND>(), 1) direct_edge_kernel
         nq += __popc(__ballot_sync(0xffffffffu, valid && q != p));
         Acc<MO, PAIR> acc;
         acc.zero();
-#pragma unroll 1
+        // the next point is in flight while the current one is evaluated
+        const double2* base = reinterpret_cast<const double2*>(A.inner + q);
+        double2 nxy = __ldg(base), nzw = __ldg(base + 1);
+        GK_UNROLL(GK_EDGE_NEAR_UNROLL)
         for (int i = 0; i < IPT; ++i) {
-          const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
-          const double2 pxy = __ldg(ptr), pzw = __ldg(ptr + 1);
+          const double2 pxy = nxy, pzw = nzw;
+          if (i + 1 < IPT) {
+            const double2* ptr = base + 2 * static_cast<size_t>(i + 1) * N;
+            nxy = __ldg(ptr);
+            nzw = __ldg(ptr + 1);
+          }
 #pragma unroll
           for (int o = 0; o < MO; ++o)
             direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att);
