@@ -1193,6 +1193,12 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
     StageArgs S{};
     const size_t nlk4 = (static_cast<size_t>(a.T.nlk) + 3) & ~size_t(3);
     const bool whole = nlk4 * 4 + a.T.nrec * rec_bytes <= budget;
+    // a table too large to stage whole but small enough to stay L1-resident
+    // (<= 300 KB of records) goes to K3e: C4 at S = 1e3 (233 KB) 145 vs 180 ms
+    // windowed-staged; C3 (548 KB) and C5 (1.1 MB) stay staged (343 vs 311,
+    // 184 vs 158 ms per 4096 rows)
+    if (a.nblk > 0 && env == nullptr && !whole && a.T.nrec * rec_bytes <= 300 * 1024)
+      return launch_table_edge<MO, KIND, DEG>(ctx, a);
     if (whole) {
       S.whole = 1;
       S.lk_cap = static_cast<uint32_t>(nlk4);

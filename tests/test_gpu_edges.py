@@ -198,14 +198,16 @@ def test_table_edge_fallback_counts_match_reference(gk, oracle, forced):
     assert np.all(np.abs(zt.cpu().numpy() - ref_t) <= B_d)
 
 
-def test_table_edge_not_used_when_table_fits_shared_memory(gk, forced):
-    """S = 1e3 on this mesh stages the whole table: per-triangle kernel"""
+def test_table_edge_dispatch_by_table_size(gk, forced):
+    """a table staged whole in shared memory stays per triangle (S = 300);
+    one too large for that but L1-sized (<= 300 KB of records) takes K3e"""
     mesh = sphere(gk, 3)
     dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
     lo, hi = dm.distance_range()
-    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=1000))
-    _, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
-    assert rep.evaluations == rep.actual_calls
+    for S, shared in ((300, False), (1000, True)):
+        t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S))
+        _, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
+        assert (rep.evaluations < rep.actual_calls) == shared, (S, t.info.nodes)
 
 
 @pytest.mark.parametrize("mode", ["direct", "lossy", "table"])
