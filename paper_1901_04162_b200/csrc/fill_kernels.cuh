@@ -425,9 +425,6 @@ __device__ __forceinline__ void direct_term(Acc<MO, KIND == kKindPair>& acc, int
 #ifndef GK_EDGE_ALLNEAR
 #define GK_EDGE_ALLNEAR 0  // A/B: every tile through the near path
 #endif
-#ifndef GK_EDGE_NEAR_UNROLL
-#define GK_EDGE_NEAR_UNROLL 1  // unroll of the near path's point loop
-#endif
 #ifndef GK_EDGE_GUNROLL
 #define GK_EDGE_GUNROLL 5  // unroll of the edge-point loop (n <= 5: full)
 #endif
@@ -550,17 +547,10 @@ __global__ void __launch_bounds__(32 * edge_warps<KIND>(), 1) direct_edge_kernel
         nq += __popc(__ballot_sync(0xffffffffu, valid && q != p));
         Acc<MO, PAIR> acc;
         acc.zero();
-        // the next point is in flight while the current one is evaluated
-        const double2* base = reinterpret_cast<const double2*>(A.inner + q);
-        double2 nxy = __ldg(base), nzw = __ldg(base + 1);
-        GK_UNROLL(GK_EDGE_NEAR_UNROLL)
+#pragma unroll 1
         for (int i = 0; i < IPT; ++i) {
-          const double2 pxy = nxy, pzw = nzw;
-          if (i + 1 < IPT) {
-            const double2* ptr = base + 2 * static_cast<size_t>(i + 1) * N;
-            nxy = __ldg(ptr);
-            nzw = __ldg(ptr + 1);
-          }
+          const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
+          const double2 pxy = __ldg(ptr), pzw = __ldg(ptr + 1);
 #pragma unroll
           for (int o = 0; o < MO; ++o)
             direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att);
