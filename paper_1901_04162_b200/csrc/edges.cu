@@ -50,8 +50,9 @@ __global__ void edge_gather_kernel(const double4* __restrict__ inner, size_t N, 
 }
 
 // max over the sides (t, s) that do not own their edge slot of
-// |inner point g of (t, s) - evaluated point n-1-g of the slot| (the reversed
-// parameterisation pairs g with n-1-g; the weights are equal)
+// |inner point g of (t, s) - its twin among the slot's evaluated points|: the
+// reversed parameterisation pairs g with n-1-g (the weights are equal), a
+// side running the owner's way (gslot bit 31) pairs g with g
 __global__ void edge_delta_kernel(const double4* __restrict__ inner, size_t N, int n,
                                   const uint32_t* __restrict__ gslot,
                                   const unsigned long long* __restrict__ owner,
@@ -63,11 +64,12 @@ __global__ void edge_delta_kernel(const double4* __restrict__ inner, size_t N, i
     const int g = static_cast<int>(i - ts * n);
     const size_t t = ts / 3;
     const int s = static_cast<int>(ts - 3 * t);
-    const uint32_t slot = gslot[ts];
+    const uint32_t slot = gslot[ts] & 0x7fffffffu;
+    const int gq = (gslot[ts] >> 31) ? g : n - 1 - g;  // the twin point of the edge's owner
     const unsigned long long mine = (static_cast<unsigned long long>(t) << 3) | (s << 1);
     if (owner[slot] != mine) {
       const double4 P = inner[static_cast<size_t>(s * n + g) * N + t];
-      const double4 Q = ep[((slot >> 5) * static_cast<size_t>(n) + (n - 1 - g)) * 32 + (slot & 31)];
+      const double4 Q = ep[((slot >> 5) * static_cast<size_t>(n) + gq) * 32 + (slot & 31)];
       const double dx = P.x - Q.x, dy = P.y - Q.y, dz = P.z - Q.z;
       d = sqrt(dx * dx + dy * dy + dz * dz);
       if (P.w != Q.w) d = INFINITY;  // weights must match exactly (symmetric rule)
@@ -175,7 +177,13 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
           R.owner.push_back((static_cast<unsigned long long>(t) << 3) | (static_cast<unsigned>(s) << 1));
         }
         li[s] = static_cast<uint16_t>(local[e]);
-        R.gslot[3 * t + s] = static_cast<uint32_t>(first_slot + local[e]);
+        // bit 31: this side runs the same way as the edge's owner (a mesh
+        // without a consistent orientation): its points pair g with g
+        const size_t slot = first_slot + local[e];
+        const unsigned long long o = R.owner[slot];
+        const uint32_t a_owner = tris[3 * (o >> 3) + ((o >> 1) & 3)];
+        const bool same = a_owner == tris[3 * t + s] && (o >> 3) != t;
+        R.gslot[3 * t + s] = static_cast<uint32_t>(slot) | (same ? 0x80000000u : 0u);
       }
       R.eidx[j] = make_ushort4(li[0], li[1], li[2], 0);
     }
