@@ -1,4 +1,5 @@
-// edges.cu -- shared-edge blocks for the direct fill (direct_edge_kernel).
+// edges.cu -- shared-edge blocks for the direct and table fills
+// (direct_edge_kernel, table_edge_kernel in fill_kernels.cuh).
 //
 // The reference evaluates, for every source triangle q, the n Gauss points of
 // each of its 3 edges (inner_points, matfill.hpp:132-144) against every outer
@@ -6,8 +7,9 @@
 // belongs to two triangles, traversed in opposite directions, so the same n
 // points (up to the rounding of a + (b - a) x vs b + (a - b) x', with the
 // Gauss-Legendre weights symmetric, quadrature.hpp:85-110) are evaluated
-// twice per outer point.  A block groups a contiguous range of source
-// triangles; each distinct edge of the block is evaluated once per outer
+// twice per outer point.  A block groups a range of source triangles in a
+// spatial (recursive-bisection) order, or in mesh order when that is about
+// as compact; each distinct edge of the block is evaluated once per outer
 // point, in the orientation of the first block triangle that uses it (those
 // points are copied from the reference-exact inner points, so they are
 // bit-identical for that triangle), and Z[p][q] is the sum of q's three edge
