@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 // spilled): the L1/L2 gathers are latency-bound, so warps beat unrolling --
 // C5 S = 1e4, 4096 rows: 12 warps fully unrolled 219 ms, 12 x 1 200 ms,
 // 16 x 5 192 ms, 16 x 1 176 ms, 16 x 2 175 ms, 20 x 1 180 ms, 24 x 1 181 ms,
-// 32 x 1 193 ms (scripts/build_variant.sh)
+// 32 x 1 193 ms, 14 x 2 191 ms, 18 x 1 190 ms (scripts/build_variant.sh)
 #ifndef GK_TEDGE_WARPS
 #define GK_TEDGE_WARPS 16
 #endif
