@@ -1059,7 +1059,9 @@ __global__ void __launch_bounds__(32 * kStagedWarps, 1)
 
 template <class K>
 void launch_kernel(gk_ctx* ctx, K kernel, const FillArgs& a, size_t smem, int threads = kThreads) {
-  if (smem > 48 * 1024)
+  // opt in whenever dynamic shared memory is used: the 48 KB default covers
+  // static + dynamic together (48 KB of edge sums + 768 B of weights failed)
+  if (smem > 0)
     GK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   int per_sm = 0;

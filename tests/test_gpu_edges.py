@@ -257,3 +257,23 @@ def test_edge_fill_parity_inconsistent_orientation(gk, oracle, forced):
     dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi)
     assert 0 < info["delta"] < 1e-15
     assert rep.evaluations < 0.8 * rep.actual_calls
+
+
+@pytest.mark.parametrize("chunks", ["1", "6", "12"])
+def test_edge_block_sizes_launch_and_agree(gk, monkeypatch, chunks):
+    """every block size launches (6 chunks put the K3e edge sums at exactly
+    48 KB of dynamic shared memory beside the static weights) and agrees with
+    the per-triangle kernels"""
+    monkeypatch.setenv("GK_EDGE", "2")
+    monkeypatch.setenv("GK_EDGE_CHUNKS", chunks)
+    mesh = sphere(gk, 3)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=10000))
+    for md, kw in ((gk.Mode.DIRECT, dict(k=2 * np.pi)), (gk.Mode.TABLE, dict(table=t))):
+        z, rep = gk.fill_rows(dm, md, **kw)
+        monkeypatch.setenv("GK_EDGE", "0")
+        z0, _ = gk.fill_rows(dm, md, **kw)
+        monkeypatch.setenv("GK_EDGE", "2")
+        rel = ((z - z0).abs() / z0.abs().clamp_min(1e-300)).max().item()
+        assert rel < 1e-12, (md, rel)
