@@ -1132,7 +1132,9 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
       const size_t esmem = kPhaseM * sizeof(double2) +
                            W * (KIND == kKindPair ? 2 : 1) * a.ecap * sizeof(double2) +
                            (ATT == 1 ? a.nhi * sizeof(double) : 0);
-      if (a.nblk > 0) {
+      // the 227 KB opt-in limit (the pair's two sums per edge at 12 chunks
+      // with many attenuation entries would exceed it): per-triangle then
+      if (a.nblk > 0 && esmem + 2048 <= 227 * 1024) {
         auto go = [&](auto kern) {
           a.ntiles = ((a.row_end - a.row_begin + W - 1) / W) * a.nblk;
           launch_kernel(ctx, kern, a, esmem, 32 * W);
