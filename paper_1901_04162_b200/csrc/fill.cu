@@ -95,13 +95,13 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   // lossless or with the phase-coupled attenuation (its ahi entries, <= 512
   // for every kind so that the fused pair stays bitwise equal to the
   // separate fills, fit beside the edge sums)
-  // table mode (K3e): far pairs are >= r_far >= r_min apart, so they never
-  // fall back below the table (the fallback counts stay the reference's); a
-  // far pair above r_max is still detected (the fill fails with out_of_range
-  // as the reference's does, its count then covering the shared evaluations).
+  // table mode (K3e): far pairs are >= max(r_far, r_min) apart, so they
+  // never fall back below the table (the fallback counts stay the
+  // reference's); a far pair above r_max is still detected (the fill fails
+  // with out_of_range as the reference's does, its count then covering the
+  // shared evaluations).
   // GK_TABLE_EDGE=0 keeps the per-triangle table kernels.
-  const bool table_edges = mode == GK_MODE_TABLE && table_edge_enabled() && table &&
-                           table->dev.r_min <= mesh->r_far;
+  const bool table_edges = mode == GK_MODE_TABLE && table_edge_enabled() && table;
   if ((mode == GK_MODE_DIRECT || table_edges) && edge_fill_enabled() &&
       mesh->nblk > 0 && mesh->edge_ratio < 0.85 && mesh->n <= 5 &&
       mesh->r_far < 0.25 * mesh->diameter &&  // else few far tiles (e.g. coordinates far from the origin)
@@ -111,7 +111,8 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
     a.ecol = mesh->ecol.p;
     a.nblk = mesh->nblk;
     a.ecap = mesh->ecap;
-    a.r_far = mesh->r_far;
+    // table mode: far pairs must also stay >= r_min (no fallback there)
+    a.r_far = table_edges ? std::fmax(mesh->r_far, table->dev.r_min) : mesh->r_far;
   }
   const int degree = table ? table->dev.degree : 3;
   switch (mesh->m) {

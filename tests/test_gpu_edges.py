@@ -181,15 +181,17 @@ def test_table_edge_fill_parity(gk, oracle, forced, m, n):
     assert rep.fallback_calls == rep_t.fallback_calls == 0
 
 
-def test_table_edge_fallback_counts_match_reference(gk, oracle, forced):
+@pytest.mark.parametrize("r_min", [0.03, 0.08])
+def test_table_edge_fallback_counts_match_reference(gk, oracle, forced, r_min):
     """a table starting above the nearest pairs: near tiles fall back exactly
-    like the reference (evaluator.hpp:199-205); far tiles never do"""
+    like the reference (evaluator.hpp:199-205); far tiles (>= max(r_far,
+    r_min) apart: r_far = 0.044 m here) never do"""
     from oracle.pyoracle import TABLE
     mesh = sphere(gk, 3)
     k = 2 * np.pi
     dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
-    assert dm.edge_info()["r_far"] > 0.03
-    t, ev = _table(gk, oracle, dm, k, 10000, r_min=0.03)
+    assert 0.03 < dm.edge_info()["r_far"] < 0.08
+    t, ev = _table(gk, oracle, dm, k, 10000, r_min=r_min)
     zt, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
     ref_t, rep_t = oracle.fill_rows(mesh.vertices, mesh.triangles, 6, 4, TABLE, k, ev=ev, threads=8)
     assert rep.fallback_calls == rep_t.fallback_calls > 0
@@ -277,3 +279,24 @@ def test_edge_block_sizes_launch_and_agree(gk, monkeypatch, chunks):
         monkeypatch.setenv("GK_EDGE", "2")
         rel = ((z - z0).abs() / z0.abs().clamp_min(1e-300)).max().item()
         assert rel < 1e-12, (md, rel)
+
+
+@pytest.mark.parametrize("m", [1, 3, 4, 6, 7])
+def test_edge_kernels_every_rule_agree_with_per_triangle(gk, forced, m):
+    """every outer rule x n = 1..5, direct (lossless and C4's lossy medium)
+    and table (K3e): the shared-edge fill agrees with the per-triangle one"""
+    mesh = sphere(gk, 3)
+    for n in range(1, 6):
+        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+        lo, hi = dm.distance_range()
+        t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=10000))
+        kl = complex(gk.wavenumber(gk.Medium(1.0, 4.0, 1.0, -0.4)))
+        for md, kw in ((gk.Mode.DIRECT, dict(k=2 * np.pi)), (gk.Mode.DIRECT, dict(k=kl)),
+                       (gk.Mode.TABLE, dict(table=t))):
+            z, rep = gk.fill_rows(dm, md, **kw)
+            forced.setenv("GK_EDGE", "0")
+            z0, rep0 = gk.fill_rows(dm, md, **kw)
+            forced.setenv("GK_EDGE", "2")
+            rel = ((z - z0).abs() / z0.abs().clamp_min(1e-300)).max().item()
+            assert rel < 1e-12, (m, n, md, rel)
+            assert rep.evaluations < rep0.evaluations == rep0.actual_calls, (m, n, md, kw.keys())
