@@ -266,7 +266,10 @@ gk_status gk_fill_check(gk_ctx* ctx, uint64_t* fallbacks);
 
 /* Fused Exp + Green fill sharing every radius (and, in TABLE mode, every
    lookup): z_exp gets the PlainExp matrix, z_green the GreenOverR matrix, each
-   bit-identical to the separate gk_fill_rows result.  The EFIE-type use the
+   bit-identical to the separate gk_fill_rows result (both run on the shared
+   edges when the separate fills do; with GK_EDGE_CHUNKS=12 and more than
+   ~200 attenuation entries the pair alone falls back to the per-triangle
+   kernel, which agrees to rounding).  The EFIE-type use the
    paper's "several tables" serve.  Reported calls count
    both kernels. */
 gk_status gk_fill_rows_pair(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode,
