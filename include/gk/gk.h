@@ -77,8 +77,8 @@ typedef struct gk_fill_report {
   uint64_t predicted_calls, actual_calls, fallback_calls;
   double wall_time_s; /* device time of the fill kernels (CUDA events) */
   /* kernel evaluations the device performed for these entries: actual_calls,
-     or fewer where the direct fill evaluates each shared edge of a closed
-     mesh once for both of its triangles (K4e) */
+     or fewer where the fill evaluates each shared edge of a closed mesh once
+     for both of its triangles (K4e direct, K3e table) */
   uint64_t evaluations;
 } gk_fill_report;
 
