@@ -300,3 +300,13 @@ def test_edge_kernels_every_rule_agree_with_per_triangle(gk, forced, m):
             rel = ((z - z0).abs() / z0.abs().clamp_min(1e-300)).max().item()
             assert rel < 1e-12, (m, n, md, rel)
             assert rep.evaluations < rep0.evaluations == rep0.actual_calls, (m, n, md, kw.keys())
+
+
+@pytest.mark.parametrize("radius,lam", [(1e-3, 1e-3), (1e3, 1e3)])
+def test_edge_fill_parity_scaled_meshes(gk, oracle, forced, radius, lam):
+    """the far threshold scales with the mesh (delta is measured on its own
+    points): millimetre and kilometre spheres stay within the bound"""
+    mesh = gk.jitter(gk.generate_sphere_mesh(radius, 3), 1901, 1e-3 * radius)
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi / lam)
+    assert 0.01 * radius < info["r_far"] < 0.1 * radius
+    assert rep.evaluations < 0.8 * rep.actual_calls
