@@ -45,3 +45,6 @@ def test_device_arm_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 1280 ** 2 * 16
     assert d["gpu_launches"] >= 3 and d["clocks"]["sm_max_mhz"]
     assert d["config"]["workload"].startswith("C2")
+    # the reference's calls per step vs the evaluations the kernel performed
+    assert 0 < d["evaluations_per_step"] <= 3 * 6 * 4 * 1280 * 1279
+    assert d["value_definition"] and d["modes"]["direct"]["evaluations_per_step"] > 0
