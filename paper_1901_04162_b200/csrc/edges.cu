@@ -250,7 +250,12 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
         }
       return cnt;
     };
-    const size_t T = std::max<size_t>(1, (cap * 61) / 100);  // ~1.6 edges per triangle
+    size_t tfrac = 61;  // leaf triangles per edge slot, percent (~1.6 edges per triangle)
+    if (const char* e = std::getenv("GK_EDGE_TFRAC")) {  // A/B
+      const long v = std::atol(e);
+      if (v >= 30 && v <= 100) tfrac = static_cast<size_t>(v);
+    }
+    const size_t T = std::max<size_t>(1, (cap * tfrac) / 100);
     std::vector<std::pair<size_t, size_t>> stack{{0, N}};
     while (!stack.empty()) {
       const auto [lo, hi] = stack.back();
