@@ -11,8 +11,20 @@ so no flush is needed between steps.
 
 Default workload: BASELINE.json configs[4] (C5, icosphere L6, N = 81920,
 m = 6, n = 4, k = 2 pi / 0.15), the metric's "vs N at 1/2/4/8 B200" config.
-Rank 0 prints one JSON line.  ``--impl reference`` times the reference's own
-CPU fill (oracle/_ref, compiled from /root/reference) on the host cores.
+Rank 0 prints one JSON line.
+
+* ``--gpus N`` with N > 1 and no WORLD_SIZE in the environment re-launches
+  itself through ``torch.distributed.run`` (one rank per GPU, 127.0.0.1);
+  under torchrun, WORLD_SIZE must equal N.
+* ``--impl reference`` times the reference's own CPU fill (oracle/_ref,
+  compiled in place from /root/reference) on the host cores, through
+  oracle/cpu_bench.py -- the reference only: this package is never imported
+  in that arm.  The GPU arm's ``cpu_baseline`` runs the same module in a clean
+  subprocess.
+* ``--selftest gloo`` runs the N-rank orchestration (self-launch, row blocks,
+  barriers, max-over-ranks timing, the JSON line) on CPU ranks over gloo,
+  with the reference's CPU fill of each rank's rows as the stand-in work: a
+  harness test, not a bench number (``impl`` says so).
 """
 from __future__ import annotations
 
@@ -58,9 +70,44 @@ def make_mesh(gk, cfg):
 
 
 def rows_of(rank, world, N):
-    """contiguous row blocks, chunk = ceil(N / world) (matfill.hpp:211-215)"""
-    from paper_1901_04162_b200.sharding import rows_of as _rows_of
-    return _rows_of(rank, world, N)
+    """contiguous row blocks, chunk = ceil(N / world) (matfill.hpp:211-215);
+    the same partition as paper_1901_04162_b200.sharding.rows_of and gk_rows_of"""
+    chunk = (N + world - 1) // world
+    b = min(N, rank * chunk)
+    return b, min(N, b + chunk)
+
+
+# the headline mode on both arms: the faster of the reference's two kernels
+# (AnalyticKernel / TableKernel at S) -- same definition in both lines
+MODE_NOTE = "faster of direct and table"
+L2_NOTE = ("no flush needed: a step writes Z (rows x N x 16 B; 107 GB for the full C5 fill) "
+           "far beyond any cache; the quadrature points (<= 47 MB) are re-read ~N times per "
+           "step, so their cache residency is the steady state")
+
+
+def config_of(cfg, S):
+    """the `config` object, identical in both arms' lines"""
+    return {"workload": cfg["name"], "mode": MODE_NOTE, "samples_per_wavelength": S,
+            "l2": L2_NOTE}
+
+
+def self_launch(args):
+    """--gpus N > 1 without torchrun: re-exec as N ranks of torch.distributed.run."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    if args.selftest is None:
+        # the driver counts the communicator's ranks from NCCL's own log
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execvpe(sys.executable, cmd, env)
 
 
 class ClockSampler:
@@ -125,80 +172,186 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def reference_sample(cfg, mesh_v, mesh_t, k, mode, lo, hi, S, threads, target_s=12.0):
-    """Row-sampled reference CPU fill: rows p = floor(s N / R)."""
-    from oracle.pyoracle import DIRECT, TABLE, Ref, SamplingConfig as RCfg
-    ref = Ref()
-    N = mesh_t.shape[0]
-    m, n = cfg["m"], cfg["n"]
-    per_row = (N - 1) * 3 * m * n
-    # ~25 ns / eval / thread on the reference (SURVEY 6): size for ~target_s of CPU work
-    R = max(threads, int(target_s / (per_row * 25e-9)))
-    R = min(N, max(1, (R // threads) * threads))
-    rows = np.array([(s * N) // R for s in range(R)], np.uint64)
-    ev, build_s = None, 0.0
-    if mode == "table":
-        t0 = time.perf_counter()
-        plan = ref.build_plan(RCfg(r_min=lo, r_max=hi, samples_per_wavelength=S),
-                              2 * math.pi / k)
-        ev = ref.evaluator(plan, k)
-        build_s = time.perf_counter() - t0
-    _, calls, wall = ref.fill_sampled_rows(mesh_v, mesh_t, m, n, TABLE if ev else DIRECT, k,
-                                           rows, ev=ev, threads=threads)
-    return {"evals": calls, "wall_s": wall, "build_s": build_s, "rows": int(R),
-            "evals_per_s": calls / wall}
+def cpu_baseline_subprocess(cfg, S, seconds, seconds_1):
+    """The reference's CPU fill timed in a CLEAN subprocess (no torch, no CUDA
+    context, no libgk.so): the same oracle/cpu_bench.py the reference arm runs,
+    so the two CPU numbers measure the same code on the same workload."""
+    import subprocess
+    cmd = [sys.executable, "-m", "oracle.cpu_bench", "--level", str(cfg["level"]),
+           "--m", str(cfg["m"]), "--n", str(cfg["n"]), "--lambda0", str(cfg["lambda0"]),
+           "--S", str(S), "--seconds", str(seconds), "--seconds-1", str(seconds_1)]
+    env = {k: v for k, v in os.environ.items() if not k.startswith(("CUDA_", "NCCL_"))}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, env=env, timeout=900)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr.strip().splitlines()[-1] if r.stderr.strip() else "failed")
+    return json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+
+
+def cpu_summary(res, S):
+    """cpu_baseline from an oracle/cpu_bench result: the faster mode at nproc
+    threads, both modes and the single-thread rates alongside."""
+    modes = res["modes"]
+    best = max(modes, key=lambda m: modes[m]["evals_per_s"])
+    b = modes[best]
+    kern = {"direct": "AnalyticKernel", "table": "TableKernel"}
+    per = {}
+    for m, e in modes.items():
+        one = e.get("single_thread")
+        per[m] = {"evals_per_s": e["evals_per_s"], "rows": e["rows"], "wall_s": e["wall_s"],
+                  "threads": e["threads"],
+                  "single_thread_evals_per_s": one["evals_per_s"] if one else None,
+                  "single_thread_rows": one["rows"] if one else None}
+        if m == "table":
+            per[m].update(S=e["S"], table_build_ms=e["table_build_ms"],
+                          table_nodes=e["table_nodes"])
+    lo, hi = res.get("table_range", (None, None))
+    return {"value": b["evals_per_s"], "unit": "evals/s", "cores": res["cores"],
+            "kind": "reference", "mode": best, "modes": per,
+            "single_thread": {"value": modes[best]["single_thread"]["evals_per_s"]
+                              if modes[best].get("single_thread") else None,
+                              "cores": 1, "mode": best},
+            "sample": f"{b['rows']} of {res['N']} rows x all columns per sample through the "
+                      f"reference's {kern[best]}::accumulate (the faster of its two modes; "
+                      f"TableKernel at S={S} over [1e-4 lambda0, 1.01 max_vertex_distance]"
+                      f"{f' = [{lo:.3g}, {hi:.5g}] m' if lo else ''}), {res['cores']} threads, "
+                      f"extrapolated linearly to the {res['total_evals_per_fill']:.3e}-evaluation "
+                      f"fill; single-thread rates alongside"}
+
+
+def repo_libs_loaded():
+    """this process's mapped shared objects under the repo (/proc/self/maps)"""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for ln in f:
+                path = ln.split()[-1] if len(ln.split()) >= 6 else ""
+                if path.startswith(ROOT) and ".so" in path:
+                    out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
 
 
 def run_reference_arm(args, cfg, rank, world):
-    """--impl reference: the reference's own CPU fill on this host's cores."""
+    """--impl reference: the reference's own CPU fill on this host's cores.
+
+    Imports nothing of this package (only oracle/cpu_bench -> oracle/_ref/
+    libgkref.so, the reference compiled in place).  Each step is a bounded
+    row sample of the configured fill; ms_per_step is that
+    sample's wall time, value its evaluations / s."""
     if rank != 0:
         return
-    import paper_1901_04162_b200 as gk  # host-only helpers: mesh generators
-    mesh = make_mesh(gk, cfg)
-    k = 2 * math.pi / cfg["lambda0"]
-    if cfg.get("eps_r_im"):
+    if cfg["kind"] != "sphere" or cfg.get("eps_r_im"):
         print(json.dumps({"impl": "reference", "unavailable":
-                          "the reference is real-k only (kernel.hpp:23-24); C4 has no reference path"}))
+                          "the reference is real-k only (kernel.hpp:23-24); C4 has no reference "
+                          "path"}), flush=True)
         return
-    from oracle.pyoracle import Oracle
-    o = Oracle()
+    from oracle.cpu_bench import Workload, cpu_threads, kernel_name
+    wl = Workload(cfg["level"], cfg["m"], cfg["n"], cfg["lambda0"])
     threads = cpu_threads()
     modes = ["direct", "table"] if args.mode == "auto" else [args.mode]
-    # the reference's own table conventions (matfill.hpp:270, SPEC.md:453)
-    hi = o.max_vertex_distance(mesh.vertices) * 1.01
-    lo = 1e-4 * cfg["lambda0"]
-    per_mode = {}
-    for mode in modes:
-        vals = []
-        for i in range(args.warmup + args.steps):
-            r = reference_sample(cfg, mesh.vertices, mesh.triangles, k, mode, lo, hi, args.S,
-                                 threads, target_s=args.cpu_seconds / len(modes))
-            if i >= args.warmup:
-                vals.append(r)
-        per_mode[mode] = {"evals_per_s": statistics.median(x["evals_per_s"] for x in vals),
-                          "rows": vals[0]["rows"],
-                          "table_build_ms": vals[0]["build_s"] * 1e3}
-    mode = max(per_mode, key=lambda x: per_mode[x]["evals_per_s"])
-    v = per_mode[mode]["evals_per_s"]
-    N = mesh.triangle_count()
-    total = 3 * cfg["m"] * cfg["n"] * N * (N - 1)
+    # every step a bounded sample: the whole K + W run stays within ~2-3 minutes
+    per_step_s = min(args.cpu_seconds, max(1.0, 150.0 / (args.steps + args.warmup)))
+    rows = {m: wl.rows_for(per_step_s, threads) for m in modes}
+    warm = {m: [] for m in modes}
+    for _ in range(args.warmup):      # warm-up samples of both modes pick the faster
+        for m in modes:
+            warm[m].append(wl.sample(m, rows[m], threads, args.S)["evals_per_s"])
+    mode = max(modes, key=lambda m: statistics.median(warm[m]) if warm[m] else 0.0)
+    timed = [wl.sample(mode, rows[mode], threads, args.S) for _ in range(args.steps)]
+    evals = sum(t["evals"] for t in timed)
+    wall = sum(t["wall_s"] for t in timed)
+    v = evals / wall
+    ms = wall / len(timed) * 1e3
+    # single thread (SURVEY 8d: threads = 1 and threads = nproc), once per mode
+    single = {m: wl.sample(m, wl.rows_for(min(6.0, args.cpu_seconds) / len(modes), 1), 1, args.S)
+              for m in modes} if args.cpu_single else {}
+    per_mode = {m: {"evals_per_s": statistics.median(warm[m]) if warm[m] else None,
+                    "rows": rows[m], "threads": threads,
+                    "single_thread_evals_per_s": single[m]["evals_per_s"] if m in single else None,
+                    "single_thread_rows": single[m]["rows"] if m in single else None}
+                for m in modes}
+    per_mode[mode]["evals_per_s"] = v
+    if "table" in modes:
+        ev, build_s, nodes = wl.evaluator(args.S)
+        per_mode["table"].update(table_build_ms=build_s * 1e3, table_nodes=nodes)
+    lo, hi = wl.table_range()
     line = {
         "impl": "reference", "metric": "green_fn_evals_per_s", "value": v, "unit": "evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total / v * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded jittered icosphere)",
-        "config": {"workload": cfg["name"], "mode": mode,
-                   "samples_per_wavelength": args.S if mode == "table" else None},
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: the reference's generate_sphere_mesh + seeded jitter "
+                "(splitmix64 seed 1901, 1e-3 m)",
+        "config": config_of(cfg, args.S),
+        "mode_used": mode,
+        "parallelism": f"{threads} host threads (std::thread row chunks, matfill.hpp:206-221)",
+        "step_definition": f"one bounded sample: {rows[mode]} of {wl.N} rows x all columns "
+                           f"through the reference's {kernel_name(mode)}::accumulate "
+                           f"(ms_per_step is the sample's wall time)",
+        "full_fill_s_extrapolated": wl.total / v,
         "modes": per_mode,
         "cpu_baseline": {"value": v, "unit": "evals/s", "cores": threads, "kind": "reference",
-                         "sample": f"{per_mode[mode]['rows']} rows x all {N} columns per step "
-                                   f"through the reference's "
-                                   f"{'TableKernel' if mode == 'table' else 'AnalyticKernel'}"
-                                   f"::accumulate (faster of its modes: {sorted(per_mode)}), "
-                                   f"extrapolated to the full {total:.3e}-eval fill"},
+                         "mode": mode,
+                         "single_thread": {"value": single[mode]["evals_per_s"]
+                                           if mode in single else None, "cores": 1},
+                         "sample": f"{rows[mode]} rows x all {wl.N} columns per step through the "
+                                   f"reference's {kernel_name(mode)}::accumulate (the faster of "
+                                   f"its modes {sorted(modes)}; TableKernel at S={args.S} over "
+                                   f"[{lo:.3g}, {hi:.5g}] m), extrapolated to the full "
+                                   f"{wl.total:.3e}-eval fill"},
         "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "repo_libs_loaded": repo_libs_loaded(),
     }
     print(json.dumps(line), flush=True)
+
+
+def run_selftest(args, cfg, rank, world):
+    """--selftest gloo: the N-rank harness on CPU ranks (no GPU).  Each rank's
+    step is the reference's CPU fill of a few rows of ITS row block; the step
+    time is bracketed by barriers and reduced with MAX over ranks, exactly
+    like the GPU arm.  Not a bench number."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    assert dist.get_world_size() == world
+    from oracle.cpu_bench import Workload
+    wl = Workload(cfg["level"], cfg["m"], cfg["n"], cfg["lambda0"])
+    rb, re = rows_of(rank, world, wl.N)
+    import numpy as np
+    rows = np.arange(rb, min(re, rb + 1 + rank), dtype=np.uint64)  # uneven work per rank
+
+    def step():
+        if rows.size:
+            wl.ref.fill_sampled_rows(wl.verts, wl.tris, wl.m, wl.n, 0, wl.k, rows, threads=1)
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    dist.barrier()
+    mine = torch.tensor([ms], dtype=torch.float64)
+    allt = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(allt, mine)
+    mx = mine.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    evals = torch.tensor([3.0 * wl.m * wl.n * rows.size * (wl.N - 1)], dtype=torch.float64)
+    dist.all_reduce(evals)
+    if rank == 0:
+        print(json.dumps({
+            "impl": f"selftest-{args.selftest}", "metric": "green_fn_evals_per_s",
+            "value": float(evals[0]) / (float(mx[0]) * 1e-3), "unit": "evals/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(mx[0]), "per_rank_ms": [float(t[0]) for t in allt],
+            "row_blocks": [list(rows_of(r, world, wl.N)) for r in range(world)],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_of(cfg, args.S),
+            "note": "harness self-test on CPU ranks (gloo): not a bench value"}), flush=True)
+    dist.destroy_process_group()
 
 
 def main():
@@ -212,34 +365,56 @@ def main():
     ap.add_argument("--S", type=int, default=10000, help="samples per wavelength (table)")
     ap.add_argument("--both-modes", type=int, default=1, help="also time the other mode")
     ap.add_argument("--cpu-baseline", type=int, default=1)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="CPU wall budget per sample at nproc threads")
+    ap.add_argument("--cpu-single", type=int, default=1,
+                    help="also time the reference at threads = 1")
     ap.add_argument("--e2e", type=int, default=1)
     ap.add_argument("--vs-n", type=int, default=1, help="also time C2/C3 fills (rank 0, N=1)")
     ap.add_argument("--c1", type=int, default=1, help="also time standalone eval_batch (C1)")
     ap.add_argument("--gather", type=int, default=1,
                     help="N > 1: also time the gather of Z to rank 0 (reported apart)")
     ap.add_argument("--pertri", type=int, default=1,
-                    help="also time the direct fill without shared edges (GK_EDGE=0)")
+                    help="also time the direct fill without shared edges (shared_edges = 0)")
     ap.add_argument("--S-alt", type=int, default=1000,
                     help="also time the table mode at this S (0 = off)")
+    ap.add_argument("--selftest", default=None, choices=["gloo"],
+                    help="CPU-only harness test of the N-rank orchestration")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
 
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        # rank 0 alone runs the host-CPU reference; other torchrun ranks exit 0
+        run_reference_arm(args, cfg, env_int("RANK", 0), env_int("WORLD_SIZE", args.gpus))
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        self_launch(args)  # does not return
     world = env_int("WORLD_SIZE", 1)
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
-    cfg = CONFIGS[args.config]
-
-    if args.impl == "reference":
-        run_reference_arm(args, cfg, rank, world)
+    if args.selftest:
+        run_selftest(args, cfg, rank, world)
         return
+    run_gpu_arm(args, cfg, rank, world, local)
 
+
+def run_gpu_arm(args, cfg, rank, world, local):
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size()}
+        sys.stderr.write(f"bench.py rank {rank}: torch.distributed {comm['backend']} "
+                         f"nranks={comm['world_size']}\n")
     import paper_1901_04162_b200 as gk
     from paper_1901_04162_b200 import sharding
     from paper_1901_04162_b200._lib import lib as _gk_lib
@@ -254,33 +429,37 @@ def main():
                        eps_r_im=cfg.get("eps_r_im", 0.0))
     k = gk.wavenumber(medium)
     rb, re = rows_of(rank, world, N)
+    assert (rb, re) == sharding.rows_of(rank, world, N)
     rows = re - rb
     dmesh = gk.DeviceMesh(mesh, spec, ctx)
     Z = torch.empty((max(rows, 1), N), dtype=torch.complex128, device=f"cuda:{local}")
     total_evals = 3 * m * n * N * (N - 1)
+    # the reference-order kernels (no shared edges): A/B only
+    per_tri = gk.FillOptions(shared_edges=0)
 
     def global_range():
         lo, hi = dmesh.distance_range(rb, re) if rows else (math.inf, 0.0)
         return sharding.global_distance_range(lo, hi, device=f"cuda:{local}")
 
+    def table_for(mode):
+        if not mode.startswith("table"):
+            return None
+        S = args.S if mode == "table" else int(mode.split("_S")[1])
+        lo, hi = global_range()
+        return gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S),
+                              medium, ctx=ctx)
+
     fill_ev = []
 
     def step(mode):
-        # "direct_pertri": the reference-order kernel without shared edges (A/B)
-        os.environ["GK_EDGE"] = "0" if mode == "direct_pertri" else "1"
-        table = None
-        if mode.startswith("table"):
-            S = args.S if mode == "table" else int(mode.split("_S")[1])
-            lo, hi = global_range()
-            table = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
-                                                     samples_per_wavelength=S), medium,
-                                   ctx=ctx)
+        table = table_for(mode)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         if rows:
             gk.fill_rows(dmesh, gk.Mode.TABLE if table else gk.Mode.DIRECT, table=table, k=k,
-                         row_begin=rb, row_end=re, out=Z, report=False)
+                         row_begin=rb, row_end=re, out=Z, report=False,
+                         options=per_tri if mode == "direct_pertri" else None)
         e1.record()
         fill_ev.append((e0, e1))
         return table
@@ -319,13 +498,7 @@ def main():
             return 3 * m * n * rows * (N - 1)
         if not rows:
             return 0
-        os.environ["GK_EDGE"] = "1"
-        table = None
-        if mode.startswith("table"):
-            S = args.S if mode == "table" else int(mode.split("_S")[1])
-            lo, hi = global_range()
-            table = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
-                                                     samples_per_wavelength=S), medium, ctx=ctx)
+        table = table_for(mode)
         _, rep = gk.fill_rows(dmesh, gk.Mode.TABLE if table else gk.Mode.DIRECT, table=table,
                               k=k, row_begin=rb, row_end=re, out=Z)
         return rep.evaluations
@@ -372,38 +545,12 @@ def main():
     chosen = args.mode if args.mode != "auto" else min(("direct", "table"),
                                                        key=lambda x: results[x]["ms_per_step"])
     main_res = results[chosen]
-    os.environ["GK_EDGE"] = "1"
-
 
     # e2e through the host-buffer C-ABI entry point (gk_fill_matrix_host), rank-local rows
     e2e = None
     if args.e2e:
         e2e = run_e2e(gk, ctx, cfg, mesh, spec, medium, chosen, args, total_evals, rank, world,
                       rb, re, dist if world > 1 else None)
-
-    cpu = None
-    if args.cpu_baseline and rank == 0 and world == 1:
-        cpu_modes = {}
-        for mode in ("direct", "table"):
-            lo, hi = dmesh.distance_range() if mode == "table" else (None, None)
-            try:
-                k_real = k.real if isinstance(k, complex) else k
-                if cfg.get("eps_r_im"):
-                    raise RuntimeError("no reference path for complex k (kernel.hpp:23-24)")
-                smp = reference_sample(cfg, mesh.vertices, mesh.triangles, k_real, mode, lo, hi,
-                                       args.S, cpu_threads(), target_s=args.cpu_seconds / 2)
-                cpu_modes[mode] = {
-                    "value": smp["evals_per_s"],
-                    "sample": f"{smp['rows']} of {N} rows x all columns through the reference's "
-                              f"{'TableKernel' if mode == 'table' else 'AnalyticKernel'}::accumulate"
-                              f" ({smp['evals']:.3e} evals in {smp['wall_s']:.2f} s"
-                              + (f"; S={args.S}, table build {smp['build_s']*1e3:.1f} ms"
-                                 if mode == "table" else "") + "), extrapolated linearly"}
-            except Exception as exc:  # report, never fake
-                cpu_modes[mode] = {"value": None, "sample": f"unavailable: {exc}"}
-        cm = cpu_modes[chosen]
-        cpu = {"value": cm["value"], "unit": "evals/s", "cores": cpu_threads(),
-               "kind": "reference", "sample": cm["sample"], "mode": chosen, "modes": cpu_modes}
 
     vs_n = None
     if args.vs_n and rank == 0 and world == 1 and args.config == "c5":
@@ -419,6 +566,22 @@ def main():
     c1 = None
     if args.c1 and rank == 0 and world == 1:
         c1 = run_c1(gk, ctx)
+
+    # the reference's CPU fill beside it (rank 0, N = 1): a clean subprocess
+    # running oracle/cpu_bench.py -- the code the reference arm runs
+    cpu = None
+    if args.cpu_baseline and rank == 0 and world == 1:
+        if cfg["kind"] != "sphere" or cfg.get("eps_r_im"):
+            cpu = {"value": None, "unit": "evals/s", "cores": cpu_threads(), "kind": "reference",
+                   "sample": "unavailable: the reference is real-k only (kernel.hpp:23-24)"}
+        else:
+            try:
+                cpu = cpu_summary(cpu_baseline_subprocess(
+                    cfg, args.S, args.cpu_seconds, min(6.0, args.cpu_seconds) if args.cpu_single
+                    else 0.0), args.S)
+            except Exception as exc:  # report, never fake
+                cpu = {"value": None, "unit": "evals/s", "cores": cpu_threads(),
+                       "kind": "reference", "sample": f"unavailable: {exc}"}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
@@ -442,12 +605,10 @@ def main():
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic: seeded jittered icosphere (splitmix64 seed 1901, 1e-3 m)",
-        "config": {"workload": cfg["name"], "mode": chosen,
-                   "samples_per_wavelength": args.S if chosen == "table" else None,
-                   "parallelism": f"row-block x{world}",
-                   "l2": "no flush: every step streams Z (rows x N x 16 B, 107 GB at C5) "
-                         "through L2; the quadrature points (<= 47 MB) are re-read ~N times "
-                         "within each step, so their L2 residency is the steady state"},
+        "config": config_of(cfg, args.S),
+        "mode_used": chosen,
+        "parallelism": f"row-block x{world}",
+        "comm": comm,
         "fill_time_s": main_res["ms_per_step"] * 1e-3,
         "value_definition": "the reference's calls per Z fill (FillReport.actual_calls = "
                             "3 m n N (N-1), matfill.hpp:200) / fill time, i.e. Z-fill time "

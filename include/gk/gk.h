@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define GK_ABI_VERSION 1
+#define GK_ABI_VERSION 2
 
 typedef enum gk_status {
   GK_OK = 0,
@@ -82,6 +82,59 @@ typedef struct gk_fill_report {
   uint64_t evaluations;
 } gk_fill_report;
 
+/* ---------------------------------------------------- kernel selection
+   Every choice the library makes between equivalent kernels, made explicit
+   per call (no environment variable or other process-global state is read).
+   The reference picks its kernel by type (AnalyticKernel / TableKernel,
+   matfill.hpp:59-87); these only choose HOW the device evaluates it.  All
+   choices give results within the same stated bound; the bit-identity
+   classes are documented in DESIGN.md §3.  Initialise with
+   gk_fill_options_init (every field GK_AUTO = the measured best). */
+#define GK_AUTO (-1)
+typedef enum gk_table_placement {
+  GK_TABLE_GLOBAL = 0, /* table read through L1/L2 */
+  GK_TABLE_SHARED = 1  /* table staged into shared memory: whole, or per-tile windows */
+} gk_table_placement;
+typedef struct gk_fill_options {
+  /* GK_AUTO: shared-edge kernels (each mesh edge evaluated once for both of
+     its triangles, DESIGN.md §5 K4e/K3e) where they pay: closed meshes of
+     >= 4096 triangles with n <= 5;  0: never (the reference's per-triangle
+     evaluation order, matfill.hpp:185-198);  1: whenever the mesh has
+     shared-edge blocks (any mesh size; TABLE mode still picks by table
+     size, GK_TABLE_GLOBAL takes them instead of staging) */
+  int shared_edges;
+  /* TABLE mode: GK_AUTO (staged when the table or a tile's window fits,
+     else through L1), or a gk_table_placement (GK_TABLE_GLOBAL: the
+     shared-edge K3e where the fill uses shared edges, else per triangle;
+     GK_TABLE_SHARED: always staged, per triangle) */
+  int table_placement;
+  /* TABLE mode: GK_AUTO / 1: arithmetic interval index on the plan's
+     uniform runs (bit-identical lookup), 0: lookup buckets only */
+  int arith_locate;
+  /* lossy DIRECT fills: GK_AUTO / 1: attenuation coupled to the phase
+     reduction, 0: separate attenuation table */
+  int lossy_phase;
+  /* DIRECT fills: GK_AUTO / 1: the n = 1..5 unrolled kernel, 0: the generic
+     runtime-loop kernel */
+  int unrolled;
+  /* gk_eval_batch* (through gk_ctx_set_fill_options): GK_AUTO / 0: the
+     phase-table direct evaluation, 1: libdevice sincos */
+  int eval_libdevice;
+  /* TABLE mode, staged: shared-memory bytes for a table window (0: 200 KB;
+     smaller values force per-tile windows and their overflow path) */
+  uint64_t smem_budget;
+} gk_fill_options;
+void gk_fill_options_init(gk_fill_options* opts);
+
+/* Shared-edge block construction at gk_mesh_create_ex (DESIGN.md §5 K4e). */
+typedef struct gk_mesh_options {
+  int shared_edges;  /* GK_AUTO / 1: build the blocks, 0: do not */
+  int edge_chunks;   /* warp-wide edge chunks per block, 1..12 (0 / GK_AUTO: 11) */
+  int edge_order;    /* GK_AUTO: the more compact; 0: mesh order; 1: bisection order */
+  int leaf_pct;      /* bisection leaf size in percent of the edge cap, 30..100 (0 / GK_AUTO: 61) */
+} gk_mesh_options;
+void gk_mesh_options_init(gk_mesh_options* opts);
+
 typedef struct gk_table_info {
   uint64_t nodes, zeros, hash_buckets, lookup_buckets;
   double r_min, r_max, t, dr_min, inv_dr_min, k_re, k_im;
@@ -102,6 +155,10 @@ gk_status gk_ctx_destroy(gk_ctx* ctx);
 gk_status gk_ctx_set_stream(gk_ctx* ctx, void* cuda_stream);
 gk_status gk_ctx_use_own_stream(gk_ctx* ctx);
 gk_status gk_ctx_synchronize(gk_ctx* ctx);
+/* The context's default kernel selection, used where a call takes no
+   gk_fill_options (or passes NULL): gk_fill_matrix_host, gk_bench_compare,
+   gk_eval_batch*.  NULL restores the library defaults. */
+gk_status gk_ctx_set_fill_options(gk_ctx* ctx, const gk_fill_options* opts);
 
 /* ------------------------------------------------------------ kernel math */
 /* gktab::wavenumber (kernel.hpp:41-44); complex for eps_r_im != 0 */
@@ -208,13 +265,18 @@ gk_status gk_eval_batch_host(gk_ctx* ctx, const gk_table* table, gk_kind kind, d
 gk_status gk_mesh_create(gk_ctx* ctx, const double* vertices, size_t nv,
                          const uint32_t* triangles, size_t nt, int outer_points,
                          int inner_points_per_edge, gk_mesh** out);
+/* gk_mesh_create with explicit shared-edge block options (NULL: defaults) */
+gk_status gk_mesh_create_ex(gk_ctx* ctx, const double* vertices, size_t nv,
+                            const uint32_t* triangles, size_t nt, int outer_points,
+                            int inner_points_per_edge, const gk_mesh_options* opts,
+                            gk_mesh** out);
 /* host copies: outer[4][nt*m] (x,y,z,w planes), inner[4][nt*3n] */
 gk_status gk_mesh_points_download(const gk_mesh* mesh, double* outer, double* inner);
 gk_status gk_mesh_destroy(gk_mesh* mesh);
 
 /* Shared-edge blocks of a mesh (no reference counterpart: the direct fill's
    evaluation-sharing structure, DESIGN.md §5 K4e).  blocks = 0 when the mesh
-   was created with GK_EDGE=0. */
+   was created with gk_mesh_options.shared_edges = 0. */
 typedef struct gk_mesh_edge_info {
   uint64_t blocks, edge_slots; /* evaluated edge slots incl. warp padding */
   double work_ratio;           /* edge_slots / (3 nt): far-tile work vs the reference */
@@ -252,10 +314,12 @@ gk_status gk_distance_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, 
    mode DIRECT = AnalyticKernel{k}, TABLE = TableKernel{table} (k from the
    table).  z is a device pointer.  report == NULL: asynchronous on the
    context stream; otherwise the call synchronizes and fills the report
-   (actual_calls = 3 m n rows (N-1), exact fallback count, kernel time). */
+   (actual_calls = 3 m n rows (N-1), exact fallback count, kernel time).
+   opts selects between equivalent kernels (NULL: the context's defaults). */
 gk_status gk_fill_rows(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                        gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
-                       gk_c128* z, size_t ldz, gk_fill_report* report);
+                       gk_c128* z, size_t ldz, const gk_fill_options* opts,
+                       gk_fill_report* report);
 
 /* Asynchronous fills (report == NULL) accumulate their fallback, out-of-range
    and zero-distance counts in the context; gk_fill_check synchronises, returns
@@ -267,15 +331,15 @@ gk_status gk_fill_check(gk_ctx* ctx, uint64_t* fallbacks);
 /* Fused Exp + Green fill sharing every radius (and, in TABLE mode, every
    lookup): z_exp gets the PlainExp matrix, z_green the GreenOverR matrix, each
    bit-identical to the separate gk_fill_rows result (both run on the shared
-   edges when the separate fills do; with GK_EDGE_CHUNKS=12 and more than
-   ~200 attenuation entries the pair alone falls back to the per-triangle
-   kernel, which agrees to rounding).  The EFIE-type use the
+   edges when the separate fills do; with 12 edge chunks per block and more
+   than ~200 attenuation entries the pair alone falls back to the
+   per-triangle kernel, which agrees to rounding).  The EFIE-type use the
    paper's "several tables" serve.  Reported calls count
    both kernels. */
 gk_status gk_fill_rows_pair(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode,
                             const gk_table* table, double k_re, double k_im, size_t row_begin,
                             size_t row_end, gk_c128* z_exp, gk_c128* z_green, size_t ldz,
-                            gk_fill_report* report);
+                            const gk_fill_options* opts, gk_fill_report* report);
 
 /* fill_matrix<Kernel> (matfill.hpp:144-228) end to end from HOST buffers:
    upload mesh, quadrature points, (TABLE) K1 range when cfg->r_min <= 0 or
@@ -295,7 +359,7 @@ gk_status gk_fill_matrix_host(gk_ctx* ctx, const double* vertices, size_t nv,
 gk_status gk_fill_rows_host(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode,
                             const gk_table* table, gk_kind kind, double k_re, double k_im,
                             size_t row_begin, size_t row_end, gk_c128* z_host, size_t ldz_host,
-                            gk_fill_report* report);
+                            const gk_fill_options* opts, gk_fill_report* report);
 
 /* compare_fills (matfill.hpp:237-254) on DEVICE matrices: componentwise max
    relative error of test against ref over `rows` rows of an N-column block

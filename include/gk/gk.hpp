@@ -15,9 +15,11 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <mutex>
 #include <ostream>
 #include <cstdint>
 #include <span>
@@ -157,7 +159,17 @@ inline TriangleMesh generate_sphere_mesh(double radius, int subdivisions) {
   return m;
 }
 
-// one B200 (RAII over gk_ctx)
+// kernel selection (gk_fill_options), every field GK_AUTO by default
+inline gk_fill_options default_fill_options() {
+  gk_fill_options o;
+  gk_fill_options_init(&o);
+  return o;
+}
+
+// one B200 (RAII over gk_ctx).  A gk_ctx is not re-entrant: objects that may
+// be called from several host threads (DeviceEvaluator as the reference's
+// Kernel, whose fill_matrix calls accumulate from `threads` workers) take
+// mutex() around every call on the context.
 class Context {
  public:
   explicit Context(int device = 0) { check(gk_ctx_create(device, &h_)); }
@@ -166,9 +178,12 @@ class Context {
   Context& operator=(const Context&) = delete;
   gk_ctx* get() const { return h_; }
   void set_stream(void* cuda_stream) { check(gk_ctx_set_stream(h_, cuda_stream)); }
+  void set_fill_options(const gk_fill_options& o) { check(gk_ctx_set_fill_options(h_, &o)); }
+  std::mutex& mutex() const { return mu_; }
 
  private:
   gk_ctx* h_ = nullptr;
+  mutable std::mutex mu_;
 };
 
 // gktab::KernelEvaluator (evaluator.hpp:102-309) with its tables on the GPU
@@ -199,27 +214,36 @@ class DeviceEvaluator {
   gk_table* get() const { return h_; }
   double k() const { return info_.k_re; }
   int lagrange_degree() const { return info_.degree; }
-  std::uint64_t fallback_count() const { return fallbacks_; }
+  // relaxed atomic like the reference's counter (evaluator.hpp:100-101, 203)
+  std::uint64_t fallback_count() const { return fallbacks_.load(std::memory_order_relaxed); }
 
-  // eval_batch (evaluator.hpp:209-221): host in, host out
+  // eval_batch (evaluator.hpp:209-221): host in, host out.  Thread-safe: the
+  // device call holds the context's mutex (the reference's evaluator is
+  // shared by its fill's worker threads, evaluator.hpp:100-101).
   std::vector<Complex> eval_batch(KernelKind kind, std::span<const double> radii) const {
     std::vector<Complex> out(radii.size());
     std::uint64_t fb = 0;
-    check(gk_eval_batch_host(ctx_->get(), h_, static_cast<gk_kind>(kind), 0.0, 0.0,
-                             radii.data(), radii.size(), reinterpret_cast<gk_c128*>(out.data()),
-                             &fb));
-    fallbacks_ += fb;
+    {
+      std::lock_guard<std::mutex> lock(ctx_->mutex());
+      check(gk_eval_batch_host(ctx_->get(), h_, static_cast<gk_kind>(kind), 0.0, 0.0,
+                               radii.data(), radii.size(),
+                               reinterpret_cast<gk_c128*>(out.data()), &fb));
+    }
+    fallbacks_.fetch_add(fb, std::memory_order_relaxed);
     return out;
   }
-  // Kernel::accumulate of one block (sum_i K(r_i) w_i) on the device
+  // Kernel::accumulate of one block (sum_i K(r_i) w_i) on the device; thread-safe
   Complex accumulate(KernelKind kind, std::span<const double> radii,
                      std::span<const double> weights) const {
     Complex out{0.0, 0.0};
     std::uint64_t fb = 0;
-    check(gk_accumulate_batch_host(ctx_->get(), h_, static_cast<gk_kind>(kind), 0.0, 0.0,
-                                   radii.data(), weights.data(), radii.size(), 1,
-                                   reinterpret_cast<gk_c128*>(&out), &fb));
-    fallbacks_ += fb;
+    {
+      std::lock_guard<std::mutex> lock(ctx_->mutex());
+      check(gk_accumulate_batch_host(ctx_->get(), h_, static_cast<gk_kind>(kind), 0.0, 0.0,
+                                     radii.data(), weights.data(), radii.size(), 1,
+                                     reinterpret_cast<gk_c128*>(&out), &fb));
+    }
+    fallbacks_.fetch_add(fb, std::memory_order_relaxed);
     return out;
   }
   Complex eval_kernel(KernelKind kind, double r) const {
@@ -232,6 +256,7 @@ class DeviceEvaluator {
   // Green with Lagrange (the device's interpolants)
   ErrorSweepReport error_sweep(KernelKind kind, InterpMethod method, std::size_t probes) const {
     gk_sweep_report r{};
+    std::lock_guard<std::mutex> lock(ctx_->mutex());
     check(gk_error_sweep(ctx_->get(), h_, static_cast<gk_kind>(kind),
                          static_cast<gk_interp>(method), probes, &r));
     ErrorSweepReport e;
@@ -266,7 +291,7 @@ class DeviceEvaluator {
   Context* ctx_;
   gk_table* h_ = nullptr;
   gk_table_info info_{};
-  mutable std::uint64_t fallbacks_ = 0;
+  mutable std::atomic<std::uint64_t> fallbacks_{0};
 };
 
 // fill_matrix<Kernel> (matfill.hpp:144-228) on the GPU, host mesh in, host

@@ -76,6 +76,23 @@ class FillReportC(C.Structure):
                 ("evaluations", C.c_uint64)]
 
 
+GK_AUTO = -1
+GK_TABLE_GLOBAL, GK_TABLE_SHARED = 0, 1
+
+
+class FillOptionsC(C.Structure):
+    """gk_fill_options (include/gk/gk.h): kernel selection per call."""
+    _fields_ = [("shared_edges", C.c_int), ("table_placement", C.c_int),
+                ("arith_locate", C.c_int), ("lossy_phase", C.c_int), ("unrolled", C.c_int),
+                ("eval_libdevice", C.c_int), ("smem_budget", C.c_uint64)]
+
+
+class MeshOptionsC(C.Structure):
+    """gk_mesh_options (include/gk/gk.h): shared-edge block construction."""
+    _fields_ = [("shared_edges", C.c_int), ("edge_chunks", C.c_int), ("edge_order", C.c_int),
+                ("leaf_pct", C.c_int)]
+
+
 class SweepReportC(C.Structure):
     _fields_ = [("probe_count", C.c_uint64), ("max_rel_re", C.c_double),
                 ("max_rel_im", C.c_double), ("max_abs", C.c_double), ("worst_r", C.c_double),
@@ -109,6 +126,7 @@ PROTOTYPES = {
     "gk_ctx_set_stream": [_vp, _vp],
     "gk_ctx_use_own_stream": [_vp],
     "gk_ctx_synchronize": [_vp],
+    "gk_ctx_set_fill_options": [_vp, C.POINTER(FillOptionsC)],
     "gk_wavenumber": [C.POINTER(Medium), _dp, _dp],
     "gk_table_build": [_vp, C.POINTER(SamplingConfigC), C.POINTER(Medium), C.c_int,
                        C.POINTER(_vp)],
@@ -125,6 +143,8 @@ PROTOTYPES = {
     "gk_eval_batch_host": [_vp, _vp, C.c_int, C.c_double, C.c_double, _vp, C.c_size_t, _vp,
                            _u64p],
     "gk_mesh_create": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.POINTER(_vp)],
+    "gk_mesh_create_ex": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int,
+                          C.POINTER(MeshOptionsC), C.POINTER(_vp)],
     "gk_mesh_points_download": [_vp, _vp, _vp],
     "gk_mesh_destroy": [_vp],
     "gk_mesh_edge_info_get": [_vp, _vp],
@@ -132,14 +152,17 @@ PROTOTYPES = {
                             _vp, _u64p, C.POINTER(C.c_int)],
     "gk_distance_range": [_vp, _vp, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_fill_rows": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_double, C.c_size_t,
-                     C.c_size_t, _vp, C.c_size_t, C.POINTER(FillReportC)],
+                     C.c_size_t, _vp, C.c_size_t, C.POINTER(FillOptionsC),
+                     C.POINTER(FillReportC)],
     "gk_fill_rows_pair": [_vp, _vp, C.c_int, _vp, C.c_double, C.c_double, C.c_size_t,
-                          C.c_size_t, _vp, _vp, C.c_size_t, C.POINTER(FillReportC)],
+                          C.c_size_t, _vp, _vp, C.c_size_t, C.POINTER(FillOptionsC),
+                          C.POINTER(FillReportC)],
     "gk_fill_matrix_host": [_vp, _vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.c_int,
                             C.POINTER(SamplingConfigC), C.POINTER(Medium), C.c_int, _vp,
                             C.POINTER(FillReportC)],
     "gk_fill_rows_host": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_double, C.c_size_t,
-                          C.c_size_t, _vp, C.c_size_t, C.POINTER(FillReportC)],
+                          C.c_size_t, _vp, C.c_size_t, C.POINTER(FillOptionsC),
+                          C.POINTER(FillReportC)],
     "gk_predicted_calls": [C.c_uint64, C.c_uint64, C.c_uint64, _u64p],
     "gk_compare_fills": [_vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_max_vertex_distance": [_vp, _vp, _dp],
@@ -162,7 +185,12 @@ PROTOTYPES = {
     "gk_device_info": [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                        C.POINTER(C.c_int)],
 }
-EXPORTS = sorted(PROTOTYPES) + ["gk_abi_version", "gk_last_error", "gk_launch_count"]
+VOID_PROTOTYPES = {
+    "gk_fill_options_init": [C.POINTER(FillOptionsC)],
+    "gk_mesh_options_init": [C.POINTER(MeshOptionsC)],
+}
+EXPORTS = sorted(PROTOTYPES) + sorted(VOID_PROTOTYPES) + [
+    "gk_abi_version", "gk_last_error", "gk_launch_count"]
 
 _lib = None
 
@@ -181,6 +209,10 @@ def lib() -> C.CDLL:
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = C.c_int
+    for name, args in VOID_PROTOTYPES.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = None
     L.gk_launch_count.restype = C.c_uint64
     L.gk_launch_count.argtypes = []
     L.gk_abi_version.restype = C.c_int

@@ -151,6 +151,7 @@ gk_status gk_ctx_create(int device, gk_ctx** out) {
                                    std::to_string(prop.major) + std::to_string(prop.minor));
     auto* c = new gk_ctx();
     c->device = device;
+    c->opts = gk::default_fill_options();
     c->sm_count = prop.multiProcessorCount;
     cudaMemPool_t pool;
     GK_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -200,6 +201,21 @@ gk_status gk_ctx_set_stream(gk_ctx* c, void* s) {
   return guarded([&] {
     check_ctx(c);
     c->stream = static_cast<cudaStream_t>(s);
+  });
+}
+
+void gk_fill_options_init(gk_fill_options* o) {
+  if (o) *o = gk::default_fill_options();
+}
+
+void gk_mesh_options_init(gk_mesh_options* o) {
+  if (o) *o = gk::default_mesh_options();
+}
+
+gk_status gk_ctx_set_fill_options(gk_ctx* c, const gk_fill_options* o) {
+  return guarded([&] {
+    check_ctx(c);
+    c->opts = o ? *o : gk::default_fill_options();
   });
 }
 
@@ -650,7 +666,17 @@ gk_status gk_accumulate_batch_host(gk_ctx* c, const gk_table* t, gk_kind kind, d
 
 gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32_t* tris,
                          size_t nt, int m, int n, gk_mesh** out) {
+  return gk_mesh_create_ex(c, verts, nv, tris, nt, m, n, nullptr, out);
+}
+
+gk_status gk_mesh_create_ex(gk_ctx* c, const double* verts, size_t nv, const uint32_t* tris,
+                            size_t nt, int m, int n, const gk_mesh_options* opts,
+                            gk_mesh** out) {
   return guarded([&] {
+    const gk_mesh_options mo = opts ? *opts : gk::default_mesh_options();
+    need(mo.edge_chunks == 0 || mo.edge_chunks == GK_AUTO ||
+             (mo.edge_chunks >= 1 && mo.edge_chunks * 32 <= gk::kEdgeCap),
+         GK_ERR_INVALID_ARGUMENT, "gk_mesh_options: edge_chunks must be 1..12");
     check_ctx(c);
     need(out != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");
     validate_spec(m, n);  // fill_matrix validates the spec first (matfill.hpp:148)
@@ -695,7 +721,7 @@ gk_status gk_mesh_create(gk_ctx* c, const double* verts, size_t nv, const uint32
       GK_CUDA(cudaMemcpyAsync(mesh->verts.p, verts, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, c->stream));
       GK_CUDA(cudaMemcpyAsync(dt.p, tris, 3 * nt * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
       gk::launch_points(mesh, mesh->verts.p, dt.p, c->stream);
-      gk::build_edge_blocks(mesh, verts, tris);
+      gk::build_edge_blocks(mesh, verts, tris, mo);
       GK_CUDA(cudaStreamSynchronize(c->stream));
     } catch (...) {
       delete mesh;
@@ -812,7 +838,8 @@ namespace {
 // fill_rows on the device for kind EXP / GREEN, or 2 = the fused pair (z: Exp, z2: Green)
 void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t, int kind,
                     double k_re, double k_im, size_t row_begin, size_t row_end, gk_c128* z,
-                    gk_c128* z2, size_t ldz, gk_fill_report* report) {
+                    gk_c128* z2, size_t ldz, const gk_fill_options* opts,
+                    gk_fill_report* report) {
   check_ctx(c);
   need(mesh != nullptr, GK_ERR_INVALID_ARGUMENT, "null mesh");
   need(mode == GK_MODE_DIRECT || mode == GK_MODE_TABLE, GK_ERR_INVALID_ARGUMENT, "bad mode");
@@ -837,7 +864,8 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
   }
   const bool counted =
-      gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, z2, ldz, cnt);
+      gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, z2, ldz, cnt,
+                      opts ? *opts : c->opts);
   if (!report) return;
   GK_CUDA(cudaEventRecord(c->ev1, c->stream));
   unsigned long long h[4];
@@ -875,21 +903,22 @@ gk_status gk_fill_check(gk_ctx* c, uint64_t* fallbacks) {
 
 gk_status gk_fill_rows(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t,
                        gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
-                       gk_c128* z, size_t ldz, gk_fill_report* report) {
+                       gk_c128* z, size_t ldz, const gk_fill_options* opts,
+                       gk_fill_report* report) {
   return guarded([&] {
     need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
     fill_rows_impl(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, nullptr, ldz,
-                   report);
+                   opts, report);
   });
 }
 
 gk_status gk_fill_rows_pair(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t,
                             double k_re, double k_im, size_t row_begin, size_t row_end,
                             gk_c128* z_exp, gk_c128* z_green, size_t ldz,
-                            gk_fill_report* report) {
+                            const gk_fill_options* opts, gk_fill_report* report) {
   return guarded([&] {
     fill_rows_impl(c, mesh, mode, t, 2, k_re, k_im, row_begin, row_end, z_exp, z_green, ldz,
-                   report);
+                   opts, report);
   });
 }
 
@@ -898,7 +927,8 @@ namespace {
 // chunked, double-buffered device fill + D2H into host memory
 void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                        gk_kind kind, double k_re, double k_im, size_t row_begin, size_t row_end,
-                       gk_c128* z_host, size_t ldz, gk_fill_report* report) {
+                       gk_c128* z_host, size_t ldz, const gk_fill_options& opts,
+                       gk_fill_report* report) {
   const size_t nt = mesh->N;
   need(ldz >= nt, GK_ERR_INVALID_ARGUMENT, "ldz_host < N");
   need(row_begin <= row_end && row_end <= nt, GK_ERR_INVALID_ARGUMENT, "bad row range");
@@ -947,7 +977,8 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       const size_t re = rb + step < row_end ? rb + step : row_end;
       const int b = static_cast<int>(idx & 1);
       if (idx >= 2) GK_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
-      counted = gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt, cnt);
+      counted = gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt,
+                                cnt, opts);
       GK_CUDA(cudaEventRecord(filled[b], c->stream));
       GK_CUDA(cudaStreamWaitEvent(copy, filled[b], 0));
       if (ldz == nt)  // contiguous rows on both sides: one linear copy
@@ -987,13 +1018,15 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
 
 gk_status gk_fill_rows_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table* t,
                             gk_kind kind, double k_re, double k_im, size_t row_begin,
-                            size_t row_end, gk_c128* z_host, size_t ldz, gk_fill_report* report) {
+                            size_t row_end, gk_c128* z_host, size_t ldz,
+                            const gk_fill_options* opts, gk_fill_report* report) {
   return guarded([&] {
     check_ctx(c);
     need(mesh != nullptr, GK_ERR_INVALID_ARGUMENT, "null mesh");
     need(kind == GK_KIND_EXP || kind == GK_KIND_GREEN, GK_ERR_INVALID_ARGUMENT, "bad kind");
     use_device(c);
-    fill_rows_to_host(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z_host, ldz, report);
+    fill_rows_to_host(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z_host, ldz,
+                      opts ? *opts : c->opts, report);
   });
 }
 
@@ -1009,8 +1042,10 @@ gk_status gk_fill_matrix_host(gk_ctx* c, const double* verts, size_t nv, const u
     need(mode != GK_MODE_TABLE || cfg, GK_ERR_INVALID_ARGUMENT, "TABLE mode needs a config");
     double k_re, k_im;
     wavenumber(*med, k_re, k_im);
-    if (gk_mesh_create(c, verts, nv, tris, nt, m, n, &mesh) != GK_OK)
-      gk::fail(GK_ERR_INVALID_ARGUMENT, g_last_error);
+    // the mesh's own status (invalid_argument, or runtime_error for a CUDA /
+    // out-of-memory failure) is the call's
+    const gk_status ms = gk_mesh_create(c, verts, nv, tris, nt, m, n, &mesh);
+    if (ms != GK_OK) gk::fail(ms, g_last_error);
     if (mode == GK_MODE_TABLE) {
       gk_sampling_config cc = *cfg;
       if (cc.r_min <= 0.0 || cc.r_max <= 0.0) {
@@ -1024,7 +1059,7 @@ gk_status gk_fill_matrix_host(gk_ctx* c, const double* verts, size_t nv, const u
       if (s != GK_OK) gk::fail(s, g_last_error);
     }
     use_device(c);
-    fill_rows_to_host(c, mesh, mode, table, kind, k_re, k_im, 0, nt, z_host, nt, report);
+    fill_rows_to_host(c, mesh, mode, table, kind, k_re, k_im, 0, nt, z_host, nt, c->opts, report);
   });
   gk_table_destroy(table);
   gk_mesh_destroy(mesh);
@@ -1059,16 +1094,16 @@ gk_status gk_bench_compare(gk_ctx* c, const double* verts, size_t nv, const uint
     zi.alloc(nt * nt, c->stream);
     gk_fill_report ra{}, ri{};
     fill_rows_impl(c, mesh, GK_MODE_DIRECT, nullptr, kind, k_re, k_im, 0, nt, za.p, nullptr, nt,
-                   &ra);
+                   nullptr, &ra);
     fill_rows_impl(c, mesh, GK_MODE_TABLE, table, kind, k_re, k_im, 0, nt, zi.p, nullptr, nt,
-                   &ri);
+                   nullptr, &ri);
     for (int rep = 1; rep < repeats; ++rep) {  // interleaved (matfill.hpp:279-284)
       gk_fill_report r2{}, r3{};
       fill_rows_impl(c, mesh, GK_MODE_DIRECT, nullptr, kind, k_re, k_im, 0, nt, za.p, nullptr,
-                     nt, &r2);
+                     nt, nullptr, &r2);
       ra.wall_time_s = std::min(ra.wall_time_s, r2.wall_time_s);
       fill_rows_impl(c, mesh, GK_MODE_TABLE, table, kind, k_re, k_im, 0, nt, zi.p, nullptr, nt,
-                     &r3);
+                     nullptr, &r3);
       ri.wall_time_s = std::min(ri.wall_time_s, r3.wall_time_s);
     }
     gk_bench_report r{};

@@ -84,7 +84,7 @@ __global__ void edge_delta_kernel(const double4* __restrict__ inner, size_t N, i
 }  // namespace
 
 EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, size_t N,
-                          size_t cap, int order_mode) {
+                          size_t cap, int order_mode, int leaf_pct) {
   // global edge ids: edges bucketed by their lower vertex (CSR), distinct
   // upper vertices numbered within each bucket
   std::vector<uint32_t> start(nv + 1, 0);
@@ -250,11 +250,9 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
         }
       return cnt;
     };
-    size_t tfrac = 61;  // leaf triangles per edge slot, percent (~1.6 edges per triangle)
-    if (const char* e = std::getenv("GK_EDGE_TFRAC")) {  // A/B
-      const long v = std::atol(e);
-      if (v >= 30 && v <= 100) tfrac = static_cast<size_t>(v);
-    }
+    // leaf triangles per edge slot, percent (~1.6 edges per triangle);
+    // gk_mesh_options.leaf_pct for A/B
+    const size_t tfrac = leaf_pct >= 30 && leaf_pct <= 100 ? static_cast<size_t>(leaf_pct) : 61;
     const size_t T = std::max<size_t>(1, (cap * tfrac) / 100);
     std::vector<std::pair<size_t, size_t>> stack{{0, N}};
     while (!stack.empty()) {
@@ -307,26 +305,23 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
   return P;
 }
 
-void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris) {
+void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,
+                       const gk_mesh_options& opts) {
   const size_t N = mesh->N, nv = mesh->nv;
   const int n = mesh->n;
   mesh->nblk = 0;
   mesh->edge_ratio = 1.0;
   mesh->r_far = INFINITY;
-  if (const char* e = std::getenv("GK_EDGE"))
-    if (e[0] == '0') return;
+  if (opts.shared_edges == 0) return;
   size_t cap = 32 * kEdgeChunksDefault;
-  if (const char* e = std::getenv("GK_EDGE_CHUNKS")) {  // block size (tests, A/B)
-    const long c = std::atol(e);
-    if (c >= 1 && c * 32 <= kEdgeCap) cap = static_cast<size_t>(c) * 32;
-  }
+  if (opts.edge_chunks >= 1 && opts.edge_chunks * 32 <= kEdgeCap)  // block size (tests, A/B)
+    cap = static_cast<size_t>(opts.edge_chunks) * 32;
   mesh->ecap = static_cast<int>(cap);
   // the edge kernels unroll the n points of an edge (n = 1..5)
   if (N > (size_t(1) << 30) || n > 5) return;
-  int order_mode = -1;
-  if (const char* e = std::getenv("GK_EDGE_ORDER"))  // 0: mesh order, 1: bisection order (A/B)
-    order_mode = e[0] == '1' ? 1 : 0;
-  EdgePlan R = plan_edge_blocks(verts, nv, tris, N, cap, order_mode);
+  // -1: the more compact of mesh and bisection order; 0 / 1 forced (A/B)
+  const int order_mode = opts.edge_order == 0 || opts.edge_order == 1 ? opts.edge_order : -1;
+  EdgePlan R = plan_edge_blocks(verts, nv, tris, N, cap, order_mode, opts.leaf_pct);
   const bool ordered = R.ordered;
   double X = 0.0;
   for (size_t i = 0; i < 3 * nv; ++i) X = std::max(X, std::fabs(verts[i]));

@@ -67,11 +67,10 @@ __global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
 #define GK_EVAL_BLOCKS_PER_SM 32  // eval_batch grid cap (blocks of 256 per SM)
 #endif
 
-// GK_EVAL_LIBDEVICE=1: eval_batch through libdevice sincos (A/B, tests)
-static bool fast_eval() {
-  const char* e = std::getenv("GK_EVAL_LIBDEVICE");
-  return !(e && e[0] == '1');
-}
+// the context's options: eval_libdevice = 1 takes libdevice sincos instead of
+// the phase table (A/B, tests); arith_locate = 0 disables the arithmetic index
+static bool fast_eval(const gk_ctx* ctx) { return ctx->opts.eval_libdevice != 1; }
+static bool arith_locate(const gk_ctx* ctx) { return ctx->opts.arith_locate != 0; }
 
 template <int KIND>
 void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, double2* out,
@@ -83,8 +82,8 @@ void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n,
   const unsigned g = static_cast<unsigned>(grid);
   TableDev T{};
   if (t) T = t->dev;
-  if (!table_arith_enabled()) T.ncoarse = 0;
-  if (!t && k_im == 0.0 && fast_eval())
+  if (!arith_locate(ctx)) T.ncoarse = 0;
+  if (!t && k_im == 0.0 && fast_eval(ctx))
     eval_batch_kernel<KIND, false, 0, true><<<g, 256, 0, ctx->stream>>>(
         r, n, out, T, k_re, k_im, w, ctx->phase_small.p, k_re * kPhaseSmall / (2.0 * kPi));
   else if (!t)
@@ -207,10 +206,10 @@ void launch_accumulate_kind(gk_ctx* ctx, const gk_table* t, const double* r, con
   const unsigned g = static_cast<unsigned>(grid);
   TableDev T{};
   if (t) T = t->dev;
-  if (!table_arith_enabled()) T.ncoarse = 0;
+  if (!arith_locate(ctx)) T.ncoarse = 0;
   const double K1s = k_re * kPhaseSmall / (2.0 * kPi);
   const double2* ptab = ctx->phase_small.p;
-  if (!t && k_im == 0.0 && fast_eval())
+  if (!t && k_im == 0.0 && fast_eval(ctx))
     accumulate_kernel<KIND, false, 0, true><<<g, 256, 0, ctx->stream>>>(
         r, wts, len, nblocks, out, T, k_re, k_im, w, ptab, K1s);
   else if (!t)

@@ -23,7 +23,8 @@ __global__ void lossy_phase_kernel(double2* tab, double* ahi, int nhi, double c)
 
 bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                  int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
-                 gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* counters) {
+                 gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* counters,
+                 const gk_fill_options& opts) {
   FillArgs a{};
   a.outer = mesh->outer.p;
   a.inner = mesh->inner.p;
@@ -39,7 +40,7 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.z2 = reinterpret_cast<double2*>(z2);
   a.ldz = ldz;
   if (table) a.T = table->dev;
-  if (!table_arith_enabled()) a.T.ncoarse = 0;
+  if (opts.arith_locate == 0) a.T.ncoarse = 0;
   a.phase = ctx->phase.p;
   a.K1 = k_re * kPhaseM / (2.0 * kPi);
   a.k_re = k_re;
@@ -50,10 +51,7 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   DevBuf<double> atten;
   DevBuf<double2> lossy_tab;
   int att = 0;
-  static const bool phase_att = [] {
-    const char* e = std::getenv("GK_LOSSY_PHASE");
-    return !(e && e[0] == '0');
-  }();
+  const bool phase_att = opts.lossy_phase != 0;
   if (mode == GK_MODE_DIRECT && k_im != 0.0 && k_im < 0.0 && k_re > 0.0 && phase_att &&
       kPi * -k_im / (k_re * kPhaseM) <= 1e-3) {
     // attenuation coupled to the phase reduction (cis_phase_att): per-fill
@@ -100,12 +98,14 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   // reference's); a far pair above r_max is still detected (the fill fails
   // with out_of_range as the reference's does, its count then covering the
   // shared evaluations).
-  // GK_TABLE_EDGE=0 keeps the per-triangle table kernels.
-  const bool table_edges = mode == GK_MODE_TABLE && table_edge_enabled() && table;
-  if ((mode == GK_MODE_DIRECT || table_edges) && edge_fill_enabled() &&
+  // opts.shared_edges = 0 keeps the per-triangle kernels; 1 takes the shared
+  // edges for any mesh size
+  const bool forced = opts.shared_edges == 1;
+  const bool table_edges = mode == GK_MODE_TABLE && table;
+  if ((mode == GK_MODE_DIRECT || table_edges) && opts.shared_edges != 0 &&
       mesh->nblk > 0 && mesh->edge_ratio < 0.85 && mesh->n <= 5 &&
       mesh->r_far < 0.25 * mesh->diameter &&  // else few far tiles (e.g. coordinates far from the origin)
-      (att == 0 || (att == 1 && a.nhi <= 512)) && (mesh->N >= 4096 || edge_fill_forced())) {
+      (att == 0 || (att == 1 && a.nhi <= 512)) && (mesh->N >= 4096 || forced)) {
     a.eblk = mesh->eblk.p;
     a.ep = mesh->ep.p;
     a.ecol = mesh->ecol.p;
@@ -116,11 +116,11 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   }
   const int degree = table ? table->dev.degree : 3;
   switch (mesh->m) {
-    case 1: return dispatch_mo<1>(ctx, a, mode, kind, degree, att);
-    case 3: return dispatch_mo<3>(ctx, a, mode, kind, degree, att);
-    case 4: return dispatch_mo<4>(ctx, a, mode, kind, degree, att);
-    case 6: return dispatch_mo<6>(ctx, a, mode, kind, degree, att);
-    case 7: return dispatch_mo<7>(ctx, a, mode, kind, degree, att);
+    case 1: return dispatch_mo<1>(ctx, a, mode, kind, degree, att, opts);
+    case 3: return dispatch_mo<3>(ctx, a, mode, kind, degree, att, opts);
+    case 4: return dispatch_mo<4>(ctx, a, mode, kind, degree, att, opts);
+    case 6: return dispatch_mo<6>(ctx, a, mode, kind, degree, att, opts);
+    case 7: return dispatch_mo<7>(ctx, a, mode, kind, degree, att, opts);
     default: fail(GK_ERR_INVALID_ARGUMENT, "QuadratureSpec: outer_points must be one of 1, 3, 4, 6, 7");
   }
 }

@@ -1116,15 +1116,12 @@ bool launch_table_edge(gk_ctx* ctx, FillArgs a) {
 
 // returns true when a shared-edge kernel ran (it counts its evaluations)
 template <int MO, int MODE, int KIND, int DEG, int ATT>
-bool launch_one(gk_ctx* ctx, FillArgs a) {
+bool launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
   if constexpr (MODE == GK_MODE_DIRECT) {
     const size_t smem = kPhaseM * sizeof(double2) +
                         (ATT == 1 ? a.nhi * sizeof(double) : 0) +
                         (ATT == 2 ? a.natten * sizeof(double) : 0);
-    static const bool use_v4 = [] {
-      const char* e = std::getenv("GK_DIRECT_V4");
-      return !(e && e[0] == '0');
-    }();
+    const bool use_v4 = o.unrolled != 0;
     // shared-edge path (edges.cu): single kind, lossless or phase-coupled
     // attenuation, n = 1..5; launch_fill leaves nblk = 0 where it does not pay
     if constexpr (ATT != 2) {
@@ -1164,14 +1161,15 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
     launch_kernel(ctx, direct_kernel<MO, KIND, ATT, 2>, a, smem);
     return false;
   } else {
-    // GK_TABLE_SMEM: 0 = L1 kernel, 2 = always stage (tests), unset/1 = auto.
-    // GK_TABLE_SMEM_BUDGET (bytes) shrinks the window budget (tests).  Read per
-    // launch so a test can exercise every path in one process.
-    const char* env = std::getenv("GK_TABLE_SMEM");
-    const int staging = env ? std::atoi(env) : 1;
-    // GK_TABLE_EDGE=2: K3e whenever the blocks allow (A/B)
-    if (a.nblk > 0 && table_edge_forced()) return launch_table_edge<MO, KIND, DEG>(ctx, a);
-    if (staging == 0) {
+    // o.table_placement: GK_TABLE_GLOBAL = through L1 (K3e where the mesh's
+    // shared-edge blocks are in use, else the per-triangle L1 kernel),
+    // GK_TABLE_SHARED = always staged per triangle (whole or per-tile
+    // windows; tests and A/B), GK_AUTO = by size.  o.smem_budget shrinks the
+    // window budget (tests).
+    const int placement = o.table_placement;
+    const bool automatic = placement != GK_TABLE_GLOBAL && placement != GK_TABLE_SHARED;
+    if (a.nblk > 0 && placement == GK_TABLE_GLOBAL) return launch_table_edge<MO, KIND, DEG>(ctx, a);
+    if (placement == GK_TABLE_GLOBAL) {
       set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
       launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
       return false;
@@ -1180,10 +1178,7 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
     constexpr bool want_e = KIND == GK_KIND_EXP || KIND == kKindPair;
     const size_t rec_bytes = static_cast<size_t>(a.T.grs) * 8 + (want_e ? 48 : 0);
     size_t budget = 200 * 1024;
-    if (const char* b = std::getenv("GK_TABLE_SMEM_BUDGET")) {
-      const long v = std::atol(b);
-      if (v >= 4096 && static_cast<size_t>(v) < budget) budget = static_cast<size_t>(v);
-    }
+    if (o.smem_budget >= 4096 && o.smem_budget < budget) budget = static_cast<size_t>(o.smem_budget);
     StageArgs S{};
     const size_t nlk4 = (static_cast<size_t>(a.T.nlk) + 3) & ~size_t(3);
     const bool whole = nlk4 * 4 + a.T.nrec * rec_bytes <= budget;
@@ -1191,7 +1186,7 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
     // (<= 300 KB of records) goes to K3e: C4 at S = 1e3 (233 KB) 145 vs 180 ms
     // windowed-staged; C3 (548 KB) and C5 (1.1 MB) stay staged (343 vs 311,
     // 184 vs 158 ms per 4096 rows)
-    if (a.nblk > 0 && env == nullptr && !whole && a.T.nrec * rec_bytes <= 300 * 1024)
+    if (a.nblk > 0 && automatic && !whole && a.T.nrec * rec_bytes <= 300 * 1024)
       return launch_table_edge<MO, KIND, DEG>(ctx, a);
     if (whole) {
       S.whole = 1;
@@ -1205,13 +1200,13 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
       // capacity (dense tables, e.g. S = 1e4 on large meshes) every tile would
       // fall back to global reads: use the L1 kernel with its wider tiles
       const double est = a.T.nrec * a.window_est / (a.T.r_max - a.T.r_min);
-      if (staging != 2 && est > 2.0 * static_cast<double>(j_cap)) {
+      if (automatic && est > 2.0 * static_cast<double>(j_cap)) {
         // shared edges (K3e) instead of the L1 kernel: both read the table
         // through L1; K3e 1.3-1.4x faster at S = 1e4 on C3/C4/C5.  Tables
         // staged in shared memory (whole or per tile window) stay per
         // triangle: faster than K3e through L1 (C5 S = 1e3: 158 vs 225 ms
         // per 4096 rows).  Not when a test forces a staging path.
-        if (a.nblk > 0 && env == nullptr) return launch_table_edge<MO, KIND, DEG>(ctx, a);
+        if (a.nblk > 0) return launch_table_edge<MO, KIND, DEG>(ctx, a);
         set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
         launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
         return false;
@@ -1239,33 +1234,34 @@ bool launch_one(gk_ctx* ctx, FillArgs a) {
 }
 
 template <int MO, int KIND>
-bool dispatch_att(gk_ctx* ctx, const FillArgs& a, int att) {
-  if (att == 1) return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 1>(ctx, a);
-  if (att == 2) return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 2>(ctx, a);
-  return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 0>(ctx, a);
+bool dispatch_att(gk_ctx* ctx, const FillArgs& a, int att, const gk_fill_options& o) {
+  if (att == 1) return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 1>(ctx, a, o);
+  if (att == 2) return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 2>(ctx, a, o);
+  return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 0>(ctx, a, o);
 }
 
 // returns true when a shared-edge kernel ran (launch_fill)
 template <int MO>
-bool dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, int att) {
+bool dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, int att,
+                 const gk_fill_options& o) {
   if (mode == GK_MODE_DIRECT) {
-    if (kind == GK_KIND_GREEN) return dispatch_att<MO, GK_KIND_GREEN>(ctx, a, att);
-    if (kind == GK_KIND_EXP) return dispatch_att<MO, GK_KIND_EXP>(ctx, a, att);
-    return dispatch_att<MO, kKindPair>(ctx, a, att);
+    if (kind == GK_KIND_GREEN) return dispatch_att<MO, GK_KIND_GREEN>(ctx, a, att, o);
+    if (kind == GK_KIND_EXP) return dispatch_att<MO, GK_KIND_EXP>(ctx, a, att, o);
+    return dispatch_att<MO, kKindPair>(ctx, a, att, o);
   }
-  if (kind == GK_KIND_EXP) return launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, 0>(ctx, a);
+  if (kind == GK_KIND_EXP) return launch_one<MO, GK_MODE_TABLE, GK_KIND_EXP, 0, 0>(ctx, a, o);
   if (kind == GK_KIND_GREEN && degree == 3)
-    return launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, 0>(ctx, a);
-  if (kind == GK_KIND_GREEN) return launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, 0>(ctx, a);
-  if (degree == 3) return launch_one<MO, GK_MODE_TABLE, kKindPair, 3, 0>(ctx, a);
-  return launch_one<MO, GK_MODE_TABLE, kKindPair, 0, 0>(ctx, a);
+    return launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 3, 0>(ctx, a, o);
+  if (kind == GK_KIND_GREEN) return launch_one<MO, GK_MODE_TABLE, GK_KIND_GREEN, 0, 0>(ctx, a, o);
+  if (degree == 3) return launch_one<MO, GK_MODE_TABLE, kKindPair, 3, 0>(ctx, a, o);
+  return launch_one<MO, GK_MODE_TABLE, kKindPair, 0, 0>(ctx, a, o);
 }
 
 // one explicit instantiation per translation unit (fill_mo<m>.cu)
-extern template bool dispatch_mo<1>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
-extern template bool dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
-extern template bool dispatch_mo<4>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
-extern template bool dispatch_mo<6>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
-extern template bool dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int);
+extern template bool dispatch_mo<1>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template bool dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template bool dispatch_mo<4>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template bool dispatch_mo<6>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template bool dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
 
 }  // namespace gk

@@ -75,6 +75,7 @@ struct gk_ctx {
   gk::DevBuf<double2> phase_small;         // eval_batch phase table (kPhaseSmall, L1-resident)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   HostFillPipe pipe;
+  gk_fill_options opts{};  // defaults for calls without options (gk_ctx_set_fill_options)
 };
 
 struct gk_table {
@@ -119,35 +120,26 @@ struct gk_mesh {
 
 namespace gk {
 
-// GK_TABLE_ARITH=0: table lookups without the arithmetic-locate fast path
-// (A/B and tests; read per launch)
-inline bool table_arith_enabled() {
-  const char* e = std::getenv("GK_TABLE_ARITH");
-  return !(e && e[0] == '0');
+// library defaults of the kernel selection (gk_fill_options_init)
+inline gk_fill_options default_fill_options() {
+  gk_fill_options o;
+  o.shared_edges = GK_AUTO;
+  o.table_placement = GK_AUTO;
+  o.arith_locate = GK_AUTO;
+  o.lossy_phase = GK_AUTO;
+  o.unrolled = GK_AUTO;
+  o.eval_libdevice = GK_AUTO;
+  o.smem_budget = 0;
+  return o;
 }
 
-// GK_EDGE=0: direct fills without the shared-edge path (A/B and tests; read
-// per launch; GK_EDGE=0 at mesh creation also skips building the blocks)
-inline bool edge_fill_enabled() {
-  const char* e = std::getenv("GK_EDGE");
-  return !(e && e[0] == '0');
-}
-
-// GK_TABLE_EDGE=0: table fills without shared edges (read per launch)
-inline bool table_edge_enabled() {
-  const char* e = std::getenv("GK_TABLE_EDGE");
-  return !(e && e[0] == '0');
-}
-
-inline bool table_edge_forced() {
-  const char* e = std::getenv("GK_TABLE_EDGE");
-  return e && e[0] == '2';
-}
-
-// GK_EDGE=2: the shared-edge path also for small meshes (tests)
-inline bool edge_fill_forced() {
-  const char* e = std::getenv("GK_EDGE");
-  return e && e[0] == '2';
+inline gk_mesh_options default_mesh_options() {
+  gk_mesh_options o;
+  o.shared_edges = GK_AUTO;
+  o.edge_chunks = 0;
+  o.edge_order = GK_AUTO;
+  o.leaf_pct = 0;
+  return o;
 }
 
 // launch accounting (gk_launch_count)
@@ -181,10 +173,11 @@ struct EdgePlan {
   bool ordered = false;
 };
 EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, size_t N,
-                          size_t cap, int order_mode);
+                          size_t cap, int order_mode, int leaf_pct = 0);
 // the device part for a mesh whose points launch_points has produced;
 // synchronises the context stream
-void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris);
+void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,
+                       const gk_mesh_options& opts);
 // max over vertex pairs of |a - b|^2 (reference summation order) -> *d2_bits
 void launch_max_vertex_d2(const double* verts, size_t nv, unsigned long long* d2_bits,
                           cudaStream_t s);
@@ -208,7 +201,8 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
 // performed into counters[3]; otherwise they equal the reference's calls.
 bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                  int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
-                 gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* d_fallbacks);
+                 gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* d_fallbacks,
+                 const gk_fill_options& opts);
 void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,
                   double* d2min, double* d2max);
 void launch_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,

@@ -180,8 +180,47 @@ def _torch():
     return torch
 
 
+@dataclass
+class FillOptions:
+    """gk_fill_options: the choice between equivalent kernels, per call
+    (AUTO = -1 everywhere = the measured best; see include/gk/gk.h)."""
+
+    shared_edges: int = _lib.GK_AUTO      # 0: per-triangle (reference order), 1: forced
+    table_placement: int = _lib.GK_AUTO   # 0: GLOBAL (L1/L2), 1: SHARED (staged)
+    arith_locate: int = _lib.GK_AUTO
+    lossy_phase: int = _lib.GK_AUTO
+    unrolled: int = _lib.GK_AUTO
+    eval_libdevice: int = _lib.GK_AUTO
+    smem_budget: int = 0
+
+    def c(self) -> _lib.FillOptionsC:
+        return _lib.FillOptionsC(self.shared_edges, self.table_placement, self.arith_locate,
+                                 self.lossy_phase, self.unrolled, self.eval_libdevice,
+                                 self.smem_budget)
+
+
+@dataclass
+class MeshOptions:
+    """gk_mesh_options: shared-edge block construction at mesh creation."""
+
+    shared_edges: int = _lib.GK_AUTO
+    edge_chunks: int = 0                  # 0: 11
+    edge_order: int = _lib.GK_AUTO        # 0: mesh order, 1: bisection order
+    leaf_pct: int = 0                     # 0: 61
+
+    def c(self) -> _lib.MeshOptionsC:
+        return _lib.MeshOptionsC(self.shared_edges, self.edge_chunks, self.edge_order,
+                                 self.leaf_pct)
+
+
+def _opts(options: FillOptions | None):
+    return C.byref(options.c()) if options is not None else None
+
+
 class Context:
-    """One gk_ctx per CUDA device, running on torch's current stream."""
+    """One gk_ctx per CUDA device, running on torch's current stream (bound
+    again by every launching call, so ``with torch.cuda.stream(s):`` is
+    honoured)."""
 
     _cache: dict[int, "Context"] = {}
 
@@ -225,6 +264,12 @@ class Context:
 
     def synchronize(self) -> None:
         check(lib().gk_ctx_synchronize(self.h), "synchronize")
+
+    def set_fill_options(self, options: FillOptions | None) -> None:
+        """The context's default kernel selection (gk_ctx_set_fill_options):
+        used by calls that take no options (fill_matrix, bench_compare,
+        eval_batch).  None restores the library defaults."""
+        check(lib().gk_ctx_set_fill_options(self.h, _opts(options)), "set_fill_options")
 
     def fill_check(self) -> int:
         """Synchronise; raise like a synchronous fill if any asynchronous fill
@@ -277,6 +322,7 @@ class DeviceTable:
         self.ctx = ctx or Context.get()
         self.cfg, self.medium = cfg, medium
         h = C.c_void_p()
+        self.ctx.bind_stream()
         check(lib().gk_table_build(self.ctx.h, C.byref(cfg.c()), C.byref(medium.c()),
                                    lagrange_degree, C.byref(h)), "KernelEvaluator")
         self.h = h
@@ -335,6 +381,7 @@ class DeviceTable:
         torch = _torch()
         r = _as_device_f64(radii, self.ctx.device)
         out = torch.empty(r.numel(), dtype=torch.int32, device=r.device)
+        self.ctx.bind_stream()
         check(lib().gk_locate(self.ctx.h, self.h, r.data_ptr() if r.numel() else None, r.numel(),
                               out.data_ptr() if r.numel() else None), "locate")
         return out
@@ -346,6 +393,7 @@ class DeviceTable:
         if method is None:
             method = InterpMethod.Linear if kind == KernelKind.PlainExp else InterpMethod.Lagrange
         r = _lib.SweepReportC()
+        self.ctx.bind_stream()
         check(lib().gk_error_sweep(self.ctx.h, self.h, int(kind), int(method), probe_count,
                                    C.byref(r)), "error_sweep")
         return ErrorSweepReport(r.probe_count, r.max_rel_re, r.max_rel_im, r.max_abs, r.worst_r,
@@ -376,6 +424,7 @@ def eval_batch(kind: KernelKind, radii, table: DeviceTable | None = None, k: com
     out = torch.empty(r.numel(), dtype=torch.complex128, device=r.device)
     fb = C.c_uint64()
     kc = complex(k)
+    ctx.bind_stream()
     check(lib().gk_eval_batch(ctx.h, table.h if table else None, int(kind), kc.real, kc.imag,
                               r.data_ptr() if r.numel() else None, r.numel(),
                               out.data_ptr() if r.numel() else None, C.byref(fb)), "eval_batch")
@@ -403,6 +452,7 @@ def accumulate_batch(kind: KernelKind, radii, weights, table: "DeviceTable | Non
     out = torch.empty(nb, dtype=torch.complex128, device=r.device)
     fb = C.c_uint64()
     kc = complex(k)
+    ctx.bind_stream()
     check(lib().gk_accumulate_batch(ctx.h, table.h if table else None, int(kind), kc.real,
                                     kc.imag, r.data_ptr() if r.numel() else None,
                                     w.data_ptr() if w.numel() else None, ln, nb,
@@ -423,11 +473,13 @@ class EvalStatus:
         self.reset()
 
     def reset(self) -> None:
+        self.ctx.bind_stream()
         check(lib().gk_eval_status_reset(self.ctx.h, self.words.data_ptr()), "eval_status")
 
     def read(self) -> int:
         """Synchronises; raises like eval_batch if any radius was invalid; returns fallbacks."""
         fb = C.c_uint64()
+        self.ctx.bind_stream()
         check(lib().gk_eval_status_read(self.ctx.h, self.words.data_ptr(), C.byref(fb)),
               "eval_batch")
         return fb.value
@@ -445,6 +497,7 @@ def eval_batch_async(kind: KernelKind, radii, out, status: EvalStatus,
                                                            and out.is_contiguous())):
         raise _lib.InvalidArgument("eval_batch_async: contiguous CUDA float64 radii and "
                                    "complex128 out[n]")
+    ctx.bind_stream()
     check(lib().gk_eval_batch_async(ctx.h, table.h if table else None, int(kind), kc.real, kc.imag,
                                     radii.data_ptr() if n else None, n,
                                     out.data_ptr() if n else None, status.words.data_ptr()),
@@ -475,13 +528,18 @@ def edge_blocks_plan(mesh: TriangleMesh, chunks: int = 11, order_mode: int = -1)
 class DeviceMesh:
     """A mesh resident on the device with its quadrature points (K0)."""
 
-    def __init__(self, mesh: TriangleMesh, spec: QuadratureSpec, ctx: Context | None = None):
+    def __init__(self, mesh: TriangleMesh, spec: QuadratureSpec, ctx: Context | None = None,
+                 options: MeshOptions | None = None):
         self.ctx = ctx or Context.get()
+        self.ctx.bind_stream()
         self.mesh, self.spec = mesh, spec
         h = C.c_void_p()
-        check(lib().gk_mesh_create(self.ctx.h, mesh.vertices.ctypes.data, mesh.vertices.shape[0],
-                                   mesh.triangles.ctypes.data, mesh.triangles.shape[0],
-                                   spec.outer_points, spec.inner_points_per_edge, C.byref(h)),
+        check(lib().gk_mesh_create_ex(self.ctx.h, mesh.vertices.ctypes.data,
+                                      mesh.vertices.shape[0], mesh.triangles.ctypes.data,
+                                      mesh.triangles.shape[0], spec.outer_points,
+                                      spec.inner_points_per_edge,
+                                      C.byref(options.c()) if options is not None else None,
+                                      C.byref(h)),
               "fill_matrix")
         self.h = h
         self.N = mesh.triangle_count()
@@ -520,6 +578,7 @@ class DeviceMesh:
     def max_vertex_distance(self) -> float:
         """max_vertex_distance (mesh.hpp:62-68), exact, on the device."""
         out = C.c_double()
+        self.ctx.bind_stream()
         check(lib().gk_max_vertex_distance(self.ctx.h, self.h, C.byref(out)),
               "max_vertex_distance")
         return out.value
@@ -528,6 +587,7 @@ class DeviceMesh:
         """K1: min/max quadrature pair distance over rows x all q != p"""
         row_end = self.N if row_end is None else row_end
         lo, hi = C.c_double(), C.c_double()
+        self.ctx.bind_stream()
         check(lib().gk_distance_range(self.ctx.h, self.h, row_begin, row_end, C.byref(lo),
                                       C.byref(hi)), "distance_range")
         return lo.value, hi.value
@@ -535,14 +595,17 @@ class DeviceMesh:
 
 def fill_rows(dmesh: DeviceMesh, mode: Mode, kind: KernelKind = KernelKind.GreenOverR,
               table: DeviceTable | None = None, k: complex = 0.0, row_begin: int = 0,
-              row_end: int | None = None, out=None, report: bool = True):
+              row_end: int | None = None, out=None, report: bool = True,
+              options: FillOptions | None = None):
     """fill_rows (matfill.hpp:169-203) for rows [row_begin,row_end) on the device.
 
     Returns (Z, FillReport | None); Z is a (rows, N) complex128 CUDA tensor.
     ``report=False`` launches asynchronously on the current stream.
+    ``options`` chooses between equivalent kernels (None: the context's).
     """
     torch = _torch()
     ctx = dmesh.ctx
+    ctx.bind_stream()
     N = dmesh.N
     row_end = N if row_end is None else row_end
     rows = row_end - row_begin
@@ -559,7 +622,7 @@ def fill_rows(dmesh: DeviceMesh, mode: Mode, kind: KernelKind = KernelKind.Green
     check(lib().gk_fill_rows(ctx.h, dmesh.h, int(mode), table.h if table else None, int(kind),
                              kc.real, kc.imag, row_begin, row_end,
                              out.data_ptr() if rows else None, out.stride(0) if rows else N,
-                             C.byref(rep) if report else None), "fill_matrix")
+                             _opts(options), C.byref(rep) if report else None), "fill_matrix")
     return out, (FillReport.from_c(rep) if report else None)
 
 
@@ -576,6 +639,7 @@ def compare_fills(test, ref, row_begin: int = 0, ctx: Context | None = None):
     rows, N = (t.shape[0], t.shape[1]) if t.dim() == 2 else (0, 0)
     assert t.dtype == r.dtype == torch.complex128 and t.is_cuda and r.is_cuda
     re, im = C.c_double(), C.c_double()
+    ctx.bind_stream()
     check(lib().gk_compare_fills(ctx.h, t.data_ptr() if t.numel() else None,
                                  r.data_ptr() if r.numel() else None, rows, N, row_begin,
                                  max(N, 1), C.byref(re), C.byref(im)), "compare_fills")
@@ -594,6 +658,7 @@ def bench_compare(mesh: TriangleMesh, spec: QuadratureSpec, medium: Medium = Med
     ctx = ctx or Context.get()
     cfg = cfg or SamplingConfig()
     r = _lib.BenchReportC()
+    ctx.bind_stream()
     check(lib().gk_bench_compare(ctx.h, mesh.vertices.ctypes.data, mesh.vertices.shape[0],
                                  mesh.triangles.ctypes.data, mesh.triangles.shape[0],
                                  spec.outer_points, spec.inner_points_per_edge,
@@ -608,11 +673,12 @@ def bench_compare(mesh: TriangleMesh, spec: QuadratureSpec, medium: Medium = Med
 
 def fill_rows_pair(dmesh: DeviceMesh, mode: Mode, table: DeviceTable | None = None,
                    k: complex = 0.0, row_begin: int = 0, row_end: int | None = None,
-                   report: bool = True):
+                   report: bool = True, options: FillOptions | None = None):
     """Fused Exp + Green fill sharing r (and the table lookup): returns
     (Z_exp, Z_green, FillReport) with each matrix identical to its separate fill."""
     torch = _torch()
     ctx = dmesh.ctx
+    ctx.bind_stream()
     N = dmesh.N
     row_end = N if row_end is None else row_end
     rows = row_end - row_begin
@@ -622,17 +688,19 @@ def fill_rows_pair(dmesh: DeviceMesh, mode: Mode, table: DeviceTable | None = No
     rep = FillReportC()
     check(lib().gk_fill_rows_pair(ctx.h, dmesh.h, int(mode), table.h if table else None, kc.real,
                                   kc.imag, row_begin, row_end, ze.data_ptr() if rows else None,
-                                  zg.data_ptr() if rows else None, N,
+                                  zg.data_ptr() if rows else None, N, _opts(options),
                                   C.byref(rep) if report else None), "fill_matrix")
     return ze, zg, (FillReport.from_c(rep) if report else None)
 
 
 def fill_rows_host(dmesh: DeviceMesh, mode: Mode, out: np.ndarray,
                    kind: KernelKind = KernelKind.GreenOverR, table: DeviceTable | None = None,
-                   k: complex = 0.0, row_begin: int = 0, row_end: int | None = None) -> FillReport:
+                   k: complex = 0.0, row_begin: int = 0, row_end: int | None = None,
+                   options: FillOptions | None = None) -> FillReport:
     """fill_rows straight into host memory (``out``: (rows, N) complex128, C order;
     pinned memory gets full PCIe bandwidth).  Chunked + double-buffered."""
     ctx = dmesh.ctx
+    ctx.bind_stream()
     N = dmesh.N
     row_end = N if row_end is None else row_end
     assert out.dtype == np.complex128 and out.flags.c_contiguous and out.shape[1] == N
@@ -641,7 +709,8 @@ def fill_rows_host(dmesh: DeviceMesh, mode: Mode, out: np.ndarray,
     rep = FillReportC()
     check(lib().gk_fill_rows_host(ctx.h, dmesh.h, int(mode), table.h if table else None,
                                   int(kind), kc.real, kc.imag, row_begin, row_end,
-                                  out.ctypes.data, N, C.byref(rep)), "fill_matrix")
+                                  out.ctypes.data, N, _opts(options), C.byref(rep)),
+          "fill_matrix")
     return FillReport.from_c(rep)
 
 
@@ -659,6 +728,7 @@ def fill_matrix(mesh: TriangleMesh, spec: QuadratureSpec, mode: Mode, medium: Me
     assert z.dtype == np.complex128 and z.flags.c_contiguous and z.shape == (N, N)
     rep = FillReportC()
     cfg_c = (cfg or SamplingConfig(r_min=0.0, r_max=0.0)).c()
+    ctx.bind_stream()
     check(lib().gk_fill_matrix_host(ctx.h, mesh.vertices.ctypes.data, mesh.vertices.shape[0],
                                     mesh.triangles.ctypes.data, N, spec.outer_points,
                                     spec.inner_points_per_edge, int(mode), C.byref(cfg_c),

@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """A/B of the shared-edge direct fill (K4e) against the per-triangle kernel
-(GK_EDGE=0) on the bench configurations: fill time, evaluations performed and
+(FillOptions(shared_edges=0)) on the bench configurations: fill time, evaluations performed and
 the largest entrywise difference relative to the entry's modulus.
 Usage: edge_ab.py [c2 c3 c4 c5] [--rows R]"""
 import os
@@ -13,10 +13,10 @@ import bench  # noqa: E402
 import paper_1901_04162_b200 as gk  # noqa: E402
 
 
-def fill(dm, k, rows, Z, reps=3):
+def fill(dm, k, rows, Z, opts, reps=3):
     best = None
     for _ in range(reps):
-        _, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, row_end=rows, out=Z)
+        _, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, row_end=rows, out=Z, options=opts)
         best = rep if best is None or rep.wall_time_s < best.wall_time_s else best
     return best
 
@@ -26,26 +26,25 @@ def main():
     rows_arg = int(sys.argv[sys.argv.index("--rows") + 1]) if "--rows" in sys.argv else 0
     chunks = sys.argv[sys.argv.index("--chunks") + 1].split(",") if "--chunks" in sys.argv else [None]
     for name, ch in [(n, c) for n in names for c in chunks]:
+        mopts = gk.MeshOptions()
         if ch:
-            os.environ["GK_EDGE_CHUNKS"] = ch
-            print(f"GK_EDGE_CHUNKS={ch}", end=" ")
+            mopts.edge_chunks = int(ch)
+            print(f"edge_chunks={ch}", end=" ")
         cfg = bench.CONFIGS[name]
         mesh = bench.make_mesh(gk, cfg)
         N = mesh.triangle_count()
         rows = rows_arg or (N if N <= 20480 else 8192)
         if "--order" in sys.argv:
-            os.environ["GK_EDGE_ORDER"] = sys.argv[sys.argv.index("--order") + 1]
-        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(cfg["m"], cfg["n"]))
+            mopts.edge_order = int(sys.argv[sys.argv.index("--order") + 1])
+        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(cfg["m"], cfg["n"]), options=mopts)
         med = gk.Medium(lambda0=cfg["lambda0"], eps_r=cfg.get("eps_r", 1.0),
                         eps_r_im=cfg.get("eps_r_im", 0.0))
         k = gk.wavenumber(med)
         info = dm.edge_info()
         Za = torch.empty((rows, N), dtype=torch.complex128, device="cuda")
         Zb = torch.empty_like(Za)
-        os.environ["GK_EDGE"] = "0"
-        ra = fill(dm, k, rows, Za)
-        os.environ["GK_EDGE"] = "2"  # forced: small meshes too
-        rb = fill(dm, k, rows, Zb)
+        ra = fill(dm, k, rows, Za, gk.FillOptions(shared_edges=0))
+        rb = fill(dm, k, rows, Zb, gk.FillOptions(shared_edges=1))  # forced: small meshes too
         d = (Zb - Za).abs()
         rel = (d / Za.abs().clamp_min(1e-300)).max().item()
         R = info["edges"] / (3.0 * N)

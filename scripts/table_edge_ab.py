@@ -1,8 +1,8 @@
 #!/usr/bin/env python3
 """A/B of the shared-edge table fill (K3e) against the per-triangle table
-kernels (GK_TABLE_EDGE=0) on the bench configurations, at S = 10^3 and 10^4.
+kernels (FillOptions(shared_edges=0)) on the bench configurations, at S = 10^3 and 10^4.
 Usage: table_edge_ab.py [c3 c4 c5] [--rows R]"""
-import os
+import os  # noqa: F401
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -12,10 +12,10 @@ import bench  # noqa: E402
 import paper_1901_04162_b200 as gk  # noqa: E402
 
 
-def fill(dm, t, rows, Z, reps=2):
+def fill(dm, t, rows, Z, opts, reps=2):
     best = None
     for _ in range(reps):
-        _, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t, row_end=rows, out=Z)
+        _, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t, row_end=rows, out=Z, options=opts)
         best = rep if best is None or rep.wall_time_s < best.wall_time_s else best
     return best
 
@@ -36,15 +36,11 @@ def main():
         Zb = torch.empty_like(Za)
         for S in (1000, 10000):
             t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S), med)
-            os.environ["GK_TABLE_EDGE"] = "0"
-            ra = fill(dm, t, rows, Za)
-            os.environ["GK_TABLE_EDGE"] = "1"
-            rb = fill(dm, t, rows, Zb)
+            ra = fill(dm, t, rows, Za, gk.FillOptions(shared_edges=0))
+            rb = fill(dm, t, rows, Zb, gk.FillOptions())
             rf = None
             if "--forced" in sys.argv:  # K3e also where the table is staged in shared memory
-                os.environ["GK_TABLE_EDGE"] = "2"
-                rf = fill(dm, t, rows, Zb)
-                os.environ["GK_TABLE_EDGE"] = "1"
+                rf = fill(dm, t, rows, Zb, gk.FillOptions(table_placement=gk.GK_TABLE_GLOBAL))
             rel = ((Zb - Za).abs() / Za.abs().clamp_min(1e-300)).max().item()
             print(f"{name} S={S} rows={rows} per-triangle {ra.wall_time_s * 1e3:.2f} ms, "
                   f"edge {rb.wall_time_s * 1e3:.2f} ms (x{ra.wall_time_s / rb.wall_time_s:.3f}); "

@@ -44,12 +44,27 @@ int main() {
     const auto a = dev.abscissae();
     for (std::size_t i = 0; i < a.size(); ++i) same_plan = same_plan && a[i] == ev.plan().abscissae[i];
   }
-  const bool ok = same_plan && rg.actual_calls == rc.actual_calls &&
-                  rg.fallback_calls == rc.fallback_calls && rc.fallback_calls > 0 &&
-                  worst < 1e-12;
+  bool ok = same_plan && rg.actual_calls == rc.actual_calls &&
+            rg.fallback_calls == rc.fallback_calls && rc.fallback_calls > 0 && worst < 1e-12;
   std::printf("plug: N=%zu calls %llu/%llu fallbacks %llu/%llu max rel diff %.3g -> %s\n",
               zc.n, (unsigned long long)rg.actual_calls, (unsigned long long)rc.actual_calls,
               (unsigned long long)rg.fallback_calls, (unsigned long long)rc.fallback_calls, worst,
               ok ? "OK" : "FAILED");
+
+  // threads = 4: the reference's fill calls accumulate from 4 worker threads
+  // at once (matfill.hpp:206-221); the device evaluator serialises its calls
+  // on the shared context and counts fallbacks atomically, so the result is
+  // the threads = 1 result and the fallback delta is the reference's
+  const gk::DeviceEvaluator dev4(ctx, gcfg, gk::Medium{1.0, 1.0, 1.0});
+  auto [z4, r4] = gktab::fill_matrix(mesh, spec, gk::DeviceTableKernel{&dev4},
+                                     gktab::KernelKind::GreenOverR, 4);
+  bool same4 = z4.z.size() == zg.z.size();
+  for (std::size_t i = 0; same4 && i < zg.z.size(); ++i) same4 = z4.z[i] == zg.z[i];
+  const bool ok4 = same4 && r4.actual_calls == rc.actual_calls &&
+                   r4.fallback_calls == rc.fallback_calls && dev4.fallback_count() == rc.fallback_calls;
+  std::printf("plug threads=4: calls %llu fallbacks %llu/%llu bitwise-equal to threads=1: %d -> %s\n",
+              (unsigned long long)r4.actual_calls, (unsigned long long)r4.fallback_calls,
+              (unsigned long long)rc.fallback_calls, same4 ? 1 : 0, ok4 ? "OK" : "FAILED");
+  ok = ok && ok4;
   return ok ? 0 : 1;
 }

@@ -143,10 +143,10 @@ int main() {
     std::vector<gk::Complex> strided(rows * ld, gk::Complex(7.0, 7.0)), dense(rows * N);
     CHECK(gk_fill_rows_host(ctx.get(), m, GK_MODE_DIRECT, nullptr, GK_KIND_GREEN, 6.283185307179586,
                             0.0, 10, 10 + rows, reinterpret_cast<gk_c128*>(strided.data()), ld,
-                            nullptr) == GK_OK);
+                            nullptr, nullptr) == GK_OK);
     CHECK(gk_fill_rows_host(ctx.get(), m, GK_MODE_DIRECT, nullptr, GK_KIND_GREEN, 6.283185307179586,
                             0.0, 10, 10 + rows, reinterpret_cast<gk_c128*>(dense.data()), N,
-                            nullptr) == GK_OK);
+                            nullptr, nullptr) == GK_OK);
     bool same = true, pad_kept = true;
     for (std::size_t r = 0; r < rows; ++r) {
       for (std::size_t q = 0; q < N; ++q) same = same && strided[r * ld + q] == dense[r * N + q];

@@ -23,7 +23,7 @@ def libgk():
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:gk_status|int|uint64_t|const char\*)\s+(gk_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:gk_status|int|uint64_t|void|const char\*)\s+(gk_\w+)\s*\(",
                                  text, re.M)))
 
 
@@ -52,7 +52,7 @@ def test_library_is_sm100a(libgk):
 
 
 def test_abi_version(libgk):
-    assert libgk.gk_abi_version() == 1
+    assert libgk.gk_abi_version() == 2
 
 
 def test_host_mesh_generators_match_oracle(libgk, oracle):

@@ -25,15 +25,28 @@ def sphere(gk, level, radius=1.0, seed=1901, amp=1e-3):
 
 
 @pytest.fixture
-def forced(monkeypatch):
-    """shared edges on small meshes, with small blocks so that far tiles exist"""
-    monkeypatch.setenv("GK_EDGE", "2")
-    monkeypatch.setenv("GK_EDGE_CHUNKS", "4")
-    return monkeypatch
+def ctx_edges(gk):
+    """the context's default kernel selection: shared edges on small meshes"""
+    ctx = gk.Context.get()
+    ctx.set_fill_options(gk.FillOptions(shared_edges=1))
+    yield ctx
+    ctx.set_fill_options(None)
 
 
-def _check(gk, oracle, mesh, m, n, k, kind=None):
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+@pytest.fixture
+def forced(gk, ctx_edges):
+    """shared edges on small meshes, with small blocks so that far tiles
+    exist: the MeshOptions to create the meshes with"""
+    return gk.MeshOptions(edge_chunks=4)
+
+
+def per_tri(gk):
+    """per-call options: the reference-order per-triangle kernels"""
+    return gk.FillOptions(shared_edges=0)
+
+
+def _check(gk, oracle, mesh, m, n, k, kind=None, mopts=None):
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n), options=mopts)
     info = dm.edge_info()
     kw = dict(k=k) if kind is None else dict(k=k, kind=kind)
     z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, **kw)
@@ -55,7 +68,7 @@ def _check(gk, oracle, mesh, m, n, k, kind=None):
 
 @pytest.mark.parametrize("m,n", [(6, 4), (7, 5), (3, 1), (1, 2)])
 def test_edge_fill_parity_sphere(gk, oracle, forced, m, n):
-    dm, info, rep = _check(gk, oracle, sphere(gk, 3), m, n, 2 * np.pi)
+    dm, info, rep = _check(gk, oracle, sphere(gk, 3), m, n, 2 * np.pi, mopts=forced)
     assert info["blocks"] > 1 and info["work_ratio"] < 0.85, info
     # the far threshold is the measured reversed-edge rounding / (32 u)
     assert 0 < info["delta"] < 1e-15
@@ -69,40 +82,37 @@ def test_edge_fill_parity_lossy_plate(gk, oracle, forced):
     row-major plate: blocks follow the bisection order."""
     mesh = gk.generate_plate_mesh(1.0, 20)
     k = complex(gk.wavenumber(gk.Medium(1.0, 4.0, 1.0, -0.4)))
-    dm, info, rep = _check(gk, oracle, mesh, 6, 4, k)
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, k, mopts=forced)
     assert info["ordered"]
     assert rep.evaluations < 0.85 * rep.actual_calls
 
 
 def test_edge_fill_exp_kind(gk, oracle, forced):
     mesh = sphere(gk, 3)
-    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi, kind=gk.KernelKind.PlainExp)
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi, kind=gk.KernelKind.PlainExp,
+                           mopts=forced)
     assert rep.evaluations < 0.8 * rep.actual_calls
 
 
 def test_edge_fill_close_to_per_triangle_fill(gk, forced):
     """same matrix as the reference-order kernel up to rounding"""
     mesh = sphere(gk, 3)
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), options=forced)
     ze, re_ = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
-    forced.setenv("GK_EDGE", "0")
-    zt, rt = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    zt, rt = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi, options=per_tri(gk))
     assert rt.evaluations == rt.actual_calls and re_.evaluations < rt.evaluations
     rel = ((ze - zt).abs() / zt.abs().clamp_min(1e-300)).max().item()
     assert rel < 1e-12
 
 
-def test_edge_near_tiles_bit_identical_to_per_triangle_fill(gk, monkeypatch):
+def test_edge_near_tiles_bit_identical_to_per_triangle_fill(gk, ctx_edges):
     """blocks as large as the mesh: every tile is near and takes the
     reference's own points in the reference's order (bitwise the v4 kernel)"""
     import torch
-    monkeypatch.setenv("GK_EDGE", "2")
-    monkeypatch.delenv("GK_EDGE_CHUNKS", raising=False)
     mesh = sphere(gk, 2)
     dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
     z1, r1 = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
-    monkeypatch.setenv("GK_EDGE", "0")
-    z0, r0 = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
+    z0, r0 = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi, options=per_tri(gk))
     assert torch.equal(z1, z0)
     assert r1.evaluations == r0.evaluations == r0.actual_calls
 
@@ -110,7 +120,7 @@ def test_edge_near_tiles_bit_identical_to_per_triangle_fill(gk, monkeypatch):
 def test_edge_row_blocks_union_bit_exact(gk, forced):
     import torch
     mesh = sphere(gk, 3)
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), options=forced)
     full, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
     N = dm.N
     parts, evals = [], 0
@@ -126,7 +136,7 @@ def test_edge_fill_host_pipeline_and_async(gk, forced):
     """the streamed host fill and the asynchronous fill take the same path"""
     import torch
     mesh = sphere(gk, 3)
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), options=forced)
     z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=2 * np.pi)
     zh = np.empty((dm.N, dm.N), np.complex128)
     reph = gk.fill_rows_host(dm, gk.Mode.DIRECT, zh, k=2 * np.pi)
@@ -136,9 +146,8 @@ def test_edge_fill_host_pipeline_and_async(gk, forced):
     assert torch.equal(za, z)
 
 
-def test_edge_blocks_skip_meshes_without_shared_edges(gk, oracle, monkeypatch):
+def test_edge_blocks_skip_meshes_without_shared_edges(gk, oracle, ctx_edges):
     """disconnected triangles share no edge: the per-triangle kernel runs"""
-    monkeypatch.setenv("GK_EDGE", "2")
     rng = np.random.default_rng(7)
     N = 300
     base = rng.uniform(-1, 1, (N, 1, 3))
@@ -167,7 +176,7 @@ def test_table_edge_fill_parity(gk, oracle, forced, m, n):
     from oracle.pyoracle import TABLE
     mesh = sphere(gk, 3)
     k = 2 * np.pi
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n), options=forced)
     t, ev = _table(gk, oracle, dm, k, 10000)
     zt, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
     zt = zt.cpu().numpy()
@@ -189,7 +198,7 @@ def test_table_edge_fallback_counts_match_reference(gk, oracle, forced, r_min):
     from oracle.pyoracle import TABLE
     mesh = sphere(gk, 3)
     k = 2 * np.pi
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), options=forced)
     assert 0.03 < dm.edge_info()["r_far"] < 0.08
     t, ev = _table(gk, oracle, dm, k, 10000, r_min=r_min)
     zt, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
@@ -204,7 +213,7 @@ def test_table_edge_dispatch_by_table_size(gk, forced):
     """a table staged whole in shared memory stays per triangle (S = 300);
     one too large for that but L1-sized (<= 300 KB of records) takes K3e"""
     mesh = sphere(gk, 3)
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), options=forced)
     lo, hi = dm.distance_range()
     for S, shared in ((300, False), (1000, True)):
         t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S))
@@ -219,7 +228,7 @@ def test_edge_fused_pair_equals_separate_fills(gk, forced, mode):
     and the table read through L1)"""
     import torch
     mesh = sphere(gk, 3)
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), options=forced)
     med = gk.Medium(1.0, 4.0, 1.0, -0.4) if mode == "lossy" else gk.Medium()
     kw = dict(k=gk.wavenumber(med))
     if mode == "table":
@@ -235,16 +244,14 @@ def test_edge_fused_pair_equals_separate_fills(gk, forced, mode):
     assert rep.evaluations == re_.evaluations + rg.evaluations < 0.8 * rep.actual_calls
 
 
-def test_edge_fill_parity_mesh_far_from_origin(gk, oracle, monkeypatch):
+def test_edge_fill_parity_mesh_far_from_origin(gk, oracle, forced):
     """a mesh 3e4 m from the origin: the two orientations of an edge still
     round to the same points up to delta (measured; the ulp of the large
     coordinate cancels between them), so the shared points stay within the
     bound on the far tiles"""
-    monkeypatch.setenv("GK_EDGE", "2")
-    monkeypatch.setenv("GK_EDGE_CHUNKS", "4")
     mesh = sphere(gk, 3)
     mesh = gk.TriangleMesh(mesh.vertices + np.array([3.0e4, 0.0, 0.0]), mesh.triangles)
-    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi)
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi, mopts=forced)
     assert rep.evaluations < 0.8 * rep.actual_calls
 
 
@@ -256,27 +263,23 @@ def test_edge_fill_parity_inconsistent_orientation(gk, oracle, forced):
     tris = mesh.triangles.copy()
     tris[::3] = tris[::3, ::-1]
     mesh = gk.TriangleMesh(mesh.vertices, tris)
-    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi)
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi, mopts=forced)
     assert 0 < info["delta"] < 1e-15
     assert rep.evaluations < 0.8 * rep.actual_calls
 
 
-@pytest.mark.parametrize("chunks", ["1", "6", "12"])
-def test_edge_block_sizes_launch_and_agree(gk, monkeypatch, chunks):
+@pytest.mark.parametrize("chunks", [1, 6, 12])
+def test_edge_block_sizes_launch_and_agree(gk, ctx_edges, chunks):
     """every block size launches (6 chunks put the K3e edge sums at exactly
     48 KB of dynamic shared memory beside the static weights) and agrees with
     the per-triangle kernels"""
-    monkeypatch.setenv("GK_EDGE", "2")
-    monkeypatch.setenv("GK_EDGE_CHUNKS", chunks)
     mesh = sphere(gk, 3)
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), options=gk.MeshOptions(edge_chunks=chunks))
     lo, hi = dm.distance_range()
     t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=10000))
     for md, kw in ((gk.Mode.DIRECT, dict(k=2 * np.pi)), (gk.Mode.TABLE, dict(table=t))):
         z, rep = gk.fill_rows(dm, md, **kw)
-        monkeypatch.setenv("GK_EDGE", "0")
-        z0, _ = gk.fill_rows(dm, md, **kw)
-        monkeypatch.setenv("GK_EDGE", "2")
+        z0, _ = gk.fill_rows(dm, md, options=per_tri(gk), **kw)
         rel = ((z - z0).abs() / z0.abs().clamp_min(1e-300)).max().item()
         assert rel < 1e-12, (md, rel)
 
@@ -287,16 +290,14 @@ def test_edge_kernels_every_rule_agree_with_per_triangle(gk, forced, m):
     and table (K3e): the shared-edge fill agrees with the per-triangle one"""
     mesh = sphere(gk, 3)
     for n in range(1, 6):
-        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n))
+        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(m, n), options=forced)
         lo, hi = dm.distance_range()
         t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=10000))
         kl = complex(gk.wavenumber(gk.Medium(1.0, 4.0, 1.0, -0.4)))
         for md, kw in ((gk.Mode.DIRECT, dict(k=2 * np.pi)), (gk.Mode.DIRECT, dict(k=kl)),
                        (gk.Mode.TABLE, dict(table=t))):
             z, rep = gk.fill_rows(dm, md, **kw)
-            forced.setenv("GK_EDGE", "0")
-            z0, rep0 = gk.fill_rows(dm, md, **kw)
-            forced.setenv("GK_EDGE", "2")
+            z0, rep0 = gk.fill_rows(dm, md, options=per_tri(gk), **kw)
             rel = ((z - z0).abs() / z0.abs().clamp_min(1e-300)).max().item()
             assert rel < 1e-12, (m, n, md, rel)
             assert rep.evaluations < rep0.evaluations == rep0.actual_calls, (m, n, md, kw.keys())
@@ -307,6 +308,6 @@ def test_edge_fill_parity_scaled_meshes(gk, oracle, forced, radius, lam):
     """the far threshold scales with the mesh (delta is measured on its own
     points): millimetre and kilometre spheres stay within the bound"""
     mesh = gk.jitter(gk.generate_sphere_mesh(radius, 3), 1901, 1e-3 * radius)
-    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi / lam)
+    dm, info, rep = _check(gk, oracle, mesh, 6, 4, 2 * np.pi / lam, mopts=forced)
     assert 0.01 * radius < info["r_far"] < 0.1 * radius
     assert rep.evaluations < 0.8 * rep.actual_calls

@@ -264,7 +264,7 @@ def test_zero_distance_pair_is_domain_error(gk, oracle):
 
 
 @pytest.mark.parametrize("level,S,r_min", [(2, 1000, None), (3, 10000, None), (2, 1000, 0.3)])
-def test_table_staging_paths_bit_identical(gk, monkeypatch, level, S, r_min):
+def test_table_staging_paths_bit_identical(gk, level, S, r_min):
     """The L1 table kernel, the shared-memory kernel with the whole table staged,
     with per-tile TMA windows, and with windows overflowing a small budget (global
     reads inside the staged kernel) all give the same bits, fallbacks included."""
@@ -273,16 +273,14 @@ def test_table_staging_paths_bit_identical(gk, monkeypatch, level, S, r_min):
     dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
     lo, hi = dm.distance_range()
     t = gk.DeviceTable(gk.SamplingConfig(r_min=r_min or lo, r_max=hi, samples_per_wavelength=S))
-    settings = [("0", None), ("2", None), ("2", "65536"), ("2", "8192")]
+    G, Sh = gk.GK_TABLE_GLOBAL, gk.GK_TABLE_SHARED
+    settings = [(G, 0), (Sh, 0), (Sh, 65536), (Sh, 8192)]
     outs = []
-    for smem, budget in settings:
-        monkeypatch.setenv("GK_TABLE_SMEM", smem)
-        if budget:
-            monkeypatch.setenv("GK_TABLE_SMEM_BUDGET", budget)
-        else:
-            monkeypatch.delenv("GK_TABLE_SMEM_BUDGET", raising=False)
-        ze, zg, rep = gk.fill_rows_pair(dm, gk.Mode.TABLE, table=t)
-        g, rg = gk.fill_rows(dm, gk.Mode.TABLE, table=t, row_begin=7, row_end=dm.N - 3)
+    for place, budget in settings:
+        o = gk.FillOptions(table_placement=place, smem_budget=budget)
+        ze, zg, rep = gk.fill_rows_pair(dm, gk.Mode.TABLE, table=t, options=o)
+        g, rg = gk.fill_rows(dm, gk.Mode.TABLE, table=t, row_begin=7, row_end=dm.N - 3,
+                             options=o)
         outs.append((ze, zg, g, rep.fallback_calls, rg.fallback_calls))
     for o in outs[1:]:
         assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
@@ -465,11 +463,11 @@ def test_fill_rows_rejects_bad_output(gk):
 
 
 @pytest.mark.parametrize("S,refine", [(1000, True), (10000, True), (300, True), (1000, False)])
-def test_table_arithmetic_locate_bit_identical(gk, monkeypatch, S, refine):
+def test_table_arithmetic_locate_bit_identical(gk, S, refine):
     """The arithmetic interval index on verified runs of the uniform base grid
     (TableDev::coarse) gives exactly the lookup path's bits: fills through the
-    staged, L1 and global-fallback paths and eval_batch, with GK_TABLE_ARITH on
-    and off."""
+    staged, L1 and global-fallback paths and eval_batch, with
+    FillOptions.arith_locate on and off."""
     import torch
     mesh = sphere(gk, 3)
     dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
@@ -478,19 +476,19 @@ def test_table_arithmetic_locate_bit_identical(gk, monkeypatch, S, refine):
                                          refine=refine), gk.Medium(lambda0=0.3))
     r = torch.linspace(lo, hi, 200001, dtype=torch.float64, device="cuda:0")
     out = {}
-    for arith in ("1", "0"):
-        monkeypatch.setenv("GK_TABLE_ARITH", arith)
+    for arith in (1, 0):
         res = []
-        for smem in ("0", "2", None):
-            if smem is None:
-                monkeypatch.delenv("GK_TABLE_SMEM", raising=False)
-            else:
-                monkeypatch.setenv("GK_TABLE_SMEM", smem)
-            ze, zg, rep = gk.fill_rows_pair(dm, gk.Mode.TABLE, table=t, row_begin=100, row_end=300)
+        for place in (gk.GK_TABLE_GLOBAL, gk.GK_TABLE_SHARED, gk.GK_AUTO):
+            o = gk.FillOptions(arith_locate=arith, table_placement=place)
+            ze, zg, rep = gk.fill_rows_pair(dm, gk.Mode.TABLE, table=t, row_begin=100,
+                                            row_end=300, options=o)
             res += [ze, zg]
-        monkeypatch.delenv("GK_TABLE_SMEM", raising=False)
-        res.append(t.eval_batch(gk.KernelKind.GreenOverR, r))
-        res.append(t.eval_batch(gk.KernelKind.PlainExp, r))
+        t.ctx.set_fill_options(gk.FillOptions(arith_locate=arith))  # eval_batch: the context's
+        try:
+            res.append(t.eval_batch(gk.KernelKind.GreenOverR, r))
+            res.append(t.eval_batch(gk.KernelKind.PlainExp, r))
+        finally:
+            t.ctx.set_fill_options(None)
         out[arith] = res
-    for a, b in zip(out["1"], out["0"]):
+    for a, b in zip(out[1], out[0]):
         assert torch.equal(a, b)

@@ -146,11 +146,19 @@ def test_nodes_reproduced_exactly(gk):
     assert np.array_equal(t.eval_batch(gk.KernelKind.PlainExp, a).cpu().numpy(), d["exp"])
 
 
-@pytest.mark.parametrize("libdevice", ["0", "1"])
-def test_eval_batch_direct_vs_glibc(gk, oracle, monkeypatch, libdevice):
+@pytest.fixture
+def eval_method(gk, request):
+    ctx = gk.Context.get()
+    ctx.set_fill_options(gk.FillOptions(eval_libdevice=request.param))
+    yield request.param
+    ctx.set_fill_options(None)
+
+
+@pytest.mark.parametrize("eval_method", [0, 1], indirect=True)
+def test_eval_batch_direct_vs_glibc(gk, oracle, eval_method):
     """direct eval_batch: the phase-table path (default, real k) and the
-    libdevice sincos path (complex k, fallbacks), both within a few ulp of glibc"""
-    monkeypatch.setenv("GK_EVAL_LIBDEVICE", libdevice)
+    libdevice sincos path (complex k, fallbacks; FillOptions.eval_libdevice
+    through the context), both within a few ulp of glibc"""
     r = splitmix64_uniform(7, 1 << 16, 1e-3, 2.0)
     r[:3] = [0.25, 0.5, 1.0]   # quarter-period known answers (test_kernel.cpp:32-81)
     k = 4.0 * math.pi
