@@ -436,10 +436,18 @@ def run_gpu_arm(args, cfg, rank, world, local):
     total_evals = 3 * m * n * N * (N - 1)
     # the reference-order kernels (no shared edges): A/B only
     per_tri = gk.FillOptions(shared_edges=0)
+    # N > 1: libgk's own NCCL communicator (C++, csrc/comm.cu); every step is
+    # gk_fill_sharded: K1 on the rank's rows + the 16-byte device all-reduce +
+    # table build (TABLE) + the fill of its rows
+    gkcomm = None
+    if world > 1:
+        gkcomm = sharding.Comm(ctx)
+        comm["gk_comm_nranks"] = gkcomm.info()[0]
 
     def global_range():
-        lo, hi = dmesh.distance_range(rb, re) if rows else (math.inf, 0.0)
-        return sharding.global_distance_range(lo, hi, device=f"cuda:{local}")
+        if gkcomm is not None:
+            return sharding.distance_range_global(gkcomm, dmesh)
+        return dmesh.distance_range(rb, re)
 
     def table_for(mode):
         if not mode.startswith("table"):
@@ -451,10 +459,25 @@ def run_gpu_arm(args, cfg, rank, world, local):
 
     fill_ev = []
 
+    def sharded_step(mode, report):
+        S = args.S if mode in ("table", "direct", "direct_pertri") else int(mode.split("_S")[1])
+        cfg_s = gk.SamplingConfig(r_min=0.0, r_max=0.0, samples_per_wavelength=S)
+        rep, _ = sharding.fill_rows_sharded(
+            gkcomm, dmesh, gk.Mode.TABLE if mode.startswith("table") else gk.Mode.DIRECT, Z,
+            cfg=cfg_s, medium=medium, options=per_tri if mode == "direct_pertri" else None,
+            report=report)
+        return rep
+
     def step(mode):
-        table = table_for(mode)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        if gkcomm is not None:
+            e0.record()
+            sharded_step(mode, False)
+            e1.record()
+            fill_ev.append((e0, e1))
+            return None
+        table = table_for(mode)
         e0.record()
         if rows:
             gk.fill_rows(dmesh, gk.Mode.TABLE if table else gk.Mode.DIRECT, table=table, k=k,
@@ -496,6 +519,8 @@ def run_gpu_arm(args, cfg, rank, world, local):
     def performed_evals(mode):
         if mode == "direct_pertri":  # the per-triangle kernel performs every reference call
             return 3 * m * n * rows * (N - 1)
+        if gkcomm is not None:
+            return sharded_step(mode, True).evaluations
         if not rows:
             return 0
         table = table_for(mode)
@@ -550,7 +575,7 @@ def run_gpu_arm(args, cfg, rank, world, local):
     e2e = None
     if args.e2e:
         e2e = run_e2e(gk, ctx, cfg, mesh, spec, medium, chosen, args, total_evals, rank, world,
-                      rb, re, dist if world > 1 else None)
+                      rb, re, dist if world > 1 else None, gkcomm)
 
     vs_n = None
     if args.vs_n and rank == 0 and world == 1 and args.config == "c5":
@@ -558,7 +583,7 @@ def run_gpu_arm(args, cfg, rank, world, local):
 
     gather = None
     if world > 1 and args.gather:
-        gather = run_gather(sharding, Z, N, rows, local, dist)
+        gather = run_gather(sharding, gkcomm, Z, N, rows, local, dist)
         if "ms" in gather:
             gather["fused"] = run_fused_gather(gk, sharding, dmesh, chosen, medium, k, args, N,
                                                rows, local, dist, global_range)
@@ -645,7 +670,7 @@ def run_gpu_arm(args, cfg, rank, world, local):
 
 
 def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals, rank, world, rb, re,
-            dist=None):
+            dist=None, gkcomm=None):
     """End to end through the C-ABI host-buffer entry points, at N ranks: each
     step every rank uploads the host mesh (H2D), generates its quadrature
     points, (TABLE) computes its range, all-reduces it and builds the table,
@@ -683,9 +708,11 @@ def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals, rank, wor
         dm = gk.DeviceMesh(mesh, spec, ctx)
         t = None
         if m == gk.Mode.TABLE:
-            lo, hi = dm.distance_range(rb, re) if rows else (math.inf, 0.0)
-            from paper_1901_04162_b200.sharding import global_distance_range
-            lo, hi = global_distance_range(lo, hi, device=f"cuda:{ctx.device}")
+            if gkcomm is not None:   # K1 on this rank's rows + the NCCL all-reduce (C++)
+                from paper_1901_04162_b200.sharding import distance_range_global
+                lo, hi = distance_range_global(gkcomm, dm)
+            else:
+                lo, hi = dm.distance_range(rb, re)
             t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
                                                  samples_per_wavelength=args.S), medium, ctx=ctx)
         for b in range(rb, re, rows_win):
@@ -713,10 +740,11 @@ def run_e2e(gk, ctx, cfg, mesh, spec, medium, mode, args, total_evals, rank, wor
             "timing": "host wall clock per step, max over ranks"}
 
 
-def run_gather(sharding, Z, N, rows, local, dist):
-    """Optional gather of all row blocks of Z to rank 0 (NCCL send/recv over
-    NVLink), timed apart from the fill.  Skipped when the
-    full matrix does not fit next to rank 0's own block."""
+def run_gather(sharding, gkcomm, Z, N, rows, local, dist):
+    """Optional gather of all row blocks of Z to rank 0 (gk_gather_rows:
+    grouped ncclSend / ncclRecv over NVLink from C++), timed apart from the
+    fill.  Skipped when the full matrix does not fit next
+    to rank 0's own block."""
     import torch
     need = N * N * 16
     ok = torch.tensor([1.0 if torch.cuda.mem_get_info(local)[0] > need + (4 << 30) else 0.0],
@@ -730,7 +758,7 @@ def run_gather(sharding, Z, N, rows, local, dist):
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    sharding.gather_rows(Z[:rows] if rows else Z[:0], N, dst=0, out=out)
+    sharding.gather_rows_nccl(gkcomm, Z, N, root=0, out=out)
     e1.record()
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{local}")
@@ -739,8 +767,8 @@ def run_gather(sharding, Z, N, rows, local, dist):
     del out
     torch.cuda.empty_cache()   # the fused variant allocates the full matrix outside torch
     return {"ms": ms, "bytes": need, "gbs": need / (ms * 1e-3) / 1e9,
-            "how": "row blocks sent to rank 0 after the fill (torch.distributed send/irecv "
-                   "over NCCL)"}
+            "how": "row blocks sent to rank 0 after the fill (gk_gather_rows: grouped "
+                   "ncclSend/ncclRecv in libgk, C++)"}
 
 
 def run_fused_gather(gk, sharding, dmesh, mode, medium, k, args, N, rows, local, dist,

@@ -411,6 +411,46 @@ gk_status gk_shared_free(gk_ctx* ctx, void* dptr);
 gk_status gk_ipc_open(gk_ctx* ctx, const unsigned char handle[GK_IPC_HANDLE_BYTES], void** dptr);
 gk_status gk_ipc_close(gk_ctx* ctx, void* dptr);
 
+/* ------------------------------------------ multi-GPU row blocks (NCCL)
+   The reference's row chunking (matfill.hpp:206-221: chunk = ceil(N /
+   threads), contiguous) as one rank per GPU.  A gk_comm wraps an NCCL
+   communicator on its context's device.  Either every process calls
+   gk_comm_init with the same 128-byte id (made once by gk_comm_unique_id and
+   shipped by the caller over any transport), or one process drives several
+   GPUs with gk_comm_init_all (one context per device; then every per-rank
+   call below must be issued from its own host thread, since NCCL
+   collectives across ranks block until all ranks have joined). */
+typedef struct gk_comm gk_comm;
+#define GK_COMM_ID_BYTES 128
+/* rows [begin, end) of `rank` out of `nranks` (host-only, no device) */
+gk_status gk_rows_of(uint64_t N, int nranks, int rank, uint64_t* row_begin, uint64_t* row_end);
+gk_status gk_comm_unique_id(unsigned char id[GK_COMM_ID_BYTES]);
+gk_status gk_comm_init(gk_ctx* ctx, const unsigned char id[GK_COMM_ID_BYTES], int nranks,
+                       int rank, gk_comm** out);
+gk_status gk_comm_init_all(gk_ctx* const* ctxs, int n, gk_comm** comms);
+gk_status gk_comm_destroy(gk_comm* comm);
+gk_status gk_comm_info(const gk_comm* comm, int* nranks, int* rank);
+/* K1 over this rank's rows + one 16-byte ncclAllReduce(MIN) of
+   {min d^2, -max d^2} on the device: the global range of gk_distance_range
+   (same widening), identical on every rank */
+gk_status gk_distance_range_global(gk_ctx* ctx, gk_comm* comm, const gk_mesh* mesh,
+                                   double* r_min, double* r_max);
+/* One rank's share of fill_matrix (matfill.hpp:144-228) over the rows
+   gk_rows_of gives it: TABLE mode computes the global range when cfg->r_min
+   or cfg->r_max <= 0 (gk_distance_range_global), builds the table (identical
+   on every rank) and fills; DIRECT fills.  z_rows (device) receives this
+   rank's rows with leading dimension ldz; report (NULL: asynchronous) covers
+   this rank's rows; r_range (may be NULL) receives the table range used. */
+gk_status gk_fill_sharded(gk_ctx* ctx, gk_comm* comm, const gk_mesh* mesh, gk_mode mode,
+                          const gk_sampling_config* cfg, const gk_medium* medium, gk_kind kind,
+                          gk_c128* z_rows, size_t ldz, const gk_fill_options* opts,
+                          gk_fill_report* report, double r_range[2]);
+/* The optional gather: every rank's row block (z_rows,
+   rows x N, leading dimension N, device) lands in its row slice of root's
+   N x N device matrix z_full (grouped ncclSend / ncclRecv, no staging). */
+gk_status gk_gather_rows(gk_ctx* ctx, gk_comm* comm, const gk_c128* z_rows, uint64_t N, int root,
+                         gk_c128* z_full);
+
 /* predicted_calls (matfill.hpp:50-56): 3 m n N^2 with the overflow guard */
 gk_status gk_predicted_calls(uint64_t N, uint64_t m, uint64_t n, uint64_t* out);
 

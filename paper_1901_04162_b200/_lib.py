@@ -164,6 +164,17 @@ PROTOTYPES = {
                           C.c_size_t, _vp, C.c_size_t, C.POINTER(FillOptionsC),
                           C.POINTER(FillReportC)],
     "gk_predicted_calls": [C.c_uint64, C.c_uint64, C.c_uint64, _u64p],
+    "gk_rows_of": [C.c_uint64, C.c_int, C.c_int, _u64p, _u64p],
+    "gk_comm_unique_id": [_vp],
+    "gk_comm_init": [_vp, _vp, C.c_int, C.c_int, C.POINTER(_vp)],
+    "gk_comm_init_all": [_vp, C.c_int, _vp],
+    "gk_comm_destroy": [_vp],
+    "gk_comm_info": [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)],
+    "gk_distance_range_global": [_vp, _vp, _vp, _dp, _dp],
+    "gk_fill_sharded": [_vp, _vp, _vp, C.c_int, C.POINTER(SamplingConfigC), C.POINTER(Medium),
+                        C.c_int, _vp, C.c_size_t, C.POINTER(FillOptionsC),
+                        C.POINTER(FillReportC), _dp],
+    "gk_gather_rows": [_vp, _vp, _vp, C.c_uint64, C.c_int, _vp],
     "gk_compare_fills": [_vp, _vp, _vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_max_vertex_distance": [_vp, _vp, _dp],
     "gk_error_sweep": [_vp, _vp, C.c_int, C.c_int, C.c_uint64, _vp],

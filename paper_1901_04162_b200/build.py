@@ -36,6 +36,7 @@ SOURCES = {
     "abi.cu": [],
     "host.cpp": [],
     "edges.cu": [],
+    "comm.cu": [],
 }
 HEADERS = ["gk_device.cuh", "gk_internal.h", "fill_kernels.cuh"]
 
@@ -76,11 +77,12 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda kv: _compile(kv[0], kv[1], verbose), SOURCES.items()))
     if _newer(objs, LIB):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lnccl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     build_cpp_test()
+    build_tools()
     return LIB
 
 
@@ -98,6 +100,26 @@ def build_cpp_test() -> str:
         if r.returncode != 0:
             raise RuntimeError(f"g++ failed for test_adapter:\n{r.stderr}")
     return CPP_TEST_BIN
+
+
+TOOL_SRC = os.path.join(PKG, "tools", "gk_sharded_fill.cpp")
+TOOL_BIN = os.path.join(OBJ, "gk_sharded_fill")
+
+
+def build_tools() -> str:
+    """The C++ multi-GPU driver (tools/gk_sharded_fill.cpp): host g++ over the
+    C ABI + the CUDA runtime, linked against libgk.so."""
+    deps = [TOOL_SRC, LIB, os.path.join(ROOT, "include", "gk", "gk.h")]
+    if _newer(deps, TOOL_BIN):
+        cuda = os.path.dirname(os.path.dirname(os.path.realpath(NVCC)))
+        cmd = ["g++", "-std=c++20", "-O2", "-pthread", "-I", os.path.join(ROOT, "include"),
+               "-I", os.path.join(cuda, "include"), TOOL_SRC, "-o", TOOL_BIN, "-L", PKG, "-lgk",
+               "-L", os.path.join(cuda, "lib64"), "-lcudart", "-Wl,-rpath,$ORIGIN/..",
+               "-Wl,-rpath," + os.path.join(cuda, "lib64")]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed for gk_sharded_fill:\n{r.stderr}")
+    return TOOL_BIN
 
 
 if __name__ == "__main__":

@@ -125,6 +125,7 @@ void use_device(const gk_ctx* c) { GK_CUDA(cudaSetDevice(c->device)); }
 }  // namespace
 
 namespace gk {
+std::string& last_error_buffer() { return g_last_error; }
 static std::atomic<unsigned long long> g_launches{0};
 void count_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 }  // namespace gk

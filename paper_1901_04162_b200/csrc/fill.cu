@@ -248,6 +248,41 @@ void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row
   *d2max = b;
 }
 
+// {min d2, -max d2} of a rank's rows as two doubles on the device (the
+// 16 bytes the multi-GPU range all-reduces with MIN, comm.cu)
+__global__ void range_pack_kernel(const unsigned long long* w, double* out2) {
+  const unsigned long long lo = w[0] < w[2] ? w[0] : w[2];
+  const unsigned long long hi = w[1] > w[3] ? w[1] : w[3];
+  out2[0] = unbits(lo);
+  out2[1] = -unbits(hi);
+}
+
+void launch_range_device(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,
+                         double* out2) {
+  cudaStream_t st = ctx->stream;
+  if (row_end <= row_begin) {  // no rows: the identity of the MIN reduction
+    const double id[2] = {INFINITY, -0.0};
+    GK_CUDA(cudaMemcpyAsync(out2, id, sizeof(id), cudaMemcpyHostToDevice, st));
+    GK_CUDA(cudaStreamSynchronize(st));  // `id` is a host stack buffer
+    return;
+  }
+  unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+  unsigned long long* w = ctx->scratch.p + 8;
+  GK_CUDA(cudaMemcpyAsync(w, init, sizeof(init), cudaMemcpyHostToDevice, st));
+  const size_t rows = row_end - row_begin;
+  const unsigned grid = static_cast<unsigned>(rows < 65535 ? rows : 65535);
+  range_sample_kernel<<<grid, 256, 0, st>>>(mesh->outer.p, mesh->inner.p, mesh->m, mesh->N,
+                                            row_begin, row_end, w);
+  range_exact_kernel<<<grid, 256, 0, st>>>(mesh->outer.p, mesh->inner.p, mesh->bounds.p,
+                                           mesh->binner.p, mesh->m, 3 * mesh->n, mesh->N,
+                                           row_begin, row_end, w);
+  range_pack_kernel<<<1, 1, 0, st>>>(w, out2);
+  count_launches(3);
+  GK_CUDA(cudaGetLastError());
+  // `init` is read by the copy engine before this frame returns
+  GK_CUDA(cudaStreamSynchronize(st));
+}
+
 // ------------------------------------------------------- phase table
 
 __global__ void phase_kernel(double2* tab, int M) {

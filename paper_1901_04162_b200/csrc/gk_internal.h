@@ -21,6 +21,36 @@ struct Error {
 
 [[noreturn]] inline void fail(gk_status s, const std::string& what) { throw Error{s, what}; }
 
+inline void need(bool ok, gk_status s, const char* what) {
+  if (!ok) fail(s, what);
+}
+
+// the thread-local message behind gk_last_error (abi.cu)
+std::string& last_error_buffer();
+
+// run an entry point's body: exceptions -> gk_status + gk_last_error message
+template <class F>
+gk_status guarded(F&& f) {
+  try {
+    f();
+    return GK_OK;
+  } catch (const Error& e) {
+    last_error_buffer() = e.what;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    last_error_buffer() = "out of host memory";
+    return GK_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    last_error_buffer() = e.what();
+    return GK_ERR_RUNTIME;
+  }
+}
+
+// rethrow a failed entry point's status (composing entry points)
+inline void ok(gk_status s) {
+  if (s != GK_OK) fail(s, last_error_buffer());
+}
+
 #define GK_CUDA(call)                                                                   \
   do {                                                                                  \
     cudaError_t gk_e_ = (call);                                                         \
@@ -205,6 +235,10 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
                  const gk_fill_options& opts);
 void launch_range(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,
                   double* d2min, double* d2max);
+// the same on the device: out2 = {min d2, -max d2} over the rows ({inf, -0}
+// for an empty range), ready for a MIN all-reduce
+void launch_range_device(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, size_t row_end,
+                         double* out2);
 void launch_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re,
                        double k_im, const double* r, size_t n, gk_c128* out,
                        unsigned long long* d_scratch);

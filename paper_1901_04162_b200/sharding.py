@@ -14,17 +14,128 @@ the thread count.  Here the same chunking runs one rank per GPU:
    with it -- every rank's fill kernel storing straight into the destination
    rank's matrix through CUDA IPC peer memory (fill_rows_gathered).
 
-Works with any torch.distributed backend: NCCL on GPUs (tensors on the
-rank's device), gloo on CPU (the tests).
+The GPU path lives in C++ behind the C ABI (csrc/comm.cu): a ``Comm`` is
+libgk's own NCCL communicator, and ``distance_range_global``,
+``fill_rows_sharded`` and ``gather_rows_nccl`` are thin wrappers of
+gk_distance_range_global / gk_fill_sharded / gk_gather_rows -- a C++ caller
+of the reference gets the same sharded fill without Python
+(tools/gk_sharded_fill.cpp).  torch.distributed only ships the 128-byte
+NCCL id here.  The torch.distributed helpers below (global_distance_range,
+gather_rows) are the same steps over any backend: gloo on CPU for the
+multi-rank tests.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 
 def rows_of(rank: int, world: int, N: int) -> tuple[int, int]:
-    """Contiguous row block [begin, end) of `rank` (matfill.hpp:211-215)."""
-    chunk = (N + world - 1) // world
-    b = min(N, rank * chunk)
-    return b, min(N, b + chunk)
+    """Contiguous row block [begin, end) of `rank` (matfill.hpp:211-215):
+    gk_rows_of, the partition the C++ sharded fill uses (host-only)."""
+    from ._lib import check, lib
+    b, e = C.c_uint64(), C.c_uint64()
+    check(lib().gk_rows_of(N, world, rank, C.byref(b), C.byref(e)), "rows_of")
+    return b.value, e.value
+
+
+class Comm:
+    """gk_comm: libgk's NCCL communicator on one context's device (C++,
+    csrc/comm.cu).  Made collectively: rank 0 creates the 128-byte id
+    (gk_comm_unique_id), the id travels over the torch.distributed group
+    (any transport would do), every rank calls gk_comm_init."""
+
+    def __init__(self, ctx, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from ._lib import check, lib
+        self.ctx = ctx
+        if dist.is_available() and dist.is_initialized():
+            nranks, rank = dist.get_world_size(group), dist.get_rank(group)
+        else:
+            nranks, rank = 1, 0
+        idb = (C.c_ubyte * 128)()
+        if rank == 0:
+            check(lib().gk_comm_unique_id(idb), "gk_comm_unique_id")
+        if nranks > 1:
+            on_dev = dist.get_backend(group) == "nccl"
+            t = torch.tensor(list(bytes(idb)), dtype=torch.uint8,
+                             device=f"cuda:{ctx.device}" if on_dev else "cpu")
+            dist.broadcast(t, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            idb = (C.c_ubyte * 128).from_buffer_copy(bytes(t.cpu().tolist()))
+        h = C.c_void_p()
+        check(lib().gk_comm_init(ctx.h, idb, nranks, rank, C.byref(h)), "gk_comm_init")
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    def info(self) -> tuple[int, int]:
+        """(nranks, rank) as the NCCL communicator reports them"""
+        from ._lib import check, lib
+        n, r = C.c_int(), C.c_int()
+        check(lib().gk_comm_info(self.h, C.byref(n), C.byref(r)), "gk_comm_info")
+        return n.value, r.value
+
+    def __del__(self):
+        from . import _lib
+        h = getattr(self, "h", None)
+        if h and _lib._lib is not None:
+            try:
+                _lib._lib.gk_comm_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self.h = None
+
+
+def distance_range_global(comm: Comm, dmesh) -> tuple[float, float]:
+    """K1 over this rank's rows + the 16-byte NCCL MIN all-reduce, on the
+    device (gk_distance_range_global)"""
+    from ._lib import check, lib
+    comm.ctx.bind_stream()
+    lo, hi = C.c_double(), C.c_double()
+    check(lib().gk_distance_range_global(comm.ctx.h, comm.h, dmesh.h, C.byref(lo), C.byref(hi)),
+          "distance_range_global")
+    return lo.value, hi.value
+
+
+def fill_rows_sharded(comm: Comm, dmesh, mode, out, cfg=None, medium=None, kind=None,
+                      options=None, report: bool = True):
+    """This rank's share of the fill (gk_fill_sharded): rows rows_of(rank)
+    into `out` (a CUDA complex128 (rows, >= N) view); TABLE with cfg.r_min or
+    cfg.r_max <= 0 takes the global K1 range.  Returns (FillReport | None,
+    (r_min, r_max) of the table or None)."""
+    from . import gktab
+    from ._lib import FillReportC, check, lib
+    kind = gktab.KernelKind.GreenOverR if kind is None else kind
+    medium = medium or gktab.Medium()
+    rb, re = rows_of(comm.rank, comm.nranks, dmesh.N)
+    rep = FillReportC()
+    rng = (C.c_double * 2)()
+    comm.ctx.bind_stream()
+    check(lib().gk_fill_sharded(comm.ctx.h, comm.h, dmesh.h, int(mode),
+                                C.byref(cfg.c()) if cfg is not None else None,
+                                C.byref(medium.c()), int(kind),
+                                out.data_ptr() if re > rb else None,
+                                out.stride(0) if re > rb else dmesh.N,
+                                C.byref(options.c()) if options is not None else None,
+                                C.byref(rep) if report else None, rng), "fill_matrix")
+    return (gktab.FillReport.from_c(rep) if report else None,
+            (rng[0], rng[1]) if int(mode) == int(gktab.Mode.TABLE) else None)
+
+
+def gather_rows_nccl(comm: Comm, z_local, N: int, root: int = 0, out=None):
+    """Every rank's row block into root's N x N device matrix (gk_gather_rows:
+    grouped ncclSend / ncclRecv, no staging).  Returns `out` on root."""
+    import torch
+
+    from ._lib import check, lib
+    rb, re = rows_of(comm.rank, comm.nranks, N)
+    if comm.rank == root and out is None:
+        out = torch.empty((N, N), dtype=torch.complex128, device=f"cuda:{comm.ctx.device}")
+    comm.ctx.bind_stream()
+    check(lib().gk_gather_rows(comm.ctx.h, comm.h,
+                               z_local.data_ptr() if re > rb else None, N, root,
+                               out.data_ptr() if comm.rank == root else None),
+          "gather_rows")
+    return out if comm.rank == root else None
 
 
 def global_distance_range(lo: float, hi: float, device=None, group=None) -> tuple[float, float]:
@@ -158,5 +269,6 @@ def evals_of_rows(rows: int, N: int, m: int, n: int) -> int:
     return 3 * m * n * rows * (N - 1) if N > 0 else 0
 
 
-__all__ = ["rows_of", "global_distance_range", "gather_rows", "fill_rows_gathered",
-           "shard_summary", "evals_of_rows"]
+__all__ = ["rows_of", "Comm", "distance_range_global", "fill_rows_sharded", "gather_rows_nccl",
+           "global_distance_range", "gather_rows", "fill_rows_gathered", "shard_summary",
+           "evals_of_rows"]

@@ -20,15 +20,15 @@ def test_abi_rejects_bad_arguments(gk):
     t = gk.DeviceTable(gk.SamplingConfig())
     N = dm.N
     calls = [
-        lambda: L.gk_fill_rows(None, dm.h, 0, None, 1, 1.0, 0.0, 0, N, None, N, None),   # null ctx
-        lambda: L.gk_fill_rows(h, None, 0, None, 1, 1.0, 0.0, 0, N, None, N, None),      # null mesh
-        lambda: L.gk_fill_rows(h, dm.h, 7, None, 1, 1.0, 0.0, 0, N, None, N, None),      # bad mode
-        lambda: L.gk_fill_rows(h, dm.h, 0, None, 5, 1.0, 0.0, 0, N, None, N, None),      # bad kind
-        lambda: L.gk_fill_rows(h, dm.h, 0, None, 1, 1.0, 0.0, 5, 2, None, N, None),      # rows
-        lambda: L.gk_fill_rows(h, dm.h, 0, None, 1, 1.0, 0.0, 0, N, None, N - 1, None),  # ldz
-        lambda: L.gk_fill_rows(h, dm.h, 0, None, 1, 1.0, 0.0, 0, N, None, N, None),      # null z
-        lambda: L.gk_fill_rows(h, dm.h, 1, None, 1, 1.0, 0.0, 0, 0, None, N, None),      # no table
-        lambda: L.gk_fill_rows(h, dm.h, 0, None, 1, -1.0, 0.0, 0, 0, None, N, None),     # k < 0
+        lambda: L.gk_fill_rows(None, dm.h, 0, None, 1, 1.0, 0.0, 0, N, None, N, None, None),   # null ctx
+        lambda: L.gk_fill_rows(h, None, 0, None, 1, 1.0, 0.0, 0, N, None, N, None, None),      # null mesh
+        lambda: L.gk_fill_rows(h, dm.h, 7, None, 1, 1.0, 0.0, 0, N, None, N, None, None),      # bad mode
+        lambda: L.gk_fill_rows(h, dm.h, 0, None, 5, 1.0, 0.0, 0, N, None, N, None, None),      # bad kind
+        lambda: L.gk_fill_rows(h, dm.h, 0, None, 1, 1.0, 0.0, 5, 2, None, N, None, None),      # rows
+        lambda: L.gk_fill_rows(h, dm.h, 0, None, 1, 1.0, 0.0, 0, N, None, N - 1, None, None),  # ldz
+        lambda: L.gk_fill_rows(h, dm.h, 0, None, 1, 1.0, 0.0, 0, N, None, N, None, None),      # null z
+        lambda: L.gk_fill_rows(h, dm.h, 1, None, 1, 1.0, 0.0, 0, 0, None, N, None, None),      # no table
+        lambda: L.gk_fill_rows(h, dm.h, 0, None, 1, -1.0, 0.0, 0, 0, None, N, None, None),     # k < 0
         lambda: L.gk_eval_batch(h, None, 1, 1.0, 0.0, None, 10, None, None),             # null buf
         lambda: L.gk_locate(h, None, None, 0, None),                                      # no table
         lambda: L.gk_table_build(h, None, None, 3, None),
@@ -42,6 +42,12 @@ def test_abi_rejects_bad_arguments(gk):
         lambda: L.gk_accumulate_batch(h, None, 1, 1.0, 0.0, None, None, 4, 2, None, None),
         lambda: L.gk_distance_range(h, dm.h, 5, 2, None, None),
         lambda: L.gk_shared_alloc(h, 0, None, None),
+        lambda: L.gk_rows_of(10, 0, 0, None, None),                                      # nranks
+        lambda: L.gk_comm_init(h, None, 1, 0, None),                                      # null id
+        lambda: L.gk_comm_init_all(None, 1, None),
+        lambda: L.gk_gather_rows(h, None, None, N, 0, None),                              # no comm
+        lambda: L.gk_distance_range_global(h, None, dm.h, None, None),
+        lambda: L.gk_fill_sharded(h, None, dm.h, 0, None, None, 1, None, N, None, None, None),
     ]
     for i, call in enumerate(calls):
         st = call()

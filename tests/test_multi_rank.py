@@ -94,3 +94,31 @@ def test_rows_of_partitions_exactly(world, N):
     assert covered == list(range(N))
     chunk = (N + world - 1) // world    # matfill.hpp:211-215
     assert all(e - b <= chunk for b, e in blocks)
+
+
+@pytest.mark.parametrize("world,N", [(1, 1280), (2, 1280), (8, 81920), (3, 80), (8, 20), (7, 5),
+                                     (5, 0)])
+def test_c_abi_rows_of_is_the_reference_chunking(world, N):
+    """gk_rows_of (host-only C ABI, used by gk_fill_sharded / gk_gather_rows)
+    gives the reference's chunks, chunk = ceil(N / threads) (matfill.hpp:211-215)"""
+    from paper_1901_04162_b200 import sharding
+    import bench
+    chunk = (N + world - 1) // world
+    for r in range(world):
+        b, e = sharding.rows_of(r, world, N)
+        assert (b, e) == bench.rows_of(r, world, N) == (min(N, r * chunk), min(N, r * chunk + chunk))
+
+
+def test_c_abi_comm_rejects_bad_arguments_without_a_device():
+    """the communicator entry points fail with a status (no crash) on bad
+    arguments; gk_rows_of validates its ranks"""
+    import ctypes as C
+    from paper_1901_04162_b200._lib import lib
+    L = lib()
+    b, e = C.c_uint64(), C.c_uint64()
+    assert L.gk_rows_of(10, 0, 0, C.byref(b), C.byref(e)) == 1
+    assert L.gk_rows_of(10, 2, 2, C.byref(b), C.byref(e)) == 1
+    assert L.gk_comm_init(None, None, 1, 0, None) == 1
+    assert L.gk_comm_init_all(None, 0, None) == 1
+    assert L.gk_gather_rows(None, None, None, 10, 0, None) == 1
+    assert L.gk_comm_destroy(None) == 0
