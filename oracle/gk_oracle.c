@@ -1274,45 +1274,108 @@ int go_pointwise_bound(const go_evaluator* ev, int kind, int method, double r, d
   return go_lagrange_bound(plan->absc + start, width, r, kind, kb, out);
 }
 
-int go_entry_bounds(const double* verts, size_t nv, const uint32_t* tris, size_t nt, int m, int n,
-                    const go_evaluator* ev, double k_abs, double ulps, size_t row_begin,
-                    size_t row_end, double* bound, size_t ldb) {
+/* one observation row of the parity tolerance */
+static int entry_bound_row(const double* o4, const double* i4, size_t N, size_t m, size_t ipt,
+                           const go_evaluator* ev, double k_abs, double rnd, size_t p,
+                           double* row) {
+  const size_t no = N * m, ni = N * ipt;
+  int s = 0;
+  row[p] = 0.0;
+  for (size_t q = 0; q < N && !s; ++q) {
+    if (q == p) continue;
+    double acc = 0.0;
+    for (size_t o = 0; o < m; ++o) {
+      const size_t oi = p * m + o;
+      for (size_t i = 0; i < ipt; ++i) {
+        const size_t ii = q * ipt + i;
+        const double dx = o4[oi] - i4[ii];
+        const double dy = o4[no + oi] - i4[ni + ii];
+        const double dz = o4[2 * no + oi] - i4[2 * ni + ii];
+        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+        double pw = 0.0;
+        if (ev && r >= ev->hash.r_min && r <= ev->hash.r_max) {
+          s = go_pointwise_bound(ev, GO_GREEN, 1, r, &pw);
+          if (s) break;
+        }
+        acc += fabs(o4[3 * no + oi] * i4[3 * ni + ii]) * (pw + rnd * (1.0 + k_abs * r) / r);
+      }
+    }
+    row[q] = acc;
+  }
+  return s;
+}
+
+typedef struct {
+  const double *o4, *i4;
+  size_t N, m, ipt;
+  const go_evaluator* ev;
+  double k_abs, rnd;
+  const uint64_t* rows;
+  size_t rb, re;
+  double* bound;
+  size_t ldb;
+  int status;
+} bound_job;
+
+static void* bound_worker(void* arg) {
+  bound_job* j = (bound_job*)arg;
+  for (size_t r = j->rb; r < j->re && !j->status; ++r)
+    j->status = entry_bound_row(j->o4, j->i4, j->N, j->m, j->ipt, j->ev, j->k_abs, j->rnd,
+                                (size_t)j->rows[r], j->bound + r * j->ldb);
+  return NULL;
+}
+
+int go_entry_bounds_rows(const double* verts, size_t nv, const uint32_t* tris, size_t nt, int m,
+                         int n, const go_evaluator* ev, double k_abs, double ulps,
+                         const uint64_t* rows, size_t nrows, int threads, double* bound,
+                         size_t ldb) {
   int s = spec_validate(m, n);
   if (s) return s;
+  if (threads < 1) return GO_INVALID;
+  for (size_t r = 0; r < nrows; ++r)
+    if (rows[r] >= nt) return GO_INVALID;
   const size_t N = nt, ipt = (size_t)(3 * n);
   const size_t no = N * (size_t)m, ni = N * ipt;
   double* o4 = (double*)malloc(4 * no * sizeof(double));
   double* i4 = (double*)malloc(4 * ni * sizeof(double));
   go_outer_points(verts, nv, tris, nt, m, o4, o4 + no, o4 + 2 * no, o4 + 3 * no);
   go_inner_points(verts, nv, tris, nt, n, i4, i4 + ni, i4 + 2 * ni, i4 + 3 * ni);
-  const double rnd = ulps * 0x1.0p-53;
-  for (size_t p = row_begin; p < row_end && !s; ++p) {
-    double* row = bound + (p - row_begin) * ldb;
-    row[p] = 0.0;
-    for (size_t q = 0; q < N && !s; ++q) {
-      if (q == p) continue;
-      double acc = 0.0;
-      for (size_t o = 0; o < (size_t)m; ++o) {
-        const size_t oi = p * (size_t)m + o;
-        for (size_t i = 0; i < ipt; ++i) {
-          const size_t ii = q * ipt + i;
-          const double dx = o4[oi] - i4[ii];
-          const double dy = o4[no + oi] - i4[ni + ii];
-          const double dz = o4[2 * no + oi] - i4[2 * ni + ii];
-          const double r = sqrt(dx * dx + dy * dy + dz * dz);
-          double pw = 0.0;
-          if (ev && r >= ev->hash.r_min && r <= ev->hash.r_max) {
-            s = go_pointwise_bound(ev, GO_GREEN, 1, r, &pw);
-            if (s) break;
-          }
-          acc += fabs(o4[3 * no + oi] * i4[3 * ni + ii]) * (pw + rnd * (1.0 + k_abs * r) / r);
-        }
-      }
-      row[q] = acc;
-    }
+  bound_job* jobs = (bound_job*)calloc((size_t)threads, sizeof(bound_job));
+  pthread_t* tids = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+  const size_t chunk = (nrows + (size_t)threads - 1) / (size_t)threads;
+  int launched = 0;
+  for (int w = 0; w < threads; ++w) {
+    const size_t b = (size_t)w * chunk, e = b + chunk < nrows ? b + chunk : nrows;
+    if (b >= e) break;
+    bound_job* j = &jobs[w];
+    j->o4 = o4; j->i4 = i4; j->N = N; j->m = (size_t)m; j->ipt = ipt; j->ev = ev;
+    j->k_abs = k_abs; j->rnd = ulps * 0x1.0p-53; j->rows = rows; j->rb = b; j->re = e;
+    j->bound = bound; j->ldb = ldb;
+    if (threads == 1) bound_worker(j);
+    else pthread_create(&tids[w], NULL, bound_worker, j);
+    ++launched;
   }
+  if (threads > 1)
+    for (int w = 0; w < launched; ++w) pthread_join(tids[w], NULL);
+  for (int w = 0; w < launched; ++w)
+    if (jobs[w].status && !s) s = jobs[w].status;
+  free(jobs);
+  free(tids);
   free(o4);
   free(i4);
+  return s;
+}
+
+int go_entry_bounds(const double* verts, size_t nv, const uint32_t* tris, size_t nt, int m, int n,
+                    const go_evaluator* ev, double k_abs, double ulps, size_t row_begin,
+                    size_t row_end, double* bound, size_t ldb) {
+  if (row_end > nt || row_begin > row_end) return GO_INVALID;
+  const size_t nrows = row_end - row_begin;
+  uint64_t* rows = (uint64_t*)malloc((nrows ? nrows : 1) * sizeof(uint64_t));
+  for (size_t r = 0; r < nrows; ++r) rows[r] = row_begin + r;
+  const int s = go_entry_bounds_rows(verts, nv, tris, nt, m, n, ev, k_abs, ulps, rows, nrows, 1,
+                                     bound, ldb);
+  free(rows);
   return s;
 }
 

@@ -167,6 +167,13 @@ int go_entry_bounds(const double* verts, size_t nv, const uint32_t* tris, size_t
                     const go_evaluator* ev, double k_abs, double ulps, size_t row_begin,
                     size_t row_end, double* bound, size_t ldb);
 
+/* The same bound for an arbitrary list of rows (bound[r * ldb + q] for
+   p = rows[r]), split over `threads` pthreads: full-size sampled-row parity. */
+int go_entry_bounds_rows(const double* verts, size_t nv, const uint32_t* tris, size_t nt, int m,
+                         int n, const go_evaluator* ev, double k_abs, double ulps,
+                         const uint64_t* rows, size_t nrows, int threads, double* bound,
+                         size_t ldb);
+
 /* Exact min / max quadrature-point pair distance over rows [row_begin,row_end)
    and all q != p (the K1 oracle; brute force). */
 int go_distance_range(const double* verts, size_t nv, const uint32_t* tris, size_t nt, int m,

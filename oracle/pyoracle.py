@@ -313,6 +313,21 @@ class Oracle:
                                     C.c_size_t(row_end), dptr(b), C.c_size_t(nt)), "bounds")
         return b
 
+    def entry_bounds_rows(self, verts, tris, m, n, ev, k_abs, rows, ulps=64.0, threads=8):
+        """entry_bounds for an arbitrary row list (full-size sampled rows)"""
+        v = np.ascontiguousarray(verts, np.float64).reshape(-1)
+        t = np.ascontiguousarray(tris, np.uint32).reshape(-1)
+        nv, nt = v.size // 3, t.size // 3
+        rws = np.ascontiguousarray(rows, np.uint64)
+        b = np.zeros((rws.size, nt), np.float64)
+        _chk(self.L.go_entry_bounds_rows(dptr(v), C.c_size_t(nv), u32ptr(t), C.c_size_t(nt),
+                                         C.c_int(m), C.c_int(n),
+                                         C.c_void_p(ev.h if ev is not None else None),
+                                         C.c_double(k_abs), C.c_double(ulps),
+                                         rws.ctypes.data_as(_u64p), C.c_size_t(rws.size),
+                                         C.c_int(threads), dptr(b), C.c_size_t(nt)), "bounds")
+        return b
+
     def distance_range(self, verts, tris, m, n, row_begin=0, row_end=None):
         v = np.ascontiguousarray(verts, np.float64).reshape(-1)
         t = np.ascontiguousarray(tris, np.uint32).reshape(-1)

@@ -17,14 +17,78 @@
 //
 // Host code is C++ throughout; torch.distributed is not needed (the Python
 // layer ships the 128-byte ncclUniqueId over whatever transport it has).
+//
+// NCCL is bound at first use (dlopen), not linked: a process that already
+// has an NCCL loaded (PyTorch bundles its own, newer one) must keep using it
+// -- a DT_NEEDED on the system libnccl.so.2 would claim the soname first and
+// break `import torch` after libgk.  Order: the libnccl.so.2 already in the
+// process, else the dynamic loader's default (the system NCCL).
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "gk_internal.h"
+
+namespace {
+
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*CommCount)(const ncclComm_t, int*);
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int*);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+const Nccl& nccl() {
+  static Nccl api{};
+  static std::string err;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) {
+      const char* e = dlerror();
+      err = std::string("NCCL not available: ") + (e ? e : "dlopen(libnccl.so.2) failed");
+      return;
+    }
+    bool ok = true;
+    auto sym = [&](auto& fn, const char* name) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name));
+      if (!fn) {
+        ok = false;
+        err = std::string("NCCL symbol missing: ") + name;
+      }
+    };
+    sym(api.GetUniqueId, "ncclGetUniqueId");
+    sym(api.CommInitRank, "ncclCommInitRank");
+    sym(api.CommDestroy, "ncclCommDestroy");
+    sym(api.CommCount, "ncclCommCount");
+    sym(api.CommUserRank, "ncclCommUserRank");
+    sym(api.AllReduce, "ncclAllReduce");
+    sym(api.Send, "ncclSend");
+    sym(api.Recv, "ncclRecv");
+    sym(api.GroupStart, "ncclGroupStart");
+    sym(api.GroupEnd, "ncclGroupEnd");
+    sym(api.GetErrorString, "ncclGetErrorString");
+    if (!ok) api = Nccl{};
+  });
+  if (!api.GetUniqueId) gk::fail(GK_ERR_RUNTIME, err);
+  return api;
+}
+
+}  // namespace
 
 struct gk_comm {
   gk_ctx* ctx = nullptr;
@@ -39,7 +103,7 @@ void nccl_ok(ncclResult_t r, const char* what) {
   if (r != ncclSuccess)
     gk::fail(r == ncclInvalidArgument || r == ncclInvalidUsage ? GK_ERR_INVALID_ARGUMENT
                                                                : GK_ERR_RUNTIME,
-             std::string(what) + ": " + ncclGetErrorString(r));
+             std::string(what) + ": " + nccl().GetErrorString(r));
 }
 
 void rows_of(uint64_t N, int nranks, int rank, uint64_t& b, uint64_t& e) {
@@ -74,7 +138,7 @@ gk_status gk_comm_unique_id(unsigned char id[GK_COMM_ID_BYTES]) {
     gk::need(id != nullptr, GK_ERR_INVALID_ARGUMENT, "null id");
     static_assert(sizeof(ncclUniqueId) == GK_COMM_ID_BYTES, "ncclUniqueId is 128 bytes");
     ncclUniqueId u;
-    nccl_ok(ncclGetUniqueId(&u), "ncclGetUniqueId");
+    nccl_ok(nccl().GetUniqueId(&u), "ncclGetUniqueId");
     std::memcpy(id, &u, sizeof(u));
   });
 }
@@ -93,10 +157,10 @@ gk_status gk_comm_init(gk_ctx* c, const unsigned char id[GK_COMM_ID_BYTES], int 
       m->ctx = c;
       m->nranks = nranks;
       m->rank = rank;
-      nccl_ok(ncclCommInitRank(&m->nccl, nranks, u, rank), "ncclCommInitRank");
+      nccl_ok(nccl().CommInitRank(&m->nccl, nranks, u, rank), "ncclCommInitRank");
       m->range.alloc(2, c->stream);
     } catch (...) {
-      if (m->nccl) ncclCommDestroy(m->nccl);
+      if (m->nccl) nccl().CommDestroy(m->nccl);
       delete m;
       throw;
     }
@@ -117,7 +181,7 @@ gk_status gk_comm_init_all(gk_ctx* const* ctxs, int n, gk_comm** comms) {
     // ncclCommInitAll's pattern: one unique id, every rank initialised inside
     // one group from this thread
     ncclUniqueId u;
-    nccl_ok(ncclGetUniqueId(&u), "ncclGetUniqueId");
+    nccl_ok(nccl().GetUniqueId(&u), "ncclGetUniqueId");
     std::vector<gk_comm*> made(static_cast<size_t>(n), nullptr);
     try {
       for (int i = 0; i < n; ++i) {
@@ -126,12 +190,12 @@ gk_status gk_comm_init_all(gk_ctx* const* ctxs, int n, gk_comm** comms) {
         made[i]->nranks = n;
         made[i]->rank = i;
       }
-      nccl_ok(ncclGroupStart(), "ncclGroupStart");
+      nccl_ok(nccl().GroupStart(), "ncclGroupStart");
       for (int i = 0; i < n; ++i) {
         GK_CUDA(cudaSetDevice(ctxs[i]->device));
-        nccl_ok(ncclCommInitRank(&made[i]->nccl, n, u, i), "ncclCommInitRank");
+        nccl_ok(nccl().CommInitRank(&made[i]->nccl, n, u, i), "ncclCommInitRank");
       }
-      nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+      nccl_ok(nccl().GroupEnd(), "ncclGroupEnd");
       for (int i = 0; i < n; ++i) {
         GK_CUDA(cudaSetDevice(ctxs[i]->device));
         made[i]->range.alloc(2, ctxs[i]->stream);
@@ -139,7 +203,7 @@ gk_status gk_comm_init_all(gk_ctx* const* ctxs, int n, gk_comm** comms) {
     } catch (...) {
       for (gk_comm* m : made)
         if (m) {
-          if (m->nccl) ncclCommDestroy(m->nccl);
+          if (m->nccl) nccl().CommDestroy(m->nccl);
           delete m;
         }
       throw;
@@ -154,7 +218,7 @@ gk_status gk_comm_destroy(gk_comm* m) {
     cudaSetDevice(m->ctx->device);
     cudaStreamSynchronize(m->ctx->stream);
     m->range.reset();
-    if (m->nccl) ncclCommDestroy(m->nccl);
+    if (m->nccl) nccl().CommDestroy(m->nccl);
     delete m;
   });
 }
@@ -163,8 +227,8 @@ gk_status gk_comm_info(const gk_comm* m, int* nranks, int* rank) {
   return gk::guarded([&] {
     gk::need(m && nranks && rank, GK_ERR_INVALID_ARGUMENT, "null argument");
     int n = 0, r = 0;
-    nccl_ok(ncclCommCount(m->nccl, &n), "ncclCommCount");
-    nccl_ok(ncclCommUserRank(m->nccl, &r), "ncclCommUserRank");
+    nccl_ok(nccl().CommCount(m->nccl, &n), "ncclCommCount");
+    nccl_ok(nccl().CommUserRank(m->nccl, &r), "ncclCommUserRank");
     *nranks = n;
     *rank = r;
   });
@@ -181,7 +245,7 @@ gk_status gk_distance_range_global(gk_ctx* c, gk_comm* m, const gk_mesh* mesh, d
     uint64_t b, e;
     rows_of(mesh->N, m->nranks, m->rank, b, e);
     gk::launch_range_device(c, mesh, b, e, m->range.p);
-    nccl_ok(ncclAllReduce(m->range.p, m->range.p, 2, ncclDouble, ncclMin, m->nccl, c->stream),
+    nccl_ok(nccl().AllReduce(m->range.p, m->range.p, 2, ncclDouble, ncclMin, m->nccl, c->stream),
             "ncclAllReduce");
     double h[2];
     GK_CUDA(cudaMemcpyAsync(h, m->range.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -240,20 +304,20 @@ gk_status gk_gather_rows(gk_ctx* c, gk_comm* m, const gk_c128* z_rows, uint64_t 
     gk::need(e == b || z_rows != nullptr, GK_ERR_INVALID_ARGUMENT, "gk_gather_rows: null z_rows");
     // complex128 rows move as pairs of doubles; every block lands in its row
     // slice of the root's matrix (no staging copy)
-    nccl_ok(ncclGroupStart(), "ncclGroupStart");
+    nccl_ok(nccl().GroupStart(), "ncclGroupStart");
     if (m->rank == root) {
       for (int r = 0; r < m->nranks; ++r) {
         uint64_t rb, re;
         rows_of(N, m->nranks, r, rb, re);
         if (r == root || re == rb) continue;
-        nccl_ok(ncclRecv(z_full + rb * N, 2 * (re - rb) * N, ncclDouble, r, m->nccl, c->stream),
+        nccl_ok(nccl().Recv(z_full + rb * N, 2 * (re - rb) * N, ncclDouble, r, m->nccl, c->stream),
                 "ncclRecv");
       }
     } else if (e > b) {
-      nccl_ok(ncclSend(z_rows, 2 * (e - b) * N, ncclDouble, root, m->nccl, c->stream),
+      nccl_ok(nccl().Send(z_rows, 2 * (e - b) * N, ncclDouble, root, m->nccl, c->stream),
               "ncclSend");
     }
-    nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+    nccl_ok(nccl().GroupEnd(), "ncclGroupEnd");
     if (m->rank == root && e > b && z_full + b * N != z_rows)
       GK_CUDA(cudaMemcpyAsync(z_full + b * N, z_rows, (e - b) * N * sizeof(gk_c128),
                               cudaMemcpyDeviceToDevice, c->stream));

@@ -5,6 +5,7 @@ import ctypes as C
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -107,3 +108,16 @@ def test_package_has_no_cpu_fallback():
             if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert not any(b in text for b in banned), f
+
+
+def test_library_does_not_link_nccl(libgk):
+    """libgk binds NCCL at first use (dlopen): a DT_NEEDED on the system
+    libnccl.so.2 would claim the soname before torch's newer NCCL and break
+    `import torch` after the package"""
+    out = subprocess.run(["readelf", "-d", os.path.join(ROOT, "paper_1901_04162_b200", "libgk.so")],
+                         capture_output=True, text=True, check=True).stdout
+    assert "nccl" not in out.lower()
+    r = subprocess.run([sys.executable, "-c", "import paper_1901_04162_b200 as gk; "
+                        "gk.generate_sphere_mesh(1.0, 1); import torch, torch.distributed; "
+                        "print('ok')"], capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-1500:]
