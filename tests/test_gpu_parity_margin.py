@@ -138,9 +138,11 @@ def test_direct_margin_64_rows(gk, oracle, ref, case):
     r = _margin(z, want, B, rows, Bs)
     r.update(rows=int(rows.size), N=N, against=against, entries=int(rows.size * (N - 1)))
     _record(name, "direct", r)
-    assert r["ratio"] <= 1.0, r
-    if name == "c2":   # small kr: within SURVEY 8c's bound without the (1 + |k| r) factor
-        assert r["ratio_survey"] <= 1.0, r
+    # measured on a B200 (profiles/r02_parity_margin.json): 0.07-0.13 of the
+    # stated bar; asserted with room for another GPU's rounding
+    assert r["ratio"] <= 0.25, r
+    if name != "c5":   # kr <= 25: within SURVEY 8c's form without the (1 + |k| r)
+        assert r["ratio_survey"] <= 1.0, r   # factor (C5's far pairs reach kr = 84: 1.06)
 
 
 @pytest.mark.parametrize("S", [1000, 10000])
@@ -174,4 +176,7 @@ def test_table_margin_64_rows(gk, oracle, ref, case, S):
          "vs_table_same_plan (bar: rounding)": vs_table, "S": S, "nodes": int(d["abscissae"].size),
          "rows": int(rows.size), "N": N, "against": against}
     _record(name, f"table_S{S}", r)
-    assert vs_direct["ratio"] <= 1.0 and vs_table["ratio"] <= 1.0, r
+    # vs direct: the interpolation bound dominates (0.65-0.94 measured, the
+    # reference's own table reaches 0.69 / 0.86 at C2); vs the
+    # reference's table on the same plan: rounding only (0.04-0.10 measured)
+    assert vs_direct["ratio"] <= 1.0 and vs_table["ratio"] <= 0.25, r
