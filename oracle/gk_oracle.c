@@ -144,7 +144,7 @@ int go_zero_crossings(double k, double r_min, double r_max, double* out, size_t 
   return GO_OK;
 }
 
-/* sampling.hpp:122-150 */
+/* SamplingPlan::validate (sampling.hpp:59-88) */
 static int plan_validate(const go_plan* p) {
   if (p->n < 2) return GO_INVALID;
   double lo = 0.0, hi = 0.0;
@@ -190,7 +190,7 @@ void go_plan_free(go_plan* p) {
   memset(p, 0, sizeof(*p));
 }
 
-/* sampling.hpp:155-168 */
+/* make_plan (sampling.hpp:92-105) */
 int go_make_plan(const double* absc, size_t n, const double* zeros, size_t nz, go_plan* out) {
   memset(out, 0, sizeof(*out));
   if (n < 2) return GO_INVALID;
@@ -212,7 +212,7 @@ int go_plan_copy_out(const go_plan* p, double* absc, double* zeros) {
   return GO_OK;
 }
 
-/* std::map<double,bool> kept (sampling.hpp:257) as a sorted array. */
+/* std::map<double,bool> kept (sampling.hpp:194) as a sorted array. */
 typedef struct {
   double* r;
   unsigned char* z;
@@ -241,7 +241,7 @@ static void kept_insert_at(kept_set* s, size_t at, double r, unsigned char z) {
   s->n++;
 }
 
-/* sampling.hpp:258-269 try_insert */
+/* sampling.hpp:195-206 try_insert */
 static void kept_try_insert(kept_set* s, double r, unsigned char is_zero, double keep_gap) {
   size_t it = kept_lower_bound(s, r);
   if (it != s->n) {
@@ -255,7 +255,7 @@ static void kept_try_insert(kept_set* s, double r, unsigned char is_zero, double
   kept_insert_at(s, it, r, is_zero);
 }
 
-/* sampling.hpp:212-299 with the medium-derived scalars passed in. */
+/* sampling.hpp:149-236 with the medium-derived scalars passed in. */
 int go_build_plan_core(const go_sampling_cfg* cfg, double k, double t_nominal, go_plan* out) {
   memset(out, 0, sizeof(*out));
   int s = go_sampling_cfg_validate(cfg);
@@ -322,7 +322,7 @@ int go_build_plan_core(const go_sampling_cfg* cfg, double k, double t_nominal, g
   return s;
 }
 
-/* sampling.hpp:212-219 */
+/* build_plan (sampling.hpp:149-236) */
 int go_build_plan(const go_sampling_cfg* cfg, const go_medium* m, go_plan* out) {
   memset(out, 0, sizeof(*out));
   int s = go_sampling_cfg_validate(cfg);

@@ -50,7 +50,7 @@ void validate_medium(const gk_medium& m) {
        "Medium: eps_r_im must be finite and <= 0 (lossy medium)");
 }
 
-// gktab::SamplingConfig::validate (sampling.hpp:30-45)
+// gktab::SamplingConfig::validate (sampling.hpp:27-45)
 void validate_cfg(const gk_sampling_config& c) {
   need(std::isfinite(c.r_min) && std::isfinite(c.r_max) && 0.0 < c.r_min && c.r_min < c.r_max,
        GK_ERR_INVALID_ARGUMENT, "SamplingConfig: need 0 < r_min < r_max, both finite");
@@ -247,7 +247,7 @@ gk_status gk_table_build(gk_ctx* c, const gk_sampling_config* cfg, const gk_medi
   return guarded([&] {
     check_ctx(c);
     need(cfg && med && out, GK_ERR_INVALID_ARGUMENT, "null argument");
-    validate_cfg(*cfg);  // build_plan validates before the medium (sampling.hpp:213)
+    validate_cfg(*cfg);  // build_plan validates before the medium (sampling.hpp:150-151)
     double k_re, k_im;
     wavenumber(*med, k_re, k_im);
     need(degree >= 1, GK_ERR_INVALID_ARGUMENT, "KernelEvaluator: lagrange_degree must be >= 1");

@@ -53,7 +53,7 @@ __global__ void points_kernel(const double* __restrict__ V, const uint32_t* __re
   const double gyc = (vy[0] + vy[1] + vy[2]) / 3.0;
   const double gzc = (vz[0] + vz[1] + vz[2]) / 3.0;
   double rho_o = 0.0, rho_i = 0.0;
-  // outer_points (matfill.hpp:116-128): a*b0 + b*b1 + c*b2, weight w*area
+  // outer_points (matfill.hpp:105-119): a*b0 + b*b1 + c*b2, weight w*area
   for (int o = 0; o < q.m; ++o) {
     const double px = vx[0] * q.b0[o] + vx[1] * q.b1[o] + vx[2] * q.b2[o];
     const double py = vy[0] * q.b0[o] + vy[1] * q.b1[o] + vy[2] * q.b2[o];
@@ -62,7 +62,7 @@ __global__ void points_kernel(const double* __restrict__ V, const uint32_t* __re
     const double dx = px - gxc, dy = py - gyc, dz = pz - gzc;
     rho_o = fmax(rho_o, sqrt(dx * dx + dy * dy + dz * dz));
   }
-  // inner_points (matfill.hpp:132-144): a + (b-a)*x on edges v0v1, v1v2, v2v0
+  // inner_points (matfill.hpp:121-133): a + (b-a)*x on edges v0v1, v1v2, v2v0
   for (int e = 0; e < 3; ++e) {
     const int a = e, b = (e + 1) % 3;
     const double lx = vx[a] - vx[b], ly = vy[a] - vy[b], lz = vz[a] - vz[b];
@@ -198,7 +198,7 @@ enum : int {
 };
 
 // zero_crossings (sampling.hpp:127-141) and the zero pass of the priority
-// insertion (sampling.hpp:271-274): zeros are > keep_gap apart, so each one
+// insertion (sampling.hpp:210-211): zeros are > keep_gap apart, so each one
 // only meets the endpoints.  Sequential: a few hundred iterations.
 __global__ void zeros_kernel(PlanScalars S, double* zeros, double* kept_zeros,
                              unsigned long long* w) {
@@ -229,7 +229,7 @@ __device__ __forceinline__ long long lower_bound_d(const double* a, long long n,
   return lo;
 }
 
-// try_insert outcome against the neighbours found so far (sampling.hpp:258-269)
+// try_insert outcome against the neighbours found so far (sampling.hpp:195-206)
 struct Nbr {
   double next, prev;
   bool equal;
@@ -252,7 +252,7 @@ __device__ __forceinline__ void see_zeros(Nbr& nb, const double* kz, long long n
   if (pos > 0) nb.see(kz[pos - 1], r);
 }
 
-// base grid pass (sampling.hpp:275-276): kept unless an endpoint or a kept
+// base grid pass (sampling.hpp:212-213): kept unless an endpoint or a kept
 // zero is within keep_gap (earlier base points are > t_eff > keep_gap away)
 __global__ void base_kernel(PlanScalars S, const double* kz, const unsigned long long* w,
                             double* vals, uint8_t* keep) {
@@ -271,7 +271,7 @@ __global__ void base_kernel(PlanScalars S, const double* kz, const unsigned long
   }
 }
 
-// refined pass (sampling.hpp:277-283): candidates z -/+ s*refined of every
+// refined pass (sampling.hpp:214-220): candidates z -/+ s*refined of every
 // zero, kept unless a kept point of a stronger class is within keep_gap
 // (windows of different zeros are disjoint on this path, checked on the host)
 __global__ void refined_kernel(PlanScalars S, const double* zeros, const double* kz,
@@ -306,7 +306,7 @@ __global__ void refined_kernel(PlanScalars S, const double* zeros, const double*
   }
 }
 
-// The exact priority insertion of build_plan (sampling.hpp:257-283) on one
+// The exact priority insertion of build_plan (sampling.hpp:194-220) on one
 // thread, for configurations whose refinement windows may interact
 // (qp < 2 side_steps refined + margin): small plans only.
 __global__ void plan_sequential_kernel(PlanScalars S, const double* zeros,
@@ -352,7 +352,7 @@ __device__ __forceinline__ unsigned long long dbits(double x) {
   return static_cast<unsigned long long>(__double_as_longlong(x));
 }
 
-// consecutive gaps: min -> dr_min, max -> t (sampling.hpp:291-296)
+// consecutive gaps: min -> dr_min, max -> t (sampling.hpp:228-233)
 __global__ void gaps_kernel(const double* a, long long n, unsigned long long* w) {
   unsigned long long lo = ~0ull, hi = 0ull;
   bool bad = false;
@@ -510,7 +510,7 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
   cudaStream_t st = ctx->stream;
   GK_CUDA(cudaEventRecord(ctx->ev0, st));
 
-  // scalar prologue (sampling.hpp:216-256), IEEE double on the host
+  // scalar prologue (sampling.hpp:150-193), IEEE double on the host
   PlanScalars S{};
   S.r_min = cfg.r_min;
   S.r_max = cfg.r_max;

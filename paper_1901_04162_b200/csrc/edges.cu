@@ -2,7 +2,7 @@
 // (direct_edge_kernel, table_edge_kernel in fill_kernels.cuh).
 //
 // The reference evaluates, for every source triangle q, the n Gauss points of
-// each of its 3 edges (inner_points, matfill.hpp:132-144) against every outer
+// each of its 3 edges (inner_points, matfill.hpp:121-133) against every outer
 // point of p (fill_rows, matfill.hpp:185-198).  On a closed mesh every edge
 // belongs to two triangles, traversed in opposite directions, so the same n
 // points (up to the rounding of a + (b - a) x vs b + (a - b) x', with the

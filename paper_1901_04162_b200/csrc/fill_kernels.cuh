@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
         const double oz = my[o][2];
         const double d2 = dist2(oxy.x, oxy.y, oz, pxy.x, pxy.y, pzw.x);
         const double y = rsqrt_fast(d2);
-        const double r = __dmul_rn(d2, y);
+        const double r = radius_of<KIND>(d2, y);
         double w = pzw.y;
         double2 cs;  // (cos kr, sin kr)
         if constexpr (ATT == 1) {
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
         for (int o = 0; o < MO; ++o) {
           const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
           const double y = rsqrt_fast(d2);
-          const double r = __dmul_rn(d2, y);
+          const double r = radius_of<KIND>(d2, y);
           double w = pzw.y;
           double2 cs;  // (cos kr, sin kr)
           if constexpr (ATT == 1) {
@@ -395,7 +395,7 @@ __device__ __forceinline__ void direct_term(Acc<MO, KIND == kKindPair>& acc, int
                                             double r_floor = 0.0) {
   const double d2 = dist2(ox, oy, oz, pxy.x, pxy.y, pzw.x);
   const double y = rsqrt_fast(d2);
-  const double r = __dmul_rn(d2, y);
+  const double r = radius_of<KIND>(d2, y);
   GK_DASSERT(r >= r_floor * (1.0 - 1e-12));
   double w = pzw.y;
   double2 cs;
@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 #pragma unroll
       for (int o = 0; o < MO; ++o) {
         const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-        const double r = __dmul_rn(d2, rsqrt_fast(d2));
+        const double r = radius_of<KIND>(d2, rsqrt_fast(d2));
         double2 v, vg = make_double2(0.0, 0.0);
         if constexpr (KIND == kKindPair) pair_table<DEG>(r, A.T, v, vg);
         else if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, A.T);
@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(32 * tedge_warps<KIND>(), 1) table_edge_kernel
 #pragma unroll
           for (int o = 0; o < MO; ++o) {
             const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-            const double r = __dmul_rn(d2, rsqrt_fast(d2));
+            const double r = radius_of<KIND>(d2, rsqrt_fast(d2));
             GK_DASSERT(r >= A.r_far * (1.0 - 1e-12));
             n_high += (r > A.T.r_max) ? NS : 0;  // out_of_range (the reference's accumulate_green)
             double2 v, vg = make_double2(0.0, 0.0);
@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(32 * tedge_warps<KIND>(), 1) table_edge_kernel
 #pragma unroll
           for (int o = 0; o < MO; ++o) {
             const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-            const double r = __dmul_rn(d2, rsqrt_fast(d2));
+            const double r = radius_of<KIND>(d2, rsqrt_fast(d2));
             double2 v, vg = make_double2(0.0, 0.0);
             table_values<KIND, DEG>(r, A.T, v, vg);
             const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
@@ -910,7 +910,7 @@ __device__ __forceinline__ void table_tile(const FillArgs& A, const TableWin& wi
 #pragma unroll
     for (int o = 0; o < MO; ++o) {
       const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-      const double r = __dmul_rn(d2, rsqrt_fast(d2));
+      const double r = radius_of<KIND>(d2, rsqrt_fast(d2));
       double2 ve = make_double2(0.0, 0.0), vg = make_double2(0.0, 0.0);
       win_eval<SMEM, DEG, WANT_E, WANT_G>(r, A.T, win, ve, vg, vc && !self);
       const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);

@@ -113,6 +113,17 @@ __device__ __forceinline__ double rsqrt_fast(double x) {
   return __fma_rn(ye, __fma_rn(0.375, e, 0.5), y);
 }
 
+// r = d2 * rsqrt(d2).  At a zero-distance pair rsqrt(0) = inf makes that
+// NaN; the Exp kind is defined there (eval_analytic(PlainExp, k, 0) = (1, 0),
+// kernel.hpp:58-60), so it takes r = 0 (Green stays NaN -> GK_ERR_DOMAIN,
+// kernel.hpp:51-53).  Compile-time: no cost for the Green fills.
+template <int KIND>
+__device__ __forceinline__ double radius_of(double d2, double y) {
+  const double r = __dmul_rn(d2, y);
+  if constexpr (KIND == GK_KIND_EXP) return d2 > 0.0 ? r : 0.0;
+  return r;
+}
+
 // bucket of r in the lookup hash (r >= r_min gives x >= 0); clamped so any
 // input (out of range, NaN) yields a readable bucket
 __device__ __forceinline__ uint32_t lookup_bucket(double r, const TableDev& t) {

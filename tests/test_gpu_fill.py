@@ -263,6 +263,33 @@ def test_zero_distance_pair_is_domain_error(gk, oracle):
         gk.fill_matrix(mesh, gk.QuadratureSpec(1, 1), gk.Mode.DIRECT, gk.Medium())
 
 
+def test_zero_distance_pair_plain_exp(gk, oracle):
+    """The same r = 0 pair with the PlainExp kind is defined: eval_analytic(PlainExp,
+    k, 0) = (1, 0) (kernel.hpp:58-60).  Direct mode returns it; table mode takes it
+    as a counted fallback below r_min (evaluator.hpp:199-205) -- as the reference."""
+    v = np.array([[0, 0, 0], [3, 0, 0], [0, 3, 0],
+                  [0.5, 1, 0], [1.5, 1, 0], [1, 1, 1]], float)
+    t = np.array([[0, 1, 2], [3, 4, 5]])
+    mesh = gk.TriangleMesh(v, t)
+    k = 2 * np.pi
+    ref, rrep = oracle.fill_rows(mesh.vertices, mesh.triangles, 1, 1, DIRECT, k, kind=EXP)
+    assert np.all(np.isfinite(ref))
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(1, 1))
+    for opts in (None, gk.FillOptions(shared_edges=0)):
+        z, rep = gk.fill_rows(dm, gk.Mode.DIRECT, kind=gk.KernelKind.PlainExp, k=k, options=opts)
+        z = z.cpu().numpy()
+        assert np.all(np.isfinite(z))
+        assert np.abs(z - ref).max() <= 1e-14
+    table = gk.DeviceTable(gk.SamplingConfig(r_min=0.1, r_max=4.0, samples_per_wavelength=1000))
+    d = table.download()
+    ev = oracle.evaluator(oracle.make_plan(d["abscissae"], d["zeros"]), k)
+    reft, treport = oracle.fill_rows(mesh.vertices, mesh.triangles, 1, 1, TABLE, k, ev=ev, kind=EXP)
+    z, rep = gk.fill_rows(dm, gk.Mode.TABLE, kind=gk.KernelKind.PlainExp, table=table)
+    z = z.cpu().numpy()
+    assert np.all(np.isfinite(z)) and np.abs(z - reft).max() <= 1e-12
+    assert rep.fallback_calls == treport.fallback_calls >= 1
+
+
 @pytest.mark.parametrize("level,S,r_min", [(2, 1000, None), (3, 10000, None), (2, 1000, 0.3)])
 def test_table_staging_paths_bit_identical(gk, level, S, r_min):
     """The L1 table kernel, the shared-memory kernel with the whole table staged,
