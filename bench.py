@@ -517,16 +517,17 @@ def run_gpu_arm(args, cfg, rank, world, local):
         return ms, fill_ms
 
     def performed_evals(mode):
-        if mode == "direct_pertri":  # the per-triangle kernel performs every reference call
-            return 3 * m * n * rows * (N - 1)
+        """(evaluations the kernel performs per step, the fill kernel's name)"""
         if gkcomm is not None:
-            return sharded_step(mode, True).evaluations
+            rep = sharded_step(mode, True)
+            return rep.evaluations, rep.path_name
         if not rows:
-            return 0
+            return 0, "none"
         table = table_for(mode)
         _, rep = gk.fill_rows(dmesh, gk.Mode.TABLE if table else gk.Mode.DIRECT, table=table,
-                              k=k, row_begin=rb, row_end=re, out=Z)
-        return rep.evaluations
+                              k=k, row_begin=rb, row_end=re, out=Z,
+                              options=per_tri if mode == "direct_pertri" else None)
+        return rep.evaluations, rep.path_name
 
     # roofline denominator: FP64 DFMA peak measured on this device now
     p64 = ctx.fp64_peak_tflops()
@@ -551,13 +552,13 @@ def run_gpu_arm(args, cfg, rank, world, local):
         # evaluations the kernel performs per launch (fewer than the
         # reference's calls on the shared-edge paths): one synchronous fill
         # outside the timed region reports them
-        performed = performed_evals(mode)
+        performed, path = performed_evals(mode)
         evals_all = performed
         if world > 1:
             t = torch.tensor([performed], dtype=torch.float64, device=f"cuda:{local}")
             dist.all_reduce(t)
             evals_all = float(t[0])
-        results[mode] = {"ms_per_step": ms, "fill_kernel_ms": fill_ms,
+        results[mode] = {"kernel": path, "ms_per_step": ms, "fill_kernel_ms": fill_ms,
                          "evals_per_s": total_evals / (ms * 1e-3),
                          "evaluations_per_step": evals_all,
                          "evaluations_performed_per_s": evals_all / (ms * 1e-3),

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define GK_ABI_VERSION 2
+#define GK_ABI_VERSION 3
 
 typedef enum gk_status {
   GK_OK = 0,
@@ -80,7 +80,18 @@ typedef struct gk_fill_report {
      or fewer where the fill evaluates each shared edge of a closed mesh once
      for both of its triangles (K4e direct, K3e table) */
   uint64_t evaluations;
+  /* the fill kernel that ran (gk_fill_path) */
+  int path;
 } gk_fill_report;
+/* The fill kernels; 0: nothing launched (empty row range). */
+typedef enum gk_fill_path {
+  GK_PATH_DIRECT = 1,        /* K4: direct, per triangle (the reference's order) */
+  GK_PATH_DIRECT_EDGE = 2,   /* K4e: direct, shared edges */
+  GK_PATH_TABLE_L1 = 3,      /* K3: table through L1, per triangle */
+  GK_PATH_TABLE_STAGED = 4,  /* K3: table staged in shared memory, per triangle */
+  GK_PATH_TABLE_EDGE = 5,    /* K3e: table through L1, shared edges */
+  GK_PATH_TABLE_SWEEP = 6    /* K3s: distance-band windows in shared memory, shared edges */
+} gk_fill_path;
 
 /* ---------------------------------------------------- kernel selection
    Every choice the library makes between equivalent kernels, made explicit
@@ -93,7 +104,10 @@ typedef struct gk_fill_report {
 #define GK_AUTO (-1)
 typedef enum gk_table_placement {
   GK_TABLE_GLOBAL = 0, /* table read through L1/L2 */
-  GK_TABLE_SHARED = 1  /* table staged into shared memory: whole, or per-tile windows */
+  GK_TABLE_SHARED = 1, /* table staged into shared memory: whole, or per-tile windows */
+  GK_TABLE_SWEEP = 2   /* shared-edge sweep (K3s): per row cluster, source blocks by
+                          distance band, each band's slice of the base-grid node values
+                          staged into shared memory */
 } gk_table_placement;
 typedef struct gk_fill_options {
   /* GK_AUTO: shared-edge kernels (each mesh edge evaluated once for both of
@@ -103,10 +117,12 @@ typedef struct gk_fill_options {
      shared-edge blocks (any mesh size; TABLE mode still picks by table
      size, GK_TABLE_GLOBAL takes them instead of staging) */
   int shared_edges;
-  /* TABLE mode: GK_AUTO (staged when the table or a tile's window fits,
-     else through L1), or a gk_table_placement (GK_TABLE_GLOBAL: the
-     shared-edge K3e where the fill uses shared edges, else per triangle;
-     GK_TABLE_SHARED: always staged, per triangle) */
+  /* TABLE mode: GK_AUTO (staged whole when the table fits; a dense table
+     through the sweep K3s where its window covers a tile, else K3e through
+     L1), or a gk_table_placement (GK_TABLE_GLOBAL: the shared-edge K3e
+     where the fill uses shared edges, else per triangle; GK_TABLE_SHARED:
+     always staged, per triangle; GK_TABLE_SWEEP: K3s where it fits, else
+     K3e) */
   int table_placement;
   /* TABLE mode: GK_AUTO / 1: arithmetic interval index on the plan's
      uniform runs (bit-identical lookup), 0: lookup buckets only */
@@ -132,6 +148,8 @@ typedef struct gk_mesh_options {
   int edge_chunks;   /* warp-wide edge chunks per block, 1..12 (0 / GK_AUTO: 11) */
   int edge_order;    /* GK_AUTO: the more compact; 0: mesh order; 1: bisection order */
   int leaf_pct;      /* bisection leaf size in percent of the edge cap, 30..100 (0 / GK_AUTO: 61) */
+  int sweep_chunks;  /* chunks per block of the table sweep's second, smaller block
+                        set (DESIGN.md §5 K3s), 1..12 (0 / GK_AUTO: 1) */
 } gk_mesh_options;
 void gk_mesh_options_init(gk_mesh_options* opts);
 
@@ -285,6 +303,10 @@ typedef struct gk_mesh_edge_info {
   uint64_t edges;              /* distinct edges summed over blocks (no padding) */
   double rho_mean;             /* mean bounding radius of a block */
   int ordered;                 /* 1: blocks follow a spatial (bisection) order of the triangles */
+  double rho_max;              /* largest bounding radius of a block */
+  /* the table sweep's block set (K3s; gk_mesh_options.sweep_chunks) */
+  uint64_t sweep_blocks, sweep_edge_slots;
+  double sweep_work_ratio, sweep_rho_max;
 } gk_mesh_edge_info;
 gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out);
 /* The host part of the shared-edge blocks, without a device (tests): cut the
@@ -294,9 +316,10 @@ gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out);
    order[nt] = the triangle at each block position; edge_index[3 nt] = the
    block-local edge index of each side of the triangle at each position;
    block_start[nt + 1] = first position of each block followed by nt;
-   block_edges[nt] = distinct edges of each block; *nblocks; *ordered. */
+   block_edges[nt] = distinct edges of each block; *nblocks; *ordered.
+   leaf_pct: bisection leaf size in percent of the edge cap (0: 61). */
 gk_status gk_edge_blocks_plan(const double* vertices, size_t nv, const uint32_t* triangles,
-                              size_t nt, int chunks, int order_mode, uint32_t* order,
+                              size_t nt, int chunks, int order_mode, int leaf_pct, uint32_t* order,
                               uint32_t* edge_index, uint32_t* block_start,
                               uint32_t* block_edges, uint64_t* nblocks, int* ordered);
 

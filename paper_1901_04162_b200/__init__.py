@@ -12,12 +12,12 @@ from .gktab import (Context, DeviceMesh, DeviceTable, ErrorSweepReport, EvalStat
                     eval_batch_async, fill_matrix, fill_rows, fill_rows_host, fill_rows_pair,
                     generate_plate_mesh, generate_sphere_mesh, jitter, predicted_calls,
                     wavenumber)
-from ._lib import (GK_AUTO, GK_TABLE_GLOBAL, GK_TABLE_SHARED, DomainError, GkError,
+from ._lib import (GK_AUTO, GK_TABLE_GLOBAL, GK_TABLE_SHARED, GK_TABLE_SWEEP, DomainError, GkError,
                    InvalidArgument, OutOfRange, OverflowErrorGk, RuntimeErrorGk, LIB_PATH)
 
 __all__ = [
     "Context", "DeviceMesh", "DeviceTable", "ErrorSweepReport", "EvalStatus", "FillOptions",
-    "FillReport", "MeshOptions", "GK_AUTO", "GK_TABLE_GLOBAL", "GK_TABLE_SHARED",
+    "FillReport", "MeshOptions", "GK_AUTO", "GK_TABLE_GLOBAL", "GK_TABLE_SHARED", "GK_TABLE_SWEEP",
     "InterpMethod", "KernelKind", "Medium", "Mode", "QuadratureSpec", "SamplingConfig",
     "TriangleMesh", "accumulate_batch", "bench_compare", "compare_fills", "edge_blocks_plan",
     "eval_batch",

@@ -73,11 +73,11 @@ class FillReportC(C.Structure):
     _fields_ = [("N", C.c_uint64), ("m", C.c_int), ("n", C.c_int),
                 ("predicted_calls", C.c_uint64), ("actual_calls", C.c_uint64),
                 ("fallback_calls", C.c_uint64), ("wall_time_s", C.c_double),
-                ("evaluations", C.c_uint64)]
+                ("evaluations", C.c_uint64), ("path", C.c_int)]
 
 
 GK_AUTO = -1
-GK_TABLE_GLOBAL, GK_TABLE_SHARED = 0, 1
+GK_TABLE_GLOBAL, GK_TABLE_SHARED, GK_TABLE_SWEEP = 0, 1, 2
 
 
 class FillOptionsC(C.Structure):
@@ -90,7 +90,7 @@ class FillOptionsC(C.Structure):
 class MeshOptionsC(C.Structure):
     """gk_mesh_options (include/gk/gk.h): shared-edge block construction."""
     _fields_ = [("shared_edges", C.c_int), ("edge_chunks", C.c_int), ("edge_order", C.c_int),
-                ("leaf_pct", C.c_int)]
+                ("leaf_pct", C.c_int), ("sweep_chunks", C.c_int)]
 
 
 class SweepReportC(C.Structure):
@@ -148,7 +148,8 @@ PROTOTYPES = {
     "gk_mesh_points_download": [_vp, _vp, _vp],
     "gk_mesh_destroy": [_vp],
     "gk_mesh_edge_info_get": [_vp, _vp],
-    "gk_edge_blocks_plan": [_vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, _vp, _vp, _vp,
+    "gk_edge_blocks_plan": [_vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.c_int, _vp, _vp,
+                            _vp,
                             _vp, _u64p, C.POINTER(C.c_int)],
     "gk_distance_range": [_vp, _vp, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_fill_rows": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_double, C.c_size_t,

@@ -38,7 +38,7 @@ SOURCES = {
     "edges.cu": [],
     "comm.cu": [],
 }
-HEADERS = ["gk_device.cuh", "gk_internal.h", "fill_kernels.cuh"]
+HEADERS = ["gk_device.cuh", "gk_internal.h", "fill_kernels.cuh", "fill_sweep.cuh"]
 
 
 def _newer(src_files, target) -> bool:

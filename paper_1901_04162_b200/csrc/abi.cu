@@ -678,6 +678,9 @@ gk_status gk_mesh_create_ex(gk_ctx* c, const double* verts, size_t nv, const uin
     need(mo.edge_chunks == 0 || mo.edge_chunks == GK_AUTO ||
              (mo.edge_chunks >= 1 && mo.edge_chunks * 32 <= gk::kEdgeCap),
          GK_ERR_INVALID_ARGUMENT, "gk_mesh_options: edge_chunks must be 1..12");
+    need(mo.sweep_chunks == 0 || mo.sweep_chunks == GK_AUTO ||
+             (mo.sweep_chunks >= 1 && mo.sweep_chunks * 32 <= gk::kEdgeCap),
+         GK_ERR_INVALID_ARGUMENT, "gk_mesh_options: sweep_chunks must be 1..12");
     check_ctx(c);
     need(out != nullptr, GK_ERR_INVALID_ARGUMENT, "null output");
     validate_spec(m, n);  // fill_matrix validates the spec first (matfill.hpp:148)
@@ -722,6 +725,13 @@ gk_status gk_mesh_create_ex(gk_ctx* c, const double* verts, size_t nv, const uin
       GK_CUDA(cudaMemcpyAsync(mesh->verts.p, verts, 3 * nv * sizeof(double), cudaMemcpyHostToDevice, c->stream));
       GK_CUDA(cudaMemcpyAsync(dt.p, tris, 3 * nt * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
       gk::launch_points(mesh, mesh->verts.p, dt.p, c->stream);
+      {
+        std::vector<double4> hb(nt);
+        GK_CUDA(cudaMemcpyAsync(hb.data(), mesh->bounds.p, nt * sizeof(double4),
+                                cudaMemcpyDeviceToHost, c->stream));
+        GK_CUDA(cudaStreamSynchronize(c->stream));
+        for (const double4& b : hb) mesh->rho_outer_max = std::fmax(mesh->rho_outer_max, b.w);
+      }
       gk::build_edge_blocks(mesh, verts, tris, mo);
       GK_CUDA(cudaStreamSynchronize(c->stream));
     } catch (...) {
@@ -735,19 +745,25 @@ gk_status gk_mesh_create_ex(gk_ctx* c, const double* verts, size_t nv, const uin
 gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out) {
   return guarded([&] {
     need(mesh != nullptr && out != nullptr, GK_ERR_INVALID_ARGUMENT, "null argument");
-    out->blocks = mesh->nblk;
-    out->edge_slots = mesh->nblk ? mesh->ep.n / static_cast<size_t>(mesh->n) : 0;
-    out->work_ratio = mesh->edge_ratio;
-    out->delta = mesh->edge_delta;
-    out->r_far = mesh->r_far;
-    out->edges = mesh->edges;
-    out->rho_mean = mesh->rho_mean;
-    out->ordered = mesh->ordered ? 1 : 0;
+    out->blocks = mesh->es.nblk;
+    out->edge_slots = mesh->es.nblk ? mesh->es.ep.n / static_cast<size_t>(mesh->n) : 0;
+    out->work_ratio = mesh->es.edge_ratio;
+    out->delta = mesh->es.edge_delta;
+    out->r_far = mesh->es.r_far;
+    out->edges = mesh->es.edges;
+    out->rho_mean = mesh->es.rho_mean;
+    out->ordered = mesh->es.ordered ? 1 : 0;
+    out->rho_max = mesh->es.rho_max;
+    out->sweep_blocks = mesh->sweep.nblk;
+    out->sweep_edge_slots = mesh->sweep.nblk ? mesh->sweep.ep.n / static_cast<size_t>(mesh->n) : 0;
+    out->sweep_work_ratio = mesh->sweep.edge_ratio;
+    out->sweep_rho_max = mesh->sweep.rho_max;
   });
 }
 
 gk_status gk_edge_blocks_plan(const double* verts, size_t nv, const uint32_t* tris, size_t nt,
-                              int chunks, int order_mode, uint32_t* order, uint32_t* edge_index,
+                              int chunks, int order_mode, int leaf_pct, uint32_t* order,
+                              uint32_t* edge_index,
                               uint32_t* block_start, uint32_t* block_edges, uint64_t* nblocks,
                               int* ordered) {
   return guarded([&] {
@@ -759,7 +775,7 @@ gk_status gk_edge_blocks_plan(const double* verts, size_t nv, const uint32_t* tr
     gk::validate_mesh(verts, nv, tris, nt);
     need(nt >= 1, GK_ERR_INVALID_ARGUMENT, "empty mesh");
     const gk::EdgePlan P = gk::plan_edge_blocks(verts, nv, tris, nt, 32 * static_cast<size_t>(chunks),
-                                                order_mode);
+                                                order_mode, leaf_pct);
     for (size_t j = 0; j < nt; ++j) {
       order[j] = P.order[j];
       edge_index[3 * j] = P.eidx[j].x;
@@ -864,7 +880,7 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
     GK_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
   }
-  const bool counted =
+  const int path =
       gk::launch_fill(c, mesh, mode, t, kind, k_re, k_im, row_begin, row_end, z, z2, ldz, cnt,
                       opts ? *opts : c->opts);
   if (!report) return;
@@ -882,7 +898,8 @@ void fill_rows_impl(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_table
   report->actual_calls = kinds * 3ull * mesh->m * mesh->n * rows * (mesh->N - 1);
   report->fallback_calls = h[0] + h[1];
   report->wall_time_s = ms * 1e-3;
-  report->evaluations = counted ? h[3] : report->actual_calls;
+  report->evaluations = gk::path_counts_evaluations(path) ? h[3] : report->actual_calls;
+  report->path = path;
   raise_fill_errors(h);
 }
 
@@ -973,13 +990,13 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
     GK_CUDA(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), c->stream));
     GK_CUDA(cudaEventRecord(c->ev0, c->stream));
     size_t idx = 0, step = first;
-    bool counted = false;
+    int path = 0;
     for (size_t rb = row_begin; rb < row_end; rb += step, step = std::min(chunk, 2 * step), ++idx) {
       const size_t re = rb + step < row_end ? rb + step : row_end;
       const int b = static_cast<int>(idx & 1);
       if (idx >= 2) GK_CUDA(cudaStreamWaitEvent(c->stream, copied[b], 0));
-      counted = gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt,
-                                cnt, opts);
+      path = gk::launch_fill(c, mesh, mode, table, kind, k_re, k_im, rb, re, dz[b], nullptr, nt,
+                             cnt, opts);
       GK_CUDA(cudaEventRecord(filled[b], c->stream));
       GK_CUDA(cudaStreamWaitEvent(copy, filled[b], 0));
       if (ldz == nt)  // contiguous rows on both sides: one linear copy
@@ -1005,7 +1022,8 @@ void fill_rows_to_host(gk_ctx* c, const gk_mesh* mesh, gk_mode mode, const gk_ta
       report->actual_calls = 3ull * mesh->m * mesh->n * (row_end - row_begin) * (nt - 1);
       report->fallback_calls = h[0] + h[1];
       report->wall_time_s = ms * 1e-3;
-      report->evaluations = counted ? h[3] : report->actual_calls;
+      report->evaluations = gk::path_counts_evaluations(path) ? h[3] : report->actual_calls;
+      report->path = path;
     }
     raise_fill_errors(h);
   } catch (...) {

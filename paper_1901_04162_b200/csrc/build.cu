@@ -176,6 +176,47 @@ __global__ void coarse_runs_kernel(const double* __restrict__ absc, size_t n, do
   coarse[c] = static_cast<int32_t>(first - static_cast<long long>(c) * 64);
 }
 
+// table sweep (TableDev::bg / be / bclean): b2p[i] = plan index of base
+// point i (r_min + i t_eff, rounded like build_plan, sampling.hpp:212-213) or
+// -1, and its node values
+__global__ void base_nodes_kernel(const double* __restrict__ absc, size_t n, double r_min,
+                                  double t_eff, long long nbase, const double2* __restrict__ ev,
+                                  const double2* __restrict__ gv, int32_t* __restrict__ b2p,
+                                  double2* __restrict__ bg, double2* __restrict__ be) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nbase;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double a = r_min + static_cast<double>(i) * t_eff;
+    size_t lo = 0, hi = n;  // lower bound of a
+    while (lo < hi) {
+      const size_t mid = (lo + hi) / 2;
+      if (absc[mid] < a) lo = mid + 1;
+      else hi = mid;
+    }
+    const bool hit = lo < n && absc[lo] == a;
+    b2p[i] = hit ? static_cast<int32_t>(lo) : -1;
+    bg[i] = hit ? gv[lo] : make_double2(0.0, 0.0);
+    be[i] = hit ? ev[lo] : make_double2(0.0, 0.0);
+  }
+}
+
+// bit k of word w: base interval i = 32 w + k has the reference's degree-3
+// stencil (start j - 1, evaluator.hpp:49-51, 251-252) on base points
+// i-1 .. i+2 as consecutive plan nodes j-1 .. j+2; zero padding past nbase
+__global__ void base_clean_kernel(const int32_t* __restrict__ b2p, long long nbase,
+                                  uint32_t nwords, uint32_t* __restrict__ bits) {
+  const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nwords) return;
+  uint32_t word = 0;
+  for (int k = 0; k < 32; ++k) {
+    const long long i = 32LL * w + k;
+    if (i < 1 || i + 2 >= nbase) continue;
+    const int32_t j0 = b2p[i - 1];
+    if (j0 >= 0 && b2p[i] == j0 + 1 && b2p[i + 1] == j0 + 2 && b2p[i + 2] == j0 + 3)
+      word |= 1u << k;
+  }
+  bits[w] = word;
+}
+
 // ---------------------------------------------------------- plan (K2)
 
 struct PlanScalars {
@@ -776,6 +817,31 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     }
     d.coarse = t->coarse.p;
   }
+  // table sweep arrays: base points 0 .. steps (base_nodes_kernel)
+  {
+    const long long nbase = S.steps + 1;
+    d.nbase = nbase < (1LL << 30) ? static_cast<uint32_t>(nbase) : 0u;
+    if (d.nbase) {
+      const uint32_t nwords = ((static_cast<uint32_t>((nbase + 31) >> 5)) + 8u) & ~3u;
+      DevBuf<int32_t> b2p;
+      b2p.alloc(static_cast<size_t>(nbase), st);
+      t->base_g.alloc(static_cast<size_t>(nbase), st);
+      t->base_e.alloc(static_cast<size_t>(nbase), st);
+      t->base_clean.alloc(nwords, st);
+      base_nodes_kernel<<<grid_for(nbase, 128), 128, 0, st>>>(
+          absc.p ? absc.p : t->absc.p, static_cast<size_t>(n), S.r_min, S.t_eff, nbase,
+          t->exp_vals.p, t->green_vals.p, b2p.p, t->base_g.p, t->base_e.p);
+      count_launches(1);
+      GK_CUDA(cudaGetLastError());
+      base_clean_kernel<<<(nwords + 127) / 128, 128, 0, st>>>(b2p.p, nbase, nwords,
+                                                               t->base_clean.p);
+      count_launches(1);
+      GK_CUDA(cudaGetLastError());
+    }
+    d.bg = t->base_g.p;
+    d.be = t->base_e.p;
+    d.bclean = t->base_clean.p;
+  }
   d.grec = t->grec.p;
   d.erec = t->erec.p;
   d.lk = t->lk.p;
@@ -799,7 +865,9 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
   info.k_im = k_im;
   info.degree = degree;
   info.device_bytes = t->absc.bytes() + t->exp_vals.bytes() + t->green_vals.bytes() +
-                      t->hash.bytes() + t->grec.bytes() + t->erec.bytes() + t->lk.bytes();
+                      t->hash.bytes() + t->grec.bytes() + t->erec.bytes() + t->lk.bytes() +
+                      t->coarse.bytes() + t->base_g.bytes() + t->base_e.bytes() +
+                      t->base_clean.bytes();
   info.build_ms = ms;
 }
 

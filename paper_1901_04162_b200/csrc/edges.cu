@@ -305,27 +305,15 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
   return P;
 }
 
-void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,
-                       const gk_mesh_options& opts) {
+namespace {
+
+// one block set of at most `cap` distinct edges per block into S
+void build_edge_set(const gk_mesh* mesh, const double* verts, const uint32_t* tris, size_t cap,
+                    int order_mode, int leaf_pct, EdgeSet& S) {
   const size_t N = mesh->N, nv = mesh->nv;
   const int n = mesh->n;
-  mesh->nblk = 0;
-  mesh->edge_ratio = 1.0;
-  mesh->r_far = INFINITY;
-  if (opts.shared_edges == 0) return;
-  size_t cap = 32 * kEdgeChunksDefault;
-  if (opts.edge_chunks >= 1 && opts.edge_chunks * 32 <= kEdgeCap)  // block size (tests, A/B)
-    cap = static_cast<size_t>(opts.edge_chunks) * 32;
-  mesh->ecap = static_cast<int>(cap);
-  // the edge kernels unroll the n points of an edge (n = 1..5)
-  if (N > (size_t(1) << 30) || n > 5) return;
-  // -1: the more compact of mesh and bisection order; 0 / 1 forced (A/B)
-  const int order_mode = opts.edge_order == 0 || opts.edge_order == 1 ? opts.edge_order : -1;
-  EdgePlan R = plan_edge_blocks(verts, nv, tris, N, cap, order_mode, opts.leaf_pct);
-  const bool ordered = R.ordered;
-  double X = 0.0;
-  for (size_t i = 0; i < 3 * nv; ++i) X = std::max(X, std::fabs(verts[i]));
-  (void)X;
+  S.ecap = static_cast<int>(cap);
+  EdgePlan R = plan_edge_blocks(verts, nv, tris, N, cap, order_mode, leaf_pct);
   const std::vector<EdgeBlock>& blocks = R.blocks;
   const std::vector<unsigned long long>& owner = R.owner;
 
@@ -335,13 +323,13 @@ void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,
   DevBuf<uint32_t> d_gslot;
   d_owner.alloc(nslots, st);
   d_gslot.alloc(3 * N, st);
-  mesh->eblk.alloc(blocks.size(), st);
-  mesh->ecol.alloc(N, st);
-  mesh->ep.alloc(nslots * n, st);
+  S.eblk.alloc(blocks.size(), st);
+  S.ecol.alloc(N, st);
+  S.ep.alloc(nslots * n, st);
   GK_CUDA(cudaMemcpyAsync(d_owner.p, owner.data(), nslots * sizeof(unsigned long long),
                           cudaMemcpyHostToDevice, st));
   GK_CUDA(cudaMemcpyAsync(d_gslot.p, R.gslot.data(), 3 * N * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-  GK_CUDA(cudaMemcpyAsync(mesh->eblk.p, blocks.data(), blocks.size() * sizeof(EdgeBlock),
+  GK_CUDA(cudaMemcpyAsync(S.eblk.p, blocks.data(), blocks.size() * sizeof(EdgeBlock),
                           cudaMemcpyHostToDevice, st));
   std::vector<uint4> ecol(N);
   for (size_t j = 0; j < N; ++j) {
@@ -349,17 +337,17 @@ void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,
     ecol[j] = make_uint4(R.order[j],
                          static_cast<uint32_t>(e.x) | (static_cast<uint32_t>(e.y) << 16), e.z, 0u);
   }
-  GK_CUDA(cudaMemcpyAsync(mesh->ecol.p, ecol.data(), N * sizeof(uint4), cudaMemcpyHostToDevice, st));
+  GK_CUDA(cudaMemcpyAsync(S.ecol.p, ecol.data(), N * sizeof(uint4), cudaMemcpyHostToDevice, st));
   const size_t work = nslots * n;
   edge_gather_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, st>>>(
-      mesh->inner.p, N, n, d_owner.p, nslots, mesh->ep.p);
+      mesh->inner.p, N, n, d_owner.p, nslots, S.ep.p);
   count_launches(1);
   GK_CUDA(cudaGetLastError());
   unsigned long long* dmax = mesh->ctx->scratch.p + 30;
   GK_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
   const size_t work2 = 3 * N * static_cast<size_t>(n);
   edge_delta_kernel<<<static_cast<unsigned>((work2 + 255) / 256), 256, 0, st>>>(
-      mesh->inner.p, N, n, d_gslot.p, d_owner.p, mesh->ep.p, dmax);
+      mesh->inner.p, N, n, d_gslot.p, d_owner.p, S.ep.p, dmax);
   count_launches(1);
   GK_CUDA(cudaGetLastError());
   unsigned long long hbits = 0;
@@ -367,15 +355,42 @@ void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,
   GK_CUDA(cudaStreamSynchronize(st));
   double delta;
   std::memcpy(&delta, &hbits, sizeof(delta));
-  mesh->nblk = blocks.size();
-  mesh->edges = R.edges;
-  mesh->rho_mean = R.rho_mean;
-  mesh->ordered = ordered;
-  mesh->edge_delta = delta;
-  mesh->edge_ratio = static_cast<double>(nslots) / (3.0 * static_cast<double>(N));
+  S.nblk = blocks.size();
+  S.edges = R.edges;
+  S.rho_mean = R.rho_mean;
+  S.rho_max = 0.0;
+  for (const EdgeBlock& B : blocks) S.rho_max = std::max(S.rho_max, B.rho);
+  S.ordered = R.ordered;
+  S.edge_delta = delta;
+  S.edge_ratio = static_cast<double>(nslots) / (3.0 * static_cast<double>(N));
   // delta / r_far = 32 u: the reversed-edge rounding stays under half the
   // per-term tolerance (u = 2^-53); a tiny floor keeps r_far > 0
-  mesh->r_far = std::isfinite(delta) ? std::max(delta * 0x1p48, 1e-300) : INFINITY;
+  S.r_far = std::isfinite(delta) ? std::max(delta * 0x1p48, 1e-300) : INFINITY;
+}
+
+}  // namespace
+
+void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,
+                       const gk_mesh_options& opts) {
+  const size_t N = mesh->N;
+  mesh->es.nblk = mesh->sweep.nblk = 0;
+  if (opts.shared_edges == 0) return;
+  size_t cap = 32 * kEdgeChunksDefault;
+  if (opts.edge_chunks >= 1 && opts.edge_chunks * 32 <= kEdgeCap)  // block size (tests, A/B)
+    cap = static_cast<size_t>(opts.edge_chunks) * 32;
+  mesh->es.ecap = static_cast<int>(cap);
+  // the edge kernels unroll the n points of an edge (n = 1..5)
+  if (N > (size_t(1) << 30) || mesh->n > 5) return;
+  // -1: the more compact of mesh and bisection order; 0 / 1 forced (A/B)
+  const int order_mode = opts.edge_order == 0 || opts.edge_order == 1 ? opts.edge_order : -1;
+  build_edge_set(mesh, verts, tris, cap, order_mode, opts.leaf_pct, mesh->es);
+  // the table sweep's set: small blocks (a band's window spans 2 (rho_rows +
+  // rho_block) of radius), always in the spatial order (its row clusters
+  // follow the same order)
+  size_t scap = 32 * kSweepChunksDefault;
+  if (opts.sweep_chunks >= 1 && opts.sweep_chunks * 32 <= kEdgeCap)
+    scap = static_cast<size_t>(opts.sweep_chunks) * 32;
+  build_edge_set(mesh, verts, tris, scap, 1, kSweepLeafPct, mesh->sweep);
 }
 
 }  // namespace gk

@@ -15,13 +15,42 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <cub/block/block_scan.cuh>
+
 #include "fill_kernels.cuh"
 
 namespace gk {
 
+// the table sweep's rows: the triangles of [rb, re) in the sweep set's
+// spatial order (block positions), compacted; one CTA, order-preserving
+__global__ void __launch_bounds__(1024) sweep_rows_kernel(const uint4* __restrict__ ecol, size_t N,
+                                                          size_t rb, size_t re,
+                                                          uint32_t* __restrict__ out) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (size_t j0 = 0; j0 < N; j0 += 1024) {
+    const size_t j = j0 + threadIdx.x;
+    uint32_t q = 0;
+    int f = 0;
+    if (j < N) {
+      q = ecol[j].x;
+      f = q >= rb && q < re;
+    }
+    int off = 0, tot = 0;
+    Scan(ts).ExclusiveSum(f, off, tot);
+    if (f) out[base + off] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) base += tot;
+    __syncthreads();
+  }
+}
+
 __global__ void lossy_phase_kernel(double2* tab, double* ahi, int nhi, double c);
 
-bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
+int launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                  int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
                  gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* counters,
                  const gk_fill_options& opts) {
@@ -46,7 +75,7 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   a.k_re = k_re;
   a.k_im = k_im;
   a.counters = counters;
-  if (row_end <= row_begin || mesh->N == 0) return false;
+  if (row_end <= row_begin || mesh->N == 0) return 0;
 
   DevBuf<double> atten;
   DevBuf<double2> lossy_tab;
@@ -103,18 +132,44 @@ bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table*
   const bool forced = opts.shared_edges == 1;
   const bool table_edges = mode == GK_MODE_TABLE && table;
   if ((mode == GK_MODE_DIRECT || table_edges) && opts.shared_edges != 0 &&
-      mesh->nblk > 0 && mesh->edge_ratio < 0.85 && mesh->n <= 5 &&
-      mesh->r_far < 0.25 * mesh->diameter &&  // else few far tiles (e.g. coordinates far from the origin)
+      mesh->es.nblk > 0 && mesh->es.edge_ratio < 0.85 && mesh->n <= 5 &&
+      mesh->es.r_far < 0.25 * mesh->diameter &&  // else few far tiles (e.g. coordinates far from the origin)
       (att == 0 || (att == 1 && a.nhi <= 512)) && (mesh->N >= 4096 || forced)) {
-    a.eblk = mesh->eblk.p;
-    a.ep = mesh->ep.p;
-    a.ecol = mesh->ecol.p;
-    a.nblk = mesh->nblk;
-    a.ecap = mesh->ecap;
+    a.eblk = mesh->es.eblk.p;
+    a.ep = mesh->es.ep.p;
+    a.ecol = mesh->es.ecol.p;
+    a.nblk = mesh->es.nblk;
+    a.ecap = mesh->es.ecap;
     // table mode: far pairs must also stay >= r_min (no fallback there)
-    a.r_far = table_edges ? std::fmax(mesh->r_far, table->dev.r_min) : mesh->r_far;
+    a.r_far = table_edges ? std::fmax(mesh->es.r_far, table->dev.r_min) : mesh->es.r_far;
   }
+  // the table sweep (K3s, fill_sweep.cuh): degree 3 (or the linear Exp
+  // kind), the mesh's small-block set under the same conditions as K3e;
+  // launch_one decides whether the window fits
   const int degree = table ? table->dev.degree : 3;
+  const EdgeSet& sw = mesh->sweep;
+  if (table_edges && a.nblk > 0 && sw.nblk > 0 && table->dev.nbase > 0 &&
+      (degree == 3 || kind == GK_KIND_EXP) && opts.table_placement != GK_TABLE_GLOBAL &&
+      opts.table_placement != GK_TABLE_SHARED) {
+    a.s_eblk = sw.eblk.p;
+    a.s_ep = sw.ep.p;
+    a.s_ecol = sw.ecol.p;
+    a.s_nblk = sw.nblk;
+    a.s_ecap = sw.ecap;
+    a.s_rho_max = sw.rho_max;
+    a.s_rho_rows = mesh->rho_outer_max * (1.0 + 1e-12);
+    a.s_rc = kSweepRowsPerCluster;
+    if (mesh->srows.n < mesh->N || mesh->srows_begin != row_begin || mesh->srows_end != row_end) {
+      if (mesh->srows.n < mesh->N) mesh->srows.alloc(mesh->N, ctx->stream);
+      sweep_rows_kernel<<<1, 1024, 0, ctx->stream>>>(sw.ecol.p, mesh->N, row_begin, row_end,
+                                                     mesh->srows.p);
+      count_launches(1);
+      GK_CUDA(cudaGetLastError());
+      mesh->srows_begin = row_begin;
+      mesh->srows_end = row_end;
+    }
+    a.s_rows = mesh->srows.p;
+  }
   switch (mesh->m) {
     case 1: return dispatch_mo<1>(ctx, a, mode, kind, degree, att, opts);
     case 3: return dispatch_mo<3>(ctx, a, mode, kind, degree, att, opts);

@@ -135,6 +135,23 @@ struct FillArgs {
   size_t nblk;
   int ecap;  // edge-sum slots per warp (>= every block's edge count)
   double r_far;
+  // table sweep (K3s, fill_sweep.cuh): the mesh's small-block edge set (put
+  // in eblk / ep / ecol / nblk / ecap when K3s runs), the in-range rows in
+  // its spatial order (clusters of s_rc), the staged window's capacity in
+  // base nodes
+  const EdgeBlock* s_eblk;
+  const double4* s_ep;
+  const uint4* s_ecol;
+  size_t s_nblk;
+  int s_ecap;
+  double s_rho_max;   // largest block radius of the sweep set
+  double s_rho_rows;  // largest outer-point radius of a row triangle
+  const uint32_t* s_rows;
+  int s_rc;
+  uint32_t s_wn;
+  double s_delta;     // band width of the tile keys
+  uint32_t* s_list;   // per-CTA tile lists [grid][s_rc * nblk] (scratch)
+  unsigned long long* s_next_cluster;  // dynamic cluster counter (zeroed per launch)
 };
 
 // Column-block walk shared by both kernels: the (column block, inner point)
@@ -685,156 +702,186 @@ __device__ __forceinline__ void table_values(double r, const TableDev& T, double
 template <int KIND>
 __host__ __device__ constexpr int tedge_warps() { return KIND == kKindPair ? 8 : GK_TEDGE_WARPS; }
 
-template <int MO, int NPE, int KIND, int DEG>
-__global__ void __launch_bounds__(32 * tedge_warps<KIND>(), 1) table_edge_kernel(const FillArgs A) {
-  constexpr int W = tedge_warps<KIND>();
+// One (row p, edge block b) tile of the table fill on shared edges (K3e,
+// K3s): the far path evaluates each distinct edge of the block once and
+// combines Z[p][q] from the edge sums in myE; a near tile runs the
+// per-triangle loop on the reference's own points.  `vals(r, v, vg)` is the
+// table lookup (K3e: global records through L1; K3s: the staged window).
+template <int MO, int NPE, int KIND, class Vals>
+__device__ __forceinline__ void table_edge_tile(const FillArgs& A, size_t p, size_t b,
+                                                double2* myE, double* sww, const Vals& vals,
+                                                unsigned long long& nev,
+                                                unsigned long long& n_low,
+                                                unsigned long long& n_high) {
   constexpr bool PAIR = KIND == kKindPair;
   constexpr int NS = PAIR ? 2 : 1;
   constexpr int IPT = 3 * NPE;
-  extern __shared__ double2 sE[];  // edge sums [W][NS][ecap]
-  __shared__ double sw[W][MO];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const size_t N = A.N;
-  double2* const myE = sE + warp * NS * A.ecap;
-  unsigned long long nev = 0, n_low = 0, n_high = 0;
-
-  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
-    const size_t tr = tile / A.nblk, b = tile - tr * A.nblk;
-    const size_t p = A.row_begin + tr * W + warp;
-    if (p >= A.row_end) continue;  // warp-uniform
-    double ox[MO], oy[MO], oz[MO];
+  double ox[MO], oy[MO], oz[MO];
 #pragma unroll
-    for (int o = 0; o < MO; ++o) {
-      const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
-      const double2 zw = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o) + 1);
-      ox[o] = xy.x;
-      oy[o] = xy.y;
-      oz[o] = zw.x;
-      if (lane == 0) sw[warp][o] = zw.y;
-    }
-    const EdgeBlock B = A.eblk[b];
-    const double4 bp = A.bounds[p];
-    const double dx = bp.x - B.cx, dy = bp.y - B.cy, dz = bp.z - B.cz;
-    const double reach = A.r_far + bp.w + B.rho;
-    const bool far = dx * dx + dy * dy + dz * dz >= reach * reach * (1.0 + 1e-12);
-    double2* const zrow = A.z + (p - A.row_begin) * A.ldz;
-    const uint4* const cols = A.ecol + B.tb;
-    const uint32_t nb = B.te - B.tb;
-    __syncwarp();
-    if (far) {
-      const int nch = static_cast<int>((B.ne + 31) >> 5);
-      GK_DASSERT(B.ne <= static_cast<uint32_t>(A.ecap) && B.tb < B.te && B.te <= N);
-      const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
-      double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
-      double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
-      for (int c = 0; c < nch; ++c) {
-        Acc<MO, PAIR> acc;
-        acc.zero();
-        GK_UNROLL(GK_TEDGE_GUNROLL)
-        for (int g = 0; g < NPE; ++g) {
-          const double2 pxy = cxy, pzw = czw;
-          const double4* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 32
-                                                : (c + 1 < nch ? (c + 1) * NPE * 32 : 0));
-          cxy = __ldg(reinterpret_cast<const double2*>(np));
-          czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
-#pragma unroll
-          for (int o = 0; o < MO; ++o) {
-            const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-            const double r = radius_of<KIND>(d2, rsqrt_fast(d2));
-            GK_DASSERT(r >= A.r_far * (1.0 - 1e-12));
-            n_high += (r > A.T.r_max) ? NS : 0;  // out_of_range (the reference's accumulate_green)
-            double2 v, vg = make_double2(0.0, 0.0);
-            table_values<KIND, DEG>(r, A.T, v, vg);
-            acc.add_values(o, pzw.y, v, vg);
-          }
-        }
-        double2 e = make_double2(0.0, 0.0), eg = make_double2(0.0, 0.0);
+  for (int o = 0; o < MO; ++o) {
+    const double2 xy = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o));
+    const double2 zw = __ldg(reinterpret_cast<const double2*>(A.outer + p * MO + o) + 1);
+    ox[o] = xy.x;
+    oy[o] = xy.y;
+    oz[o] = zw.x;
+    if (lane == 0) sww[o] = zw.y;
+  }
+  const EdgeBlock B = A.eblk[b];
+  const double4 bp = A.bounds[p];
+  const double dx = bp.x - B.cx, dy = bp.y - B.cy, dz = bp.z - B.cz;
+  const double reach = A.r_far + bp.w + B.rho;
+  const bool far = dx * dx + dy * dy + dz * dz >= reach * reach * (1.0 + 1e-12);
+  double2* const zrow = A.z + (p - A.row_begin) * A.ldz;
+  const uint4* const cols = A.ecol + B.tb;
+  const uint32_t nb = B.te - B.tb;
+  __syncwarp();
+  if (far) {
+    const int nch = static_cast<int>((B.ne + 31) >> 5);
+    GK_DASSERT(B.ne <= static_cast<uint32_t>(A.ecap) && B.tb < B.te && B.te <= N);
+    const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
+    double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
+    double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
+    for (int c = 0; c < nch; ++c) {
+      Acc<MO, PAIR> acc;
+      acc.zero();
+      GK_UNROLL(GK_TEDGE_GUNROLL)
+      for (int g = 0; g < NPE; ++g) {
+        const double2 pxy = cxy, pzw = czw;
+        const double4* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 32
+                                              : (c + 1 < nch ? (c + 1) * NPE * 32 : 0));
+        cxy = __ldg(reinterpret_cast<const double2*>(np));
+        czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
 #pragma unroll
         for (int o = 0; o < MO; ++o) {
-          const double w = sw[warp][o];
-          e.x = __fma_rn(w, acc.e[o].x, e.x);
-          e.y = __fma_rn(w, acc.e[o].y, e.y);
-          if constexpr (PAIR) {
-            eg.x = __fma_rn(w, acc.g[o].x, eg.x);
-            eg.y = __fma_rn(w, acc.g[o].y, eg.y);
-          }
-        }
-        myE[c * 32 + lane] = e;
-        if constexpr (PAIR) myE[A.ecap + c * 32 + lane] = eg;
-      }
-      nev += static_cast<unsigned long long>(B.ne) * NPE * MO * NS;
-      __syncwarp();
-      for (uint32_t jb = 0; jb < nb; jb += 32) {
-        const uint32_t j = jb + lane;
-        if (j < nb) {
-          const uint4 col = __ldg(cols + j);  // (q, e0 | e1 << 16, e2)
-          GK_DASSERT(col.x < N && (col.y & 0xffffu) < B.ne && (col.y >> 16) < B.ne && col.z < B.ne);
-          const double2 e0 = myE[col.y & 0xffffu], e1 = myE[col.y >> 16], e2 = myE[col.z];
-          __stcs(zrow + col.x, make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y));
-          if constexpr (PAIR) {
-            const double2* G = myE + A.ecap;
-            const double2 g0 = G[col.y & 0xffffu], g1 = G[col.y >> 16], g2 = G[col.z];
-            __stcs(A.z2 + (p - A.row_begin) * A.ldz + col.x,
-                   make_double2(g0.x + g1.x + g2.x, g0.y + g1.y + g2.y));
-          }
+          const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
+          const double r = radius_of<KIND>(d2, rsqrt_fast(d2));
+          GK_DASSERT(r >= A.r_far * (1.0 - 1e-12));
+          n_high += (r > A.T.r_max) ? NS : 0;  // out_of_range (the reference's accumulate_green)
+          double2 v, vg = make_double2(0.0, 0.0);
+          vals(r, v, vg);
+          acc.add_values(o, pzw.y, v, vg);
         }
       }
-      __syncwarp();
-    } else {
-      unsigned nq = 0;
-      for (uint32_t jb = 0; jb < nb; jb += 32) {
-        const uint32_t j = jb + lane;
-        const bool valid = j < nb;
-        const size_t q = __ldg(cols + (valid ? j : nb - 1)).x;
-        const bool self = q == p;
-        nq += __popc(__ballot_sync(0xffffffffu, valid && !self));
-        Acc<MO, PAIR> acc;
-        acc.zero();
-#pragma unroll 1
-        for (int i = 0; i < IPT; ++i) {
-          const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
-          const double2 pxy = __ldg(ptr), pzw = __ldg(ptr + 1);
+      double2 e = make_double2(0.0, 0.0), eg = make_double2(0.0, 0.0);
 #pragma unroll
-          for (int o = 0; o < MO; ++o) {
-            const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
-            const double r = radius_of<KIND>(d2, rsqrt_fast(d2));
-            double2 v, vg = make_double2(0.0, 0.0);
-            table_values<KIND, DEG>(r, A.T, v, vg);
-            const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
-            if (__any_sync(0xffffffffu, oob)) {
-              if (oob) {
-                if (!self && valid) {
-                  // the reference's eval_kernel fallback (evaluator.hpp:199-205)
-                  if constexpr (PAIR) {
-                    v = analytic_sincos(GK_KIND_EXP, A.T.k_re, A.T.k_im, r);
-                    vg = analytic_sincos(GK_KIND_GREEN, A.T.k_re, A.T.k_im, r);
-                  } else {
-                    v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
-                  }
-                  if (r > A.T.r_max) n_high += NS; else n_low += NS;
-                } else {
-                  v = vg = make_double2(0.0, 0.0);
-                }
-              }
-            }
-            acc.add_values(o, pzw.y, v, vg);
-          }
+      for (int o = 0; o < MO; ++o) {
+        const double w = sww[o];
+        e.x = __fma_rn(w, acc.e[o].x, e.x);
+        e.y = __fma_rn(w, acc.e[o].y, e.y);
+        if constexpr (PAIR) {
+          eg.x = __fma_rn(w, acc.g[o].x, eg.x);
+          eg.y = __fma_rn(w, acc.g[o].y, eg.y);
         }
-        acc.finish([&](int o) { return sw[warp][o]; }, self, valid, A.z, A.z2,
-                   (p - A.row_begin) * A.ldz + q, A.counters + 2);
       }
-      nev += static_cast<unsigned long long>(nq) * IPT * MO * NS;
+      myE[c * 32 + lane] = e;
+      if constexpr (PAIR) myE[A.ecap + c * 32 + lane] = eg;
+    }
+    nev += static_cast<unsigned long long>(B.ne) * NPE * MO * NS;
+    __syncwarp();
+    for (uint32_t jb = 0; jb < nb; jb += 32) {
+      const uint32_t j = jb + lane;
+      if (j < nb) {
+        const uint4 col = __ldg(cols + j);  // (q, e0 | e1 << 16, e2)
+        GK_DASSERT(col.x < N && (col.y & 0xffffu) < B.ne && (col.y >> 16) < B.ne && col.z < B.ne);
+        const double2 e0 = myE[col.y & 0xffffu], e1 = myE[col.y >> 16], e2 = myE[col.z];
+        __stcs(zrow + col.x, make_double2(e0.x + e1.x + e2.x, e0.y + e1.y + e2.y));
+        if constexpr (PAIR) {
+          const double2* G = myE + A.ecap;
+          const double2 g0 = G[col.y & 0xffffu], g1 = G[col.y >> 16], g2 = G[col.z];
+          __stcs(A.z2 + (p - A.row_begin) * A.ldz + col.x,
+                 make_double2(g0.x + g1.x + g2.x, g0.y + g1.y + g2.y));
+        }
+      }
     }
     __syncwarp();
+  } else {
+    unsigned nq = 0;
+    for (uint32_t jb = 0; jb < nb; jb += 32) {
+      const uint32_t j = jb + lane;
+      const bool valid = j < nb;
+      const size_t q = __ldg(cols + (valid ? j : nb - 1)).x;
+      const bool self = q == p;
+      nq += __popc(__ballot_sync(0xffffffffu, valid && !self));
+      Acc<MO, PAIR> acc;
+      acc.zero();
+#pragma unroll 1
+      for (int i = 0; i < IPT; ++i) {
+        const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
+        const double2 pxy = __ldg(ptr), pzw = __ldg(ptr + 1);
+#pragma unroll
+        for (int o = 0; o < MO; ++o) {
+          const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);
+          const double r = radius_of<KIND>(d2, rsqrt_fast(d2));
+          double2 v, vg = make_double2(0.0, 0.0);
+          vals(r, v, vg);
+          const bool oob = !(r >= A.T.r_min && r <= A.T.r_max);
+          if (__any_sync(0xffffffffu, oob)) {
+            if (oob) {
+              if (!self && valid) {
+                // the reference's eval_kernel fallback (evaluator.hpp:199-205)
+                if constexpr (PAIR) {
+                  v = analytic_sincos(GK_KIND_EXP, A.T.k_re, A.T.k_im, r);
+                  vg = analytic_sincos(GK_KIND_GREEN, A.T.k_re, A.T.k_im, r);
+                } else {
+                  v = analytic_sincos(KIND, A.T.k_re, A.T.k_im, r);
+                }
+                if (r > A.T.r_max) n_high += NS; else n_low += NS;
+              } else {
+                v = vg = make_double2(0.0, 0.0);
+              }
+            }
+          }
+          acc.add_values(o, pzw.y, v, vg);
+        }
+      }
+      acc.finish([&](int o) { return sww[o]; }, self, valid, A.z, A.z2,
+                 (p - A.row_begin) * A.ldz + q, A.counters + 2);
+    }
+    nev += static_cast<unsigned long long>(nq) * IPT * MO * NS;
   }
+  __syncwarp();
+}
+
+// per-warp counters -> the fill's global counters (one atomic per warp)
+__device__ __forceinline__ void flush_counters(const FillArgs& A, unsigned long long nev,
+                                               unsigned long long n_low,
+                                               unsigned long long n_high) {
   for (int o = 16; o; o >>= 1) {
     n_low += __shfl_xor_sync(0xffffffffu, n_low, o);
     n_high += __shfl_xor_sync(0xffffffffu, n_high, o);
   }
+  const int lane = threadIdx.x & 31;
   if (lane == 0 && n_low) atomicAdd(A.counters, n_low);
   if (lane == 0 && n_high) atomicAdd(A.counters + 1, n_high);
   if (lane == 0 && nev) atomicAdd(A.counters + 3, nev);
 }
+
+template <int MO, int NPE, int KIND, int DEG>
+__global__ void __launch_bounds__(32 * tedge_warps<KIND>(), 1) table_edge_kernel(const FillArgs A) {
+  constexpr int W = tedge_warps<KIND>();
+  constexpr int NS = KIND == kKindPair ? 2 : 1;
+  extern __shared__ double2 sE[];  // edge sums [W][NS][ecap]
+  __shared__ double sw[W][MO];
+  const int warp = threadIdx.x >> 5;
+  double2* const myE = sE + warp * NS * A.ecap;
+  unsigned long long nev = 0, n_low = 0, n_high = 0;
+  const auto vals = [&](double r, double2& v, double2& vg) { table_values<KIND, DEG>(r, A.T, v, vg); };
+  for (size_t tile = blockIdx.x; tile < A.ntiles; tile += gridDim.x) {
+    const size_t tr = tile / A.nblk, b = tile - tr * A.nblk;
+    const size_t p = A.row_begin + tr * W + warp;
+    if (p >= A.row_end) continue;  // warp-uniform
+    table_edge_tile<MO, NPE, KIND>(A, p, b, myE, sw[warp], vals, nev, n_low, n_high);
+  }
+  flush_counters(A, nev, n_low, n_high);
+}
+
+}  // namespace gk
+
+#include "fill_sweep.cuh"
+
+namespace gk {
 
 // ------------------------------------------------ K3 with a shared-memory table
 //
@@ -1096,13 +1143,13 @@ void launch_v4(gk_ctx* ctx, FillArgs a, size_t smem) {
 
 // K3e launch (edge sums in shared memory, the table through L1)
 template <int MO, int KIND, int DEG>
-bool launch_table_edge(gk_ctx* ctx, FillArgs a) {
+int launch_table_edge(gk_ctx* ctx, FillArgs a) {
   constexpr int W = tedge_warps<KIND>();
   const size_t esmem = static_cast<size_t>(W) * (KIND == kKindPair ? 2 : 1) * a.ecap * sizeof(double2);
   auto go = [&](auto kern) {
     a.ntiles = ((a.row_end - a.row_begin + W - 1) / W) * a.nblk;
     launch_kernel(ctx, kern, a, esmem, 32 * W);
-    return true;
+    return static_cast<int>(GK_PATH_TABLE_EDGE);
   };
   switch (a.ipt) {
     case 3: return go(table_edge_kernel<MO, 1, KIND, DEG>);
@@ -1114,9 +1161,89 @@ bool launch_table_edge(gk_ctx* ctx, FillArgs a) {
   }
 }
 
-// returns true when a shared-edge kernel ran (it counts its evaluations)
+// K3s launch (fill_sweep.cuh): the window takes the shared memory the edge
+// sums and the band table leave (smem_budget caps it: tests force small
+// windows and many bands); false when the window cannot cover a tile's
+// radius spread with room for a band, or the bands would be too many (the
+// caller takes K3e)
+template <int MO, int KIND>
+bool launch_table_sweep(gk_ctx* ctx, FillArgs a, size_t budget) {
+  constexpr int W = sweep_warps<KIND>();
+  constexpr int NS = KIND == kKindPair ? 2 : 1;
+  constexpr int NWIN = KIND == kKindPair ? 2 : 1;
+  const size_t fixed = static_cast<size_t>(W) * NS * a.s_ecap * 16 + (2 * kSweepBands + 1) * 4 + 64;
+  const size_t limit = 227 * 1024 - 3072;  // opt-in maximum less the static shared memory
+  if (fixed + 4096 > limit) return false;
+  size_t avail = limit - fixed;
+  if (budget >= 4096 && budget < avail) avail = budget;
+  // 16 B per node and window, 1 bit per node
+  size_t wn = (avail * 8) / (128 * NWIN + 1);
+  const size_t whole = (static_cast<size_t>(a.T.nbase) + kSweepMargin + 31) & ~size_t(31);
+  if (wn > whole) wn = whole;
+  wn &= ~size_t(31);
+  const double cap_r = (static_cast<double>(wn) - kSweepMargin) * a.T.t_eff;
+  const double spread = 2.0 * (a.s_rho_max + a.s_rho_rows) * (1.0 + 1e-9);
+  const double delta = cap_r - spread;
+  // keys lie in [-spread / 2, r_max]: the bands of any cluster
+  if (wn < 64 || !(delta >= 0.1 * cap_r) ||
+      (a.T.r_max + spread) / delta + 2.0 > static_cast<double>(kSweepBands))
+    return false;
+  const size_t nbw = ((wn >> 5) + 8) & ~size_t(3);
+  const size_t smem = NWIN * wn * 16 + nbw * 4 + fixed - 64;
+  a.s_wn = static_cast<uint32_t>(wn);
+  a.s_delta = delta;
+  a.eblk = a.s_eblk;
+  a.ep = a.s_ep;
+  a.ecol = a.s_ecol;
+  a.nblk = a.s_nblk;
+  a.ecap = a.s_ecap;
+  const size_t clusters = (a.row_end - a.row_begin + a.s_rc - 1) / a.s_rc;
+  size_t grid = static_cast<size_t>(ctx->sm_count);
+  if (grid > clusters) grid = clusters;
+  DevBuf<uint32_t> list;  // stream-ordered: freed after the launch completes
+  const size_t nlist = (grid * a.s_rc * a.nblk + 1) & ~size_t(1);
+  list.alloc(nlist + 2, ctx->stream);
+  a.s_list = list.p;
+  a.s_next_cluster = reinterpret_cast<unsigned long long*>(list.p + nlist);
+  GK_CUDA(cudaMemsetAsync(a.s_next_cluster, 0, sizeof(unsigned long long), ctx->stream));
+  auto go = [&](auto kern) {
+    GK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    kern<<<static_cast<unsigned>(grid), 32 * W, smem, ctx->stream>>>(a);
+    count_launches(1);
+    GK_CUDA(cudaGetLastError());
+    return true;
+  };
+  switch (a.ipt) {
+    case 3: return go(table_sweep_kernel<MO, 1, KIND>);
+    case 6: return go(table_sweep_kernel<MO, 2, KIND>);
+    case 9: return go(table_sweep_kernel<MO, 3, KIND>);
+    case 12: return go(table_sweep_kernel<MO, 4, KIND>);
+    case 15: return go(table_sweep_kernel<MO, 5, KIND>);
+    default: return false;
+  }
+}
+
+// K3s for a kind; the fused pair whose two windows do not fit runs as the
+// two single-kind sweeps (Exp into z, Green into z2): the same bits as the
+// separate fills, which keeps the pair bitwise equal to them
+template <int MO, int KIND>
+bool try_sweep(gk_ctx* ctx, const FillArgs& a, size_t budget) {
+  if (launch_table_sweep<MO, KIND>(ctx, a, budget)) return true;
+  if constexpr (KIND == kKindPair) {
+    FillArgs ag = a;
+    ag.z = a.z2;
+    if (!launch_table_sweep<MO, GK_KIND_EXP>(ctx, a, budget)) return false;
+    if (!launch_table_sweep<MO, GK_KIND_GREEN>(ctx, ag, budget))
+      fail(GK_ERR_RUNTIME, "table sweep: the Green window does not fit where the Exp one does");
+    return true;
+  }
+  return false;
+}
+
+// returns the gk_fill_path that ran (the shared-edge paths count their evaluations)
 template <int MO, int MODE, int KIND, int DEG, int ATT>
-bool launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
+int launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
   if constexpr (MODE == GK_MODE_DIRECT) {
     const size_t smem = kPhaseM * sizeof(double2) +
                         (ATT == 1 ? a.nhi * sizeof(double) : 0) +
@@ -1135,7 +1262,7 @@ bool launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
         auto go = [&](auto kern) {
           a.ntiles = ((a.row_end - a.row_begin + W - 1) / W) * a.nblk;
           launch_kernel(ctx, kern, a, esmem, 32 * W);
-          return true;
+          return static_cast<int>(GK_PATH_DIRECT_EDGE);
         };
         switch (a.ipt) {
           case 3: return go(direct_edge_kernel<MO, 1, KIND, ATT>);
@@ -1149,17 +1276,17 @@ bool launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
     }
     if (use_v4) {
       switch (a.ipt) {  // n = 1..5 Gauss points per edge: fully unrolled fast path
-        case 3: launch_v4<MO, 3, KIND, ATT>(ctx, a, smem); return false;
-        case 6: launch_v4<MO, 6, KIND, ATT>(ctx, a, smem); return false;
-        case 9: launch_v4<MO, 9, KIND, ATT>(ctx, a, smem); return false;
-        case 12: launch_v4<MO, 12, KIND, ATT>(ctx, a, smem); return false;
-        case 15: launch_v4<MO, 15, KIND, ATT>(ctx, a, smem); return false;
+        case 3: launch_v4<MO, 3, KIND, ATT>(ctx, a, smem); return static_cast<int>(GK_PATH_DIRECT);
+        case 6: launch_v4<MO, 6, KIND, ATT>(ctx, a, smem); return static_cast<int>(GK_PATH_DIRECT);
+        case 9: launch_v4<MO, 9, KIND, ATT>(ctx, a, smem); return static_cast<int>(GK_PATH_DIRECT);
+        case 12: launch_v4<MO, 12, KIND, ATT>(ctx, a, smem); return static_cast<int>(GK_PATH_DIRECT);
+        case 15: launch_v4<MO, 15, KIND, ATT>(ctx, a, smem); return static_cast<int>(GK_PATH_DIRECT);
         default: break;
       }
     }
     set_tiling(ctx, a, kRowsPerTile, 2);
     launch_kernel(ctx, direct_kernel<MO, KIND, ATT, 2>, a, smem);
-    return false;
+    return static_cast<int>(GK_PATH_DIRECT);
   } else {
     // o.table_placement: GK_TABLE_GLOBAL = through L1 (K3e where the mesh's
     // shared-edge blocks are in use, else the per-triangle L1 kernel),
@@ -1167,12 +1294,22 @@ bool launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
     // windows; tests and A/B), GK_AUTO = by size.  o.smem_budget shrinks the
     // window budget (tests).
     const int placement = o.table_placement;
-    const bool automatic = placement != GK_TABLE_GLOBAL && placement != GK_TABLE_SHARED;
+    const bool automatic = placement != GK_TABLE_GLOBAL && placement != GK_TABLE_SHARED &&
+                           placement != GK_TABLE_SWEEP;
+    // K3s where launch_fill found it eligible (degree 3 / Exp, shared edges):
+    // on request here, and under GK_AUTO for the dense tables below
+    constexpr bool kSweepable = DEG == 3 || KIND == GK_KIND_EXP;
+    if constexpr (kSweepable) {
+      if (a.s_nblk > 0 && placement == GK_TABLE_SWEEP &&
+          try_sweep<MO, KIND>(ctx, a, o.smem_budget))
+        return static_cast<int>(GK_PATH_TABLE_SWEEP);
+    }
+    if (placement == GK_TABLE_SWEEP && a.nblk > 0) return launch_table_edge<MO, KIND, DEG>(ctx, a);
     if (a.nblk > 0 && placement == GK_TABLE_GLOBAL) return launch_table_edge<MO, KIND, DEG>(ctx, a);
     if (placement == GK_TABLE_GLOBAL) {
       set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
       launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
-      return false;
+      return static_cast<int>(GK_PATH_TABLE_L1);
     }
     // shared-memory window sizing: whole table if it fits, else proportional caps
     constexpr bool want_e = KIND == GK_KIND_EXP || KIND == kKindPair;
@@ -1201,6 +1338,13 @@ bool launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
       // fall back to global reads: use the L1 kernel with its wider tiles
       const double est = a.T.nrec * a.window_est / (a.T.r_max - a.T.r_min);
       if (automatic && est > 2.0 * static_cast<double>(j_cap)) {
+        // the sweep (K3s): the table in shared memory per distance band, on
+        // shared edges -- C5 S = 1e4 112 vs 174 ms (K3e) per 4096 rows, C3
+        // 242 vs 328, C4 156 vs 193 (scripts/sweep_ab.py)
+        if constexpr (kSweepable) {
+          if (a.s_nblk > 0 && try_sweep<MO, KIND>(ctx, a, 0))
+            return static_cast<int>(GK_PATH_TABLE_SWEEP);
+        }
         // shared edges (K3e) instead of the L1 kernel: both read the table
         // through L1; K3e 1.3-1.4x faster at S = 1e4 on C3/C4/C5.  Tables
         // staged in shared memory (whole or per tile window) stay per
@@ -1209,7 +1353,7 @@ bool launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
         if (a.nblk > 0) return launch_table_edge<MO, KIND, DEG>(ctx, a);
         set_tiling(ctx, a, GK_TABLE_WARPS, GK_TABLE_CTAS);
         launch_kernel(ctx, table_kernel<MO, KIND, DEG>, a, 0, 32 * GK_TABLE_WARPS);
-        return false;
+        return static_cast<int>(GK_PATH_TABLE_L1);
       }
       S.j_cap = static_cast<uint32_t>(j_cap);
       S.lk_cap = static_cast<uint32_t>(((budget - j_cap * rec_bytes) / 4) & ~size_t(3));
@@ -1229,20 +1373,20 @@ bool launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
     k<<<static_cast<unsigned>(grid), 32 * kStagedWarps, smem, ctx->stream>>>(a, S);
     count_launches(1);
     GK_CUDA(cudaGetLastError());
-    return false;
+    return static_cast<int>(GK_PATH_TABLE_STAGED);
   }
 }
 
 template <int MO, int KIND>
-bool dispatch_att(gk_ctx* ctx, const FillArgs& a, int att, const gk_fill_options& o) {
+int dispatch_att(gk_ctx* ctx, const FillArgs& a, int att, const gk_fill_options& o) {
   if (att == 1) return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 1>(ctx, a, o);
   if (att == 2) return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 2>(ctx, a, o);
   return launch_one<MO, GK_MODE_DIRECT, KIND, 0, 0>(ctx, a, o);
 }
 
-// returns true when a shared-edge kernel ran (launch_fill)
+// returns the gk_fill_path that ran (launch_fill)
 template <int MO>
-bool dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, int att,
+int dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int degree, int att,
                  const gk_fill_options& o) {
   if (mode == GK_MODE_DIRECT) {
     if (kind == GK_KIND_GREEN) return dispatch_att<MO, GK_KIND_GREEN>(ctx, a, att, o);
@@ -1258,10 +1402,10 @@ bool dispatch_mo(gk_ctx* ctx, const FillArgs& a, gk_mode mode, int kind, int deg
 }
 
 // one explicit instantiation per translation unit (fill_mo<m>.cu)
-extern template bool dispatch_mo<1>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
-extern template bool dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
-extern template bool dispatch_mo<4>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
-extern template bool dispatch_mo<6>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
-extern template bool dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template int dispatch_mo<1>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template int dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template int dispatch_mo<4>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template int dispatch_mo<6>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
+extern template int dispatch_mo<7>(gk_ctx*, const FillArgs&, gk_mode, int, int, int, const gk_fill_options&);
 
 }  // namespace gk

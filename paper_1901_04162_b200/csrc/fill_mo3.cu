@@ -3,6 +3,6 @@
 #include "fill_kernels.cuh"
 
 namespace gk {
-template bool dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int,
+template int dispatch_mo<3>(gk_ctx*, const FillArgs&, gk_mode, int, int, int,
                               const gk_fill_options&);
 }  // namespace gk

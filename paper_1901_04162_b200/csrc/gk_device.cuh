@@ -74,6 +74,16 @@ struct TableDev {
   const int32_t* coarse;
   uint32_t ncoarse;  // 0: off
   double t_eff, inv_t;
+  // table sweep (K3s): node values on the base grid -- bg[i] / be[i] is the
+  // Green / Exp value of plan node r_min + i t_eff (zero where that base point
+  // is not a plan node), i = 0 .. nbase-1 -- and one bit per base interval i,
+  // set where the reference's degree-3 stencil of the interval is base points
+  // i-1 .. i+2 as consecutive plan nodes (equally spaced: the Lagrange
+  // weights are the uniform ones)
+  const double2* bg;
+  const double2* be;
+  const uint32_t* bclean;  // nbase / 32 + 8 words (zero-padded)
+  uint32_t nbase;
 };
 
 // Shared-edge fills (direct_edge_kernel, table_edge_kernel; edges.cu): a
@@ -89,6 +99,8 @@ struct TableDev {
 // L1 for the block's points (12 chunks: 228 KB carveout, 28 KB of L1).
 constexpr int kEdgeCap = 384;
 constexpr int kEdgeChunksDefault = 11;
+constexpr int kSweepChunksDefault = 1;  // the table sweep's block set (K3s)
+constexpr int kSweepLeafPct = 50;      // its bisection leaves: 50 % of the edge cap
 struct EdgeBlock {
   uint32_t tb, te, c0, ne;
   double cx, cy, cz, rho;

@@ -85,6 +85,26 @@ struct DevBuf {
   size_t bytes() const { return n * sizeof(T); }
 };
 
+// One set of shared-edge blocks over a mesh (edges.cu): every distinct edge
+// of a block of source triangles is evaluated once and serves the (usually
+// two) triangles that share it; used for (row, block) pairs at least r_far
+// apart.  A mesh keeps two: `es` (11-chunk blocks: K4e / K3e) and `sweep`
+// (small blocks: the table sweep K3s, whose shared-memory window must cover a
+// block's radius spread).
+struct EdgeSet {
+  DevBuf<EdgeBlock> eblk;  // [nblk]
+  DevBuf<double4> ep;      // [chunks][n][32] edge points (owner orientation)
+  DevBuf<uint4> ecol;      // [N] by block position: (triangle, e0 | e1 << 16, e2, 0)
+  uint64_t edges = 0;
+  int ecap = 0;  // edges per block (shared-memory slots per warp)
+  double rho_mean = 0.0, rho_max = 0.0;
+  bool ordered = false;
+  size_t nblk = 0;
+  double r_far = INFINITY;   // pairs this far apart absorb the reversed-edge rounding
+  double edge_delta = 0.0;   // max |point - reversed-edge point| over shared sides
+  double edge_ratio = 1.0;   // evaluated edge slots / (3 N): the far-path work fraction
+};
+
 }  // namespace gk
 
 // gk_fill_rows_host's double-buffered fill -> D2H pipeline, kept by the
@@ -118,6 +138,8 @@ struct gk_table {
   gk::DevBuf<double> grec, erec;
   gk::DevBuf<uint32_t> lk;
   gk::DevBuf<int32_t> coarse;  // arithmetic-locate runs (TableDev::coarse)
+  gk::DevBuf<double2> base_g, base_e;  // table sweep: node values by base index (TableDev::bg / be)
+  gk::DevBuf<uint32_t> base_clean;     // table sweep: uniform-stencil bits (TableDev::bclean)
   std::vector<double> zeros;  // zero_locations (host copy)
 };
 
@@ -127,25 +149,19 @@ struct gk_mesh {
   int m = 0, n = 0;
   double diameter = 0.0;  // bounding-box diagonal of the vertices (bounds every pair distance)
   double mean_edge = 0.0; // edge of the mean-area equilateral triangle (tile window estimate)
+  double rho_outer_max = 0.0;  // largest bounds[].w (a row's outer points about its centroid)
   gk::DevBuf<double4> outer;  // [N * m]    (x, y, z, w)
   gk::DevBuf<double4> inner;  // [3n][N]    (x, y, z, w), column-major in q
   gk::DevBuf<double4> bounds; // [N]        (cx, cy, cz, rho_outer), rho_inner in binner
   gk::DevBuf<double> binner;  // [N]
   gk::DevBuf<double> verts;   // [3 nv] vertices (max_vertex_distance)
-  // shared-edge blocks (build_edge_blocks): every distinct edge of a block of
-  // source triangles is evaluated once and serves the (usually two)
-  // triangles that share it; used for (row, block) pairs at least r_far apart
-  gk::DevBuf<gk::EdgeBlock> eblk;  // [nblk]
-  gk::DevBuf<double4> ep;          // [chunks][n][32] edge points (owner orientation)
-  gk::DevBuf<uint4> ecol;          // [N] by block position: (triangle, e0 | e1 << 16, e2, 0)
-  uint64_t edges = 0;
-  int ecap = 0;  // edges per block (shared-memory slots per warp)
-  double rho_mean = 0.0;
-  bool ordered = false;
-  size_t nblk = 0;
-  double r_far = INFINITY;   // pairs this far apart absorb the reversed-edge rounding
-  double edge_delta = 0.0;   // max |point - reversed-edge point| over shared sides
-  double edge_ratio = 1.0;   // evaluated edges / (3 N): the far-path work fraction
+  // shared-edge blocks (build_edge_blocks): the K4e / K3e set and the
+  // table sweep's small blocks
+  gk::EdgeSet es, sweep;
+  // the table sweep's row clusters: in-range rows in the sweep set's spatial
+  // order, cached for the last row range (gk_fill_rows)
+  mutable gk::DevBuf<uint32_t> srows;
+  mutable size_t srows_begin = 0, srows_end = 0, srows_n = 0;
 };
 
 namespace gk {
@@ -169,7 +185,12 @@ inline gk_mesh_options default_mesh_options() {
   o.edge_chunks = 0;
   o.edge_order = GK_AUTO;
   o.leaf_pct = 0;
+  o.sweep_chunks = 0;
   return o;
+}
+
+inline bool path_counts_evaluations(int path) {
+  return path == GK_PATH_DIRECT_EDGE || path == GK_PATH_TABLE_EDGE || path == GK_PATH_TABLE_SWEEP;
 }
 
 // launch accounting (gk_launch_count)
@@ -227,9 +248,10 @@ void launch_compare(gk_ctx* ctx, const gk_c128* test, const gk_c128* ref, size_t
 void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg, double k_zero,
                         double t_nominal, double k_re, double k_im, int degree);
 // kind: GK_KIND_EXP, GK_KIND_GREEN, or 2 = fused pair (z = Exp, z2 = Green).
-// Returns true when the shared-edge kernel ran: it counts the evaluations it
-// performed into counters[3]; otherwise they equal the reference's calls.
-bool launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
+// Returns the gk_fill_path that ran (0: none); the shared-edge paths count
+// the evaluations they performed into counters[3], elsewhere they equal the
+// reference's calls (path_counts_evaluations).
+int launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* table,
                  int kind, double k_re, double k_im, size_t row_begin, size_t row_end,
                  gk_c128* z, gk_c128* z2, size_t ldz, unsigned long long* d_fallbacks,
                  const gk_fill_options& opts);

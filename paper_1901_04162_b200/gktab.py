@@ -115,11 +115,17 @@ class FillReport:
     table_build_s: float = 0.0
     # kernel evaluations the device performed (<= actual_calls: shared edges)
     evaluations: int = 0
+    # the fill kernel that ran (gk_fill_path: PATH_NAMES)
+    path: int = 0
 
     @classmethod
     def from_c(cls, r: FillReportC) -> "FillReport":
         return cls(r.N, r.m, r.n, r.predicted_calls, r.actual_calls, r.fallback_calls,
-                   r.wall_time_s, evaluations=r.evaluations)
+                   r.wall_time_s, evaluations=r.evaluations, path=r.path)
+
+    @property
+    def path_name(self) -> str:
+        return PATH_NAMES.get(self.path, "none")
 
 
 @dataclass
@@ -199,6 +205,11 @@ class FillOptions:
                                  self.smem_budget)
 
 
+# gk_fill_path (include/gk/gk.h): the fill kernels of DESIGN.md §5
+PATH_NAMES = {1: "direct", 2: "direct_edge", 3: "table_l1", 4: "table_staged",
+              5: "table_edge", 6: "table_sweep"}
+
+
 @dataclass
 class MeshOptions:
     """gk_mesh_options: shared-edge block construction at mesh creation."""
@@ -207,10 +218,11 @@ class MeshOptions:
     edge_chunks: int = 0                  # 0: 11
     edge_order: int = _lib.GK_AUTO        # 0: mesh order, 1: bisection order
     leaf_pct: int = 0                     # 0: 61
+    sweep_chunks: int = 0                 # 0: 1 (the table sweep's block set)
 
     def c(self) -> _lib.MeshOptionsC:
         return _lib.MeshOptionsC(self.shared_edges, self.edge_chunks, self.edge_order,
-                                 self.leaf_pct)
+                                 self.leaf_pct, self.sweep_chunks)
 
 
 def _opts(options: FillOptions | None):
@@ -504,7 +516,8 @@ def eval_batch_async(kind: KernelKind, radii, out, status: EvalStatus,
           "eval_batch")
 
 
-def edge_blocks_plan(mesh: TriangleMesh, chunks: int = 11, order_mode: int = -1) -> dict:
+def edge_blocks_plan(mesh: TriangleMesh, chunks: int = 11, order_mode: int = -1,
+                     leaf_pct: int = 0) -> dict:
     """The host part of the shared-edge blocks (gk_edge_blocks_plan; no
     device needed): block positions, triangle order and block-local edge
     indices."""
@@ -517,7 +530,7 @@ def edge_blocks_plan(mesh: TriangleMesh, chunks: int = 11, order_mode: int = -1)
     ordered = C.c_int()
     check(lib().gk_edge_blocks_plan(mesh.vertices.ctypes.data, mesh.vertices.shape[0],
                                     mesh.triangles.ctypes.data, nt, chunks, order_mode,
-                                    order.ctypes.data, eidx.ctypes.data, start.ctypes.data,
+                                    leaf_pct, order.ctypes.data, eidx.ctypes.data, start.ctypes.data,
                                     nedge.ctypes.data, C.byref(nb), C.byref(ordered)),
           "edge_blocks_plan")
     n = nb.value
@@ -563,9 +576,12 @@ class DeviceMesh:
 
     def edge_info(self) -> dict:
         """Shared-edge blocks of the direct fill (gk_mesh_edge_info_get)."""
-        out = (C.c_double * 8)()
+        out = (C.c_double * 13)()
         check(lib().gk_mesh_edge_info_get(self.h, C.cast(out, C.c_void_p)), "edge_info")
         raw = bytes(out)
+        rho_max = np.frombuffer(raw[64:72], np.float64)[0]
+        s_blocks, s_slots = np.frombuffer(raw[72:88], np.uint64)
+        s_ratio, s_rho = np.frombuffer(raw[88:104], np.float64)
         blocks, slots = np.frombuffer(raw[:16], np.uint64)
         ratio, delta, r_far = np.frombuffer(raw[16:40], np.float64)
         edges = np.frombuffer(raw[40:48], np.uint64)[0]
@@ -573,7 +589,9 @@ class DeviceMesh:
         ordered = np.frombuffer(raw[56:60], np.int32)[0]
         return dict(blocks=int(blocks), edge_slots=int(slots), work_ratio=float(ratio),
                     delta=float(delta), r_far=float(r_far), edges=int(edges),
-                    rho_mean=float(rho), ordered=bool(ordered))
+                    rho_mean=float(rho), ordered=bool(ordered), rho_max=float(rho_max),
+                    sweep=dict(blocks=int(s_blocks), edge_slots=int(s_slots),
+                               work_ratio=float(s_ratio), rho_max=float(s_rho)))
 
     def max_vertex_distance(self) -> float:
         """max_vertex_distance (mesh.hpp:62-68), exact, on the device."""

@@ -21,6 +21,10 @@ dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(cfg["m"], cfg["n"]))
 med = gk.Medium(lambda0=cfg["lambda0"], eps_r=cfg.get("eps_r", 1.0), eps_r_im=cfg.get("eps_r_im", 0.0))
 k = gk.wavenumber(med)
 t = None
+opts = None
+if mode in ("sweep", "tedge"):  # the table through the sweep (K3s) / K3e
+    opts = gk.FillOptions(table_placement=gk.GK_TABLE_SWEEP if mode == "sweep" else gk.GK_TABLE_GLOBAL)
+    mode = "table"
 if mode == "table":
     lo, hi = dm.distance_range()
     t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S), med)
@@ -32,6 +36,6 @@ for _ in range(2):
         Z = None
     else:
         z, rep = gk.fill_rows(dm, gk.Mode.TABLE if t else gk.Mode.DIRECT, table=t, k=k,
-                              row_end=rows, out=Z)
-print(f"{sys.argv[1]} {mode} rows={rows} N={N} fill {rep.wall_time_s*1e3:.3f} ms "
+                              row_end=rows, out=Z, options=opts)
+print(f"{sys.argv[1]} {mode} {rep.path_name} rows={rows} N={N} fill {rep.wall_time_s*1e3:.3f} ms "
       f"{rep.actual_calls / rep.wall_time_s:.3e} evals/s fallbacks={rep.fallback_calls}")

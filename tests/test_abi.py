@@ -53,7 +53,7 @@ def test_library_is_sm100a(libgk):
 
 
 def test_abi_version(libgk):
-    assert libgk.gk_abi_version() == 2
+    assert libgk.gk_abi_version() == 3
 
 
 def test_host_mesh_generators_match_oracle(libgk, oracle):
