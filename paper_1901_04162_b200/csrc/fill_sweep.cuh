@@ -40,7 +40,7 @@
 namespace gk {
 
 #ifndef GK_SWEEP_WARPS
-#define GK_SWEEP_WARPS 12
+#define GK_SWEEP_WARPS 24  // measured: 12 -> 24 warps (80 registers, 72 B spill) C5 S=1e4 253 -> 227 ms per 8192 rows
 #endif
 template <int KIND>
 __host__ __device__ constexpr int sweep_warps() { return KIND == kKindPair ? 8 : GK_SWEEP_WARPS; }
@@ -48,6 +48,15 @@ __host__ __device__ constexpr int sweep_warps() { return KIND == kKindPair ? 8 :
 #define GK_SWEEP_RC 32
 #endif
 constexpr int kSweepRowsPerCluster = GK_SWEEP_RC;  // rows per cluster (<= 32: one warp's lanes)
+#ifndef GK_SWEEP_ORDERED
+#define GK_SWEEP_ORDERED 0  // 1: warp-aggregated scatter (a warp's tiles of a band stay in order)
+#endif
+#ifndef GK_SWEEP_TREE
+#define GK_SWEEP_TREE 0  // 1: the four-term sums as two pairs (shorter dependency chain)
+#endif
+#ifndef GK_SWEEP_CHUNK
+#define GK_SWEEP_CHUNK 1  // largest claim (tiles) from a band's list
+#endif
 constexpr int kSweepBands = 512;  // bands per cluster (launch_table_sweep checks the bound)
 constexpr int kSweepMargin = 16;  // base nodes of the window kept as margin (8 per side)
 
@@ -87,8 +96,13 @@ __device__ __forceinline__ void sweep_values(double r, const SweepWin& W, const 
     const double hb = __fma_rn(s, 0.5, -0.5);              // (s - 1) / 2
     const double h2 = __fma_rn(s, hb, -1.0);               // (s + 1)(s - 2) / 2
     const double w0 = sb * cm, w3 = sb * a6, w1 = h2 * b, w2 = -h2 * s;
+#if GK_SWEEP_TREE
+    g.x = __fma_rn(w1, f1.x, w0 * f0.x) + __fma_rn(w3, f3.x, w2 * f2.x);
+    g.y = __fma_rn(w1, f1.y, w0 * f0.y) + __fma_rn(w3, f3.y, w2 * f2.y);
+#else
     g.x = __fma_rn(w3, f3.x, __fma_rn(w2, f2.x, __fma_rn(w1, f1.x, w0 * f0.x)));
     g.y = __fma_rn(w3, f3.y, __fma_rn(w2, f2.y, __fma_rn(w1, f1.y, w0 * f0.y)));
+#endif
   }
   if constexpr (WANT_E) {  // linear (evaluator.hpp:22-30)
     const double2 e0 = W.e[ic], e1 = W.e[ic + 1];
@@ -165,7 +179,10 @@ __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kerne
     const uint32_t* const rows = A.s_rows + rb;
     if (warp == 0 && lane < nr) s_row[lane] = A.bounds[rows[lane]];
     __syncthreads();
-    const size_t ntile = static_cast<size_t>(nr) * A.nblk;  // tile t: block t / nr, row t % nr
+    // tile t = (block t / nr, row t % nr): block-major, so that a warp's
+    // consecutive claims mostly share the block (its edge points stay in L1)
+    const size_t nblk = A.nblk;
+    const size_t ntile = static_cast<size_t>(nr) * nblk;
     // pass 1: key range
     double kmin = CUDART_INF, kmax = -CUDART_INF;
     for (size_t t = threadIdx.x; t < ntile; t += blockDim.x) {
@@ -216,10 +233,22 @@ __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kerne
     __syncthreads();
     for (int b = threadIdx.x; b < nbands; b += blockDim.x) s_cur[b] = s_off[b];
     __syncthreads();
-    // pass 3: scatter the tiles by band
-    for (size_t t = threadIdx.x; t < ntile; t += blockDim.x) {
-      const int band = band_of(sweep_key(A.eblk, t / nr, s_row[t % nr]));
-      glist[atomicAdd(&s_cur[band], 1)] = static_cast<uint32_t>(t);
+    // pass 3: scatter the tiles by band; a warp's 32 consecutive tiles of one
+    // band stay consecutive (one atomic per band and warp)
+    for (size_t t0 = static_cast<size_t>(warp) * 32; t0 < ntile; t0 += blockDim.x) {
+      const size_t t = t0 + lane;
+      const int band = t < ntile ? band_of(sweep_key(A.eblk, t / nr, s_row[t % nr])) : -1;
+      if (!GK_SWEEP_ORDERED) {
+        if (band >= 0) glist[atomicAdd(&s_cur[band], 1)] = static_cast<uint32_t>(t);
+        continue;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, band);
+      const int leader = __ffs(peers) - 1;
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      int base = 0;
+      if (band >= 0 && lane == leader) base = atomicAdd(&s_cur[band], __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (band >= 0) glist[base + rank] = static_cast<uint32_t>(t);
     }
     __syncthreads();  // s_cur[band] == s_off[band + 1]: the claim cursors (counting down)
     for (int kb = 0; kb < nbands; ++kb) {
@@ -248,15 +277,26 @@ __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kerne
       }
       mbar_wait(&bar, phase);
       phase ^= 1u;
+      // guided claims from the top of the band's list: chunks of up to 8
+      // tiles, shrinking as the band drains
       for (;;) {
-        int idx = 0;
-        if (lane == 0) idx = atomicSub(&s_cur[kb], 1) - 1;
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx < lo) break;
-        const uint32_t t = glist[idx];
-        const size_t b = t / nr;
-        const size_t p = rows[t - b * nr];
-        table_edge_tile<MO, NPE, KIND>(A, p, b, myE, sw[warp], vals, nev, n_low, n_high);
+        int hi = 0, take = 0;
+        if (lane == 0) {
+          const int left = *reinterpret_cast<volatile int*>(&s_cur[kb]) - lo;
+          take = left / (2 * W);
+          take = take < 1 ? 1 : (take > GK_SWEEP_CHUNK ? GK_SWEEP_CHUNK : take);
+          hi = atomicSub(&s_cur[kb], take);
+        }
+        hi = __shfl_sync(0xffffffffu, hi, 0);
+        take = __shfl_sync(0xffffffffu, take, 0);
+        if (hi <= lo) break;
+        const int end = hi - take > lo ? hi - take : lo;
+        for (int idx = hi - 1; idx >= end; --idx) {
+          const uint32_t t = glist[idx];
+          const size_t b = t / nr;
+          const size_t r = t - b * nr;
+          table_edge_tile<MO, NPE, KIND>(A, rows[r], b, myE, sw[warp], vals, nev, n_low, n_high);
+        }
       }
       __syncthreads();  // the window is restaged for the next band
     }

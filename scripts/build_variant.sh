@@ -19,5 +19,6 @@ for f in fill fill_mo1 fill_mo3 fill_mo4 fill_mo6 fill_mo7 eval; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$ROOT/scripts/_variants/libgk_$NAME.so" \
-  "$B/build.cu.o" "${OBJS[@]}" "$B/abi.cu.o" "$B/host.cpp.o" "$B/edges.cu.o" -lcudart
+  "$B/build.cu.o" "${OBJS[@]}" "$B/abi.cu.o" "$B/host.cpp.o" "$B/edges.cu.o" "$B/comm.cu.o" \
+  -lcudart -ldl
 echo "$ROOT/scripts/_variants/libgk_$NAME.so"

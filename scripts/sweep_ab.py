@@ -42,11 +42,15 @@ def main():
         med = gk.Medium(lambda0=cfg["lambda0"], eps_r=cfg.get("eps_r", 1.0),
                         eps_r_im=cfg.get("eps_r_im", 0.0))
         lo, hi = dm.distance_range()
-        Za = torch.empty((rows, N), dtype=torch.complex128, device="cuda")
-        Zb = torch.empty_like(Za)
+        Zb = torch.empty((rows, N), dtype=torch.complex128, device="cuda")
+        Za = Zb if "--only" in sys.argv else torch.empty_like(Zb)
         for S in (10000, 1000):
             t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S), med)
             rs = fill(dm, t, rows, Zb, gk.FillOptions(table_placement=gk.GK_TABLE_SWEEP))
+            if "--only" in sys.argv:
+                print(f"{name} S={S} rows={rows}: {rs.path_name} {rs.wall_time_s * 1e3:.2f} ms "
+                      f"({rs.evaluations / rs.wall_time_s:.3e}/s performed)", flush=True)
+                continue
             re_ = fill(dm, t, rows, Za, gk.FillOptions(table_placement=gk.GK_TABLE_GLOBAL))
             rel = ((Zb - Za).abs() / Za.abs().clamp_min(1e-300)).max().item()
             rst = fill(dm, t, rows, Za, gk.FillOptions(table_placement=gk.GK_TABLE_SHARED,
