@@ -152,6 +152,7 @@ struct FillArgs {
   double s_delta;     // band width of the tile keys
   uint32_t* s_list;   // per-CTA tile lists [grid][s_rc * nblk] (scratch)
   unsigned long long* s_next_cluster;  // dynamic cluster counter (zeroed per launch)
+  size_t s_full;      // clusters of s_rc rows; the rest hold s_rc / 2
 };
 
 // Column-block walk shared by both kernels: the (column block, inner point)
@@ -1200,6 +1201,7 @@ bool launch_table_sweep(gk_ctx* ctx, FillArgs a, size_t budget) {
   const size_t clusters = (a.row_end - a.row_begin + a.s_rc - 1) / a.s_rc;
   size_t grid = static_cast<size_t>(ctx->sm_count);
   if (grid > clusters) grid = clusters;
+  a.s_full = clusters > grid ? clusters - grid : 0;
   DevBuf<uint32_t> list;  // stream-ordered: freed after the launch completes
   const size_t nlist = (grid * a.s_rc * a.nblk + 1) & ~size_t(1);
   list.alloc(nlist + 2, ctx->stream);

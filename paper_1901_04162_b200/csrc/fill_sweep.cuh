@@ -166,7 +166,10 @@ __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kerne
   uint32_t phase = 0;
 
   const size_t nrows = A.row_end - A.row_begin;
-  const size_t ncl = (nrows + RC - 1) / RC;
+  // clusters 0 .. s_full-1 hold RC rows; the last round's rows go in clusters
+  // of RC / 2 (a shorter tail when the dynamic schedule drains)
+  const size_t nfull = A.s_full;
+  const size_t ncl = nfull + (nrows - nfull * RC + RC / 2 - 1) / (RC / 2);
   __shared__ size_t s_cl;
   for (;;) {
     // clusters are taken dynamically (the last word of the list scratch)
@@ -174,8 +177,9 @@ __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kerne
     __syncthreads();
     const size_t cl = s_cl;
     if (cl >= ncl) break;
-    const size_t rb = cl * RC;
-    const int nr = static_cast<int>(nrows - rb < static_cast<size_t>(RC) ? nrows - rb : RC);
+    const size_t rb = cl < nfull ? cl * RC : nfull * RC + (cl - nfull) * (RC / 2);
+    const size_t rc = cl < nfull ? RC : RC / 2;
+    const int nr = static_cast<int>(nrows - rb < rc ? nrows - rb : rc);
     const uint32_t* const rows = A.s_rows + rb;
     if (warp == 0 && lane < nr) s_row[lane] = A.bounds[rows[lane]];
     __syncthreads();
