@@ -12,50 +12,103 @@ namespace gk {
 // (eval_kernel -> eval_exp/eval_green or eval_analytic, evaluator.hpp:199-205)
 enum : unsigned { V_OK = 0, V_INVALID = 1, V_DOMAIN = 2, V_RANGE = 3 };
 
+// One radius of eval_batch (evaluator.hpp:199-205 / kernel.hpp:48-61):
 // FAST (table == NULL, real k): cis_phase_small + a correctly rounded
-// reciprocal instead of libdevice sincos and a division
-template <int KIND, bool TABLE, int DEG, bool FAST = false>
-__global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
-                                  double2* __restrict__ out, TableDev T, double k_re,
-                                  double k_im, unsigned long long* w,
-                                  const double2* __restrict__ ptab = nullptr, double K1s = 0.0) {
-  unsigned long long fb = 0;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const double r = radii[i];
-    unsigned bad = V_OK;
-    double2 v = make_double2(0.0, 0.0);
-    if (TABLE && r >= T.r_min) {
-      if (!(r <= T.r_max)) {
-        bad = V_RANGE;
-      } else if (KIND == GK_KIND_EXP) {
-        v = exp_table(r, T);
-      } else {
-        v = DEG == 3 ? green_table<3>(r, T) : green_table_any(r, T);
-      }
+// reciprocal instead of libdevice sincos and a division; SMEM: the table's
+// base-grid node values staged whole in shared memory (the table sweep's
+// window, gk_device.cuh sweep_values), the global records where an interval
+// is not a uniform stencil
+template <int KIND, bool TABLE, int DEG, bool FAST, bool SMEM>
+__device__ __forceinline__ double2 eval_value(double r, size_t i, const TableDev& T,
+                                              const SweepWin& win, double k_re, double k_im,
+                                              const double2* ptab, double K1s,
+                                              unsigned long long& fb, unsigned long long* w) {
+  unsigned bad = V_OK;
+  double2 v = make_double2(0.0, 0.0);
+  if (TABLE && r >= T.r_min) {
+    if (!(r <= T.r_max)) {
+      bad = V_RANGE;
+    } else if constexpr (SMEM) {
+      double2 vg;
+      sweep_values<KIND, true>(r, win, T, v, vg);
+    } else if (KIND == GK_KIND_EXP) {
+      v = exp_table(r, T);
     } else {
-      if (KIND == GK_KIND_GREEN) {
-        if (r == 0.0) bad = V_DOMAIN;
-        else if (!(r > 0.0)) bad = V_INVALID;
-      } else if (!(r >= 0.0)) {
-        bad = V_INVALID;
-      }
-      if (bad == V_OK) {
-        if constexpr (FAST) {
-          const double2 cs = cis_phase_small(r, K1s, ptab);  // (cos kr, sin kr)
-          v = make_double2(cs.x, -cs.y);
-          if (KIND == GK_KIND_GREEN) {
-            const double y = __drcp_rn(r);
-            v = make_double2(__dmul_rn(v.x, y), __dmul_rn(v.y, y));
-          }
-        } else {
-          v = analytic_sincos(KIND, k_re, k_im, r);
-        }
-        if (TABLE) ++fb;
-      }
+      v = DEG == 3 ? green_table<3>(r, T) : green_table_any(r, T);
     }
-    if (bad) atomicMin(w + 1, (static_cast<unsigned long long>(i) << 3) | bad);
-    out[i] = v;
+  } else {
+    if (KIND == GK_KIND_GREEN) {
+      if (r == 0.0) bad = V_DOMAIN;
+      else if (!(r > 0.0)) bad = V_INVALID;
+    } else if (!(r >= 0.0)) {
+      bad = V_INVALID;
+    }
+    if (bad == V_OK) {
+      if constexpr (FAST) {
+        const double2 cs = cis_phase_small(r, K1s, ptab);  // (cos kr, sin kr)
+        v = make_double2(cs.x, -cs.y);
+        if (KIND == GK_KIND_GREEN) {
+          const double y = __drcp_rn(r);
+          v = make_double2(__dmul_rn(v.x, y), __dmul_rn(v.y, y));
+        }
+      } else {
+        v = analytic_sincos(KIND, k_re, k_im, r);
+      }
+      if (TABLE) ++fb;
+    }
+  }
+  if (bad) atomicMin(w + 1, (static_cast<unsigned long long>(i) << 3) | bad);
+  return v;
+}
+
+// K5: RPT radii per thread, all loaded before any is evaluated (the stream's
+// bytes in flight), evict-first loads and stores; one wave of CTAs
+template <int KIND, bool TABLE, int DEG, bool FAST, bool SMEM, int RPT>
+__global__ void __launch_bounds__(SMEM ? 1024 : 256)
+    eval_batch_kernel(const double* __restrict__ radii, size_t n, double2* __restrict__ out,
+                      TableDev T, double k_re, double k_im, unsigned long long* w,
+                      const double2* __restrict__ ptab, double K1s) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  // programmatic dependent launch (launch_pdl): let the next launch of the
+  // stream be scheduled now, and wait for the previous one's memory before
+  // reading -- back-to-back batches overlap launch and tail
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  SweepWin win{};
+  if constexpr (SMEM) {
+    // the whole base grid: nodes [0, nbase) and its clean bits
+    __shared__ uint64_t bar;
+    const int nbase = static_cast<int>(T.nbase);
+    const int nbw = (((nbase + 31) >> 5) + 8) & ~3;
+    double2* const s_v = reinterpret_cast<double2*>(smem);
+    uint32_t* const s_bits = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(nbase) * 16);
+    if (threadIdx.x == 0) {
+      mbar_init(&bar);
+      mbar_expect_tx(&bar, static_cast<uint32_t>(nbase) * 16u + static_cast<uint32_t>(nbw) * 4u);
+      tma_load_1d(s_v, KIND == GK_KIND_EXP ? T.be : T.bg, static_cast<uint32_t>(nbase) * 16u, &bar);
+      tma_load_1d(s_bits, T.bclean, static_cast<uint32_t>(nbw) * 4u, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    win = SweepWin{s_v, s_v, s_bits, 0, 0, nbase, -T.r_min * T.inv_t, T.inv_t};
+  }
+  unsigned long long fb = 0;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i0 < n;
+       i0 += stride * RPT) {
+    double r[RPT];
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const size_t i = i0 + k * stride;
+      r[k] = i < n ? __ldcs(radii + i) : 1.0;
+    }
+#pragma unroll
+    for (int k = 0; k < RPT; ++k) {
+      const size_t i = i0 + k * stride;
+      if (i < n)
+        __stcs(out + i, eval_value<KIND, TABLE, DEG, FAST, SMEM>(r[k], i, T, win, k_re, k_im, ptab,
+                                                                 K1s, fb, w));
+    }
   }
   if (TABLE) {
     for (int o = 16; o; o >>= 1) fb += __shfl_xor_sync(0xffffffffu, fb, o);
@@ -63,8 +116,11 @@ __global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
   }
 }
 
-#ifndef GK_EVAL_BLOCKS_PER_SM
-#define GK_EVAL_BLOCKS_PER_SM 32  // eval_batch grid cap (blocks of 256 per SM)
+#ifndef GK_EVAL_RPT
+#define GK_EVAL_RPT 4  // radii per thread in the direct kernels (loads in flight)
+#endif
+#ifndef GK_EVAL_RPT_TABLE
+#define GK_EVAL_RPT_TABLE 1  // ... in the table kernels (gather-latency bound)
 #endif
 
 // the context's options: eval_libdevice = 1 takes libdevice sincos instead of
@@ -72,28 +128,69 @@ __global__ void eval_batch_kernel(const double* __restrict__ radii, size_t n,
 static bool fast_eval(const gk_ctx* ctx) { return ctx->opts.eval_libdevice != 1; }
 static bool arith_locate(const gk_ctx* ctx) { return ctx->opts.arith_locate != 0; }
 
+// launch with the programmatic-stream-serialization attribute: the kernel
+// may start while the stream's previous kernel drains (it waits on
+// griddepcontrol.wait before touching memory the previous one may write)
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GK_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
+// staged table: the base-grid values + bits fit two CTAs of 1024 per SM
+constexpr size_t kEvalStageMax = 110 * 1024;
+
 template <int KIND>
 void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n, double2* out,
                       double k_re, double k_im, unsigned long long* w) {
-  size_t grid = (n + 255) / 256;
-  const size_t cap = static_cast<size_t>(ctx->sm_count) * GK_EVAL_BLOCKS_PER_SM;
-  if (grid > cap) grid = cap;
-  if (grid < 1) grid = 1;
-  const unsigned g = static_cast<unsigned>(grid);
   TableDev T{};
   if (t) T = t->dev;
   if (!arith_locate(ctx)) T.ncoarse = 0;
-  if (!t && k_im == 0.0 && fast_eval(ctx))
-    eval_batch_kernel<KIND, false, 0, true><<<g, 256, 0, ctx->stream>>>(
-        r, n, out, T, k_re, k_im, w, ctx->phase_small.p, k_re * kPhaseSmall / (2.0 * kPi));
-  else if (!t)
-    eval_batch_kernel<KIND, false, 0><<<g, 256, 0, ctx->stream>>>(r, n, out, T, k_re, k_im, w);
-  else if (KIND == GK_KIND_GREEN && T.degree == 3)
-    eval_batch_kernel<KIND, true, 3><<<g, 256, 0, ctx->stream>>>(r, n, out, T, k_re, k_im, w);
-  else
-    eval_batch_kernel<KIND, true, 0><<<g, 256, 0, ctx->stream>>>(r, n, out, T, k_re, k_im, w);
+  const double2* ptab = ctx->phase_small.p;
+  const double K1s = k_re * kPhaseSmall / (2.0 * kPi);
+  cudaStream_t st = ctx->stream;
+  constexpr int RPT = GK_EVAL_RPT, RPTT = GK_EVAL_RPT_TABLE;
+  // one wave: 8 CTAs of 256 (2 of 1024 staged) per SM, rpt radii per thread
+  auto grid_of = [&](size_t threads, size_t per_sm, int rpt) {
+    size_t g = (n + threads * rpt - 1) / (threads * rpt);
+    const size_t cap = static_cast<size_t>(ctx->sm_count) * per_sm;
+    if (g > cap) g = cap;
+    return static_cast<unsigned>(g < 1 ? 1 : g);
+  };
+  const size_t stage = t ? static_cast<size_t>(T.nbase) * 16 +
+                               static_cast<size_t>((((T.nbase + 31) >> 5) + 8) & ~3u) * 4
+                         : 0;
+  if (!t && k_im == 0.0 && fast_eval(ctx)) {
+    launch_pdl(eval_batch_kernel<KIND, false, 0, true, false, RPT>, grid_of(256, 8, RPT), 256, 0, st,
+               r, n, out, T, k_re, k_im, w, ptab, K1s);
+  } else if (!t) {
+    launch_pdl(eval_batch_kernel<KIND, false, 0, false, false, RPT>, grid_of(256, 8, RPT), 256, 0, st,
+               r, n, out, T, k_re, k_im, w, ptab, K1s);
+  } else if ((KIND == GK_KIND_EXP || T.degree == 3) && T.nbase > 0 && stage <= kEvalStageMax &&
+             ctx->opts.table_placement != GK_TABLE_GLOBAL) {
+    auto kern = eval_batch_kernel<KIND, true, 3, false, true, RPTT>;
+    GK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(stage)));
+    launch_pdl(kern, grid_of(1024, 2, RPTT), 1024, stage, st, r, n, out, T, k_re, k_im, w, ptab,
+               K1s);
+  } else if (KIND == GK_KIND_GREEN && T.degree == 3) {
+    launch_pdl(eval_batch_kernel<KIND, true, 3, false, false, RPTT>, grid_of(256, 8, RPTT), 256,
+               0, st, r, n, out, T, k_re, k_im, w, ptab, K1s);
+  } else {
+    launch_pdl(eval_batch_kernel<KIND, true, 0, false, false, RPTT>, grid_of(256, 8, RPTT), 256,
+               0, st, r, n, out, T, k_re, k_im, w, ptab, K1s);
+  }
   count_launches(1);
-  GK_CUDA(cudaGetLastError());
 }
 
 void launch_eval_batch(gk_ctx* ctx, const gk_table* table, gk_kind kind, double k_re, double k_im,

@@ -28,7 +28,6 @@ namespace gk {
 constexpr int kRowsPerTile = 8;  // one row per warp
 constexpr int kMaxColBlocks = 32;  // 32-column blocks per tile (adaptive, see launch_fill)
 constexpr int kThreads = 32 * kRowsPerTile;
-constexpr int kKindPair = 2;  // fused Exp + Green fill sharing r
 #ifndef GK_TABLE_WARPS
 #define GK_TABLE_WARPS 8  // table_kernel (L1 path): rows per CTA
 #endif
@@ -172,44 +171,6 @@ struct InnerWalk {
     zw = __ldg(p + 1);
   }
 };
-
-// --------------------------------------------------- TMA bulk-copy helpers
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
 
 // one-shot copy of `bytes` (multiple of 16, 16 B aligned) global -> shared,
 // issued by thread 0 as a TMA bulk copy; every thread waits on the mbarrier
@@ -691,13 +652,6 @@ __global__ void __launch_bounds__(32 * GK_TABLE_WARPS, GK_TABLE_CTAS) table_kern
 #endif
 
 // the kind's table value v (the fused pair: Exp in v, Green in vg)
-template <int KIND, int DEG>
-__device__ __forceinline__ void table_values(double r, const TableDev& T, double2& v, double2& vg) {
-  if constexpr (KIND == kKindPair) pair_table<DEG>(r, T, v, vg);
-  else if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, T);
-  else if constexpr (DEG == 3) v = green_table<3>(r, T);
-  else v = green_table_any(r, T);
-}
 
 // the fused pair carries two sums per edge: 8 warps
 template <int KIND>

@@ -60,66 +60,6 @@ constexpr int kSweepRowsPerCluster = GK_SWEEP_RC;  // rows per cluster (<= 32: o
 constexpr int kSweepBands = 512;  // bands per cluster (launch_table_sweep checks the bound)
 constexpr int kSweepMargin = 16;  // base nodes of the window kept as margin (8 per side)
 
-// the staged window of one band
-struct SweepWin {
-  const double2* g;      // Green node values of base points i0 .. i0 + wn - 1
-  const double2* e;      // Exp node values
-  const uint32_t* bits;  // clean bits, words w0 ..
-  int i0, w0, wn;
-  double x0, inv_t;  // x = fma(r, inv_t, x0) = (r - r_min) / t_eff
-};
-
-// K(r) for the kind through the window, or the global records where the
-// interval is not a uniform stencil inside the window
-template <int KIND>
-__device__ __forceinline__ void sweep_values(double r, const SweepWin& W, const TableDev& T,
-                                             double2& v, double2& vg) {
-  constexpr bool WANT_G = KIND != GK_KIND_EXP, WANT_E = KIND != GK_KIND_GREEN;
-  const double x = __fma_rn(r, W.inv_t, W.x0);
-  const double yv = __dadd_rd(x, kMagic52);  // floor(x) + 2^52 (0 <= x < 2^31 in range)
-  const int i = __double2loint(yv);
-  const double s = x - (yv - kMagic52);  // in [0, 1)
-  const int ii = i - W.i0;
-  bool ok = static_cast<unsigned>(ii - 1) < static_cast<unsigned>(W.wn - 4);
-  const int ic = ok ? ii : 1;  // clamped: the window reads stay in bounds
-  const int ia = W.i0 + ic;
-  ok = ok && ((W.bits[(ia >> 5) - W.w0] >> (ia & 31)) & 1u);
-  double2 g = make_double2(0.0, 0.0), e = make_double2(0.0, 0.0);
-  if constexpr (WANT_G) {
-    // uniform cubic Lagrange weights on nodes -1, 0, 1, 2
-    const double2* f = W.g + (ic - 1);
-    const double2 f0 = f[0], f1 = f[1], f2 = f[2], f3 = f[3];
-    const double b = s - 1.0;
-    const double sb = s * b;
-    const double cm = __fma_rn(s, -1.0 / 6.0, 1.0 / 3.0);  // -(s - 2) / 6
-    const double a6 = __fma_rn(s, 1.0 / 6.0, 1.0 / 6.0);   // (s + 1) / 6
-    const double hb = __fma_rn(s, 0.5, -0.5);              // (s - 1) / 2
-    const double h2 = __fma_rn(s, hb, -1.0);               // (s + 1)(s - 2) / 2
-    const double w0 = sb * cm, w3 = sb * a6, w1 = h2 * b, w2 = -h2 * s;
-#if GK_SWEEP_TREE
-    g.x = __fma_rn(w1, f1.x, w0 * f0.x) + __fma_rn(w3, f3.x, w2 * f2.x);
-    g.y = __fma_rn(w1, f1.y, w0 * f0.y) + __fma_rn(w3, f3.y, w2 * f2.y);
-#else
-    g.x = __fma_rn(w3, f3.x, __fma_rn(w2, f2.x, __fma_rn(w1, f1.x, w0 * f0.x)));
-    g.y = __fma_rn(w3, f3.y, __fma_rn(w2, f2.y, __fma_rn(w1, f1.y, w0 * f0.y)));
-#endif
-  }
-  if constexpr (WANT_E) {  // linear (evaluator.hpp:22-30)
-    const double2 e0 = W.e[ic], e1 = W.e[ic + 1];
-    e.x = __fma_rn(s, e1.x - e0.x, e0.x);
-    e.y = __fma_rn(s, e1.y - e0.y, e0.y);
-  }
-  if constexpr (KIND == kKindPair) {
-    v = e;
-    vg = g;
-  } else if constexpr (KIND == GK_KIND_GREEN) {
-    v = g;
-  } else {
-    v = e;
-  }
-  if (!ok) table_values<KIND, 3>(r, T, v, vg);
-}
-
 // lower end of the tile's radii: |c_p - c_b| - rho_p - rho_b
 __device__ __forceinline__ double sweep_key(const EdgeBlock* eb, size_t b, double4 cp) {
   const EdgeBlock& B = eb[b];

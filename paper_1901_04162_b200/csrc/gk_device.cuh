@@ -339,6 +339,132 @@ __device__ __forceinline__ void win_eval(double r, const TableDev& t, const Tabl
   }
 }
 
+// --------------------------------------------------- TMA bulk-copy helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+constexpr int kKindPair = 2;  // fused Exp + Green sharing r
+
+template <int KIND, int DEG>
+__device__ __forceinline__ void table_values(double r, const TableDev& T, double2& v, double2& vg) {
+  if constexpr (KIND == kKindPair) pair_table<DEG>(r, T, v, vg);
+  else if constexpr (KIND == GK_KIND_EXP) v = exp_table(r, T);
+  else if constexpr (DEG == 3) v = green_table<3>(r, T);
+  else v = green_table_any(r, T);
+}
+
+// a staged window of base-grid node values (the table sweep K3s,
+// fill_sweep.cuh, and the staged eval_batch, eval.cu)
+struct SweepWin {
+  const double2* g;      // Green node values of base points i0 .. i0 + wn - 1
+  const double2* e;      // Exp node values
+  const uint32_t* bits;  // clean bits, words w0 ..
+  int i0, w0, wn;
+  double x0, inv_t;  // x = fma(r, inv_t, x0) = (r - r_min) / t_eff
+};
+
+// K(r) for the kind through the window, or the global records where the
+// interval is not a uniform stencil inside the window
+// EXACT: the interval and s from the rounded base points themselves (like
+// arith_locate), so that s = 0 exactly at a node and nodes are reproduced
+// exactly (evaluator.hpp:259-262; the standalone eval_batch); the fills
+// need only the tolerance and take s from x = (r - r_min) / t_eff directly
+template <int KIND, bool EXACT = false>
+__device__ __forceinline__ void sweep_values(double r, const SweepWin& W, const TableDev& T,
+                                             double2& v, double2& vg) {
+  constexpr bool WANT_G = KIND != GK_KIND_EXP, WANT_E = KIND != GK_KIND_GREEN;
+  const double x = __fma_rn(r, W.inv_t, W.x0);
+  const double yv = __dadd_rd(x, kMagic52);  // floor(x) + 2^52 (0 <= x < 2^31 in range)
+  int i = __double2loint(yv);
+  double s;
+  if constexpr (EXACT) {
+    double a0 = base_point(T, i), a1 = base_point(T, i + 1);
+    if (r < a0) {
+      --i;
+      a0 = base_point(T, i);
+    } else if (r >= a1) {
+      ++i;
+      a0 = a1;
+    }
+    s = (r - a0) * W.inv_t;
+  } else {
+    s = x - (yv - kMagic52);  // in [0, 1)
+  }
+  const int ii = i - W.i0;
+  bool ok = static_cast<unsigned>(ii - 1) < static_cast<unsigned>(W.wn - 4);
+  const int ic = ok ? ii : 1;  // clamped: the window reads stay in bounds
+  const int ia = W.i0 + ic;
+  ok = ok && ((W.bits[(ia >> 5) - W.w0] >> (ia & 31)) & 1u);
+  double2 g = make_double2(0.0, 0.0), e = make_double2(0.0, 0.0);
+  if constexpr (WANT_G) {
+    // uniform cubic Lagrange weights on nodes -1, 0, 1, 2
+    const double2* f = W.g + (ic - 1);
+    const double2 f0 = f[0], f1 = f[1], f2 = f[2], f3 = f[3];
+    const double b = s - 1.0;
+    const double sb = s * b;
+    const double cm = __fma_rn(s, -1.0 / 6.0, 1.0 / 3.0);  // -(s - 2) / 6
+    const double a6 = __fma_rn(s, 1.0 / 6.0, 1.0 / 6.0);   // (s + 1) / 6
+    const double hb = __fma_rn(s, 0.5, -0.5);              // (s - 1) / 2
+    const double h2 = __fma_rn(s, hb, -1.0);               // (s + 1)(s - 2) / 2
+    const double w0 = sb * cm, w3 = sb * a6, w1 = h2 * b, w2 = -h2 * s;
+#if GK_SWEEP_TREE
+    g.x = __fma_rn(w1, f1.x, w0 * f0.x) + __fma_rn(w3, f3.x, w2 * f2.x);
+    g.y = __fma_rn(w1, f1.y, w0 * f0.y) + __fma_rn(w3, f3.y, w2 * f2.y);
+#else
+    g.x = __fma_rn(w3, f3.x, __fma_rn(w2, f2.x, __fma_rn(w1, f1.x, w0 * f0.x)));
+    g.y = __fma_rn(w3, f3.y, __fma_rn(w2, f2.y, __fma_rn(w1, f1.y, w0 * f0.y)));
+#endif
+  }
+  if constexpr (WANT_E) {  // linear (evaluator.hpp:22-30)
+    const double2 e0 = W.e[ic], e1 = W.e[ic + 1];
+    e.x = __fma_rn(s, e1.x - e0.x, e0.x);
+    e.y = __fma_rn(s, e1.y - e0.y, e0.y);
+  }
+  if constexpr (KIND == kKindPair) {
+    v = e;
+    vg = g;
+  } else if constexpr (KIND == GK_KIND_GREEN) {
+    v = g;
+  } else {
+    v = e;
+  }
+  if (!ok) table_values<KIND, 3>(r, T, v, vg);
+}
+
 // ------------------------------------------------------------ direct math
 
 // exp(-j k r) from a phase table tab[M] = (cos 2pi i/M, sin 2pi i/M) in
