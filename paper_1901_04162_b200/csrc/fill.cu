@@ -89,14 +89,14 @@ int launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* 
     const double c = k_im / a.K1;
     a.nhi = static_cast<int>(a.K1 * mesh->diameter / kPhaseM) + 2;
     const size_t nhi2 = (static_cast<size_t>(a.nhi) + 1) / 2;  // double2 slots
-    lossy_tab.alloc(kPhaseM + nhi2, ctx->stream);
-    const int nthreads = kPhaseM > a.nhi ? kPhaseM : a.nhi;
+    lossy_tab.alloc(kPhaseSlots + nhi2, ctx->stream);
+    const int nthreads = kPhaseSlots > a.nhi ? kPhaseSlots : a.nhi;
     lossy_phase_kernel<<<(nthreads + 255) / 256, 256, 0, ctx->stream>>>(
-        lossy_tab.p, reinterpret_cast<double*>(lossy_tab.p + kPhaseM), a.nhi, c);
+        lossy_tab.p, reinterpret_cast<double*>(lossy_tab.p + kPhaseSlots), a.nhi, c);
     count_launches(1);
     GK_CUDA(cudaGetLastError());
     a.phase = lossy_tab.p;
-    a.ahi = reinterpret_cast<const double*>(lossy_tab.p + kPhaseM);
+    a.ahi = reinterpret_cast<const double*>(lossy_tab.p + kPhaseSlots);
     a.q1 = c;
     a.q2 = c * c / 2.0;
     a.q3 = c * c * c / 6.0;
@@ -184,10 +184,11 @@ int launch_fill(gk_ctx* ctx, const gk_mesh* mesh, gk_mode mode, const gk_table* 
 // ahi[h] = exp(c M h), c = k_im / K1 (cis_phase_att)
 __global__ void lossy_phase_kernel(double2* tab, double* ahi, int nhi, double c) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < kPhaseM) {
+  if (i < kPhaseSlots) {  // slot i holds angle index i >> kPhaseCopyLog2
+    const int lo = i >> kPhaseCopyLog2;
     double s, co;
-    sincospi(2.0 * i / kPhaseM, &s, &co);
-    const double e = exp(c * i);
+    sincospi(2.0 * lo / kPhaseM, &s, &co);
+    const double e = exp(c * lo);
     tab[i] = make_double2(co * e, s * e);
   }
   if (i < nhi) ahi[i] = exp(c * (static_cast<double>(kPhaseM) * i));
@@ -340,20 +341,22 @@ void launch_range_device(gk_ctx* ctx, const gk_mesh* mesh, size_t row_begin, siz
 
 // ------------------------------------------------------- phase table
 
-__global__ void phase_kernel(double2* tab, int M) {
+// tab[slot] = (cos, sin)(2 pi (slot >> copy_log2) / M)
+__global__ void phase_kernel(double2* tab, int M, int copy_log2) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= M) return;
+  if (i >= (M << copy_log2)) return;
   double s, c;
-  sincospi(2.0 * i / M, &s, &c);
+  sincospi(2.0 * (i >> copy_log2) / M, &s, &c);
   tab[i] = make_double2(c, s);
 }
 
 void init_phase_table(gk_ctx* ctx) {
-  ctx->phase.alloc(kPhaseM, ctx->stream);
-  phase_kernel<<<(kPhaseM + 255) / 256, 256, 0, ctx->stream>>>(ctx->phase.p, kPhaseM);
+  ctx->phase.alloc(kPhaseSlots, ctx->stream);
+  phase_kernel<<<(kPhaseSlots + 255) / 256, 256, 0, ctx->stream>>>(ctx->phase.p, kPhaseM,
+                                                                    kPhaseCopyLog2);
   ctx->phase_small.alloc(kPhaseSmall, ctx->stream);
   phase_kernel<<<(kPhaseSmall + 255) / 256, 256, 0, ctx->stream>>>(ctx->phase_small.p,
-                                                                  kPhaseSmall);
+                                                                  kPhaseSmall, 0);
   count_launches(2);
   GK_CUDA(cudaGetLastError());
 }

@@ -195,8 +195,8 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
   extern __shared__ double2 tab[];  // kPhaseM phase entries (128 KB) [+ attenuation table]
   __shared__ double so[kRowsPerTile][MO][4];
   __shared__ uint64_t bar;
-  stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
-  double* att = reinterpret_cast<double*>(tab + kPhaseM);
+  stage_bulk(tab, A.phase, kPhaseSlots * sizeof(double2), &bar);
+  double* att = reinterpret_cast<double*>(tab + kPhaseSlots);
   if constexpr (ATT == 1)
     for (int i = threadIdx.x; i < A.nhi; i += blockDim.x) att[i] = A.ahi[i];
   if constexpr (ATT == 2)
@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
   extern __shared__ double2 tab[];  // kPhaseM phase entries (128 KB) [+ attenuation table]
   __shared__ double sw[kWarpsV4][MO];
   __shared__ uint64_t bar;
-  stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
-  double* att = reinterpret_cast<double*>(tab + kPhaseM);
+  stage_bulk(tab, A.phase, kPhaseSlots * sizeof(double2), &bar);
+  double* att = reinterpret_cast<double*>(tab + kPhaseSlots);
   if constexpr (ATT == 1)
     for (int i = threadIdx.x; i < A.nhi; i += blockDim.x) att[i] = A.ahi[i];
   if constexpr (ATT == 2)
@@ -423,8 +423,8 @@ __global__ void __launch_bounds__(32 * edge_warps<KIND>(), 1) direct_edge_kernel
   extern __shared__ double2 tab[];  // phase [kPhaseM] | edge sums [W][NS][ecap] | attenuation
   __shared__ double sw[W][MO];
   __shared__ uint64_t bar;
-  stage_bulk(tab, A.phase, kPhaseM * sizeof(double2), &bar);
-  double2* const sE = tab + kPhaseM;
+  stage_bulk(tab, A.phase, kPhaseSlots * sizeof(double2), &bar);
+  double2* const sE = tab + kPhaseSlots;
   double* att = reinterpret_cast<double*>(sE + W * NS * A.ecap);
   if constexpr (ATT == 1)
     for (int i = threadIdx.x; i < A.nhi; i += blockDim.x) att[i] = A.ahi[i];
@@ -1201,7 +1201,7 @@ bool try_sweep(gk_ctx* ctx, const FillArgs& a, size_t budget) {
 template <int MO, int MODE, int KIND, int DEG, int ATT>
 int launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
   if constexpr (MODE == GK_MODE_DIRECT) {
-    const size_t smem = kPhaseM * sizeof(double2) +
+    const size_t smem = kPhaseSlots * sizeof(double2) +
                         (ATT == 1 ? a.nhi * sizeof(double) : 0) +
                         (ATT == 2 ? a.natten * sizeof(double) : 0);
     const bool use_v4 = o.unrolled != 0;
@@ -1209,7 +1209,7 @@ int launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
     // attenuation, n = 1..5; launch_fill leaves nblk = 0 where it does not pay
     if constexpr (ATT != 2) {
       constexpr int W = edge_warps<KIND>();
-      const size_t esmem = kPhaseM * sizeof(double2) +
+      const size_t esmem = kPhaseSlots * sizeof(double2) +
                            W * (KIND == kKindPair ? 2 : 1) * a.ecap * sizeof(double2) +
                            (ATT == 1 ? a.nhi * sizeof(double) : 0);
       // the 227 KB opt-in limit (the pair's two sums per edge at 12 chunks

@@ -51,6 +51,11 @@ constexpr double kMagicRint = 6755399441055744.0; // 1.5 * 2^52
 // 0.00715 D^4 = 1.5e-16 (0.7 ulp of 1) for one DMUL instead of FMA + DMUL.
 constexpr int kPhaseM = 8192;
 constexpr int kPhaseLog2 = 13;
+// table entries per angle (1: one table).  Tried: 8 lane-interleaved copies of
+// a 1024-entry table (conflict-free LDS.128, 2 more FP64 ops for the longer
+// polynomials) -- C5 K4e 502 vs 468 ms, K4 883 vs 799 ms: not adopted
+constexpr int kPhaseCopyLog2 = 0;
+constexpr int kPhaseSlots = kPhaseM << kPhaseCopyLog2;  // table entries (double2)
 // c = -1/2 + b D^2, b = (sqrt 2 - 1)/12: the error x(-1/2 - c) + x^2/24,
 // x = delta^2, equioscillates at x = D^2 and x = -12(-1/2 - c)
 constexpr double kPhaseD = kPi / kPhaseM;
@@ -473,18 +478,29 @@ __device__ __forceinline__ void sweep_values(double r, const SweepWin& W, const 
 //   cos(theta0 + delta) = C0 (1 + v) - S0 s,  sin(theta0 + delta) = S0 (1 + v) + C0 s
 // with v = cos(delta) - 1 = kCosMinimax delta^2 and s = delta - delta^3/6.
 // Returns (Re, -Im) of exp(-j k r) = (cos kr, sin kr): 11 FP64 ops + 1 LDS.128.
-__device__ __forceinline__ double2 cis_phase(double r, double K1, const double2* tab) {
+// table slot of angle index n (the lane's copy in the interleaved layout)
+__device__ __forceinline__ unsigned phase_slot(unsigned n) {
+  return ((n & (kPhaseM - 1)) << kPhaseCopyLog2) | (threadIdx.x & ((1u << kPhaseCopyLog2) - 1u));
+}
+
+// v = cos(delta) - 1 and s = sin(delta) for delta = 2 pi f / M
+__device__ __forceinline__ void phase_poly(double f, double& v, double& s) {
   constexpr double C = 2.0 * kPi / kPhaseM;
+  const double g = __dmul_rn(f, f);
   constexpr double a1 = kCosMinimax * C * C;
   constexpr double s1 = C;
   constexpr double s3 = -C * C * C / 6.0;
+  v = __dmul_rn(a1, g);
+  s = __dmul_rn(f, __fma_rn(s3, g, s1));
+}
+
+__device__ __forceinline__ double2 cis_phase(double r, double K1, const double2* tab) {
   const double t = __fma_rn(r, K1, kMagicRint);
   const double nf = t - kMagicRint;
   const double f = __fma_rn(r, K1, -nf);
-  const int idx = __double2loint(t) & (kPhaseM - 1);
-  const double g = __dmul_rn(f, f);
-  const double v = __dmul_rn(a1, g);
-  const double s = __dmul_rn(f, __fma_rn(s3, g, s1));
+  const unsigned idx = phase_slot(static_cast<unsigned>(__double2loint(t)));
+  double v, s;
+  phase_poly(f, v, s);
   const double2 T = tab[idx];
   const double c = __fma_rn(-T.y, s, __fma_rn(T.x, v, T.x));
   const double sn = __fma_rn(T.x, s, __fma_rn(T.y, v, T.y));
@@ -529,20 +545,15 @@ struct PhaseAtt {
 };
 __device__ __forceinline__ double2 cis_phase_att(double r, double K1, const double2* tab,
                                                  const PhaseAtt& pa, double& att) {
-  constexpr double C = 2.0 * kPi / kPhaseM;
-  constexpr double a1 = kCosMinimax * C * C;
-  constexpr double s1 = C;
-  constexpr double s3 = -C * C * C / 6.0;
   const double t = __fma_rn(r, K1, kMagicRint);
   const double nf = t - kMagicRint;
   const double f = __fma_rn(r, K1, -nf);
   const unsigned n = static_cast<unsigned>(__double2loint(t));
-  const unsigned idx = n & (kPhaseM - 1);
+  const unsigned idx = phase_slot(n);
   unsigned hi = n >> kPhaseLog2;
   hi = hi < static_cast<unsigned>(pa.nhi) ? hi : static_cast<unsigned>(pa.nhi - 1);
-  const double g = __dmul_rn(f, f);
-  const double v = __dmul_rn(a1, g);
-  const double s = __dmul_rn(f, __fma_rn(s3, g, s1));
+  double v, s;
+  phase_poly(f, v, s);
   const double2 T = tab[idx];
   const double c = __fma_rn(-T.y, s, __fma_rn(T.x, v, T.x));
   const double sn = __fma_rn(T.x, s, __fma_rn(T.y, v, T.y));

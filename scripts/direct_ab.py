@@ -1,0 +1,38 @@
+#!/usr/bin/env python3
+"""Direct-fill timings (K4e shared edges and K4 per triangle) on the bench
+configurations, full matrices; for A/B of libgk builds (GK_LIB=...).
+Usage: direct_ab.py [c3 c4 c5] [--reps R]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1901_04162_b200 as gk  # noqa: E402
+
+
+def main():
+    names = [a for a in sys.argv[1:] if a in bench.CONFIGS] or ["c3", "c4", "c5"]
+    reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 3
+    for name in names:
+        cfg = bench.CONFIGS[name]
+        mesh = bench.make_mesh(gk, cfg)
+        N = mesh.triangle_count()
+        dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(cfg["m"], cfg["n"]))
+        med = gk.Medium(lambda0=cfg["lambda0"], eps_r=cfg.get("eps_r", 1.0),
+                        eps_r_im=cfg.get("eps_r_im", 0.0))
+        k = gk.wavenumber(med)
+        Z = torch.empty((N, N), dtype=torch.complex128, device="cuda")
+        for label, opts in (("edge", None), ("pertri", gk.FillOptions(shared_edges=0))):
+            best = None
+            for _ in range(reps):
+                _, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, out=Z, options=opts)
+                best = rep if best is None or rep.wall_time_s < best.wall_time_s else best
+            print(f"{name} {label} {best.path_name}: {best.wall_time_s * 1e3:.2f} ms "
+                  f"({best.evaluations / best.wall_time_s:.3e} performed/s)", flush=True)
+        del Z
+
+
+if __name__ == "__main__":
+    main()
