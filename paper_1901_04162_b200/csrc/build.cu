@@ -217,6 +217,45 @@ __global__ void base_clean_kernel(const int32_t* __restrict__ b2p, long long nba
   bits[w] = word;
 }
 
+// patch flags: every plan interval j overlapping a base interval i whose
+// clean bit is clear (i = 0 .. nbase-2), or the tail [a_{nbase-1}, r_max]
+// (i = nbase-1, with the r_max sentinel n-1), gets flag[j] = 1
+__global__ void patch_flag_kernel(const double* __restrict__ absc, size_t n, double r_min,
+                                  double t_eff, double r_max, long long nbase,
+                                  const uint32_t* __restrict__ bits, uint8_t* __restrict__ flag) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nbase;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const bool tail = i == nbase - 1;
+    if (!tail && ((bits[i >> 5] >> (i & 31)) & 1u)) continue;
+    const double lo = r_min + static_cast<double>(i) * t_eff;
+    const double hi = tail ? r_max : r_min + static_cast<double>(i + 1) * t_eff;
+    // jl: the last node <= lo (the interval holding lo); jh: the last node < hi
+    size_t a = 0, b = n;
+    while (a < b) {
+      const size_t mid = (a + b) / 2;
+      if (absc[mid] <= lo) a = mid + 1;
+      else b = mid;
+    }
+    const size_t jl = a > 0 ? a - 1 : 0;
+    a = jl;
+    b = n;
+    while (a < b) {
+      const size_t mid = (a + b) / 2;
+      if (absc[mid] < hi) a = mid + 1;
+      else b = mid;
+    }
+    const size_t jh = a > 0 ? a - 1 : 0;
+    for (size_t j = jl; j <= jh && j < n; ++j) flag[j] = 1;
+    if (tail) flag[n - 1] = 1;
+  }
+}
+
+__global__ void patch_left_kernel(const double* __restrict__ absc, const uint32_t* __restrict__ pj,
+                                  const int* __restrict__ np, double* __restrict__ pa) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < *np; k += gridDim.x * blockDim.x)
+    pa[k] = absc[pj[k]];
+}
+
 // ---------------------------------------------------------- plan (K2)
 
 struct PlanScalars {
@@ -841,6 +880,40 @@ void build_table_device(gk_ctx* ctx, gk_table* t, const gk_sampling_config& cfg,
     d.bg = t->base_g.p;
     d.be = t->base_e.p;
     d.bclean = t->base_clean.p;
+    d.npatch = 0;
+    if (d.nbase) {  // the non-uniform intervals' list (TableDev::pj / pa)
+      const double* ab = absc.p ? absc.p : t->absc.p;
+      DevBuf<uint8_t> flag;
+      flag.alloc(static_cast<size_t>(n), st);
+      GK_CUDA(cudaMemsetAsync(flag.p, 0, static_cast<size_t>(n), st));
+      patch_flag_kernel<<<grid_for(nbase, 128), 128, 0, st>>>(ab, static_cast<size_t>(n), S.r_min,
+                                                              S.t_eff, cfg.r_max, nbase,
+                                                              t->base_clean.p, flag.p);
+      count_launches(1);
+      GK_CUDA(cudaGetLastError());
+      t->patch_j.alloc(static_cast<size_t>(n), st);
+      DevBuf<int> np;
+      np.alloc(1, st);
+      size_t tb = 0;
+      cub::CountingInputIterator<uint32_t> idx(0u);
+      GK_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, idx, flag.p, t->patch_j.p, np.p,
+                                         static_cast<int>(n), st));
+      DevBuf<char> tmp;
+      tmp.alloc(tb, st);
+      GK_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, idx, flag.p, t->patch_j.p, np.p,
+                                         static_cast<int>(n), st));
+      count_launches(2);
+      t->patch_a.alloc(static_cast<size_t>(n), st);
+      patch_left_kernel<<<grid_for(n, 256), 256, 0, st>>>(ab, t->patch_j.p, np.p, t->patch_a.p);
+      count_launches(1);
+      GK_CUDA(cudaGetLastError());
+      int hnp = 0;
+      GK_CUDA(cudaMemcpyAsync(&hnp, np.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      GK_CUDA(cudaStreamSynchronize(st));
+      d.npatch = static_cast<uint32_t>(hnp);
+    }
+    d.pj = t->patch_j.p;
+    d.pa = t->patch_a.p;
   }
   d.grec = t->grec.p;
   d.erec = t->erec.p;

@@ -90,7 +90,10 @@ __global__ void __launch_bounds__(SMEM ? 1024 : 256)
     }
     __syncthreads();
     mbar_wait(&bar, 0);
-    win = SweepWin{s_v, s_v, s_bits, 0, 0, nbase, -T.r_min * T.inv_t, T.inv_t};
+    // non-uniform intervals read the global records (staging their records
+    // here cost more than it saved in a microsecond kernel: 21.6 vs 15.9 us)
+    win = SweepWin{s_v, s_v, s_bits, 0, 0, nbase, -T.r_min * T.inv_t, T.inv_t,
+                   nullptr, nullptr, nullptr, 0};
   }
   unsigned long long fb = 0;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;

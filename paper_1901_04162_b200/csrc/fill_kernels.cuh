@@ -1126,21 +1126,33 @@ bool launch_table_sweep(gk_ctx* ctx, FillArgs a, size_t budget) {
   constexpr int W = sweep_warps<KIND>();
   constexpr int NS = KIND == kKindPair ? 2 : 1;
   constexpr int NWIN = KIND == kKindPair ? 2 : 1;
-  const size_t fixed = static_cast<size_t>(W) * NS * a.s_ecap * 16 + (2 * kSweepBands + 1) * 4 + 64;
+  constexpr size_t patch_bytes = kSweepPatch * (8 + (KIND != GK_KIND_EXP ? 80 : 0) +
+                                                (KIND != GK_KIND_GREEN ? 48 : 0));
   const size_t limit = 227 * 1024 - 3072;  // opt-in maximum less the static shared memory
-  if (fixed + 4096 > limit) return false;
-  size_t avail = limit - fixed;
-  if (budget >= 4096 && budget < avail) avail = budget;
-  // 16 B per node and window, 1 bit per node
-  size_t wn = (avail * 8) / (128 * NWIN + 1);
-  const size_t whole = (static_cast<size_t>(a.T.nbase) + kSweepMargin + 31) & ~size_t(31);
-  if (wn > whole) wn = whole;
-  wn &= ~size_t(31);
+  // window nodes for a shared-memory budget: 16 B per node and window, 1 bit
+  const auto window_of = [&](size_t fixed) -> size_t {
+    if (fixed + 4096 > limit) return 0;
+    size_t avail = limit - fixed;
+    if (budget >= 4096 && budget < avail) avail = budget;
+    size_t wn = (avail * 8) / (128 * NWIN + 1);
+    const size_t whole = (static_cast<size_t>(a.T.nbase) + kSweepMargin + 31) & ~size_t(31);
+    if (wn > whole) wn = whole;
+    return wn & ~size_t(31);
+  };
+  const size_t base_fixed = static_cast<size_t>(W) * NS * a.s_ecap * 16 +
+                            (((2 * kSweepBands + 1) * 4 + 15) & ~size_t(15)) + 64;
+  // the staged records of non-uniform intervals pay where a window holds at
+  // most kSweepPatch of them (with room to spare)
+  size_t wn = window_of(base_fixed + patch_bytes);
+  const bool patch = a.T.npatch > 0 && wn > 0 &&
+                     static_cast<double>(a.T.npatch) * wn / a.T.nbase <= 0.7 * kSweepPatch;
+  if (!patch) wn = window_of(base_fixed);
+  const size_t fixed = base_fixed + (patch ? patch_bytes : 0);
   const double cap_r = (static_cast<double>(wn) - kSweepMargin) * a.T.t_eff;
   const double spread = 2.0 * (a.s_rho_max + a.s_rho_rows) * (1.0 + 1e-9);
   const double delta = cap_r - spread;
   // keys lie in [-spread / 2, r_max]: the bands of any cluster
-  if (wn < 64 || !(delta >= 0.1 * cap_r) ||
+  if (wn < 64 || !(delta >= 0.05 * cap_r) ||
       (a.T.r_max + spread) / delta + 2.0 > static_cast<double>(kSweepBands))
     return false;
   const size_t nbw = ((wn >> 5) + 8) & ~size_t(3);
@@ -1170,12 +1182,13 @@ bool launch_table_sweep(gk_ctx* ctx, FillArgs a, size_t budget) {
     GK_CUDA(cudaGetLastError());
     return true;
   };
+  const auto pick = [&](auto with, auto without) { return patch ? go(with) : go(without); };
   switch (a.ipt) {
-    case 3: return go(table_sweep_kernel<MO, 1, KIND>);
-    case 6: return go(table_sweep_kernel<MO, 2, KIND>);
-    case 9: return go(table_sweep_kernel<MO, 3, KIND>);
-    case 12: return go(table_sweep_kernel<MO, 4, KIND>);
-    case 15: return go(table_sweep_kernel<MO, 5, KIND>);
+    case 3: return pick(table_sweep_kernel<MO, 1, KIND, true>, table_sweep_kernel<MO, 1, KIND, false>);
+    case 6: return pick(table_sweep_kernel<MO, 2, KIND, true>, table_sweep_kernel<MO, 2, KIND, false>);
+    case 9: return pick(table_sweep_kernel<MO, 3, KIND, true>, table_sweep_kernel<MO, 3, KIND, false>);
+    case 12: return pick(table_sweep_kernel<MO, 4, KIND, true>, table_sweep_kernel<MO, 4, KIND, false>);
+    case 15: return pick(table_sweep_kernel<MO, 5, KIND, true>, table_sweep_kernel<MO, 5, KIND, false>);
     default: return false;
   }
 }
@@ -1281,6 +1294,15 @@ int launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
     // 184 vs 158 ms per 4096 rows)
     if (a.nblk > 0 && automatic && !whole && a.T.nrec * rec_bytes <= 300 * 1024)
       return launch_table_edge<MO, KIND, DEG>(ctx, a);
+    // every larger table: the sweep (K3s, the table in shared memory per
+    // distance band on shared edges) where its window covers a tile.  Full
+    // C5: S = 1e4 1.91 s (K3e 3.54 s), S = 1e3 2.53 s (staged per-triangle
+    // windows 3.16 s); per 8192 rows C3 S = 1e3 102 vs 125 ms
+    // (scripts/sweep_ab.py)
+    if constexpr (kSweepable) {
+      if (automatic && !whole && a.s_nblk > 0 && try_sweep<MO, KIND>(ctx, a, 0))
+        return static_cast<int>(GK_PATH_TABLE_SWEEP);
+    }
     if (whole) {
       S.whole = 1;
       S.lk_cap = static_cast<uint32_t>(nlk4);
@@ -1294,13 +1316,6 @@ int launch_one(gk_ctx* ctx, FillArgs a, const gk_fill_options& o) {
       // fall back to global reads: use the L1 kernel with its wider tiles
       const double est = a.T.nrec * a.window_est / (a.T.r_max - a.T.r_min);
       if (automatic && est > 2.0 * static_cast<double>(j_cap)) {
-        // the sweep (K3s): the table in shared memory per distance band, on
-        // shared edges -- C5 S = 1e4 112 vs 174 ms (K3e) per 4096 rows, C3
-        // 242 vs 328, C4 156 vs 193 (scripts/sweep_ab.py)
-        if constexpr (kSweepable) {
-          if (a.s_nblk > 0 && try_sweep<MO, KIND>(ctx, a, 0))
-            return static_cast<int>(GK_PATH_TABLE_SWEEP);
-        }
         // shared edges (K3e) instead of the L1 kernel: both read the table
         // through L1; K3e 1.3-1.4x faster at S = 1e4 on C3/C4/C5.  Tables
         // staged in shared memory (whole or per tile window) stay per

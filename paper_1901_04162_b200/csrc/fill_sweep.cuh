@@ -51,13 +51,16 @@ constexpr int kSweepRowsPerCluster = GK_SWEEP_RC;  // rows per cluster (<= 32: o
 #ifndef GK_SWEEP_ORDERED
 #define GK_SWEEP_ORDERED 0  // 1: warp-aggregated scatter (a warp's tiles of a band stay in order)
 #endif
-#ifndef GK_SWEEP_TREE
-#define GK_SWEEP_TREE 0  // 1: the four-term sums as two pairs (shorter dependency chain)
-#endif
 #ifndef GK_SWEEP_CHUNK
 #define GK_SWEEP_CHUNK 1  // largest claim (tiles) from a band's list
 #endif
 constexpr int kSweepBands = 512;  // bands per cluster (launch_table_sweep checks the bound)
+// staged records of non-uniform intervals per band: S = 1e4 windows need
+// ~100 (C5); sparser tables (S = 1e3: ~700 per window) read them globally
+#ifndef GK_SWEEP_PATCH
+#define GK_SWEEP_PATCH 128
+#endif
+constexpr int kSweepPatch = GK_SWEEP_PATCH;
 constexpr int kSweepMargin = 16;  // base nodes of the window kept as margin (8 per side)
 
 // lower end of the tile's radii: |c_p - c_b| - rho_p - rho_b
@@ -67,7 +70,7 @@ __device__ __forceinline__ double sweep_key(const EdgeBlock* eb, size_t b, doubl
   return sqrt(dx * dx + dy * dy + dz * dz) - B.rho - cp.w;
 }
 
-template <int MO, int NPE, int KIND>
+template <int MO, int NPE, int KIND, bool PATCH>
 __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kernel(const FillArgs A) {
   constexpr int W = sweep_warps<KIND>();
   constexpr bool WANT_G = KIND != GK_KIND_EXP, WANT_E = KIND != GK_KIND_GREEN;
@@ -87,6 +90,14 @@ __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kerne
   sp += static_cast<size_t>(W) * NS * A.ecap * 16;
   int* const s_off = reinterpret_cast<int*>(sp);  // [kSweepBands + 1] band offsets
   int* const s_cur = s_off + kSweepBands + 1;     // [kSweepBands] scatter / claim cursors
+  sp += ((2 * kSweepBands + 1) * 4 + 15) & ~15;
+  // the non-uniform intervals' records (TableDev::pj)
+  double* const s_pa = reinterpret_cast<double*>(sp);
+  if (PATCH) sp += kSweepPatch * 8;
+  double* const s_pg = reinterpret_cast<double*>(sp);
+  if (PATCH && WANT_G) sp += kSweepPatch * 80;
+  double* const s_pe = reinterpret_cast<double*>(sp);
+  __shared__ int s_pk[2];
   __shared__ double sw[W][MO];
   __shared__ uint64_t bar;
   __shared__ double s_red[W][2];
@@ -98,8 +109,11 @@ __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kerne
   const int nbase = static_cast<int>(A.T.nbase);
   const int nwords = (((nbase + 31) >> 5) + 8) & ~3;  // allocated bit words
   uint32_t* const glist = A.s_list + static_cast<size_t>(blockIdx.x) * RC * A.nblk;
-  SweepWin win{s_g, s_e, s_bits, 0, 0, wn, -A.T.r_min * A.T.inv_t, A.T.inv_t};
-  const auto vals = [&](double r, double2& v, double2& vg) { sweep_values<KIND>(r, win, A.T, v, vg); };
+  SweepWin win{s_g, s_e, s_bits, 0, 0, wn, -A.T.r_min * A.T.inv_t, A.T.inv_t,
+               s_pa, s_pg, s_pe, 0};
+  const auto vals = [&](double r, double2& v, double2& vg) {
+    sweep_values<KIND, false, PATCH>(r, win, A.T, v, vg);
+  };
   unsigned long long nev = 0, n_low = 0, n_high = 0;
   if (threadIdx.x == 0) mbar_init(&bar);
   __syncthreads();
@@ -218,6 +232,14 @@ __global__ void __launch_bounds__(32 * sweep_warps<KIND>(), 1) table_sweep_kerne
         if (WANT_G) tma_load_1d(s_g, A.T.bg + i0, nn * 16u, &bar);
         if (WANT_E) tma_load_1d(s_e, A.T.be + i0, nn * 16u, &bar);
         tma_load_1d(s_bits, A.T.bclean + w0, nw * 4u, &bar);
+      }
+      // the non-uniform intervals' records the window's radii can meet
+      if (PATCH) {
+        win.np = stage_patches<WANT_G, WANT_E>(
+            A.T, A.T.r_min + i0 * A.T.t_eff,
+            i0 + win.wn >= nbase ? A.T.r_max : A.T.r_min + (i0 + win.wn) * A.T.t_eff,
+            kSweepPatch, s_pa, s_pg, s_pe, s_pk);
+        __syncthreads();
       }
       mbar_wait(&bar, phase);
       phase ^= 1u;

@@ -89,6 +89,13 @@ struct TableDev {
   const double2* be;
   const uint32_t* bclean;  // nbase / 32 + 8 words (zero-padded)
   uint32_t nbase;
+  // the plan intervals overlapping a base interval whose bit is clear (and the
+  // tail [a_{nbase-1}, r_max] with the r_max sentinel): pj[k] = plan interval,
+  // pa[k] = its left node, ascending -- the sweep stages their records so
+  // that non-uniform stencils are read from shared memory too
+  const uint32_t* pj;
+  const double* pa;
+  uint32_t npatch;
 };
 
 // Shared-edge fills (direct_edge_kernel, table_edge_kernel; edges.cu): a
@@ -400,7 +407,95 @@ struct SweepWin {
   const uint32_t* bits;  // clean bits, words w0 ..
   int i0, w0, wn;
   double x0, inv_t;  // x = fma(r, inv_t, x0) = (r - r_min) / t_eff
+  // staged patch records (TableDev::pj / pa): np intervals with left nodes
+  // pa[], Green records pg[] (10 doubles: a_j, a_j+1, c0..c3) and Exp records
+  // pe[] (6 doubles: a_j, a_j+1, e_j, slope)
+  const double* pa;
+  const double* pg;
+  const double* pe;
+  int np;
 };
+
+// the staged record of the plan interval holding r, evaluated exactly like
+// the global records (green_table<3> / exp_table / pair_table<3>: same
+// record, same operations, so the same bits); false when no staged record
+// holds r (the caller reads the global records)
+template <int KIND>
+__device__ __forceinline__ bool patch_values(double r, const SweepWin& W, double2& v, double2& vg) {
+  constexpr bool WANT_G = KIND != GK_KIND_EXP, WANT_E = KIND != GK_KIND_GREEN;
+  int lo = 0, hi = W.np;  // first staged record with pa > r
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (W.pa[mid] <= r) lo = mid + 1;
+    else hi = mid;
+  }
+  const int k = lo - 1;
+  if (k < 0) return false;
+  const double* rg = W.pg + 10 * k;
+  const double* re = W.pe + 6 * k;
+  if (!(r < (WANT_G ? rg[1] : re[1]))) return false;
+  const double u = r - W.pa[k];
+  double2 e = make_double2(0.0, 0.0), g = make_double2(0.0, 0.0);
+  if constexpr (WANT_E) {
+    e.x = __fma_rn(re[4], u, re[2]);
+    e.y = __fma_rn(re[5], u, re[3]);
+  }
+  if constexpr (WANT_G) {
+    g = make_double2(rg[8], rg[9]);
+#pragma unroll
+    for (int c = 2; c >= 0; --c) {
+      g.x = __fma_rn(g.x, u, rg[2 + 2 * c]);
+      g.y = __fma_rn(g.y, u, rg[3 + 2 * c]);
+    }
+  }
+  if constexpr (KIND == kKindPair) {
+    v = e;
+    vg = g;
+  } else if constexpr (KIND == GK_KIND_GREEN) {
+    v = g;
+  } else {
+    v = e;
+  }
+  return true;
+}
+
+// stage the patch records a window of radii [a_lo, a_hi] can need (all of
+// them, or none when they exceed cap) into pa / pg / pe; every thread of the CTA calls it, a __syncthreads
+// follows before use.  Returns the count (the same in every thread).
+template <bool WANT_G, bool WANT_E>
+__device__ __forceinline__ int stage_patches(const TableDev& T, double a_lo, double a_hi, int cap,
+                                             double* pa, double* pg, double* pe, int* s_k) {
+  if (threadIdx.x == 0) {
+    const int n = static_cast<int>(T.npatch);
+    int lo = 0, hi = n;  // first k with pa > a_lo
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (T.pa[mid] <= a_lo) lo = mid + 1;
+      else hi = mid;
+    }
+    const int k0 = lo > 0 ? lo - 1 : 0;
+    hi = n;  // first k with pa > a_hi
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (T.pa[mid] <= a_hi) lo = mid + 1;
+      else hi = mid;
+    }
+    const int cnt = lo - k0;
+    s_k[0] = k0;
+    s_k[1] = cnt <= cap ? cnt : 0;  // all or none: a partial list costs its misses a search
+  }
+  __syncthreads();
+  const int k0 = s_k[0], cnt = s_k[1];
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) pa[i] = T.pa[k0 + i];
+  if (WANT_G)
+    for (int i = threadIdx.x; i < 10 * cnt; i += blockDim.x)
+      pg[i] = T.grec[static_cast<size_t>(T.pj[k0 + i / 10]) * 10 + i % 10];
+  if (WANT_E)
+    for (int i = threadIdx.x; i < 6 * cnt; i += blockDim.x)
+      pe[i] = T.erec[static_cast<size_t>(T.pj[k0 + i / 6]) * 6 + i % 6];
+  return cnt;
+}
+
 
 // K(r) for the kind through the window, or the global records where the
 // interval is not a uniform stencil inside the window
@@ -408,7 +503,11 @@ struct SweepWin {
 // arith_locate), so that s = 0 exactly at a node and nodes are reproduced
 // exactly (evaluator.hpp:259-262; the standalone eval_batch); the fills
 // need only the tolerance and take s from x = (r - r_min) / t_eff directly
-template <int KIND, bool EXACT = false>
+// PATCH: non-uniform intervals first look for a staged record (the window
+// stages them when they are few, S = 1e4); without it they go straight to
+// the global records (dense zero windows, S = 1e3: the lookup would cost more
+// than it saves -- C3 S = 1e3 102 vs 136 ms per 8192 rows)
+template <int KIND, bool EXACT = false, bool PATCH = false>
 __device__ __forceinline__ void sweep_values(double r, const SweepWin& W, const TableDev& T,
                                              double2& v, double2& vg) {
   constexpr bool WANT_G = KIND != GK_KIND_EXP, WANT_E = KIND != GK_KIND_GREEN;
@@ -430,10 +529,10 @@ __device__ __forceinline__ void sweep_values(double r, const SweepWin& W, const 
     s = x - (yv - kMagic52);  // in [0, 1)
   }
   const int ii = i - W.i0;
-  bool ok = static_cast<unsigned>(ii - 1) < static_cast<unsigned>(W.wn - 4);
-  const int ic = ok ? ii : 1;  // clamped: the window reads stay in bounds
+  const bool win = static_cast<unsigned>(ii - 1) < static_cast<unsigned>(W.wn - 4);
+  const int ic = win ? ii : 1;  // clamped: the window reads stay in bounds
   const int ia = W.i0 + ic;
-  ok = ok && ((W.bits[(ia >> 5) - W.w0] >> (ia & 31)) & 1u);
+  const bool ok = win && ((W.bits[(ia >> 5) - W.w0] >> (ia & 31)) & 1u);
   double2 g = make_double2(0.0, 0.0), e = make_double2(0.0, 0.0);
   if constexpr (WANT_G) {
     // uniform cubic Lagrange weights on nodes -1, 0, 1, 2
@@ -446,13 +545,8 @@ __device__ __forceinline__ void sweep_values(double r, const SweepWin& W, const 
     const double hb = __fma_rn(s, 0.5, -0.5);              // (s - 1) / 2
     const double h2 = __fma_rn(s, hb, -1.0);               // (s + 1)(s - 2) / 2
     const double w0 = sb * cm, w3 = sb * a6, w1 = h2 * b, w2 = -h2 * s;
-#if GK_SWEEP_TREE
-    g.x = __fma_rn(w1, f1.x, w0 * f0.x) + __fma_rn(w3, f3.x, w2 * f2.x);
-    g.y = __fma_rn(w1, f1.y, w0 * f0.y) + __fma_rn(w3, f3.y, w2 * f2.y);
-#else
     g.x = __fma_rn(w3, f3.x, __fma_rn(w2, f2.x, __fma_rn(w1, f1.x, w0 * f0.x)));
     g.y = __fma_rn(w3, f3.y, __fma_rn(w2, f2.y, __fma_rn(w1, f1.y, w0 * f0.y)));
-#endif
   }
   if constexpr (WANT_E) {  // linear (evaluator.hpp:22-30)
     const double2 e0 = W.e[ic], e1 = W.e[ic + 1];
@@ -467,7 +561,11 @@ __device__ __forceinline__ void sweep_values(double r, const SweepWin& W, const 
   } else {
     v = e;
   }
-  if (!ok) table_values<KIND, 3>(r, T, v, vg);
+  if constexpr (PATCH) {
+    if (!ok && !(win && patch_values<KIND>(r, W, v, vg))) table_values<KIND, 3>(r, T, v, vg);
+  } else {
+    if (!ok) table_values<KIND, 3>(r, T, v, vg);
+  }
 }
 
 // ------------------------------------------------------------ direct math

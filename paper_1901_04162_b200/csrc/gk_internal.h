@@ -140,6 +140,8 @@ struct gk_table {
   gk::DevBuf<int32_t> coarse;  // arithmetic-locate runs (TableDev::coarse)
   gk::DevBuf<double2> base_g, base_e;  // table sweep: node values by base index (TableDev::bg / be)
   gk::DevBuf<uint32_t> base_clean;     // table sweep: uniform-stencil bits (TableDev::bclean)
+  gk::DevBuf<uint32_t> patch_j;        // table sweep: non-uniform intervals (TableDev::pj)
+  gk::DevBuf<double> patch_a;          // ... their left nodes (TableDev::pa)
   std::vector<double> zeros;  // zero_locations (host copy)
 };
 
