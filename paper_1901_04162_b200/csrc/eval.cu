@@ -45,7 +45,7 @@ __device__ __forceinline__ double2 eval_value(double r, size_t i, const TableDev
     }
     if (bad == V_OK) {
       if constexpr (FAST) {
-        const double2 cs = cis_phase_small(r, K1s, ptab);  // (cos kr, sin kr)
+        const double2 cs = cis_phase_small<!TABLE>(r, K1s, ptab);  // (cos kr, sin kr)
         v = make_double2(cs.x, -cs.y);
         if (KIND == GK_KIND_GREEN) {
           const double y = __drcp_rn(r);
@@ -63,8 +63,13 @@ __device__ __forceinline__ double2 eval_value(double r, size_t i, const TableDev
 
 // K5: RPT radii per thread, all loaded before any is evaluated (the stream's
 // bytes in flight), evict-first loads and stores; one wave of CTAs
+#ifndef GK_EVAL_FAST_THREADS
+#define GK_EVAL_FAST_THREADS 512  // direct eval_batch CTA (the phase table staged per CTA)
+#endif
+constexpr int kEvalFastThreads = GK_EVAL_FAST_THREADS;
+
 template <int KIND, bool TABLE, int DEG, bool FAST, bool SMEM, int RPT>
-__global__ void __launch_bounds__(SMEM ? 1024 : 256)
+__global__ void __launch_bounds__(SMEM ? 1024 : (FAST ? kEvalFastThreads : 256))
     eval_batch_kernel(const double* __restrict__ radii, size_t n, double2* __restrict__ out,
                       TableDev T, double k_re, double k_im, unsigned long long* w,
                       const double2* __restrict__ ptab, double K1s) {
@@ -73,6 +78,21 @@ __global__ void __launch_bounds__(SMEM ? 1024 : 256)
   // stream be scheduled now, and wait for the previous one's memory before
   // reading -- back-to-back batches overlap launch and tail
   asm volatile("griddepcontrol.launch_dependents;");
+  if constexpr (FAST) {
+    // the 16 KB phase table into shared memory: random 16-byte gathers cost
+    // ~9 wavefronts per warp there against up to 32 through L1.  It is made
+    // once per context, so it is staged before waiting on the previous launch
+    __shared__ uint64_t pbar;
+    double2* const s_tab = reinterpret_cast<double2*>(smem);
+    if (threadIdx.x == 0) {
+      mbar_init(&pbar);
+      mbar_expect_tx(&pbar, kPhaseSmall * 16u);
+      tma_load_1d(s_tab, ptab, kPhaseSmall * 16u, &pbar);
+    }
+    __syncthreads();
+    mbar_wait(&pbar, 0);
+    ptab = s_tab;
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   SweepWin win{};
   if constexpr (SMEM) {
@@ -174,8 +194,9 @@ void launch_eval_kind(gk_ctx* ctx, const gk_table* t, const double* r, size_t n,
                                static_cast<size_t>((((T.nbase + 31) >> 5) + 8) & ~3u) * 4
                          : 0;
   if (!t && k_im == 0.0 && fast_eval(ctx)) {
-    launch_pdl(eval_batch_kernel<KIND, false, 0, true, false, RPT>, grid_of(256, 8, RPT), 256, 0, st,
-               r, n, out, T, k_re, k_im, w, ptab, K1s);
+    constexpr int FT = kEvalFastThreads;
+    launch_pdl(eval_batch_kernel<KIND, false, 0, true, false, RPT>, grid_of(FT, 2048 / FT, RPT),
+               FT, kPhaseSmall * 16, st, r, n, out, T, k_re, k_im, w, ptab, K1s);
   } else if (!t) {
     launch_pdl(eval_batch_kernel<KIND, false, 0, false, false, RPT>, grid_of(256, 8, RPT), 256, 0, st,
                r, n, out, T, k_re, k_im, w, ptab, K1s);

@@ -610,6 +610,9 @@ __device__ __forceinline__ double2 cis_phase(double r, double K1, const double2*
 // microsecond kernel): |delta| <= pi/1024, cos delta - 1 to delta^4 and
 // sin delta to delta^5 (dropped terms < 1.2e-18).  13 FP64 ops.
 constexpr int kPhaseSmall = 1024;
+// SMEM_TAB: tab is the table staged in shared memory (a plain load; __ldg
+// would issue a global load on a shared address)
+template <bool SMEM_TAB = false>
 __device__ __forceinline__ double2 cis_phase_small(double r, double K1s, const double2* tab) {
   constexpr double C = 2.0 * kPi / kPhaseSmall;
   constexpr double a1 = -C * C / 2.0, a2 = C * C * C * C / 24.0;
@@ -621,7 +624,7 @@ __device__ __forceinline__ double2 cis_phase_small(double r, double K1s, const d
   const double g = __dmul_rn(f, f);
   const double v = __dmul_rn(g, __fma_rn(a2, g, a1));
   const double s = __dmul_rn(f, __fma_rn(__fma_rn(s5, g, s3), g, s1));
-  const double2 T = __ldg(tab + idx);
+  const double2 T = SMEM_TAB ? tab[idx] : __ldg(tab + idx);
   const double c = __fma_rn(-T.y, s, __fma_rn(T.x, v, T.x));
   const double sn = __fma_rn(T.x, s, __fma_rn(T.y, v, T.y));
   return make_double2(c, sn);
