@@ -149,7 +149,7 @@ typedef struct gk_mesh_options {
   int edge_order;    /* GK_AUTO: the more compact; 0: mesh order; 1: bisection order */
   int leaf_pct;      /* bisection leaf size in percent of the edge cap, 30..100 (0 / GK_AUTO: 61) */
   int sweep_chunks;  /* chunks per block of the table sweep's second, smaller block
-                        set (DESIGN.md §5 K3s), 1..12 (0 / GK_AUTO: 1) */
+                        set (DESIGN.md §5 K3s), 1..12 (0 / GK_AUTO: 2) */
 } gk_mesh_options;
 void gk_mesh_options_init(gk_mesh_options* opts);
 
@@ -317,9 +317,11 @@ gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out);
    block-local edge index of each side of the triangle at each position;
    block_start[nt + 1] = first position of each block followed by nt;
    block_edges[nt] = distinct edges of each block; *nblocks; *ordered.
-   leaf_pct: bisection leaf size in percent of the edge cap (0: 61). */
+   leaf_pct: bisection leaf size in percent of the edge cap (0: 61); rho_cap > 0:
+   bisection leaves wider than rho_cap (vertex radius) are split too. */
 gk_status gk_edge_blocks_plan(const double* vertices, size_t nv, const uint32_t* triangles,
-                              size_t nt, int chunks, int order_mode, int leaf_pct, uint32_t* order,
+                              size_t nt, int chunks, int order_mode, int leaf_pct,
+                              double rho_cap, uint32_t* order,
                               uint32_t* edge_index, uint32_t* block_start,
                               uint32_t* block_edges, uint64_t* nblocks, int* ordered);
 

@@ -148,8 +148,8 @@ PROTOTYPES = {
     "gk_mesh_points_download": [_vp, _vp, _vp],
     "gk_mesh_destroy": [_vp],
     "gk_mesh_edge_info_get": [_vp, _vp],
-    "gk_edge_blocks_plan": [_vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.c_int, _vp, _vp,
-                            _vp,
+    "gk_edge_blocks_plan": [_vp, C.c_size_t, _vp, C.c_size_t, C.c_int, C.c_int, C.c_int,
+                            C.c_double, _vp, _vp, _vp,
                             _vp, _u64p, C.POINTER(C.c_int)],
     "gk_distance_range": [_vp, _vp, C.c_size_t, C.c_size_t, _dp, _dp],
     "gk_fill_rows": [_vp, _vp, C.c_int, _vp, C.c_int, C.c_double, C.c_double, C.c_size_t,

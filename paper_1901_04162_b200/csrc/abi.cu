@@ -762,8 +762,8 @@ gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out) {
 }
 
 gk_status gk_edge_blocks_plan(const double* verts, size_t nv, const uint32_t* tris, size_t nt,
-                              int chunks, int order_mode, int leaf_pct, uint32_t* order,
-                              uint32_t* edge_index,
+                              int chunks, int order_mode, int leaf_pct, double rho_cap,
+                              uint32_t* order, uint32_t* edge_index,
                               uint32_t* block_start, uint32_t* block_edges, uint64_t* nblocks,
                               int* ordered) {
   return guarded([&] {
@@ -775,7 +775,7 @@ gk_status gk_edge_blocks_plan(const double* verts, size_t nv, const uint32_t* tr
     gk::validate_mesh(verts, nv, tris, nt);
     need(nt >= 1, GK_ERR_INVALID_ARGUMENT, "empty mesh");
     const gk::EdgePlan P = gk::plan_edge_blocks(verts, nv, tris, nt, 32 * static_cast<size_t>(chunks),
-                                                order_mode, leaf_pct);
+                                                order_mode, leaf_pct, rho_cap);
     for (size_t j = 0; j < nt; ++j) {
       order[j] = P.order[j];
       edge_index[3 * j] = P.eidx[j].x;

@@ -84,7 +84,7 @@ __global__ void edge_delta_kernel(const double4* __restrict__ inner, size_t N, i
 }  // namespace
 
 EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, size_t N,
-                          size_t cap, int order_mode, int leaf_pct) {
+                          size_t cap, int order_mode, int leaf_pct, double rho_cap) {
   // global edge ids: edges bucketed by their lower vertex (CSR), distinct
   // upper vertices numbered within each bucket
   std::vector<uint32_t> start(nv + 1, 0);
@@ -250,6 +250,24 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
         }
       return cnt;
     };
+    // bounding radius of the vertices of triangles sorder[lo, hi) about their
+    // mean (the block radius of make_blocks, without its rounding margin)
+    auto rho_of = [&](size_t lo, size_t hi) {
+      double c[3] = {0.0, 0.0, 0.0};
+      for (size_t j = lo; j < hi; ++j)
+        for (int s = 0; s < 3; ++s)
+          for (int d = 0; d < 3; ++d)
+            c[d] += verts[3 * static_cast<size_t>(tris[3 * static_cast<size_t>(sorder[j]) + s]) + d];
+      for (double& x : c) x /= 3.0 * static_cast<double>(hi - lo);
+      double rho = 0.0;
+      for (size_t j = lo; j < hi; ++j)
+        for (int s = 0; s < 3; ++s) {
+          const double* v = verts + 3 * static_cast<size_t>(tris[3 * static_cast<size_t>(sorder[j]) + s]);
+          const double dx = v[0] - c[0], dy = v[1] - c[1], dz = v[2] - c[2];
+          rho = std::max(rho, std::sqrt(dx * dx + dy * dy + dz * dz));
+        }
+      return rho;
+    };
     // leaf triangles per edge slot, percent (~1.6 edges per triangle);
     // gk_mesh_options.leaf_pct for A/B
     const size_t tfrac = leaf_pct >= 30 && leaf_pct <= 100 ? static_cast<size_t>(leaf_pct) : 61;
@@ -261,7 +279,7 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
       const size_t c = hi - lo;
       size_t mid;
       if (c <= T) {
-        if (edges_of(lo, hi) <= cap || c == 1) {
+        if ((edges_of(lo, hi) <= cap && (rho_cap <= 0.0 || rho_of(lo, hi) <= rho_cap)) || c == 1) {
           cuts.push_back(lo);
           continue;
         }
@@ -308,12 +326,21 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
 namespace {
 
 // one block set of at most `cap` distinct edges per block into S
+// rho_cap_rel > 0: leaves whose radius exceeds rho_cap_rel x the mean block
+// radius of an uncapped plan are split (a second plan): the table sweep's
+// window must cover the largest block's radius spread
 void build_edge_set(const gk_mesh* mesh, const double* verts, const uint32_t* tris, size_t cap,
-                    int order_mode, int leaf_pct, EdgeSet& S) {
+                    int order_mode, int leaf_pct, EdgeSet& S, double rho_cap_rel = 0.0) {
   const size_t N = mesh->N, nv = mesh->nv;
   const int n = mesh->n;
   S.ecap = static_cast<int>(cap);
   EdgePlan R = plan_edge_blocks(verts, nv, tris, N, cap, order_mode, leaf_pct);
+  if (rho_cap_rel > 0.0 && R.ordered) {
+    double rmax = 0.0;
+    for (const EdgeBlock& B : R.blocks) rmax = std::max(rmax, B.rho);
+    if (rmax > rho_cap_rel * R.rho_mean)
+      R = plan_edge_blocks(verts, nv, tris, N, cap, order_mode, leaf_pct, rho_cap_rel * R.rho_mean);
+  }
   const std::vector<EdgeBlock>& blocks = R.blocks;
   const std::vector<unsigned long long>& owner = R.owner;
 
@@ -390,7 +417,7 @@ void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,
   size_t scap = 32 * kSweepChunksDefault;
   if (opts.sweep_chunks >= 1 && opts.sweep_chunks * 32 <= kEdgeCap)
     scap = static_cast<size_t>(opts.sweep_chunks) * 32;
-  build_edge_set(mesh, verts, tris, scap, 1, kSweepLeafPct, mesh->sweep);
+  build_edge_set(mesh, verts, tris, scap, 1, kSweepLeafPct, mesh->sweep, kSweepRhoCap);
 }
 
 }  // namespace gk

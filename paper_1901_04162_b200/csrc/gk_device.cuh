@@ -111,8 +111,9 @@ struct TableDev {
 // L1 for the block's points (12 chunks: 228 KB carveout, 28 KB of L1).
 constexpr int kEdgeCap = 384;
 constexpr int kEdgeChunksDefault = 11;
-constexpr int kSweepChunksDefault = 1;  // the table sweep's block set (K3s)
+constexpr int kSweepChunksDefault = 2;  // the table sweep's block set (K3s)
 constexpr int kSweepLeafPct = 50;      // its bisection leaves: 50 % of the edge cap
+constexpr double kSweepRhoCap = 1.2;   // and no leaf wider than 1.2x the mean block radius
 struct EdgeBlock {
   uint32_t tb, te, c0, ne;
   double cx, cy, cz, rho;

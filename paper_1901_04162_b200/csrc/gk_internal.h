@@ -226,7 +226,7 @@ struct EdgePlan {
   bool ordered = false;
 };
 EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, size_t N,
-                          size_t cap, int order_mode, int leaf_pct = 0);
+                          size_t cap, int order_mode, int leaf_pct = 0, double rho_cap = 0.0);
 // the device part for a mesh whose points launch_points has produced;
 // synchronises the context stream
 void build_edge_blocks(gk_mesh* mesh, const double* verts, const uint32_t* tris,

@@ -218,7 +218,7 @@ class MeshOptions:
     edge_chunks: int = 0                  # 0: 11
     edge_order: int = _lib.GK_AUTO        # 0: mesh order, 1: bisection order
     leaf_pct: int = 0                     # 0: 61
-    sweep_chunks: int = 0                 # 0: 1 (the table sweep's block set)
+    sweep_chunks: int = 0                 # 0: 2 (the table sweep's block set)
 
     def c(self) -> _lib.MeshOptionsC:
         return _lib.MeshOptionsC(self.shared_edges, self.edge_chunks, self.edge_order,
@@ -517,7 +517,7 @@ def eval_batch_async(kind: KernelKind, radii, out, status: EvalStatus,
 
 
 def edge_blocks_plan(mesh: TriangleMesh, chunks: int = 11, order_mode: int = -1,
-                     leaf_pct: int = 0) -> dict:
+                     leaf_pct: int = 0, rho_cap: float = 0.0) -> dict:
     """The host part of the shared-edge blocks (gk_edge_blocks_plan; no
     device needed): block positions, triangle order and block-local edge
     indices."""
@@ -530,7 +530,8 @@ def edge_blocks_plan(mesh: TriangleMesh, chunks: int = 11, order_mode: int = -1,
     ordered = C.c_int()
     check(lib().gk_edge_blocks_plan(mesh.vertices.ctypes.data, mesh.vertices.shape[0],
                                     mesh.triangles.ctypes.data, nt, chunks, order_mode,
-                                    leaf_pct, order.ctypes.data, eidx.ctypes.data, start.ctypes.data,
+                                    leaf_pct, rho_cap, order.ctypes.data, eidx.ctypes.data,
+                                    start.ctypes.data,
                                     nedge.ctypes.data, C.byref(nb), C.byref(ordered)),
           "edge_blocks_plan")
     n = nb.value

@@ -176,8 +176,13 @@ def test_sweep_dispatch_by_table_density(gk, ctx_edges):
     """GK_AUTO: a dense table (S = 1e4 here) goes to the sweep, a table staged
     whole stays per triangle (S = 300); GK_TABLE_GLOBAL keeps K3e"""
     mesh = sphere(gk, 3)
-    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
+    # one-chunk sweep blocks: the L3 sphere's two-chunk blocks (rho 0.6 m) are
+    # too wide for a window at S = 1e4, lambda = 1 (the dispatch then takes K3e)
+    dm = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4), options=gk.MeshOptions(sweep_chunks=1))
+    dm2 = gk.DeviceMesh(mesh, gk.QuadratureSpec(6, 4))
     lo, hi = dm.distance_range()
+    t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=10000))
+    assert gk.fill_rows(dm2, gk.Mode.TABLE, table=t)[1].path_name == "table_edge"
     for S, want in ((10000, "table_sweep"), (300, "table_staged")):
         t = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=S))
         _, rep = gk.fill_rows(dm, gk.Mode.TABLE, table=t)
