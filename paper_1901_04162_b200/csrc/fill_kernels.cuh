@@ -46,19 +46,23 @@ struct Acc {
       if constexpr (PAIR) g[o] = make_double2(0.0, 0.0);
     }
   }
-  // acc += w * (c - j s) for kind KIND; y = 1/r for the Green weight
+  // acc += w (1 + v) (c - j s) for kind KIND (the tan form of the rotation,
+  // cis_phase_tan: cos(delta) = 1 + v goes into the weight); y = 1/r
   template <int KIND>
-  __device__ __forceinline__ void add(int o, double w, double y, double2 cs) {
+  __device__ __forceinline__ void add_tan(int o, double w, double y, double c, double s, double v) {
     if constexpr (KIND == kKindPair) {
-      e[o].x = __fma_rn(w, cs.x, e[o].x);
-      e[o].y = __fma_rn(-w, cs.y, e[o].y);
-      const double wg = __dmul_rn(w, y);
-      g[o].x = __fma_rn(wg, cs.x, g[o].x);
-      g[o].y = __fma_rn(-wg, cs.y, g[o].y);
+      const double we = __fma_rn(w, v, w);
+      e[o].x = __fma_rn(we, c, e[o].x);
+      e[o].y = __fma_rn(-we, s, e[o].y);
+      const double b = __dmul_rn(w, y);
+      const double wg = __fma_rn(b, v, b);
+      g[o].x = __fma_rn(wg, c, g[o].x);
+      g[o].y = __fma_rn(-wg, s, g[o].y);
     } else {
-      const double wk = KIND == GK_KIND_GREEN ? __dmul_rn(w, y) : w;
-      e[o].x = __fma_rn(wk, cs.x, e[o].x);
-      e[o].y = __fma_rn(-wk, cs.y, e[o].y);
+      const double b = KIND == GK_KIND_GREEN ? __dmul_rn(w, y) : w;
+      const double wk = __fma_rn(b, v, b);
+      e[o].x = __fma_rn(wk, c, e[o].x);
+      e[o].y = __fma_rn(-wk, s, e[o].y);
     }
   }
   // acc += w * v (table values: v = K(r) for the kind, vg = Green for the pair)
@@ -185,8 +189,9 @@ __device__ __forceinline__ void stage_bulk(void* dst, const void* src, uint32_t 
   mbar_wait(bar, 0);
 }
 
-// K4: direct evaluation.  Per eval: 6 (r^2) + 6 (rsqrt, r) + 11 (phase,
-// table lookup, complex combine) + 3 (weight, accumulate) = 26 FP64 ops.
+// K4: direct evaluation.  Per eval: 6 (r^2) + 6 (rsqrt, r) + 8 (phase, table
+// lookup, rotation in the tan form) + 4 (weight with cos(delta), accumulate)
+// = 25 FP64 ops.
 // The warp's outer points sit in shared memory (broadcast loads, one
 // wavefront each) instead of registers, so ~80 registers per thread allow 3
 // CTAs (24 warps) per SM to hide the FP64 dependency latency.
@@ -250,16 +255,16 @@ __global__ void __launch_bounds__(kThreads, MINB) direct_kernel(const FillArgs A
         const double y = rsqrt_fast(d2);
         const double r = radius_of<KIND>(d2, y);
         double w = pzw.y;
-        double2 cs;  // (cos kr, sin kr)
+        double c, sn, v;  // (cos kr, sin kr) / (1 + v)
         if constexpr (ATT == 1) {
           double a;
-          cs = cis_phase_att(r, A.K1, tab, pa, a);
+          cis_phase_att_tan(r, A.K1, tab, pa, a, c, sn, v);
           w = __dmul_rn(w, a);
         } else {
-          cs = cis_phase(r, A.K1, tab);
+          cis_phase_tan(r, A.K1, tab, c, sn, v);
           if constexpr (ATT == 2) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
         }
-        acc.template add<KIND>(o, w, y, cs);
+        acc.template add_tan<KIND>(o, w, y, c, sn, v);
       }
       if (block_done) {  // column block complete: finish the entry
         acc.finish([&](int o) { return my[o][3]; }, qc == p, vc, A.z, A.z2,
@@ -343,16 +348,16 @@ __global__ void __launch_bounds__(32 * warps_v4<KIND>(), 1) direct_kernel_v4(con
           const double y = rsqrt_fast(d2);
           const double r = radius_of<KIND>(d2, y);
           double w = pzw.y;
-          double2 cs;  // (cos kr, sin kr)
+          double c, sn, v;  // (cos kr, sin kr) / (1 + v)
           if constexpr (ATT == 1) {
             double a;
-            cs = cis_phase_att(r, A.K1, tab, pa, a);
+            cis_phase_att_tan(r, A.K1, tab, pa, a, c, sn, v);
             w = __dmul_rn(w, a);
           } else {
-            cs = cis_phase(r, A.K1, tab);
+            cis_phase_tan(r, A.K1, tab, c, sn, v);
             if constexpr (ATT == 2) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
           }
-          acc.template add<KIND>(o, w, y, cs);
+          acc.template add_tan<KIND>(o, w, y, c, sn, v);
         }
       }
       const size_t q = q0 + 32 * static_cast<size_t>(cb) + lane;
@@ -377,16 +382,16 @@ __device__ __forceinline__ void direct_term(Acc<MO, KIND == kKindPair>& acc, int
   const double r = radius_of<KIND>(d2, y);
   GK_DASSERT(r >= r_floor * (1.0 - 1e-12));
   double w = pzw.y;
-  double2 cs;
+  double c, sn, v;  // (cos kr, sin kr) / (1 + v)
   if constexpr (ATT == 1) {
     double a;
-    cs = cis_phase_att(r, A.K1, tab, pa, a);
+    cis_phase_att_tan(r, A.K1, tab, pa, a, c, sn, v);
     w = __dmul_rn(w, a);
   } else {
-    cs = cis_phase(r, A.K1, tab);
+    cis_phase_tan(r, A.K1, tab, c, sn, v);
     if constexpr (ATT == 2) w = __dmul_rn(w, atten_table(r, A.KA, att, A.natten));
   }
-  acc.template add<KIND>(o, w, y, cs);
+  acc.template add_tan<KIND>(o, w, y, c, sn, v);
 }
 
 // K4e: the direct fill with shared edges (edges.cu).  A tile is 12 rows x one

@@ -49,12 +49,15 @@ constexpr double kMagicRint = 6755399441055744.0; // 1.5 * 2^52
 // delta - delta^3/6 (dropped delta^5/120 < 7e-20); cos delta - 1 = c delta^2
 // with c the minimax constant on [0, D^2] (kCosMinimax): max error
 // 0.00715 D^4 = 1.5e-16 (0.7 ulp of 1) for one DMUL instead of FMA + DMUL.
-constexpr int kPhaseM = 8192;
-constexpr int kPhaseLog2 = 13;
+#ifndef GK_PHASE_COPYLOG2
+#define GK_PHASE_COPYLOG2 0
+#endif
+constexpr int kPhaseLog2 = 13 - GK_PHASE_COPYLOG2;
+constexpr int kPhaseM = 1 << kPhaseLog2;
 // table entries per angle (1: one table).  Tried: 8 lane-interleaved copies of
 // a 1024-entry table (conflict-free LDS.128, 2 more FP64 ops for the longer
 // polynomials) -- C5 K4e 502 vs 468 ms, K4 883 vs 799 ms: not adopted
-constexpr int kPhaseCopyLog2 = 0;
+constexpr int kPhaseCopyLog2 = GK_PHASE_COPYLOG2;
 constexpr int kPhaseSlots = kPhaseM << kPhaseCopyLog2;  // table entries (double2)
 // c = -1/2 + b D^2, b = (sqrt 2 - 1)/12: the error x(-1/2 - c) + x^2/24,
 // x = delta^2, equioscillates at x = D^2 and x = -12(-1/2 - c)
@@ -586,11 +589,54 @@ __device__ __forceinline__ unsigned phase_slot(unsigned n) {
 __device__ __forceinline__ void phase_poly(double f, double& v, double& s) {
   constexpr double C = 2.0 * kPi / kPhaseM;
   const double g = __dmul_rn(f, f);
-  constexpr double a1 = kCosMinimax * C * C;
   constexpr double s1 = C;
   constexpr double s3 = -C * C * C / 6.0;
-  v = __dmul_rn(a1, g);
-  s = __dmul_rn(f, __fma_rn(s3, g, s1));
+  if constexpr (kPhaseM >= 8192) {
+    constexpr double a1 = kCosMinimax * C * C;
+    v = __dmul_rn(a1, g);
+    s = __dmul_rn(f, __fma_rn(s3, g, s1));
+  } else {  // coarser tables: one more term each (M = 1024: dropped < 1.2e-18)
+    constexpr double a1 = -C * C / 2.0, a2 = C * C * C * C / 24.0;
+    constexpr double s5 = C * C * C * C * C / 120.0;
+    v = __dmul_rn(g, __fma_rn(a2, g, a1));
+    s = __dmul_rn(f, __fma_rn(__fma_rn(s5, g, s3), g, s1));
+  }
+}
+
+// The same rotation in the tan form (the fills' direct term): with
+// tau = tan(delta) = delta + delta^3/3 (+ 2 delta^5/15 for coarser tables;
+// dropped terms < 1.2e-18) and 1 + v = cos(delta),
+//   cos(theta0 + delta) = (1 + v) (C0 - tau S0),  sin(theta0 + delta) = (1 + v) (S0 + tau C0):
+// the caller folds 1 + v into the term's weight (Acc::add_tan), one FP64
+// operation fewer per term than cis_phase + Acc::add.
+__device__ __forceinline__ void phase_poly_tan(double f, double& v, double& tau) {
+  constexpr double C = 2.0 * kPi / kPhaseM;
+  constexpr double t1 = C, t3 = C * C * C / 3.0;
+  const double g = __dmul_rn(f, f);
+  if constexpr (kPhaseM >= 8192) {
+    constexpr double a1 = kCosMinimax * C * C;
+    v = __dmul_rn(a1, g);
+    tau = __dmul_rn(f, __fma_rn(t3, g, t1));
+  } else {
+    constexpr double a1 = -C * C / 2.0, a2 = C * C * C * C / 24.0;
+    constexpr double t5 = 2.0 * C * C * C * C * C / 15.0;
+    v = __dmul_rn(g, __fma_rn(a2, g, a1));
+    tau = __dmul_rn(f, __fma_rn(__fma_rn(t5, g, t3), g, t1));
+  }
+}
+
+// (c, sn) = (cos kr, sin kr) / (1 + v): 8 FP64 ops + 1 LDS.128
+__device__ __forceinline__ void cis_phase_tan(double r, double K1, const double2* tab, double& c,
+                                              double& sn, double& v) {
+  const double t = __fma_rn(r, K1, kMagicRint);
+  const double nf = t - kMagicRint;
+  const double f = __fma_rn(r, K1, -nf);
+  const unsigned idx = phase_slot(static_cast<unsigned>(__double2loint(t)));
+  double tau;
+  phase_poly_tan(f, v, tau);
+  const double2 T = tab[idx];
+  c = __fma_rn(-tau, T.y, T.x);
+  sn = __fma_rn(tau, T.x, T.y);
 }
 
 __device__ __forceinline__ double2 cis_phase(double r, double K1, const double2* tab) {
@@ -637,16 +683,19 @@ __device__ __forceinline__ double2 cis_phase_small(double r, double K1s, const d
 // factor is folded into the (per-fill) scaled phase table
 // tab[lo] = (cos, sin)(2 pi lo / M) exp(c lo), the second is ahi[hi] (a few
 // entries), the third a degree-4 polynomial in f (|c f| <= 1e-3 by
-// construction: dropped term < 1e-17).  Returns the rotation like cis_phase
-// and the attenuation factor in *att: 6 FP64 ops more than lossless
+// construction: dropped term < 1e-17).  Gives the rotation like cis_phase_tan
+// and the attenuation factor in att: 6 FP64 ops more than lossless
 // (4 polynomial + 1 product, + 1 for the weight at the call site).
 struct PhaseAtt {
   const double* ahi;
   int nhi;
   double q1, q2, q3, q4;  // c, c^2/2, c^3/6, c^4/24
 };
-__device__ __forceinline__ double2 cis_phase_att(double r, double K1, const double2* tab,
-                                                 const PhaseAtt& pa, double& att) {
+// The rotation in the tan form (see cis_phase_tan): (c, sn) = (cos kr, sin kr)
+// exp(c lo) / (1 + v), and the attenuation's remaining factor in att
+__device__ __forceinline__ void cis_phase_att_tan(double r, double K1, const double2* tab,
+                                                  const PhaseAtt& pa, double& att, double& c,
+                                                  double& sn, double& v) {
   const double t = __fma_rn(r, K1, kMagicRint);
   const double nf = t - kMagicRint;
   const double f = __fma_rn(r, K1, -nf);
@@ -654,14 +703,13 @@ __device__ __forceinline__ double2 cis_phase_att(double r, double K1, const doub
   const unsigned idx = phase_slot(n);
   unsigned hi = n >> kPhaseLog2;
   hi = hi < static_cast<unsigned>(pa.nhi) ? hi : static_cast<unsigned>(pa.nhi - 1);
-  double v, s;
-  phase_poly(f, v, s);
+  double tau;
+  phase_poly_tan(f, v, tau);
   const double2 T = tab[idx];
-  const double c = __fma_rn(-T.y, s, __fma_rn(T.x, v, T.x));
-  const double sn = __fma_rn(T.x, s, __fma_rn(T.y, v, T.y));
+  c = __fma_rn(-tau, T.y, T.x);
+  sn = __fma_rn(tau, T.x, T.y);
   const double p = __fma_rn(__fma_rn(__fma_rn(__fma_rn(pa.q4, f, pa.q3), f, pa.q2), f, pa.q1), f, 1.0);
   att = __dmul_rn(pa.ahi[hi], p);
-  return make_double2(c, sn);
 }
 
 // exp(-x) for x = -k_im r >= 0 (lossy media) from a shared table
