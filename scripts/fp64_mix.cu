@@ -75,8 +75,8 @@ __global__ void __launch_bounds__(256, 2) kC(double* sink, int iters, const doub
 // 22 FP64 ops shaped like one term of the expanded far path (far_term): the
 // squared distance as a chain of four 3-register FMAs, the folded weight, the
 // tan-form rotation; 6 independent "evals" per iteration
-template <int TPB>
-__global__ void __launch_bounds__(TPB, 768 / TPB) kD(double* sink, int iters, const double* in) {
+template <int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) kD(double* sink, int iters, const double* in) {
   double ax[6], ay[6], az[6], aA[6], ex[6], ey[6];
   for (int k = 0; k < 6; ++k) {
     ax[k] = in[threadIdx.x % 32 + k] * 1e-3 + 0.5;
@@ -116,8 +116,8 @@ __global__ void __launch_bounds__(TPB, 768 / TPB) kD(double* sink, int iters, co
 
 // kC's mix (the difference form) in the same shape as kD: per-o coordinates
 // and two accumulators per o
-template <int TPB, bool TAN>
-__global__ void __launch_bounds__(TPB, 768 / TPB) kE(double* sink, int iters, const double* in) {
+template <int TPB, bool TAN, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) kE(double* sink, int iters, const double* in) {
   double ox[6], oy[6], oz[6], ex[6], ey[6];
   for (int k = 0; k < 6; ++k) {
     ox[k] = in[threadIdx.x % 32 + k] * 1e-3 + 0.5;
@@ -166,6 +166,57 @@ __global__ void __launch_bounds__(TPB, 768 / TPB) kE(double* sink, int iters, co
   if (r == 1234.5) sink[0] = r;
 }
 
+// kE's difference-form term with features of kC switched in one at a time
+// (F bit 0: K1 immediate; 1: the three coordinates taken from one array of 6;
+// 2: 6 accumulators instead of 12; 3: the table entry = (x[o], y) instead of
+// two loop-invariant registers): which of them costs kE its 15 % against kC
+template <int F>
+__global__ void __launch_bounds__(384, 1) kF(double* sink, int iters, const double* in) {
+  double ox[6], oy[6], oz[6], ex[6], ey[6];
+  for (int k = 0; k < 6; ++k) {
+    ox[k] = in[threadIdx.x % 32 + k] * 1e-3 + 0.5;
+    oy[k] = in[threadIdx.x % 32 + k + 6] * 1e-3 + 0.4;
+    oz[k] = in[threadIdx.x % 32 + k + 12] * 1e-3 + 0.3;
+    ex[k] = ey[k] = 0;
+  }
+  double px = in[1], py = in[2], pz = in[3], w = in[4], K1r = in[6], tx = in[7], ty = in[8];
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int o = 0; o < 6; ++o) {
+      const double cx = ox[o], cy = (F & 2) ? ox[(o + 1) % 6] : oy[o], cz = (F & 2) ? ox[(o + 2) % 6] : oz[o];
+      double dx = cx - px, dy = cy - py, dz = cz - pz;
+      double d2 = __fma_rn(dz, dz, __fma_rn(dy, dy, __dmul_rn(dx, dx)));
+      double y = d2 * 0.7;
+      double e = __fma_rn(-d2, __dmul_rn(y, y), 1.0);
+      double ye = __dmul_rn(y, e);
+      y = __fma_rn(ye, __fma_rn(0.375, e, 0.5), y);
+      double r = __dmul_rn(d2, y);
+      const double K1 = (F & 1) ? 13.7 : K1r;
+      double t = __fma_rn(r, K1, 6755399441055744.0);
+      double nf = t - 6755399441055744.0;
+      double f = __fma_rn(r, K1, -nf);
+      double g = __dmul_rn(f, f);
+      double v = __dmul_rn(g, -1e-6);
+      double sd = __dmul_rn(f, __fma_rn(-1e-10, g, 1.5e-3));
+      const double Tx = (F & 8) ? cx : tx, Ty = (F & 8) ? y : ty;
+      double c = __fma_rn(-Ty, sd, __fma_rn(Tx, v, Tx));
+      double sn = __fma_rn(Tx, sd, __fma_rn(Ty, v, Ty));
+      double wg = __dmul_rn(w, y);
+      if (F & 4) {
+        ex[o] = __fma_rn(wg, c, ex[o]);
+        ex[(o + 3) % 6] = __fma_rn(-wg, sn, ex[(o + 3) % 6]);
+      } else {
+        ex[o] = __fma_rn(wg, c, ex[o]);
+        ey[o] = __fma_rn(-wg, sn, ey[o]);
+      }
+    }
+    px += 1e-12; py -= 1e-12; tx += 1e-13; ty -= 1e-13;
+  }
+  double r = 0;
+  for (int k = 0; k < 6; ++k) r += ex[k] + ey[k];
+  if (r == 1234.5) sink[0] = r;
+}
+
 int main() {
   double *sink, *in;
   cudaMalloc(&sink, 8);
@@ -202,13 +253,22 @@ int main() {
   // evaluations per second per SM matter, not lane-ops: the line also gives
   // cycles per warp-eval per SMSP = 4 * 32 * ops / (lane-ops/clk/SM)
   tpb = 384;
-  run("E difference form 26 ops, 12 warps (1 CTA/SM)", [&](int g, int it) { kE<384, false><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
-  run("E' difference + tan 25 ops, 12 warps        ", [&](int g, int it) { kE<384, true><<<g, 384>>>(sink, it, in); }, 6 * 25.0, 1, 8192);
-  run("D expanded 22 ops, 12 warps (1 CTA/SM)       ", [&](int g, int it) { kD<384><<<g, 384>>>(sink, it, in); }, 6 * 22.0, 1, 8192);
+  run("E difference form 26 ops, 12 warps, <= 80 regs ", [&](int g, int it) { kE<384, false, 2><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
+  run("E' difference + tan 25 ops, 12 warps, <= 80   ", [&](int g, int it) { kE<384, true, 2><<<g, 384>>>(sink, it, in); }, 6 * 25.0, 1, 8192);
+  run("D expanded 22 ops, 12 warps, <= 80 regs       ", [&](int g, int it) { kD<384, 2><<<g, 384>>>(sink, it, in); }, 6 * 22.0, 1, 8192);
+  run("E  difference 26 ops, 12 warps, <= 168 regs  ", [&](int g, int it) { kE<384, false, 1><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
+  run("E' difference + tan 25 ops, <= 168 regs      ", [&](int g, int it) { kE<384, true, 1><<<g, 384>>>(sink, it, in); }, 6 * 25.0, 1, 8192);
+  run("D  expanded 22 ops, <= 168 regs              ", [&](int g, int it) { kD<384, 1><<<g, 384>>>(sink, it, in); }, 6 * 22.0, 1, 8192);
+  run("F0 = E                                       ", [&](int g, int it) { kF<0><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
+  run("F1 K1 immediate                              ", [&](int g, int it) { kF<1><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
+  run("F2 shared coordinates                        ", [&](int g, int it) { kF<2><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
+  run("F4 6 accumulators                            ", [&](int g, int it) { kF<4><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
+  run("F8 table entry from live registers           ", [&](int g, int it) { kF<8><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
+  run("F15 all (= C's shape)                        ", [&](int g, int it) { kF<15><<<g, 384>>>(sink, it, in); }, 6 * 26.0, 1, 8192);
   tpb = 256;
-  run("E difference form 26 ops, 24 warps (3 CTA/SM)", [&](int g, int it) { kE<256, false><<<g, 256>>>(sink, it, in); }, 6 * 26.0, 3, 8192);
-  run("E' difference + tan 25 ops, 24 warps        ", [&](int g, int it) { kE<256, true><<<g, 256>>>(sink, it, in); }, 6 * 25.0, 3, 8192);
-  run("D expanded 22 ops, 24 warps (3 CTA/SM)       ", [&](int g, int it) { kD<256><<<g, 256>>>(sink, it, in); }, 6 * 22.0, 3, 8192);
+  run("E difference form 26 ops, 24 warps (3 CTA/SM)", [&](int g, int it) { kE<256, false, 3><<<g, 256>>>(sink, it, in); }, 6 * 26.0, 3, 8192);
+  run("E' difference + tan 25 ops, 24 warps        ", [&](int g, int it) { kE<256, true, 3><<<g, 256>>>(sink, it, in); }, 6 * 25.0, 3, 8192);
+  run("D expanded 22 ops, 24 warps (3 CTA/SM)       ", [&](int g, int it) { kD<256, 3><<<g, 256>>>(sink, it, in); }, 6 * 22.0, 3, 8192);
   cudaDeviceSynchronize();
   std::printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
