@@ -746,7 +746,7 @@ gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out) {
   return guarded([&] {
     need(mesh != nullptr && out != nullptr, GK_ERR_INVALID_ARGUMENT, "null argument");
     out->blocks = mesh->es.nblk;
-    out->edge_slots = mesh->es.nblk ? mesh->es.ep.n / static_cast<size_t>(mesh->n) : 0;
+    out->edge_slots = mesh->es.nblk ? mesh->es.ep.n / (2 * static_cast<size_t>(mesh->n)) : 0;
     out->work_ratio = mesh->es.edge_ratio;
     out->delta = mesh->es.edge_delta;
     out->r_far = mesh->es.r_far;
@@ -755,7 +755,7 @@ gk_status gk_mesh_edge_info_get(const gk_mesh* mesh, gk_mesh_edge_info* out) {
     out->ordered = mesh->es.ordered ? 1 : 0;
     out->rho_max = mesh->es.rho_max;
     out->sweep_blocks = mesh->sweep.nblk;
-    out->sweep_edge_slots = mesh->sweep.nblk ? mesh->sweep.ep.n / static_cast<size_t>(mesh->n) : 0;
+    out->sweep_edge_slots = mesh->sweep.nblk ? mesh->sweep.ep.n / (2 * static_cast<size_t>(mesh->n)) : 0;
     out->sweep_work_ratio = mesh->sweep.edge_ratio;
     out->sweep_rho_max = mesh->sweep.rho_max;
   });

@@ -38,7 +38,7 @@ namespace {
 // owner slot code: (t << 3) | (side << 1) | pad
 __global__ void edge_gather_kernel(const double4* __restrict__ inner, size_t N, int n,
                                    const unsigned long long* __restrict__ owner, size_t nslots,
-                                   double4* __restrict__ ep) {
+                                   double2* __restrict__ ep) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   if (i >= nslots * n) return;
   const size_t slot = i / n;
@@ -48,7 +48,11 @@ __global__ void edge_gather_kernel(const double4* __restrict__ inner, size_t N, 
   const int s = static_cast<int>((o >> 1) & 3);
   double4 P = inner[static_cast<size_t>(s * n + g) * N + t];
   if (o & 1) P.w = 0.0;  // padding lane: a real point of the block, zero weight
-  ep[((slot >> 5) * n + g) * 32 + (slot & 31)] = P;
+  // two planes per point, (x, y) and (z, w): a warp's load of either is one
+  // 512-byte run
+  const size_t at = ((slot >> 5) * n + g) * 64 + (slot & 31);
+  ep[at] = make_double2(P.x, P.y);
+  ep[at + 32] = make_double2(P.z, P.w);
 }
 
 // max over the sides (t, s) that do not own their edge slot of
@@ -58,7 +62,7 @@ __global__ void edge_gather_kernel(const double4* __restrict__ inner, size_t N, 
 __global__ void edge_delta_kernel(const double4* __restrict__ inner, size_t N, int n,
                                   const uint32_t* __restrict__ gslot,
                                   const unsigned long long* __restrict__ owner,
-                                  const double4* __restrict__ ep, unsigned long long* dmax) {
+                                  const double2* __restrict__ ep, unsigned long long* dmax) {
   const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
   double d = 0.0;
   if (i < 3 * N * static_cast<size_t>(n)) {
@@ -71,10 +75,11 @@ __global__ void edge_delta_kernel(const double4* __restrict__ inner, size_t N, i
     const unsigned long long mine = (static_cast<unsigned long long>(t) << 3) | (s << 1);
     if (owner[slot] != mine) {
       const double4 P = inner[static_cast<size_t>(s * n + g) * N + t];
-      const double4 Q = ep[((slot >> 5) * static_cast<size_t>(n) + gq) * 32 + (slot & 31)];
-      const double dx = P.x - Q.x, dy = P.y - Q.y, dz = P.z - Q.z;
+      const size_t at = ((slot >> 5) * static_cast<size_t>(n) + gq) * 64 + (slot & 31);
+      const double2 Qxy = ep[at], Qzw = ep[at + 32];
+      const double dx = P.x - Qxy.x, dy = P.y - Qxy.y, dz = P.z - Qzw.x;
       d = sqrt(dx * dx + dy * dy + dz * dz);
-      if (P.w != Q.w) d = INFINITY;  // weights must match exactly (symmetric rule)
+      if (P.w != Qzw.y) d = INFINITY;  // weights must match exactly (symmetric rule)
     }
   }
   for (int off = 16; off > 0; off >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, off));
@@ -352,7 +357,7 @@ void build_edge_set(const gk_mesh* mesh, const double* verts, const uint32_t* tr
   d_gslot.alloc(3 * N, st);
   S.eblk.alloc(blocks.size(), st);
   S.ecol.alloc(N, st);
-  S.ep.alloc(nslots * n, st);
+  S.ep.alloc(nslots * n * 2, st);
   GK_CUDA(cudaMemcpyAsync(d_owner.p, owner.data(), nslots * sizeof(unsigned long long),
                           cudaMemcpyHostToDevice, st));
   GK_CUDA(cudaMemcpyAsync(d_gslot.p, R.gslot.data(), 3 * N * sizeof(uint32_t), cudaMemcpyHostToDevice, st));

@@ -133,7 +133,7 @@ struct FillArgs {
                                  // [3] kernel evaluations performed
   // shared-edge fill (direct_edge_kernel, edges.cu)
   const EdgeBlock* eblk;
-  const double4* ep;
+  const double2* ep;  // [chunk][n][2][32]: (x, y) and (z, w) planes
   const uint4* ecol;  // per block position: (triangle q, e0 | e1 << 16, e2, 0)
   size_t nblk;
   int ecap;  // edge-sum slots per warp (>= every block's edge count)
@@ -143,7 +143,7 @@ struct FillArgs {
   // its spatial order (clusters of s_rc), the staged window's capacity in
   // base nodes
   const EdgeBlock* s_eblk;
-  const double4* s_ep;
+  const double2* s_ep;
   const uint4* s_ecol;
   size_t s_nblk;
   int s_ecap;
@@ -468,19 +468,19 @@ __global__ void __launch_bounds__(32 * edge_warps<KIND>(), 1) direct_edge_kernel
     if (far) {
       const int nch = static_cast<int>((B.ne + 31) >> 5);
       GK_DASSERT(B.ne <= static_cast<uint32_t>(A.ecap) && B.tb < B.te && B.te <= N);
-      const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
-      double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
-      double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
+      const double2* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 64 + lane;
+      double2 cxy = __ldg(ep);
+      double2 czw = __ldg(ep + 32);
       for (int c = 0; c < nch; ++c) {
         Acc<MO, PAIR> acc;
         acc.zero();
         GK_UNROLL(GK_EDGE_GUNROLL)
         for (int g = 0; g < NPE; ++g) {
           const double2 pxy = cxy, pzw = czw;
-          const double4* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 32
-                                                : (c + 1 < nch ? (c + 1) * NPE * 32 : 0));
-          cxy = __ldg(reinterpret_cast<const double2*>(np));
-          czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
+          const double2* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 64
+                                                : (c + 1 < nch ? (c + 1) * NPE * 64 : 0));
+          cxy = __ldg(np);
+          czw = __ldg(np + 32);
 #pragma unroll
           for (int o = 0; o < MO; ++o)
             direct_term<MO, KIND, ATT>(acc, o, ox[o], oy[o], oz[o], pxy, pzw, A, tab, pa, att,
@@ -700,19 +700,19 @@ __device__ __forceinline__ void table_edge_tile(const FillArgs& A, size_t p, siz
   if (far) {
     const int nch = static_cast<int>((B.ne + 31) >> 5);
     GK_DASSERT(B.ne <= static_cast<uint32_t>(A.ecap) && B.tb < B.te && B.te <= N);
-    const double4* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 32 + lane;
-    double2 cxy = __ldg(reinterpret_cast<const double2*>(ep));
-    double2 czw = __ldg(reinterpret_cast<const double2*>(ep) + 1);
+    const double2* ep = A.ep + static_cast<size_t>(B.c0) * NPE * 64 + lane;
+    double2 cxy = __ldg(ep);
+    double2 czw = __ldg(ep + 32);
     for (int c = 0; c < nch; ++c) {
       Acc<MO, PAIR> acc;
       acc.zero();
       GK_UNROLL(GK_TEDGE_GUNROLL)
       for (int g = 0; g < NPE; ++g) {
         const double2 pxy = cxy, pzw = czw;
-        const double4* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 32
-                                              : (c + 1 < nch ? (c + 1) * NPE * 32 : 0));
-        cxy = __ldg(reinterpret_cast<const double2*>(np));
-        czw = __ldg(reinterpret_cast<const double2*>(np) + 1);
+        const double2* np = ep + (g + 1 < NPE ? (c * NPE + g + 1) * 64
+                                              : (c + 1 < nch ? (c + 1) * NPE * 64 : 0));
+        cxy = __ldg(np);
+        czw = __ldg(np + 32);
 #pragma unroll
         for (int o = 0; o < MO; ++o) {
           const double d2 = dist2(ox[o], oy[o], oz[o], pxy.x, pxy.y, pzw.x);

@@ -104,8 +104,8 @@ struct TableDev {
 // Shared-edge fills (direct_edge_kernel, table_edge_kernel; edges.cu): a
 // block is the range [tb, te) of block positions (a bisection order of the
 // source triangles, or the mesh order) and the distinct edges its triangles
-// use (ne <= the mesh's edge cap), whose points sit at ep[c0 * n * 32 ...] as
-// [chunk][point][32 lanes].  (cx, cy, cz, rho) bounds every inner point of
+// use (ne <= the mesh's edge cap), whose points sit at ep[c0 * n * 64 ...] as
+// [chunk][point][(x, y) | (z, w)][32 lanes] double2.  (cx, cy, cz, rho) bounds every inner point of
 // the block.
 //
 // Edge cap: 11 warp-wide chunks (352 edges) by default, 1..12 with

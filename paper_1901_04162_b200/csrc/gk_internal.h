@@ -93,7 +93,7 @@ struct DevBuf {
 // block's radius spread).
 struct EdgeSet {
   DevBuf<EdgeBlock> eblk;  // [nblk]
-  DevBuf<double4> ep;      // [chunks][n][32] edge points (owner orientation)
+  DevBuf<double2> ep;      // [chunks][n][2][32] edge points (owner orientation): (x, y) and (z, w) planes
   DevBuf<uint4> ecol;      // [N] by block position: (triangle, e0 | e1 << 16, e2, 0)
   uint64_t edges = 0;
   int ecap = 0;  // edges per block (shared-memory slots per warp)

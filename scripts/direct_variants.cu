@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "gk/gk.h"
 #include "gk_device.cuh"
 
 using namespace gk;

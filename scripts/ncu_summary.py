@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarise ncu reports into the markdown/JSON kept under profiles/.
 
-usage: ncu_summary.py OUT_PREFIX REPORT.ncu-rep [REPORT.ncu-rep ...]
+usage: ncu_summary.py OUT_PREFIX REPORT.ncu-rep|REPORT.raw.csv [...]
 Reads each report with `ncu -i --page raw --csv` (no GPU needed) and writes
 OUT_PREFIX.md (table of the counters the north star asks for) and
 OUT_PREFIX.json (the same values, machine readable).
@@ -42,8 +42,13 @@ METRICS = [
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
+    # a report, or its `ncu -i REPORT --page raw --csv` export (made on the GPU
+    # box when the report itself is too large to bring back)
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     return {h: (v, u) for h, u, v in zip(rows[0], rows[1], rows[2])}
 
@@ -53,7 +58,7 @@ def main():
     data = {}
     for rep in reps:
         d = raw(rep)
-        name = os.path.basename(rep).replace(".ncu-rep", "")
+        name = os.path.basename(rep).replace(".ncu-rep", "").replace(".raw.csv", "")
         vals = {"kernel": d.get("Kernel Name", ("?", ""))[0]}
         for label, key in METRICS:
             if key is None:
