@@ -311,6 +311,13 @@ EdgePlan plan_edge_blocks(const double* verts, size_t nv, const uint32_t* tris, 
       stack.push_back({lo, mid});
     }
     std::sort(cuts.begin(), cuts.end());
+    // within a leaf the order is free: ascending triangle index, so that a
+    // warp's 32 stores of one row fall on as few 128-byte lines of Z as the
+    // mesh numbering allows (subdivided meshes number siblings consecutively)
+    for (size_t i = 0; i < cuts.size(); ++i) {
+      const size_t lo = cuts[i], hi = i + 1 < cuts.size() ? cuts[i + 1] : N;
+      std::sort(sorder.begin() + lo, sorder.begin() + hi);
+    }
   }
   Blocks Rm = make_blocks(&sorder, &cuts);
   bool ordered = order_mode < 0 ? Rm.rho_mean < 0.75 * R.rho_mean : order_mode == 1;
