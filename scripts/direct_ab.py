@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Direct-fill timings (K4e shared edges and K4 per triangle) on the bench
 configurations, full matrices; for A/B of libgk builds (GK_LIB=...).
-Usage: direct_ab.py [c3 c4 c5] [--reps R]"""
+Usage: direct_ab.py [c3 c4 c5] [--reps R] [--leaf P1,P2,...] [--chunks C1,C2,...]
+(--leaf / --chunks: K4e only, one line per bisection leaf size / block size)"""
 import os
 import sys
 
@@ -24,6 +25,23 @@ def main():
                         eps_r_im=cfg.get("eps_r_im", 0.0))
         k = gk.wavenumber(med)
         Z = torch.empty((N, N), dtype=torch.complex128, device="cuda")
+        leaf = sys.argv[sys.argv.index("--leaf") + 1].split(",") if "--leaf" in sys.argv else []
+        chunks = sys.argv[sys.argv.index("--chunks") + 1].split(",") if "--chunks" in sys.argv else [0]
+        for lp in leaf:
+            for ch in chunks:
+                dmv = gk.DeviceMesh(mesh, gk.QuadratureSpec(cfg["m"], cfg["n"]),
+                                    options=gk.MeshOptions(leaf_pct=int(lp), edge_chunks=int(ch)))
+                best = None
+                for _ in range(reps):
+                    _, rep = gk.fill_rows(dmv, gk.Mode.DIRECT, k=k, out=Z)
+                    best = rep if best is None or rep.wall_time_s < best.wall_time_s else best
+                info = dmv.edge_info()
+                print(f"{name} leaf_pct={lp} chunks={ch or 'default'} blocks={info['blocks']} "
+                      f"slots/3N={info['work_ratio']:.4f}: {best.wall_time_s * 1e3:.2f} ms "
+                      f"(evaluations {best.evaluations / best.actual_calls:.4f})", flush=True)
+                del dmv
+        if leaf:
+            continue
         for label, opts in (("edge", None), ("pertri", gk.FillOptions(shared_edges=0))):
             best = None
             for _ in range(reps):
