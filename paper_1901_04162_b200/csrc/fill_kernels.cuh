@@ -412,6 +412,9 @@ __device__ __forceinline__ void direct_term(Acc<MO, KIND == kKindPair>& acc, int
 #ifndef GK_EDGE_GUNROLL
 #define GK_EDGE_GUNROLL 5  // unroll of the edge-point loop (n <= 5: full)
 #endif
+#ifndef GK_EDGE_NEAR_UNROLL
+#define GK_EDGE_NEAR_UNROLL 1  // unroll of the near tiles' point loop (A/B)
+#endif
 #define GK_PRAGMA(x) _Pragma(#x)
 #define GK_UNROLL(n) GK_PRAGMA(unroll n)
 
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(32 * edge_warps<KIND>(), 1) direct_edge_kernel
         nq += __popc(__ballot_sync(0xffffffffu, valid && q != p));
         Acc<MO, PAIR> acc;
         acc.zero();
-#pragma unroll 1
+        GK_UNROLL(GK_EDGE_NEAR_UNROLL)
         for (int i = 0; i < IPT; ++i) {
           const double2* ptr = reinterpret_cast<const double2*>(A.inner + static_cast<size_t>(i) * N + q);
           const double2 pxy = __ldg(ptr), pzw = __ldg(ptr + 1);

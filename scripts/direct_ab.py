@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Direct-fill timings (K4e shared edges and K4 per triangle) on the bench
 configurations, full matrices; for A/B of libgk builds (GK_LIB=...).
-Usage: direct_ab.py [c3 c4 c5] [--reps R] [--leaf P1,P2,...] [--chunks C1,C2,...]
+Usage: direct_ab.py [c3 c4 c5] [--reps R] [--edge-only] [--leaf P1,P2,...] [--chunks C1,C2,...]
 (--leaf / --chunks: K4e only, one line per bisection leaf size / block size)"""
 import os
 import sys
@@ -42,7 +42,10 @@ def main():
                 del dmv
         if leaf:
             continue
-        for label, opts in (("edge", None), ("pertri", gk.FillOptions(shared_edges=0))):
+        variants = (("edge", None), ("pertri", gk.FillOptions(shared_edges=0)))
+        if "--edge-only" in sys.argv:
+            variants = variants[:1]
+        for label, opts in variants:
             best = None
             for _ in range(reps):
                 _, rep = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, out=Z, options=opts)
