@@ -608,7 +608,8 @@ __device__ __forceinline__ void phase_poly(double f, double& v, double& s) {
 // dropped terms < 1.2e-18) and 1 + v = cos(delta),
 //   cos(theta0 + delta) = (1 + v) (C0 - tau S0),  sin(theta0 + delta) = (1 + v) (S0 + tau C0):
 // the caller folds 1 + v into the term's weight (Acc::add_tan), one FP64
-// operation fewer per term than cis_phase + Acc::add.
+// operation fewer per term than the sin/cos form (cis_phase below, kept for
+// the ablation harnesses under scripts/).
 __device__ __forceinline__ void phase_poly_tan(double f, double& v, double& tau) {
   constexpr double C = 2.0 * kPi / kPhaseM;
   constexpr double t1 = C, t3 = C * C * C / 3.0;
