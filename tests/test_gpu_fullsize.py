@@ -98,10 +98,11 @@ def test_table_fullsize_vs_oracle(gk, oracle, case, S):
         assert rep.fallback_calls == orep.fallback_calls == 0   # K1 range is exact
 
 
-def test_row_blocks_tile_the_full_matrix_checksum(gk, case):
+@pytest.mark.parametrize("mode", ["direct", "table"])
+def test_row_blocks_tile_the_full_matrix_checksum(gk, case, mode):
     """Size-independent property at full size: filling [0, N) in one call and
-    in 3 uneven row blocks gives bitwise the same rows (sum of |Z| checked
-    block by block, plus the full row equality of the block seams)."""
+    in 3 uneven row blocks gives bitwise the same rows, in direct mode and
+    through the dense table (the sum of |Z| is accumulated block by block)."""
     import torch
     name, c, mesh, med, dm = case
     k = gk.wavenumber(med)
@@ -115,10 +116,17 @@ def test_row_blocks_tile_the_full_matrix_checksum(gk, case):
         need = 16 * N * (N + max(e - b for b, e in zip(cuts[:-1], cuts[1:]))) + (4 << 30)
         if free < need:
             pytest.skip(f"C5 needs {need / 2**30:.0f} GiB free, the device has {free / 2**30:.0f}")
-    full, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k)
+    kw = dict(k=k)
+    md = gk.Mode.DIRECT
+    if mode == "table":  # the dense table (S = 1e4): the sweep K3s on C3-C5
+        lo, hi = dm.distance_range()
+        kw = dict(table=gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi,
+                                                         samples_per_wavelength=10000), med))
+        md = gk.Mode.TABLE
+    full, _ = gk.fill_rows(dm, md, **kw)
     total = 0.0
     for b, e in zip(cuts[:-1], cuts[1:]):
-        part, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, row_begin=b, row_end=e)
+        part, _ = gk.fill_rows(dm, md, row_begin=b, row_end=e, **kw)
         for r0 in range(b, e, 2048):  # bitwise, 2048 rows at a time (no matrix-sized temporaries)
             r1 = min(e, r0 + 2048)
             assert torch.equal(part[r0 - b:r1 - b], full[r0:r1]), (name, r0)
