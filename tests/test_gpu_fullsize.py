@@ -202,3 +202,21 @@ def test_table_against_direct_whole_matrix(gk, case):
     torch.cuda.empty_cache()
     print(f"{name}: max |Z_table - Z_direct| / |Z_direct| over all {N}x{N} entries = {worst:.3e}")
     assert worst < {"c3": 5e-7, "c4": 2e-6, "c5": 1e-8}[name], worst
+
+
+def test_fused_pair_equals_separate_fills_full_width(gk, case):
+    """gk_fill_rows_pair at the configurations' full width (8192 rows x all N
+    columns): Exp and Green from one pass, bitwise equal to the two separate
+    fills, through the default kernels of each configuration."""
+    import torch
+    name, c, mesh, med, dm = case
+    k = gk.wavenumber(med)
+    rows = min(dm.N, 8192)
+    ze, zg, rep = gk.fill_rows_pair(dm, gk.Mode.DIRECT, k=k, row_end=rows)
+    e, re_ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, kind=gk.KernelKind.PlainExp, row_end=rows)
+    assert torch.equal(ze, e)
+    del e
+    g, rg = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, kind=gk.KernelKind.GreenOverR, row_end=rows)
+    assert torch.equal(zg, g)
+    assert rep.actual_calls == re_.actual_calls + rg.actual_calls
+    assert rep.evaluations == re_.evaluations + rg.evaluations
