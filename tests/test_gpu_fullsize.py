@@ -220,3 +220,42 @@ def test_fused_pair_equals_separate_fills_full_width(gk, case):
     assert torch.equal(zg, g)
     assert rep.actual_calls == re_.actual_calls + rg.actual_calls
     assert rep.evaluations == re_.evaluations + rg.evaluations
+
+
+def test_scale_invariance_is_bitwise(gk, case):
+    """Size-independent property: scaling the mesh and the wavelength by 2
+    scales every radius by 2 and leaves k r unchanged, so Z (weights x 8, 1/r
+    x 1/2) scales by exactly 4.  Powers of two commute with every rounding on
+    the path (points, block plan, far test, rsqrt seed and Newton step, phase
+    reduction, attenuation, sums), so the direct fill must reproduce that
+    bitwise -- at the configurations' full width, through their default
+    kernels."""
+    import torch
+    name, c, mesh, med, dm = case
+    rows = min(dm.N, 8192)
+    z1, r1 = gk.fill_rows(dm, gk.Mode.DIRECT, k=gk.wavenumber(med), row_end=rows)
+    mesh2 = gk.TriangleMesh(mesh.vertices * 2.0, mesh.triangles)
+    med2 = gk.Medium(lambda0=2.0 * c["lambda0"], eps_r=c.get("eps_r", 1.0),
+                     eps_r_im=c.get("eps_r_im", 0.0))
+    dm2 = gk.DeviceMesh(mesh2, gk.QuadratureSpec(c["m"], c["n"]))
+    z2, r2 = gk.fill_rows(dm2, gk.Mode.DIRECT, k=gk.wavenumber(med2), row_end=rows)
+    assert r2.path_name == r1.path_name and r2.evaluations == r1.evaluations
+    z1 *= 4.0
+    assert torch.equal(z2, z1)
+    del z1, z2
+    # the table scales too: the plan's nodes and zeros double, the node values
+    # halve, the interval records scale by powers of two -- the same property
+    # through the paper's method (S = 1e4: the sweep K3s on C3-C5)
+    lo, hi = dm.distance_range()
+    lo2, hi2 = dm2.distance_range()
+    assert (lo2, hi2) == (2.0 * lo, 2.0 * hi)
+    t1 = gk.DeviceTable(gk.SamplingConfig(r_min=lo, r_max=hi, samples_per_wavelength=10000), med)
+    t2 = gk.DeviceTable(gk.SamplingConfig(r_min=lo2, r_max=hi2, samples_per_wavelength=10000), med2)
+    d1, d2 = t1.download(), t2.download()
+    assert np.array_equal(d2["abscissae"], 2.0 * d1["abscissae"])
+    assert np.array_equal(d2["green"], 0.5 * d1["green"]) and np.array_equal(d2["exp"], d1["exp"])
+    y1, s1 = gk.fill_rows(dm, gk.Mode.TABLE, table=t1, row_end=rows)
+    y2, s2 = gk.fill_rows(dm2, gk.Mode.TABLE, table=t2, row_end=rows)
+    assert s2.path_name == s1.path_name and s2.fallback_calls == s1.fallback_calls == 0
+    y1 *= 4.0
+    assert torch.equal(y2, y1)
