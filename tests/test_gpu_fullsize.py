@@ -259,3 +259,26 @@ def test_scale_invariance_is_bitwise(gk, case):
     assert s2.path_name == s1.path_name and s2.fallback_calls == s1.fallback_calls == 0
     y1 *= 4.0
     assert torch.equal(y2, y1)
+
+
+def test_triangle_permutation_permutes_the_matrix_bitwise(gk, case):
+    """Size-independent property of the per-triangle kernels (the reference's
+    evaluation order): renumbering the triangles permutes rows and columns and
+    changes nothing else -- an entry does not depend on its tile, column block
+    or lane.  Bitwise, whole matrix (C5: skipped, two 107 GB matrices)."""
+    import torch
+    name, c, mesh, med, dm = case
+    if name == "c5":
+        pytest.skip("two 107 GB matrices")
+    k = gk.wavenumber(med)
+    N = dm.N
+    opts = gk.FillOptions(shared_edges=0)
+    z1, _ = gk.fill_rows(dm, gk.Mode.DIRECT, k=k, options=opts)
+    perm = np.random.default_rng(1901).permutation(N)
+    mesh2 = gk.TriangleMesh(mesh.vertices, mesh.triangles[perm])
+    dm2 = gk.DeviceMesh(mesh2, gk.QuadratureSpec(c["m"], c["n"]))
+    z2, _ = gk.fill_rows(dm2, gk.Mode.DIRECT, k=k, options=opts)
+    p = torch.as_tensor(perm, device=z1.device)
+    for r0 in range(0, N, 2048):  # Z2[i][j] = Z1[perm[i]][perm[j]]
+        rows = p[r0:r0 + 2048]
+        assert torch.equal(z2[r0:r0 + 2048], z1[rows][:, p]), (name, r0)
